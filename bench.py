@@ -1,0 +1,440 @@
+#!/usr/bin/env python
+"""bench.py -- BanaServe (arXiv 2510.13223) hot path on B200: layer-wise KV migration
+overlapped with 2-way split decode attention + exact LSE merge.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "C2"): Llama-2-7B shape (32 layers, 32 q/kv heads,
+head_dim 128, bf16 KV), decode batch 64 at 2048 tokens.  Two serving instances --
+decode D (home) and prefill P -- each own a paged pool.  Every request's KV is split
+2-way (tokens [0,1024) in D, [1024,2048) offloaded to P: attention-level migration,
+PAPER.md:207-237 Fig. 4).  During each decode step 3 more 2048-token requests are handed
+off P -> D layer by layer on a side stream (Fig. 6; lookahead 1, event
+gated).  At N=1 both instances share GPU 0 (virtual instances).  One step = all 32
+layers of: migrate(l) || [split attention on D, on P -> LSE merge -> bf16 O].
+
+value = decode tokens/s of the step (B / step time), inputs resident in HBM; pools are
+70 GiB >> 126 MB L2, so no L2 flush is needed.  e2e = the same through host buffers
+(q H2D from pinned memory and O/lse D2H every step).  The CPU oracle is timed beside
+it on a bounded sample (cpu_baseline).  N>1 (torchrun): independent replicas per GPU
+(weak scaling); see DESIGN.md §Multi-GPU.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "split decode-attn HBM GB/s & tokens/s; layer-wise KV migrate NVLink GB/s"
+SHAPE = synth.LLAMA2_7B
+BATCH, SEQ, N_SHARDS, N_HANDOFF = 64, 2048, 2, 3
+WORKLOAD = ("C2: Llama-2-7B shape (L=32, Hq=Hkv=32, d=128, bf16 KV), decode B=64 x 2048 "
+            "tokens, KV split 2-way decode/prefill pool, 3 x 2048-token requests handed off "
+            "prefill->decode layer-wise per step")
+FALLBACK_HBM_GBS = 6650.0
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_attention.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d.get("source")
+    return None, None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if self.proc is None:
+            return None
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.f.name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------------------
+# the workload on the device
+# --------------------------------------------------------------------------------------
+
+def build_workload(bs, device, seed=0, layers=None):
+    from paper_2510_13223_b200.pipeline import LayerwiseDecodeStep, MigrationJob, Shard
+
+    L = SHAPE.n_layers if layers is None else layers
+    lens = np.full(BATCH, SEQ, dtype=np.int64)
+    ks = synth.block_aligned_split(lens, N_SHARDS)
+    handoff_blocks = N_HANDOFF * synth.ceil_div(SEQ, SHAPE.bs)
+    case = synth.device_shards(SHAPE, lens, ks, seed=seed, device=device,
+                               spare_blocks=handoff_blocks, layers=L)
+    pools = []
+    for pt, bt in zip(case.pools, case.block_tables):
+        pool = bs.KVPool(L, pt.shape[1], SHAPE.hkv, SHAPE.d, base=pt.reshape(-1))
+        # register the placement with the allocator: take everything, return the free ids
+        pool.alloc(pool.num_blocks)
+        used = set(int(x) for x in bt.ravel() if x >= 0)
+        pool.free(sorted(set(range(pool.num_blocks)) - used))
+        pools.append(pool)
+    D, P = pools
+    # hand-off requests: their KV sits in P's spare blocks; D allocates destinations
+    src_ids = P.alloc(handoff_blocks)
+    assert src_ids == handoff_src_ids(case, handoff_blocks)
+    dst_ids = D.alloc(handoff_blocks)
+    shards = [Shard(pool, torch.from_numpy(bt).to(device), j)
+              for j, (pool, bt) in enumerate(zip(pools, case.block_tables))]
+    job = MigrationJob(P, D, torch.tensor(src_ids, dtype=torch.int32, device=device),
+                       torch.tensor(dst_ids, dtype=torch.int32, device=device))
+    step = LayerwiseDecodeStep(shards, torch.from_numpy(ks).to(device), SHAPE.hq, L,
+                               synth.default_scale(SHAPE.d), migrations=[job], lookahead=1)
+    return case, pools, shards, job, step, ks
+
+
+def handoff_src_ids(case, n):
+    """The hand-off requests' blocks in the prefill pool P: its n lowest unused ids."""
+    bt = case.block_tables[1]
+    used = set(int(x) for x in bt.ravel() if x >= 0)
+    return [i for i in range(case.pools[1].shape[1]) if i not in used][:n]
+
+
+def attn_bytes_per_layer(ks):
+    """Algorithmic bytes of the attention launches of one layer:
+    per (request, shard): len*2*Hkv*d*2 (KV) + Hq*d*2 (q) + Hq*(d+2)*4 (partials)
+    + 4*ceil(len/16) (block table)."""
+    tot = 0
+    for j in range(ks.shape[1] - 1):
+        for n in (ks[:, j + 1] - ks[:, j]):
+            n = int(n)
+            tot += n * 2 * SHAPE.hkv * SHAPE.d * 2 + SHAPE.hq * SHAPE.d * 2 + \
+                SHAPE.hq * (SHAPE.d + 2) * 4 + 4 * synth.ceil_div(n, SHAPE.bs)
+    return tot
+
+
+def run_ours(args, rank, world, device):
+    import paper_2510_13223_b200 as bs
+
+    torch.cuda.set_device(device)
+    case, pools, shards, job, step, ks = build_workload(bs, device, seed=rank)
+    L = SHAPE.n_layers
+    q = case.q
+    out = torch.empty((L, BATCH, SHAPE.hq, SHAPE.d), dtype=torch.bfloat16, device=device)
+    lse = torch.empty((L, BATCH, SHAPE.hq), dtype=torch.float32, device=device)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        step.enqueue(q, out, lse)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, kernel events live on their launching streams --------
+    K = args.steps
+    timers = [[tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in range(L)]
+              for _ in range(K)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        t0.record()
+        for k in range(K):
+            step.enqueue(q, out, lse, timers=timers[k])
+        t1.record()
+        torch.cuda.synchronize()
+    barrier()
+    ms = t0.elapsed_time(t1) / K
+    attn_ms = [a.elapsed_time(b) for tk in timers for (a, b, _, _) in tk]
+    mig_ms = [c.elapsed_time(d) for tk in timers for (_, _, c, d) in tk]
+    ms_t = torch.tensor([ms], device=device)
+    if world > 1:
+        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+
+    # ---- e2e: same step through host buffers ----------------------------------------
+    q_host = q.cpu().pin_memory()
+    out_host = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+    lse_host = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
+    q_dev = torch.empty_like(q)
+    cur = torch.cuda.current_stream()
+    for _ in range(2):
+        q_dev.copy_(q_host, non_blocking=True)
+        step.enqueue(q_dev, out, lse)
+        out_host.copy_(out, non_blocking=True)
+        lse_host.copy_(lse, non_blocking=True)
+        cur.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(K):
+        q_dev.copy_(q_host, non_blocking=True)
+        step.enqueue(q_dev, out, lse)
+        out_host.copy_(out, non_blocking=True)
+        lse_host.copy_(lse, non_blocking=True)
+        cur.synchronize()  # the next decode step needs this step's result on the host
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1) / K], device=device)
+    if world > 1:
+        torch.distributed.all_reduce(e2e_ms, op=torch.distributed.ReduceOp.MAX)
+    e2e_ms = float(e2e_ms.item())
+
+    # ---- derived numbers ----------------------------------------------------------------
+    a_bytes = attn_bytes_per_layer(ks)
+    mig_bytes = job.src_ids.numel() * pools[0].chunk_bytes  # per layer, counted once
+    attn_avg_ms = statistics.fmean(attn_ms)
+    mig_avg_ms = statistics.fmean(mig_ms)
+    attn_gbs = a_bytes / (attn_avg_ms * 1e-3) / 1e9
+    mig_gbs = mig_bytes / (mig_avg_ms * 1e-3) / 1e9
+    peak, peak_src = peaks()
+    traffic, traffic_src = ncu_traffic()
+    tokens_s = BATCH * world / (ms_max * 1e-3)
+    res = {
+        "metric": METRIC,
+        "value": round(tokens_s, 2),
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": K,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_max, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (seeded N(0,1) bf16 KV/q, Llama-2-7B shape, random-init; no weights)",
+        "config": {
+            "workload": WORKLOAD,
+            "layers": L, "batch": BATCH, "seq_len": SEQ, "num_q_heads": SHAPE.hq,
+            "num_kv_heads": SHAPE.hkv, "head_dim": SHAPE.d, "kv_shards": N_SHARDS,
+            "handoff_requests_per_step": N_HANDOFF, "parallelism": f"replicas{world}" if world > 1 else "1 GPU, 2 virtual instances",
+            "l2": "no flush: resident pools 70 GiB >> 126 MB L2",
+        },
+        "attn_hbm_gbs": round(attn_gbs, 1),
+        "attn_ms_per_layer": round(attn_avg_ms, 5),
+        "migrate_gbs": round(mig_gbs, 1),
+        "migrate_ms_per_layer": round(mig_avg_ms, 5),
+        "migrate_bytes_per_layer": mig_bytes,
+        "migrate_transport": "local HBM copy (N=1: both instances on GPU 0; NVLink needs N>=2)",
+        "roofline": {
+            "bound": "hbm", "kernel": "split_decode_attn (2 shard launches per layer)",
+            "achieved": round(attn_gbs, 1), "peak": peak, "peak_source": peak_src,
+            "unit": "GB/s", "frac": round(attn_gbs / peak, 4),
+            "traffic": traffic, "traffic_source": traffic_src,
+            "algorithmic_bytes_per_layer": a_bytes,
+        },
+        "gpu_launches": step.launches_per_step * K,
+        "e2e": {"value": round(BATCH * world / (e2e_ms * 1e-3), 2), "unit": "tokens/s",
+                "ms_per_step": round(e2e_ms, 4),
+                "h2d_bytes_per_step": q.numel() * q.element_size(),
+                "d2h_bytes_per_step": out.numel() * out.element_size() + lse.numel() * lse.element_size()},
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline(case, budget_s=args.cpu_seconds)
+    return res
+
+
+# --------------------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline and --impl reference)
+# --------------------------------------------------------------------------------------
+
+def oracle_sample(case, req_ids, layer, handoff_chunks: int):
+    """Host copies for one oracle sample (inputs from the seeded generator, not kernels)."""
+    sp, sbt, sks, sq = synth.extract_requests(case, req_ids, layer)
+    P = case.pools[1]
+    ids = torch.tensor(handoff_src_ids(case, handoff_chunks), dtype=torch.long, device=P.device)
+    src = P[layer:layer + 1].index_select(1, ids).cpu().view(torch.int16).numpy().view(np.uint16)
+    return sp, sbt, sks, sq, np.ascontiguousarray(src)
+
+
+def time_oracle_sample(sample, scale):
+    import oracle
+    sp, sbt, sks, sq, src = sample
+    n_chunks = src.shape[1]
+    dst = np.empty_like(src)
+    t = time.perf_counter()
+    parts = [oracle.attention_shard(p, 0, sq, bt, sks, j, scale) for j, (p, bt) in enumerate(zip(sp, sbt))]
+    oracle.merge_partials([x[0] for x in parts], [x[1] for x in parts], [x[2] for x in parts])
+    ta = time.perf_counter() - t
+    t = time.perf_counter()
+    oracle.migrate_layer(src, dst, 0, np.arange(n_chunks), np.arange(n_chunks))
+    tm = time.perf_counter() - t
+    return ta, tm
+
+
+def cpu_baseline(case, budget_s=12.0, reqs_per_sample=8):
+    """Time the oracle (as it stands) on sampled (request, layer) units until ~budget_s of
+    CPU work, then extrapolate to the full step: T = L*(B/r * t_attn + H/h * t_mig)."""
+    import oracle
+    oracle.lib()
+    scale = synth.default_scale(SHAPE.d)
+    handoff_chunks = synth.ceil_div(SEQ, SHAPE.bs)  # one hand-off request's chunks
+    ta_tot = tm_tot = 0.0
+    layers = 0
+    t_start = time.perf_counter()
+    for layer in range(SHAPE.n_layers):
+        req = [(layer * reqs_per_sample + i) % BATCH for i in range(reqs_per_sample)]
+        s = oracle_sample(case, req, layer, handoff_chunks)
+        ta, tm = time_oracle_sample(s, scale)
+        ta_tot += ta
+        tm_tot += tm
+        layers += 1
+        if time.perf_counter() - t_start > budget_s:
+            break
+    t_attn = ta_tot / layers * (BATCH / reqs_per_sample)
+    t_mig = tm_tot / layers * N_HANDOFF
+    t_step = SHAPE.n_layers * (t_attn + t_mig)
+    return {"value": round(BATCH / t_step, 4), "unit": "tokens/s", "kind": "oracle",
+            "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count())),
+            "sample": (f"{layers} layers x {reqs_per_sample} requests (both shards + merge) + "
+                       f"1 hand-off request's chunks per layer, fp64 C oracle; extrapolated "
+                       f"linearly to B={BATCH}, {N_HANDOFF} hand-offs, {SHAPE.n_layers} layers"),
+            "measured_seconds": round(ta_tot + tm_tot, 3)}
+
+
+def run_reference(args, rank, world, device):
+    """--impl reference: the CPU oracle as the reference arm, per step a bounded sample."""
+    import oracle
+
+    oracle.lib()
+    # the same seeded workload, laid out by synth (torch RNG) only -- no product code
+    gen_dev = device if torch.cuda.is_available() else torch.device("cpu")
+    nl = 2 if torch.cuda.is_available() else 1
+    lens = np.full(BATCH, SEQ, dtype=np.int64)
+    ks = synth.block_aligned_split(lens, N_SHARDS)
+    handoff_chunks = synth.ceil_div(SEQ, SHAPE.bs)
+    case = synth.device_shards(SHAPE, lens, ks, seed=0, device=gen_dev,
+                               spare_blocks=N_HANDOFF * handoff_chunks, layers=nl)
+    scale = synth.default_scale(SHAPE.d)
+    reqs = 2
+    samples = [oracle_sample(case, [(2 * i) % BATCH, (2 * i + 1) % BATCH], i % nl,
+                             handoff_chunks) for i in range(2)]
+    for i in range(args.warmup):
+        time_oracle_sample(samples[i % 2], scale)
+    ta = tm = 0.0
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        a, m = time_oracle_sample(samples[i % 2], scale)
+        ta += a
+        tm += m
+    wall = time.perf_counter() - t0
+    t_step = SHAPE.n_layers * (ta / args.steps * BATCH / reqs + tm / args.steps * N_HANDOFF)
+    v = BATCH / t_step
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
+    sample = (f"per step: 1 layer x {reqs} requests (both shards + merge) + 1 hand-off request's "
+              f"chunks, fp64 C oracle; extrapolated to B={BATCH}, {N_HANDOFF} hand-offs, "
+              f"{SHAPE.n_layers} layers")
+    return {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(t_step * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "parallelism": "CPU oracle"},
+            "cpu_baseline": {"value": round(v, 4), "unit": "tokens/s", "kind": "oracle",
+                             "cores": cores, "sample": sample},
+            "e2e": {"value": round(v, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "measured_seconds": round(wall, 3)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warning: --warmup < 3 violates the timing rules; using 3")
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    device = torch.device("cuda", local)
+    if args.impl == "reference":  # rank 0 alone runs it; other ranks exit without work
+        if rank == 0:
+            print(json.dumps(run_reference(args, rank, world, device)), flush=True)
+        return
+    if world > 1:
+        torch.cuda.set_device(device)
+        torch.distributed.init_process_group("nccl", device_id=device)
+    try:
+        res = run_ours(args, rank, world, device)
+        if rank == 0:
+            print(json.dumps(res), flush=True)
+    finally:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

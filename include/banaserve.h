@@ -1,0 +1,169 @@
+/*
+ * banaserve.h -- C-ABI of the B200-native (sm_100a) hot path of BanaServe
+ * (arXiv 2510.13223): attention-level KV-cache migration + split decode attention
+ * + exact log-sum-exp merge.  Citations are to /root/reference/PAPER.md lines
+ * ("PAPER.md:<line>", section, equation); readings R-Ax are listed in DESIGN.md.
+ *
+ * Conventions (apply to every entry point):
+ *  - All functions are extern "C", never throw, and return bs_status.  On a non-OK
+ *    status nothing has been enqueued and bs_last_error() (thread-local) describes it.
+ *  - Device work is enqueued asynchronously on the caller's stream (`stream` is a
+ *    cudaStream_t passed as void*; NULL = legacy default stream).  No call synchronises
+ *    the device, allocates device memory, or copies host<->device on the hot path.
+ *  - The caller owns every device buffer and stream (PyTorch provides them).  A pool
+ *    handle owns only host metadata (geometry + the block allocator); it never frees
+ *    the device memory it describes.
+ *  - Host-visible arguments are validated (NULLs, ranges, alignment, supported shapes).
+ *    Device arrays (block tables, ids, splits) are NOT validated: out-of-range ids are
+ *    undefined behaviour, as for any CUDA kernel argument.
+ *  - Supported shapes: bf16 KV, block_size 16, head_dim 64 or 128, query group
+ *    G = num_q_heads / num_kv_heads in {1, 2, 4, 8}.  Others -> BS_ERR_UNSUPPORTED.
+ */
+#ifndef BANASERVE_H_
+#define BANASERVE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BS_ABI_VERSION 1
+
+typedef enum {
+  BS_OK = 0,
+  BS_ERR_INVALID_ARG = 1,
+  BS_ERR_OUT_OF_BLOCKS = 2,
+  BS_ERR_UNSUPPORTED = 3,
+  BS_ERR_CUDA = 4,
+  BS_ERR_NCCL = 5
+} bs_status;
+
+enum { BS_DTYPE_BF16 = 0 };
+
+/* Thread-local text for the most recent non-OK status on this thread. */
+const char* bs_last_error(void);
+/* BS_ABI_VERSION of the loaded library. */
+int32_t bs_abi_version(void);
+
+/* ------------------------------------------------------------------------------ */
+/* H0: paged KV pool + block allocator.                                             */
+/* vLLM-style paged KV ("PagedAttention ... block-level KV Cache"),   */
+/* memory reallocation cost T_mem_realloc of eq. 28.              */
+/*                                                                                  */
+/* Device layout (reading D4), bf16, row-major:                                     */
+/*   pool[layer][block][kv: 0=K,1=V][kv_head][slot: 0..15][dim: 0..head_dim-1]      */
+/* so one (layer, block) "chunk" = 2*Hkv*16*head_dim*2 bytes is contiguous, and one */
+/* (layer, block, K|V, kv_head) "page" = 16*head_dim*2 bytes (4 KiB at d=128) too.  */
+/* Block ids are shared by all layers.                                              */
+/* ------------------------------------------------------------------------------ */
+typedef struct {
+  int32_t num_layers;    /* L >= 1                                   */
+  int32_t num_blocks;    /* physical blocks per layer, >= 1           */
+  int32_t block_size;    /* tokens per block; must be 16              */
+  int32_t num_kv_heads;  /* Hkv >= 1                                  */
+  int32_t head_dim;      /* 64 or 128                                 */
+  int32_t dtype;         /* BS_DTYPE_BF16                             */
+  int32_t device;        /* CUDA ordinal that owns the memory         */
+} bs_kv_pool_desc;
+
+typedef struct bs_kv_pool bs_kv_pool; /* opaque host handle */
+
+/* Bytes of device memory a pool with this geometry needs (L*num_blocks*chunk). 0 on bad desc. */
+size_t bs_kv_pool_bytes(const bs_kv_pool_desc* desc);
+/* Bytes of one (layer, block) chunk: 2*Hkv*block_size*head_dim*2. 0 on bad desc. */
+size_t bs_kv_chunk_bytes(const bs_kv_pool_desc* desc);
+
+/* Describe caller-owned device memory `base` (>= bs_kv_pool_bytes, 256-B aligned) as a
+ * pool.  All blocks start free.  `base` may be a peer-mapped pointer to another GPU's
+ * pool (a "remote view"): migrate calls then write over NVLink (P2P push). */
+bs_status bs_kv_pool_create(const bs_kv_pool_desc* desc, void* base, bs_kv_pool** out);
+/* Free the host handle (never the device memory). NULL is a no-op. */
+bs_status bs_kv_pool_destroy(bs_kv_pool* pool);
+/* Allocate n block ids into out_ids (host array): lowest free ids first, ascending;
+ * all-or-nothing -> BS_ERR_OUT_OF_BLOCKS with no state change (reading R-A12). */
+bs_status bs_kv_pool_alloc(bs_kv_pool* pool, int32_t n, int32_t* out_ids);
+/* Return n ids (host array).  Any id out of range, not allocated, or repeated ->
+ * BS_ERR_INVALID_ARG with no state change. */
+bs_status bs_kv_pool_free(bs_kv_pool* pool, int32_t n, const int32_t* ids);
+/* Number of free blocks (or -1 for NULL). */
+int32_t bs_kv_pool_num_free(const bs_kv_pool* pool);
+
+/* ------------------------------------------------------------------------------ */
+/* H2: one layer of block migration -- gather from the source pool, send, scatter   */
+/* into the destination pool (attention-level migration PAPER.md:207-214, :239-244, */
+/* eq. 11; "without semantic change", eq. 5).                      */
+/*   for i < n: dst.chunk(layer, dst_ids[i]) <- src.chunk(layer, src_ids[i])       */
+/* Whole chunks (K and V, all heads, all 16 slots, pad slots included), bit-exact.  */
+/* src_ids / dst_ids: DEVICE int32 arrays [n] readable on the current device; dst   */
+/* ids must be distinct (caller contract).  src and dst must have equal             */
+/* num_kv_heads / head_dim / block_size / num_layers.  Same device, or dst a remote */
+/* view (peer-mapped), or src a remote view (P2P pull).  n == 0 is a no-op.          */
+/* method: BS_MIGRATE_AUTO picks the fastest; VEC16 = 16-byte vector LDG/STG copy;  */
+/* BULK = TMA bulk copies (cp.async.bulk) global->smem->global.                      */
+/* ------------------------------------------------------------------------------ */
+enum { BS_MIGRATE_AUTO = 0, BS_MIGRATE_VEC16 = 1, BS_MIGRATE_BULK = 2 };
+
+bs_status bs_kv_migrate_layer(const bs_kv_pool* src, bs_kv_pool* dst, int32_t layer,
+                              const int32_t* src_ids, const int32_t* dst_ids, int32_t n,
+                              void* stream);
+bs_status bs_kv_migrate_layer_ex(const bs_kv_pool* src, bs_kv_pool* dst, int32_t layer,
+                                 const int32_t* src_ids, const int32_t* dst_ids, int32_t n,
+                                 int32_t method, void* stream);
+
+/* Two-sided transport halves (pack / unpack), for a send/recv transport (NCCL) that
+ * moves one contiguous staging buffer per layer: staging[i] = chunk(layer, ids[i]).
+ * staging: DEVICE buffer of n * bs_kv_chunk_bytes bytes, 16-B aligned. */
+bs_status bs_kv_gather_layer(const bs_kv_pool* src, int32_t layer, const int32_t* ids, int32_t n,
+                             void* staging, void* stream);
+bs_status bs_kv_scatter_layer(bs_kv_pool* dst, int32_t layer, const int32_t* ids, int32_t n,
+                              const void* staging, void* stream);
+
+/* ------------------------------------------------------------------------------ */
+/* H4: decode attention over this instance's shard `shard_id` of every request's KV  */
+/* (split attention, eqs. 6-9, corrected per readings R-A1..R-A11): */
+/*   shard j of request b = global tokens [kv_split[b][j], kv_split[b][j+1]), stored */
+/*   in shard-local order: local token u at block block_tables[b][u/16], slot u%16.  */
+/*   q-head h attends kv-head floor(h / G).                                          */
+/*   s_u = scale * <q_bh, k_u>;  m = max_u s_u;  l = sum_u exp(s_u - m);             */
+/*   o~  = sum_u exp(s_u - m) v_u / l                (fp32, natural-log units)      */
+/*   empty shard: m = -inf, l = 0, o~ = 0.                                            */
+/* q            DEVICE bf16 [batch][num_q_heads][head_dim]                            */
+/* block_tables DEVICE int32 [batch][max_blocks] physical ids in `pool`               */
+/* kv_split     DEVICE int32 [batch][n_shards+1], non-decreasing                      */
+/* o_part       DEVICE fp32 [batch][num_q_heads][head_dim]                            */
+/* m, l         DEVICE fp32 [batch][num_q_heads]                                      */
+/* workspace    DEVICE scratch for the intra-GPU split-K (bytes from                  */
+/*              bs_split_decode_attention_workspace_size, 0 allowed if it says 0).    */
+/*              Must be zero-filled once before first use; every call leaves it       */
+/*              zero-filled again.  Not shareable between concurrently running calls. */
+/* max_blocks must be >= ceil(len of the longest shard / 16).                          */
+/* ------------------------------------------------------------------------------ */
+bs_status bs_split_decode_attention_workspace_size(const bs_kv_pool* pool, int32_t batch,
+                                                   int32_t num_q_heads, int32_t max_blocks,
+                                                   size_t* bytes);
+bs_status bs_split_decode_attention(const bs_kv_pool* pool, int32_t layer, const void* q,
+                                    int32_t batch, int32_t num_q_heads,
+                                    const int32_t* block_tables, int32_t max_blocks,
+                                    const int32_t* kv_split, int32_t n_shards, int32_t shard_id,
+                                    float scale, float* o_part, float* m, float* l,
+                                    void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------ */
+/* H6: exact LSE merge of n shard partials (eq. 10, R-A4, R-A14):   */
+/*   lse_j = m_j + ln l_j (-inf if l_j = 0);  lse = logsumexp_j lse_j;                */
+/*   out = sum_j exp(lse_j - lse) o~_j, fixed order j = 0..n-1; all empty -> 0, -inf. */
+/* o_parts/m_parts/l_parts: HOST arrays of n DEVICE pointers (layouts as in H4).      */
+/* out: DEVICE bf16 [batch][num_q_heads][head_dim] (round-to-nearest-even).           */
+/* lse_out: DEVICE fp32 [batch][num_q_heads] or NULL.  1 <= n_parts <= 16.             */
+/* ------------------------------------------------------------------------------ */
+bs_status bs_merge_partials(int32_t n_parts, const float* const* o_parts,
+                            const float* const* m_parts, const float* const* l_parts,
+                            int32_t batch, int32_t num_q_heads, int32_t head_dim, void* out,
+                            float* lse_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BANASERVE_H_ */

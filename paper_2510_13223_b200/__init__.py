@@ -1,0 +1,237 @@
+"""B200-native (sm_100a) hot path of BanaServe (arXiv 2510.13223).
+
+Thin ctypes binding over the C-ABI in ``include/banaserve.h`` (``libbanaserve.so``):
+argument marshalling only -- every step of the path runs in the library's CUDA kernels.
+PyTorch is used for device memory and streams.  There is no CPU fallback: importing
+this package without the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+from . import build as _build
+
+__all__ = [
+    "BSError", "lib", "KVPool", "kv_migrate_layer", "kv_gather_layer", "kv_scatter_layer",
+    "split_decode_attention", "split_decode_attention_workspace_size", "merge_partials",
+    "MIGRATE_AUTO", "MIGRATE_VEC16", "MIGRATE_BULK", "EXPORTED_SYMBOLS",
+]
+
+MIGRATE_AUTO, MIGRATE_VEC16, MIGRATE_BULK = 0, 1, 2
+BS_OK, BS_ERR_INVALID_ARG, BS_ERR_OUT_OF_BLOCKS, BS_ERR_UNSUPPORTED, BS_ERR_CUDA, BS_ERR_NCCL = range(6)
+
+# every entry point include/banaserve.h declares
+EXPORTED_SYMBOLS = (
+    "bs_last_error", "bs_abi_version", "bs_kv_pool_bytes", "bs_kv_chunk_bytes",
+    "bs_kv_pool_create", "bs_kv_pool_destroy", "bs_kv_pool_alloc", "bs_kv_pool_free",
+    "bs_kv_pool_num_free", "bs_kv_migrate_layer", "bs_kv_migrate_layer_ex",
+    "bs_kv_gather_layer", "bs_kv_scatter_layer", "bs_split_decode_attention_workspace_size",
+    "bs_split_decode_attention", "bs_merge_partials",
+)
+
+
+class BSError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[bs_status {status}] {msg}")
+        self.status = status
+
+
+class _Desc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in
+                ("num_layers", "num_blocks", "block_size", "num_kv_heads", "head_dim", "dtype",
+                 "device")]
+
+
+_i32, _p, _sz, _f32 = ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_float
+_lib = None
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def lib():
+    """Load libbanaserve.so (building it if the sources are newer and nvcc exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = _build.LIB
+    try:
+        path = _build.build()
+    except Exception as e:  # no nvcc on this machine: use the shipped .so if present
+        if not os.path.exists(path):
+            raise ImportError(f"libbanaserve.so missing and cannot be built: {e}") from e
+    L = ctypes.CDLL(path)
+    sig = {
+        "bs_last_error": ([], ctypes.c_char_p),
+        "bs_abi_version": ([], _i32),
+        "bs_kv_pool_bytes": ([ctypes.POINTER(_Desc)], _sz),
+        "bs_kv_chunk_bytes": ([ctypes.POINTER(_Desc)], _sz),
+        "bs_kv_pool_create": ([ctypes.POINTER(_Desc), _p, ctypes.POINTER(_p)], _i32),
+        "bs_kv_pool_destroy": ([_p], _i32),
+        "bs_kv_pool_alloc": ([_p, _i32, _p], _i32),
+        "bs_kv_pool_free": ([_p, _i32, _p], _i32),
+        "bs_kv_pool_num_free": ([_p], _i32),
+        "bs_kv_migrate_layer": ([_p, _p, _i32, _p, _p, _i32, _p], _i32),
+        "bs_kv_migrate_layer_ex": ([_p, _p, _i32, _p, _p, _i32, _i32, _p], _i32),
+        "bs_kv_gather_layer": ([_p, _i32, _p, _i32, _p, _p], _i32),
+        "bs_kv_scatter_layer": ([_p, _i32, _p, _i32, _p, _p], _i32),
+        "bs_split_decode_attention_workspace_size": ([_p, _i32, _i32, _i32, ctypes.POINTER(_sz)], _i32),
+        "bs_split_decode_attention": ([_p, _i32, _p, _i32, _i32, _p, _i32, _p, _i32, _i32, _f32,
+                                       _p, _p, _p, _p, _sz, _p], _i32),
+        "bs_merge_partials": ([_i32, _p, _p, _p, _i32, _i32, _i32, _p, _p, _p], _i32),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def _check(status: int) -> None:
+    if status != BS_OK:
+        raise BSError(status, lib().bs_last_error().decode())
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, torch.cuda.Stream):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def _dptr(t: torch.Tensor | None, dtype=None) -> int | None:
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"expected {dtype}, got {t.dtype}")
+    return t.data_ptr()
+
+
+class KVPool:
+    """A paged bf16 KV pool ``[L][num_blocks][2][Hkv][16][head_dim]`` on one GPU.
+
+    The device memory is a torch tensor (``self.data``); the C handle owns only the
+    geometry and the block allocator (lowest-free-first, all-or-nothing).
+    """
+
+    def __init__(self, num_layers: int, num_blocks: int, num_kv_heads: int, head_dim: int,
+                 device=None, base: torch.Tensor | None = None, block_size: int = 16):
+        device = torch.device(device if device is not None else "cuda")
+        if device.index is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.desc = _Desc(num_layers, num_blocks, block_size, num_kv_heads, head_dim, 0, device.index)
+        nbytes = lib().bs_kv_pool_bytes(ctypes.byref(self.desc))
+        if nbytes == 0:
+            raise BSError(BS_ERR_UNSUPPORTED, "unsupported pool geometry")
+        if base is None:
+            base = torch.empty(nbytes // 2, dtype=torch.bfloat16, device=device)
+        if base.numel() * base.element_size() < nbytes:
+            raise ValueError("base tensor too small")
+        self.base = base
+        self.data = base.view(torch.bfloat16).reshape(-1)[: nbytes // 2].view(
+            num_layers, num_blocks, 2, num_kv_heads, block_size, head_dim)
+        h = _p()
+        _check(lib().bs_kv_pool_create(ctypes.byref(self.desc), _dptr(base), ctypes.byref(h)))
+        self.handle = h
+        self.num_layers, self.num_blocks = num_layers, num_blocks
+        self.num_kv_heads, self.head_dim, self.block_size = num_kv_heads, head_dim, block_size
+        self.device = device
+        self.nbytes = nbytes
+        self.chunk_bytes = lib().bs_kv_chunk_bytes(ctypes.byref(self.desc))
+
+    def alloc(self, n: int) -> list:
+        buf = (ctypes.c_int32 * max(n, 1))()
+        _check(lib().bs_kv_pool_alloc(self.handle, n, buf))
+        return list(buf[:n])
+
+    def free(self, ids) -> None:
+        ids = [int(x) for x in ids]
+        buf = (ctypes.c_int32 * max(len(ids), 1))(*ids)
+        _check(lib().bs_kv_pool_free(self.handle, len(ids), buf))
+
+    @property
+    def num_free(self) -> int:
+        return lib().bs_kv_pool_num_free(self.handle)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            lib().bs_kv_pool_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def kv_migrate_layer(src: KVPool, dst: KVPool, layer: int, src_ids: torch.Tensor,
+                     dst_ids: torch.Tensor, method: int = MIGRATE_AUTO, stream=None) -> None:
+    """H2: dst.chunk(layer, dst_ids[i]) <- src.chunk(layer, src_ids[i]) (device int32 ids)."""
+    n = src_ids.numel()
+    if dst_ids.numel() != n:
+        raise ValueError("src_ids / dst_ids length mismatch")
+    _check(lib().bs_kv_migrate_layer_ex(src.handle, dst.handle, layer,
+                                        _dptr(src_ids, torch.int32), _dptr(dst_ids, torch.int32),
+                                        n, method, _stream(stream)))
+
+
+def kv_gather_layer(src: KVPool, layer: int, ids: torch.Tensor, staging: torch.Tensor,
+                    stream=None) -> None:
+    _check(lib().bs_kv_gather_layer(src.handle, layer, _dptr(ids, torch.int32), ids.numel(),
+                                    _dptr(staging), _stream(stream)))
+
+
+def kv_scatter_layer(dst: KVPool, layer: int, ids: torch.Tensor, staging: torch.Tensor,
+                     stream=None) -> None:
+    _check(lib().bs_kv_scatter_layer(dst.handle, layer, _dptr(ids, torch.int32), ids.numel(),
+                                     _dptr(staging), _stream(stream)))
+
+
+def split_decode_attention_workspace_size(pool: KVPool, batch: int, num_q_heads: int,
+                                          max_blocks: int) -> int:
+    out = _sz()
+    _check(lib().bs_split_decode_attention_workspace_size(pool.handle, batch, num_q_heads,
+                                                          max_blocks, ctypes.byref(out)))
+    return out.value
+
+
+def split_decode_attention(pool: KVPool, layer: int, q: torch.Tensor, block_tables: torch.Tensor,
+                           kv_split: torch.Tensor, shard_id: int, scale: float, o: torch.Tensor,
+                           m: torch.Tensor, l: torch.Tensor, workspace: torch.Tensor | None = None,
+                           stream=None) -> None:
+    """H4: partial (o~, m, l) of shard ``shard_id`` for every request.
+
+    q bf16 [B,Hq,d]; block_tables int32 [B,max_blocks]; kv_split int32 [B,n+1];
+    o fp32 [B,Hq,d]; m, l fp32 [B,Hq]; workspace zero-filled once (see header)."""
+    B, hq, d = q.shape
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check(lib().bs_split_decode_attention(
+        pool.handle, layer, _dptr(q, torch.bfloat16), B, hq, _dptr(block_tables, torch.int32),
+        block_tables.shape[1], _dptr(kv_split, torch.int32), kv_split.shape[1] - 1, shard_id,
+        float(scale), _dptr(o, torch.float32), _dptr(m, torch.float32), _dptr(l, torch.float32),
+        _dptr(workspace), ws_bytes, _stream(stream)))
+
+
+def merge_partials(o_parts, m_parts, l_parts, out: torch.Tensor, lse: torch.Tensor | None = None,
+                   stream=None) -> None:
+    """H6: exact LSE merge of n partials into bf16 ``out`` [B,Hq,d] (+ fp32 lse [B,Hq])."""
+    n = len(o_parts)
+    B, hq, d = out.shape
+    arr = ctypes.c_void_p * n
+    o_arr = arr(*[_dptr(t, torch.float32) for t in o_parts])
+    m_arr = arr(*[_dptr(t, torch.float32) for t in m_parts])
+    l_arr = arr(*[_dptr(t, torch.float32) for t in l_parts])
+    _check(lib().bs_merge_partials(n, o_arr, m_arr, l_arr, B, hq, d, _dptr(out, torch.bfloat16),
+                                   _dptr(lse, torch.float32) if lse is not None else None,
+                                   _stream(stream)))

@@ -1,0 +1,523 @@
+// H4: paged GQA split decode attention over one KV shard (split attention of
+// PAPER.md:216-231, eqs. 6-9, with readings R-A1..R-A11: token-range split, explicit
+// scale, max-shifted exponentials, shard-local block tables, masked pad slots).
+//
+// Output per (request b, q-head h): the partial triple (o~ normalised by the local
+// denominator, m, l) in fp32, natural-log units -- exactly what bs_merge_partials
+// (eq. 10) consumes.
+//
+// Design (DESIGN.md §Kernels / attention):
+//  * HBM-bound (0.5*G FMA per KV byte): CUDA cores, no tensor cores.
+//  * grid = (nsplit, Hkv, B); a CTA owns one (request, kv-head, block range) and serves
+//    all G query heads of the group, so every K/V page is read from HBM exactly once.
+//  * 4 warps per CTA, each an independent pipeline over every 4th block of the range:
+//    lane 0 streams the block's K page and V page (16 x d bf16 each, contiguous in the
+//    pool) into a STAGES-deep shared-memory ring with TMA bulk copies (cp.async.bulk +
+//    mbarrier complete_tx); block ids come from a shared-memory copy of the block table.
+//  * lane l owns head dims [l*d/32, (l+1)*d/32): q*k partials for all 16 tokens are
+//    reduced with a 16-shuffle reduce-scatter (lane pair 2t,2t+1 ends with token t),
+//    online softmax in log2 units (q pre-scaled by scale*log2e, ex2), p broadcast via
+//    shared memory, p*V accumulated with packed FFMA2.
+//  * the 4 warp states are merged in shared memory; with intra-GPU split-K (nsplit > 1)
+//    each CTA writes a partial to the workspace and the last-arriving CTA of the
+//    (request, kv-head) merges all partials in fixed order (deterministic), resets the
+//    arrival counter, and writes the shard output.  One launch either way.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace bs {
+namespace {
+
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kWarps = 4;
+constexpr int kBtMax = 512;     // blocks per CTA range (bt cached in smem)
+constexpr int kMaxSplit = 64;   // intra-GPU split-K limit
+
+struct AttnParams {
+  const uint8_t* kv;  // pool base + layer * layer_bytes
+  int64_t chunk_bytes;
+  int64_t v_off;      // Hkv * page bytes: K page -> V page of the same head
+  const __nv_bfloat16* q;
+  const int32_t* bt;
+  int32_t max_blocks;
+  const int32_t* kv_split;
+  int32_t n_shards, shard_id;
+  float scale_log2;
+  int32_t hq, hkv;
+  int32_t nsplit, bps;
+  float* o;
+  float* m;
+  float* l;
+  float* ws_o;
+  float* ws_ml;
+  int32_t* ws_cnt;
+};
+
+template <int D, int G, int STAGES>
+struct Smem {
+  static constexpr int kPage = 16 * D * 2;
+  static constexpr int kStage = 2 * kPage;
+  static constexpr int kRing = kWarps * STAGES * kStage;
+  static constexpr int kBtOff = kRing;
+  static constexpr int kPOff = kBtOff + kBtMax * 4;
+  static constexpr int kBarOff = kPOff + kWarps * G * 16 * 4;
+  static constexpr int kMlOff = kBarOff + kWarps * STAGES * 8;
+  static constexpr int kWOff = kMlOff + kWarps * G * 2 * 4;
+  static constexpr int kFlagOff = kWOff + G * kMaxSplit * 4;
+  static constexpr int kTotal = kFlagOff + 16;
+  static_assert(kWarps * G * D * 4 <= kRing, "combine buffer must fit in the ring");
+};
+
+__device__ __forceinline__ float2 bf2_to_f2(uint32_t w) {
+  return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+}
+
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  return __ffma2_rn(a, b, c);
+}
+
+// Sum 16 per-lane partials over the 32 lanes; lane pair (2t, 2t+1) returns token t's total.
+__device__ __forceinline__ float reduce_scatter16(float (&v)[16], int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float send = b4 ? v[i] : v[i + 8];
+    const float keep = b4 ? v[i + 8] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = b3 ? v[i] : v[i + 4];
+    const float keep = b3 ? v[i + 4] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = b2 ? v[i] : v[i + 2];
+    const float keep = b2 ? v[i + 2] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  {
+    const float send = b1 ? v[0] : v[1];
+    const float keep = b1 ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+
+template <int D, int G, int STAGES>
+__global__ void __launch_bounds__(kWarps * 32, 2) split_decode_attn(const AttnParams p) {
+  using S = Smem<D, G, STAGES>;
+  constexpr int DPL = D / 32;  // head dims per lane (4 or 2)
+  constexpr int DP2 = DPL / 2;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int sp = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
+
+  const int32_t* ks = p.kv_split + (int64_t)b * (p.n_shards + 1) + p.shard_id;
+  const int32_t len = max(__ldg(ks + 1) - __ldg(ks), 0);
+  const int32_t nblk = (len + 15) >> 4;
+  const int32_t blo = sp * p.bps;
+  const int32_t nb_cta = max(min(nblk, blo + p.bps) - blo, 0);
+
+  int32_t* s_bt = reinterpret_cast<int32_t*>(smem + S::kBtOff);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBarOff) + warp * STAGES;
+  float* s_p = reinterpret_cast<float*>(smem + S::kPOff) + warp * G * 16;
+  uint8_t* ring = smem + warp * STAGES * S::kStage;
+
+  for (int i = threadIdx.x; i < nb_cta; i += blockDim.x)
+    s_bt[i] = __ldg(p.bt + (int64_t)b * p.max_blocks + blo + i);
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&bars[s], 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+
+  const int nmine = nb_cta > warp ? (nb_cta - warp + kWarps - 1) / kWarps : 0;
+  const uint8_t* kv_head = p.kv + (int64_t)g * S::kPage;
+  uint64_t policy = 0;
+  if (lane == 0) policy = ptx::policy_evict_first();
+  auto issue = [&](int k) {
+    const int s = k % STAGES;
+    const int64_t phys = s_bt[warp + k * kWarps];
+    const uint8_t* kp = kv_head + phys * p.chunk_bytes;
+    uint8_t* dst = ring + s * S::kStage;
+    ptx::mbar_expect_tx(&bars[s], 2 * S::kPage);
+    ptx::bulk_g2s_evict_first(dst, kp, S::kPage, &bars[s], policy);
+    ptx::bulk_g2s_evict_first(dst + S::kPage, kp + p.v_off, S::kPage, &bars[s], policy);
+  };
+  if (lane == 0) {
+    for (int k = 0; k < min(STAGES, nmine); ++k) issue(k);
+  }
+
+  // q for the G heads of this group, this lane's dims, pre-scaled into log2 units
+  float2 qv[G][DP2];
+  {
+    const __nv_bfloat16* qp = p.q + ((int64_t)b * p.hq + g * G) * D + lane * DPL;
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      if constexpr (DPL == 4) {
+        const uint2 w = *reinterpret_cast<const uint2*>(qp + h * D);
+        float2 a = bf2_to_f2(w.x), c = bf2_to_f2(w.y);
+        qv[h][0] = make_float2(a.x * p.scale_log2, a.y * p.scale_log2);
+        qv[h][1] = make_float2(c.x * p.scale_log2, c.y * p.scale_log2);
+      } else {
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(qp + h * D);
+        float2 a = bf2_to_f2(w);
+        qv[h][0] = make_float2(a.x * p.scale_log2, a.y * p.scale_log2);
+      }
+    }
+  }
+
+  float m_run[G], l_run[G];
+  float2 acc[G][DP2];
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    m_run[h] = -INFINITY;
+    l_run[h] = 0.f;
+#pragma unroll
+    for (int e = 0; e < DP2; ++e) acc[h][e] = make_float2(0.f, 0.f);
+  }
+
+  for (int k = 0; k < nmine; ++k) {
+    const int s = k % STAGES;
+    ptx::mbar_wait(&bars[s], (uint32_t)((k / STAGES) & 1));
+    const uint8_t* sk = ring + s * S::kStage;
+    const uint8_t* sv = sk + S::kPage;
+    const int blk = blo + warp + k * kWarps;  // block index within the shard
+    const int nvalid = min(16, len - blk * 16);
+
+    // ---- scores: s_t = <q_h, k_t> (log2 units) -------------------------------------
+    float2 kf[16][DP2];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      if constexpr (DPL == 4) {
+        const uint2 w = *reinterpret_cast<const uint2*>(sk + t * D * 2 + lane * 8);
+        kf[t][0] = bf2_to_f2(w.x);
+        kf[t][1] = bf2_to_f2(w.y);
+      } else {
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(sk + t * D * 2 + lane * 4);
+        kf[t][0] = bf2_to_f2(w);
+      }
+    }
+    const bool valid = (lane >> 1) < nvalid;
+    float alpha[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      float v[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        float2 a = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int e = 0; e < DP2; ++e) a = ffma2(qv[h][e], kf[t][e], a);
+        v[t] = a.x + a.y;
+      }
+      float sc = reduce_scatter16(v, lane);
+      sc = valid ? sc : -INFINITY;
+      float mb = sc;
+      mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 2));
+      mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 4));
+      mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 8));
+      mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 16));
+      const float mn = fmaxf(m_run[h], mb);  // finite: slot 0 of every block is valid
+      alpha[h] = exp2f(m_run[h] - mn);
+      const float pr = exp2f(sc - mn);
+      l_run[h] = l_run[h] * alpha[h] + ((lane & 1) ? 0.f : pr);
+      m_run[h] = mn;
+      if (!(lane & 1)) s_p[h * 16 + (lane >> 1)] = pr;
+    }
+    __syncwarp();
+
+    // ---- o = alpha * o + sum_t p_t v_t ----------------------------------------------
+#pragma unroll
+    for (int h = 0; h < G; ++h)
+#pragma unroll
+      for (int e = 0; e < DP2; ++e) acc[h][e] = make_float2(acc[h][e].x * alpha[h], acc[h][e].y * alpha[h]);
+#pragma unroll
+    for (int t4 = 0; t4 < 16; t4 += 4) {
+      float4 pp[G];
+#pragma unroll
+      for (int h = 0; h < G; ++h) pp[h] = *reinterpret_cast<const float4*>(s_p + h * 16 + t4);
+#pragma unroll
+      for (int tt = 0; tt < 4; ++tt) {
+        const int t = t4 + tt;
+        if (t < nvalid) {  // pad slots hold garbage (NaN-poisoned in tests): skip, don't scale
+          float2 vf[DP2];
+          if constexpr (DPL == 4) {
+            const uint2 w = *reinterpret_cast<const uint2*>(sv + t * D * 2 + lane * 8);
+            vf[0] = bf2_to_f2(w.x);
+            vf[1] = bf2_to_f2(w.y);
+          } else {
+            const uint32_t w = *reinterpret_cast<const uint32_t*>(sv + t * D * 2 + lane * 4);
+            vf[0] = bf2_to_f2(w);
+          }
+#pragma unroll
+          for (int h = 0; h < G; ++h) {
+            const float pt = tt == 0 ? pp[h].x : tt == 1 ? pp[h].y : tt == 2 ? pp[h].z : pp[h].w;
+            const float2 p2 = make_float2(pt, pt);
+#pragma unroll
+            for (int e = 0; e < DP2; ++e) acc[h][e] = ffma2(p2, vf[e], acc[h][e]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && k + STAGES < nmine) {
+      ptx::fence_proxy_async_smem();
+      issue(k + STAGES);
+    }
+  }
+
+  // ---- merge the 4 warp states in shared memory ------------------------------------
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    float x = l_run[h];
+    x += __shfl_xor_sync(0xffffffffu, x, 1);
+    x += __shfl_xor_sync(0xffffffffu, x, 2);
+    x += __shfl_xor_sync(0xffffffffu, x, 4);
+    x += __shfl_xor_sync(0xffffffffu, x, 8);
+    x += __shfl_xor_sync(0xffffffffu, x, 16);
+    l_run[h] = x;
+  }
+  __syncthreads();  // every warp finished with its ring; reuse it for the combine
+  float* s_acc = reinterpret_cast<float*>(smem);  // [kWarps][G][D]
+  float* s_ml = reinterpret_cast<float*>(smem + S::kMlOff);
+  float* s_w = reinterpret_cast<float*>(smem + S::kWOff);
+  int* s_flag = reinterpret_cast<int*>(smem + S::kFlagOff);
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+#pragma unroll
+    for (int e = 0; e < DP2; ++e)
+      *reinterpret_cast<float2*>(s_acc + (warp * G + h) * D + lane * DPL + 2 * e) = acc[h][e];
+    if (lane == 0) {
+      s_ml[(warp * G + h) * 2] = m_run[h];
+      s_ml[(warp * G + h) * 2 + 1] = l_run[h];
+    }
+  }
+  __syncthreads();
+
+  for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
+    const int h = idx / D, x = idx - h * D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) M = fmaxf(M, s_ml[(w * G + h) * 2]);
+    float L = 0.f, O = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const float mw = s_ml[(w * G + h) * 2];
+      if (mw != -INFINITY) {
+        const float f = exp2f(mw - M);
+        L += s_ml[(w * G + h) * 2 + 1] * f;
+        O += s_acc[(w * G + h) * D + x] * f;
+      }
+    }
+    const int64_t row = (int64_t)b * p.hq + g * G + h;
+    const bool any = L > 0.f;
+    if (p.nsplit == 1) {
+      p.o[row * D + x] = any ? O / L : 0.f;
+      if (x == 0) {
+        p.m[row] = any ? M * kLn2 : -INFINITY;
+        p.l[row] = L;
+      }
+    } else {
+      const int64_t part = row * p.nsplit + sp;
+      p.ws_o[part * D + x] = any ? O / L : 0.f;
+      if (x == 0) {
+        p.ws_ml[part * 2] = any ? M : -INFINITY;  // log2 units
+        p.ws_ml[part * 2 + 1] = L;
+      }
+    }
+  }
+  if (p.nsplit == 1) return;
+
+  // ---- intra-GPU split-K: the last CTA of this (request, kv-head) merges ------------
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t* cnt = p.ws_cnt + (int64_t)b * p.hkv + g;
+    const int prev = atomicAdd(cnt, 1);
+    const int last = prev == p.nsplit - 1;
+    if (last) *cnt = 0;  // every CTA has arrived: re-arm for the next call
+    s_flag[0] = last;
+  }
+  __syncthreads();
+  if (!s_flag[0]) return;
+  __threadfence();
+  if (threadIdx.x < G) {  // per-head weights w_j = l_j 2^(m_j - M) / L, fixed order
+    const int h = threadIdx.x;
+    const int64_t row = (int64_t)b * p.hq + g * G + h;
+    const float* ml = p.ws_ml + row * p.nsplit * 2;
+    float M = -INFINITY;
+    for (int j = 0; j < p.nsplit; ++j) M = fmaxf(M, __ldcg(ml + 2 * j));
+    float L = 0.f;
+    for (int j = 0; j < p.nsplit; ++j) {
+      const float mj = __ldcg(ml + 2 * j);
+      const float wj = mj == -INFINITY ? 0.f : __ldcg(ml + 2 * j + 1) * exp2f(mj - M);
+      s_w[h * kMaxSplit + j] = wj;
+      L += wj;
+    }
+    for (int j = 0; j < p.nsplit; ++j) s_w[h * kMaxSplit + j] = L > 0.f ? s_w[h * kMaxSplit + j] / L : 0.f;
+    p.m[row] = L > 0.f ? M * kLn2 : -INFINITY;
+    p.l[row] = L;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
+    const int h = idx / D, x = idx - h * D;
+    const int64_t row = (int64_t)b * p.hq + g * G + h;
+    const float* po = p.ws_o + row * p.nsplit * D + x;
+    float O = 0.f;
+    for (int j = 0; j < p.nsplit; ++j) O += s_w[h * kMaxSplit + j] * __ldcg(po + (int64_t)j * D);
+    p.o[row * D + x] = O;
+  }
+}
+
+struct Plan {
+  int nsplit, bps;
+  size_t ws_bytes, off_ml, off_cnt;
+};
+
+bs_status make_plan(int batch, int hq, int hkv, int d, int max_blocks, Plan* out) {
+  const int sms = sm_count(current_device());
+  const int64_t base = (int64_t)batch * hkv;
+  const int64_t target = (int64_t)sms * 2 * 2;  // two waves of 2 CTAs/SM
+  int nsplit = 1;
+  if (base < target) nsplit = (int)((target + base - 1) / base);
+  const int min_bps = kWarps * 2;
+  nsplit = std::min(nsplit, kMaxSplit);
+  nsplit = std::min(nsplit, std::max(1, (max_blocks + min_bps - 1) / min_bps));
+  int bps = std::max(1, (max_blocks + nsplit - 1) / nsplit);
+  bps = std::max(bps, (max_blocks + kMaxSplit - 1) / kMaxSplit);
+  if (bps > kBtMax) {
+    bps = kBtMax;
+    if ((max_blocks + bps - 1) / bps > kMaxSplit)
+      return set_error(BS_ERR_UNSUPPORTED, "max_blocks %d exceeds %d", max_blocks,
+                       kBtMax * kMaxSplit);
+  }
+  nsplit = std::max(1, (max_blocks + bps - 1) / bps);
+  Plan pl{};
+  pl.nsplit = nsplit;
+  pl.bps = bps;
+  if (nsplit > 1) {
+    const size_t parts = (size_t)batch * hq * nsplit;
+    pl.off_ml = parts * d * 4;
+    pl.off_cnt = pl.off_ml + parts * 2 * 4;
+    pl.ws_bytes = pl.off_cnt + (size_t)batch * hkv * 4;
+  }
+  *out = pl;
+  return BS_OK;
+}
+
+template <int D, int G>
+bs_status launch_attn_t(const AttnParams& p, int batch, cudaStream_t stream) {
+  constexpr int STAGES = D == 128 ? 3 : 6;
+  using S = Smem<D, G, STAGES>;
+  static int configured_dev = -1;
+  const int dev = current_device();
+  if (configured_dev != dev) {
+    cudaFuncSetAttribute(split_decode_attn<D, G, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         S::kTotal);
+    configured_dev = dev;
+  }
+  dim3 grid(p.nsplit, p.hkv, batch);
+  split_decode_attn<D, G, STAGES><<<grid, kWarps * 32, S::kTotal, stream>>>(p);
+  return check_launch("split_decode_attn");
+}
+
+template <int D>
+bs_status launch_attn_d(const AttnParams& p, int G, int batch, cudaStream_t stream) {
+  switch (G) {
+    case 1: return launch_attn_t<D, 1>(p, batch, stream);
+    case 2: return launch_attn_t<D, 2>(p, batch, stream);
+    case 4: return launch_attn_t<D, 4>(p, batch, stream);
+    case 8: return launch_attn_t<D, 8>(p, batch, stream);
+  }
+  return set_error(BS_ERR_UNSUPPORTED, "query group G=%d not in {1,2,4,8}", G);
+}
+
+}  // namespace
+}  // namespace bs
+
+extern "C" {
+
+bs_status bs_split_decode_attention_workspace_size(const bs_kv_pool* pool, int32_t batch,
+                                                   int32_t num_q_heads, int32_t max_blocks,
+                                                   size_t* bytes) {
+  BS_REQUIRE(pool && bytes, "bs_split_decode_attention_workspace_size: NULL argument");
+  BS_REQUIRE(batch >= 0 && max_blocks >= 1 && num_q_heads >= 1,
+             "bs_split_decode_attention_workspace_size: bad batch/max_blocks/heads");
+  bs::Plan pl;
+  bs_status st = bs::make_plan(batch, num_q_heads, pool->desc.num_kv_heads, pool->desc.head_dim,
+                               max_blocks, &pl);
+  if (st != BS_OK) return st;
+  *bytes = pl.ws_bytes;
+  return BS_OK;
+}
+
+bs_status bs_split_decode_attention(const bs_kv_pool* pool, int32_t layer, const void* q,
+                                    int32_t batch, int32_t num_q_heads,
+                                    const int32_t* block_tables, int32_t max_blocks,
+                                    const int32_t* kv_split, int32_t n_shards, int32_t shard_id,
+                                    float scale, float* o_part, float* m, float* l,
+                                    void* workspace, size_t workspace_bytes, void* stream) {
+  BS_REQUIRE(pool, "bs_split_decode_attention: NULL pool");
+  const int hkv = pool->desc.num_kv_heads, d = pool->desc.head_dim;
+  BS_REQUIRE(layer >= 0 && layer < pool->desc.num_layers, "bs_split_decode_attention: layer %d out of range",
+             layer);
+  BS_REQUIRE(batch >= 0, "bs_split_decode_attention: batch < 0");
+  if (batch == 0) return BS_OK;
+  BS_REQUIRE(num_q_heads >= hkv && num_q_heads % hkv == 0,
+             "bs_split_decode_attention: num_q_heads %d not a multiple of Hkv %d", num_q_heads, hkv);
+  BS_REQUIRE(max_blocks >= 1, "bs_split_decode_attention: max_blocks < 1");
+  BS_REQUIRE(n_shards >= 1 && shard_id >= 0 && shard_id < n_shards,
+             "bs_split_decode_attention: shard %d of %d", shard_id, n_shards);
+  BS_REQUIRE(q && block_tables && kv_split && o_part && m && l,
+             "bs_split_decode_attention: NULL device pointer");
+  BS_REQUIRE(((uintptr_t)q & 15) == 0 && ((uintptr_t)o_part & 15) == 0,
+             "bs_split_decode_attention: q/o_part must be 16-B aligned");
+  BS_REQUIRE(scale > 0.f && scale == scale, "bs_split_decode_attention: bad scale");
+  bs::Plan pl;
+  bs_status st = bs::make_plan(batch, num_q_heads, hkv, d, max_blocks, &pl);
+  if (st != BS_OK) return st;
+  BS_REQUIRE(pl.ws_bytes == 0 || (workspace && workspace_bytes >= pl.ws_bytes &&
+                                  ((uintptr_t)workspace & 15) == 0),
+             "bs_split_decode_attention: workspace needs %zu bytes (got %zu)", pl.ws_bytes,
+             workspace_bytes);
+  bs::AttnParams p{};
+  p.kv = pool->base + (size_t)layer * pool->layer_bytes;
+  p.chunk_bytes = (int64_t)pool->chunk_bytes;
+  p.v_off = (int64_t)hkv * pool->page_bytes;
+  p.q = static_cast<const __nv_bfloat16*>(q);
+  p.bt = block_tables;
+  p.max_blocks = max_blocks;
+  p.kv_split = kv_split;
+  p.n_shards = n_shards;
+  p.shard_id = shard_id;
+  p.scale_log2 = scale * bs::kLog2e;
+  p.hq = num_q_heads;
+  p.hkv = hkv;
+  p.nsplit = pl.nsplit;
+  p.bps = pl.bps;
+  p.o = o_part;
+  p.m = m;
+  p.l = l;
+  if (pl.ws_bytes) {
+    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    p.ws_o = reinterpret_cast<float*>(ws);
+    p.ws_ml = reinterpret_cast<float*>(ws + pl.off_ml);
+    p.ws_cnt = reinterpret_cast<int32_t*>(ws + pl.off_cnt);
+  }
+  const int G = num_q_heads / hkv;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (d == 128) return bs::launch_attn_d<128>(p, G, batch, s);
+  return bs::launch_attn_d<64>(p, G, batch, s);
+}
+
+}  // extern "C"

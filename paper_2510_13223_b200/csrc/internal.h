@@ -1,0 +1,44 @@
+// Internal helpers shared by the library's translation units (never installed).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <mutex>
+#include <set>
+#include <string>
+
+#include "banaserve.h"
+
+struct bs_kv_pool {
+  bs_kv_pool_desc desc;
+  uint8_t* base = nullptr;
+  size_t chunk_bytes = 0;   // one (layer, block): K+V pages of all heads
+  size_t page_bytes = 0;    // one (layer, block, K|V, head)
+  size_t layer_bytes = 0;   // num_blocks * chunk_bytes
+  std::mutex mu;            // guards the allocator
+  std::set<int32_t> free_ids;
+};
+
+namespace bs {
+
+bs_status set_error(bs_status st, const char* fmt, ...);
+bs_status check_launch(const char* what);
+int sm_count(int device);
+int current_device();
+
+inline bs_status ok() { return BS_OK; }
+
+// Launchers (defined in the .cu files).
+bs_status launch_copy_chunks(const uint8_t* src_base, const int32_t* src_ids, uint8_t* dst_base,
+                             const int32_t* dst_ids, int32_t n, size_t chunk_bytes,
+                             size_t page_bytes, int method, cudaStream_t stream);
+
+}  // namespace bs
+
+#define BS_REQUIRE(cond, ...)                                          \
+  do {                                                                 \
+    if (!(cond)) return bs::set_error(BS_ERR_INVALID_ARG, __VA_ARGS__); \
+  } while (0)

@@ -1,0 +1,246 @@
+// H2: per-layer KV block migration -- gather -> send -> scatter fused into one copy
+// kernel (attention-level migration, eq. 11; the copy is
+// "without semantic change", eq. 5).
+//
+// The unit of work is one page (one (layer, block, K|V, kv_head) = 16*d*2 bytes, 4 KiB
+// at d=128): pages are contiguous in the pool layout, so every copy is a straight
+// 16-byte-aligned memcpy.  Two kernels:
+//   * copy_pages_vec16: warp per page, 16-byte LDG (L1::no_allocate) / STG, all loads of
+//     a page issued before its stores (8 x 16 B in flight per lane at d=128).  When the
+//     destination (or source) base is a peer-mapped pointer the stores (loads) travel over
+//     NVLink -- the P2P "push" (or "pull") transport with no staging.
+//   * copy_pages_bulk: one elected thread per CTA streams pages through a shared-memory
+//     ring with TMA bulk copies (cp.async.bulk global->shared with an mbarrier, then
+//     cp.async.bulk shared->global in bulk groups); no registers touch the payload.
+#include <cuda_runtime.h>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace bs {
+namespace {
+
+__device__ __forceinline__ int4 ld_stream(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void st_stream(int4* p, const int4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+template <int PAGE_BYTES>
+__global__ void __launch_bounds__(256) copy_pages_vec16(const uint8_t* __restrict__ src_base,
+                                                        const int32_t* __restrict__ src_ids,
+                                                        uint8_t* __restrict__ dst_base,
+                                                        const int32_t* __restrict__ dst_ids,
+                                                        int32_t n, int32_t pages_per_chunk,
+                                                        int64_t chunk_bytes) {
+  constexpr int V = PAGE_BYTES / (16 * 32);  // int4 per lane per page
+  const int lane = threadIdx.x & 31;
+  const int wpc = blockDim.x >> 5;
+  const int64_t total = (int64_t)n * pages_per_chunk;
+  for (int64_t p = (int64_t)blockIdx.x * wpc + (threadIdx.x >> 5); p < total;
+       p += (int64_t)gridDim.x * wpc) {
+    const int32_t i = (int32_t)(p / pages_per_chunk);
+    const int32_t j = (int32_t)(p - (int64_t)i * pages_per_chunk);
+    const int64_t si = src_ids ? __ldg(src_ids + i) : i;
+    const int64_t di = dst_ids ? __ldg(dst_ids + i) : i;
+    const int4* s = reinterpret_cast<const int4*>(src_base + si * chunk_bytes +
+                                                  (int64_t)j * PAGE_BYTES) + lane;
+    int4* d = reinterpret_cast<int4*>(dst_base + di * chunk_bytes + (int64_t)j * PAGE_BYTES) + lane;
+    int4 r[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) r[v] = ld_stream(s + v * 32);
+#pragma unroll
+    for (int v = 0; v < V; ++v) st_stream(d + v * 32, r[v]);
+  }
+}
+
+// ---- TMA bulk ring -------------------------------------------------------------------
+
+using ptx::bulk_g2s;
+using ptx::mbar_expect_tx;
+using ptx::mbar_init;
+using ptx::mbar_wait;
+using ptx::smem_u32;
+
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(smem_src)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;"); }
+
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+constexpr int kBulkStages = 16;  // ring slots (pages)
+constexpr int kBulkAhead = 8;    // loads in flight ahead of the store front
+
+template <int PAGE_BYTES>
+__global__ void __launch_bounds__(32) copy_pages_bulk(const uint8_t* __restrict__ src_base,
+                                                      const int32_t* __restrict__ src_ids,
+                                                      uint8_t* __restrict__ dst_base,
+                                                      const int32_t* __restrict__ dst_ids,
+                                                      int32_t n, int32_t pages_per_chunk,
+                                                      int64_t chunk_bytes) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bars[kBulkStages];
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < kBulkStages; ++s) mbar_init(&bars[s], 1);
+  ptx::fence_mbar_init();
+
+  const int64_t total = (int64_t)n * pages_per_chunk;
+  // this CTA's pages: p = blockIdx.x + k * gridDim.x, k = 0..mine-1
+  const int64_t mine = total > blockIdx.x ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  auto src_of = [&](int64_t k) {
+    const int64_t p = blockIdx.x + k * gridDim.x;
+    const int32_t i = (int32_t)(p / pages_per_chunk);
+    const int32_t j = (int32_t)(p - (int64_t)i * pages_per_chunk);
+    const int64_t si = src_ids ? __ldg(src_ids + i) : i;
+    return src_base + si * chunk_bytes + (int64_t)j * PAGE_BYTES;
+  };
+  auto dst_of = [&](int64_t k) {
+    const int64_t p = blockIdx.x + k * gridDim.x;
+    const int32_t i = (int32_t)(p / pages_per_chunk);
+    const int32_t j = (int32_t)(p - (int64_t)i * pages_per_chunk);
+    const int64_t di = dst_ids ? __ldg(dst_ids + i) : i;
+    return dst_base + di * chunk_bytes + (int64_t)j * PAGE_BYTES;
+  };
+  auto issue_load = [&](int64_t k) {
+    const int s = (int)(k % kBulkStages);
+    mbar_expect_tx(&bars[s], PAGE_BYTES);
+    bulk_g2s(smem + (size_t)s * PAGE_BYTES, src_of(k), PAGE_BYTES, &bars[s]);
+  };
+  for (int64_t k = 0; k < mine && k < kBulkAhead; ++k) issue_load(k);
+  for (int64_t k = 0; k < mine; ++k) {
+    const int s = (int)(k % kBulkStages);
+    mbar_wait(&bars[s], (uint32_t)((k / kBulkStages) & 1));
+    bulk_s2g(dst_of(k), smem + (size_t)s * PAGE_BYTES, PAGE_BYTES);
+    bulk_commit();
+    const int64_t nk = k + kBulkAhead;
+    if (nk < mine) {
+      // slot of nk was last read by the store of page nk - kBulkStages; at most
+      // kBulkStages - kBulkAhead - 1 younger stores may still be reading smem.
+      bulk_wait_read<kBulkStages - kBulkAhead - 1>();
+      issue_load(nk);
+    }
+  }
+  bulk_wait_all();
+}
+
+template <int PAGE_BYTES>
+bs_status launch_copy_t(const uint8_t* src_base, const int32_t* src_ids, uint8_t* dst_base,
+                        const int32_t* dst_ids, int32_t n, int32_t ppc, int64_t chunk, int method,
+                        cudaStream_t stream) {
+  const int64_t total = (int64_t)n * ppc;
+  const int sms = sm_count(current_device());
+  if (method == BS_MIGRATE_BULK) {
+    const int smem = kBulkStages * PAGE_BYTES;
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(copy_pages_bulk<PAGE_BYTES>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      configured = true;
+    }
+    int64_t grid = std::min<int64_t>(total, (int64_t)sms * 3);
+    copy_pages_bulk<PAGE_BYTES><<<(unsigned)grid, 32, smem, stream>>>(
+        src_base, src_ids, dst_base, dst_ids, n, ppc, chunk);
+    return check_launch("copy_pages_bulk");
+  }
+  const int wpc = 8;
+  int64_t grid = std::min<int64_t>((total + wpc - 1) / wpc, (int64_t)sms * 8);
+  copy_pages_vec16<PAGE_BYTES><<<(unsigned)grid, wpc * 32, 0, stream>>>(
+      src_base, src_ids, dst_base, dst_ids, n, ppc, chunk);
+  return check_launch("copy_pages_vec16");
+}
+
+}  // namespace
+
+bs_status launch_copy_chunks(const uint8_t* src_base, const int32_t* src_ids, uint8_t* dst_base,
+                             const int32_t* dst_ids, int32_t n, size_t chunk_bytes,
+                             size_t page_bytes, int method, cudaStream_t stream) {
+  if (n == 0) return BS_OK;
+  const int32_t ppc = (int32_t)(chunk_bytes / page_bytes);
+  if (method == BS_MIGRATE_AUTO) method = BS_MIGRATE_VEC16;
+  if (page_bytes == 4096)
+    return launch_copy_t<4096>(src_base, src_ids, dst_base, dst_ids, n, ppc, (int64_t)chunk_bytes,
+                               method, stream);
+  if (page_bytes == 2048)
+    return launch_copy_t<2048>(src_base, src_ids, dst_base, dst_ids, n, ppc, (int64_t)chunk_bytes,
+                               method, stream);
+  return set_error(BS_ERR_UNSUPPORTED, "page size %zu", page_bytes);
+}
+
+}  // namespace bs
+
+static bool same_geometry(const bs_kv_pool* a, const bs_kv_pool* b) {
+  return a->desc.num_layers == b->desc.num_layers && a->desc.num_kv_heads == b->desc.num_kv_heads &&
+         a->desc.head_dim == b->desc.head_dim && a->desc.block_size == b->desc.block_size &&
+         a->desc.dtype == b->desc.dtype;
+}
+
+extern "C" {
+
+bs_status bs_kv_migrate_layer_ex(const bs_kv_pool* src, bs_kv_pool* dst, int32_t layer,
+                                 const int32_t* src_ids, const int32_t* dst_ids, int32_t n,
+                                 int32_t method, void* stream) {
+  BS_REQUIRE(src && dst, "bs_kv_migrate_layer: NULL pool");
+  BS_REQUIRE(same_geometry(src, dst), "bs_kv_migrate_layer: src/dst geometry differs");
+  BS_REQUIRE(layer >= 0 && layer < src->desc.num_layers, "bs_kv_migrate_layer: layer %d out of [0,%d)",
+             layer, src->desc.num_layers);
+  BS_REQUIRE(n >= 0, "bs_kv_migrate_layer: n < 0");
+  BS_REQUIRE(n == 0 || (src_ids && dst_ids), "bs_kv_migrate_layer: NULL ids");
+  BS_REQUIRE(method >= BS_MIGRATE_AUTO && method <= BS_MIGRATE_BULK,
+             "bs_kv_migrate_layer: bad method %d", method);
+  return bs::launch_copy_chunks(src->base + (size_t)layer * src->layer_bytes, src_ids,
+                                dst->base + (size_t)layer * dst->layer_bytes, dst_ids, n,
+                                src->chunk_bytes, src->page_bytes, method,
+                                static_cast<cudaStream_t>(stream));
+}
+
+bs_status bs_kv_migrate_layer(const bs_kv_pool* src, bs_kv_pool* dst, int32_t layer,
+                              const int32_t* src_ids, const int32_t* dst_ids, int32_t n,
+                              void* stream) {
+  return bs_kv_migrate_layer_ex(src, dst, layer, src_ids, dst_ids, n, BS_MIGRATE_AUTO, stream);
+}
+
+bs_status bs_kv_gather_layer(const bs_kv_pool* src, int32_t layer, const int32_t* ids, int32_t n,
+                             void* staging, void* stream) {
+  BS_REQUIRE(src, "bs_kv_gather_layer: NULL pool");
+  BS_REQUIRE(layer >= 0 && layer < src->desc.num_layers, "bs_kv_gather_layer: layer out of range");
+  BS_REQUIRE(n >= 0, "bs_kv_gather_layer: n < 0");
+  BS_REQUIRE(n == 0 || (ids && staging), "bs_kv_gather_layer: NULL ids/staging");
+  BS_REQUIRE(((uintptr_t)staging & 15) == 0, "bs_kv_gather_layer: staging not 16-B aligned");
+  return bs::launch_copy_chunks(src->base + (size_t)layer * src->layer_bytes, ids,
+                                static_cast<uint8_t*>(staging), nullptr, n, src->chunk_bytes,
+                                src->page_bytes, BS_MIGRATE_AUTO, static_cast<cudaStream_t>(stream));
+}
+
+bs_status bs_kv_scatter_layer(bs_kv_pool* dst, int32_t layer, const int32_t* ids, int32_t n,
+                              const void* staging, void* stream) {
+  BS_REQUIRE(dst, "bs_kv_scatter_layer: NULL pool");
+  BS_REQUIRE(layer >= 0 && layer < dst->desc.num_layers, "bs_kv_scatter_layer: layer out of range");
+  BS_REQUIRE(n >= 0, "bs_kv_scatter_layer: n < 0");
+  BS_REQUIRE(n == 0 || (ids && staging), "bs_kv_scatter_layer: NULL ids/staging");
+  BS_REQUIRE(((uintptr_t)staging & 15) == 0, "bs_kv_scatter_layer: staging not 16-B aligned");
+  return bs::launch_copy_chunks(static_cast<const uint8_t*>(staging), nullptr,
+                                dst->base + (size_t)layer * dst->layer_bytes, ids, n,
+                                dst->chunk_bytes, dst->page_bytes, BS_MIGRATE_AUTO,
+                                static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

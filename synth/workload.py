@@ -223,6 +223,71 @@ def toy_case(seed: int = 0):
     return dense, ks, place_shards(dense, ks, seed=seed)
 
 
+@dataclasses.dataclass
+class DeviceShards:
+    """Full-size case generated directly in device memory (bench / sampled parity).
+    pools[j]: torch bf16 [L][NB][2][Hkv][bs][d]; block_tables[j]: numpy int32 [B][mb];
+    kv_split numpy int32 [B][n+1]; q torch bf16 [L][B][Hq][d]."""
+    shape: Shape
+    seq_lens: np.ndarray
+    kv_split: np.ndarray
+    pools: list
+    block_tables: list
+    q: "torch.Tensor"
+
+
+def device_shards(shape: Shape, seq_lens, kv_split: np.ndarray, seed: int, device,
+                  spare_blocks: int = 0, layers: int | None = None) -> DeviceShards:
+    """Seeded N(0,1) bf16 K/V (+ per-channel V bias) and q generated on ``device`` with a
+    torch CUDA generator; block placement from a seeded CPU permutation (fragmented
+    pool).  Pad slots keep their random values (attention must mask them)."""
+    L = shape.n_layers if layers is None else layers
+    gd = torch.Generator(device=device)
+    gd.manual_seed(int(seed))
+    gc = _gen(seed + 104729)
+    B = len(seq_lens)
+    n = kv_split.shape[1] - 1
+    pools, bts = [], []
+    for j in range(n):
+        lens = (kv_split[:, j + 1] - kv_split[:, j]).astype(np.int64)
+        nblk = [ceil_div(int(x), shape.bs) for x in lens]
+        nb = int(sum(nblk)) + spare_blocks
+        nb = max(nb, 1)
+        perm = torch.randperm(nb, generator=gc).numpy()
+        pool = torch.randn((L, nb, 2, shape.hkv, shape.bs, shape.d), generator=gd, device=device,
+                           dtype=torch.bfloat16)
+        bias = (torch.rand((L, shape.hkv, 1, shape.d), generator=gd, device=device) * 2 - 1)
+        pool[:, :, 1] += bias.to(torch.bfloat16)[:, None]
+        mb = max(1, max(nblk))
+        bt = np.full((B, mb), -1, dtype=np.int32)
+        nxt = 0
+        for b in range(B):
+            bt[b, :nblk[b]] = perm[nxt:nxt + nblk[b]]
+            nxt += nblk[b]
+        pools.append(pool)
+        bts.append(bt)
+    q = torch.randn((L, B, shape.hq, shape.d), generator=gd, device=device, dtype=torch.bfloat16)
+    return DeviceShards(shape, np.asarray(seq_lens), kv_split, pools, bts, q)
+
+
+def extract_requests(case: DeviceShards, req_ids, layer: int):
+    """Copy the blocks of a few requests of one layer to the host as a compact case
+    (uint16 pools renumbered 0..k-1, block tables, kv_split, q) for the oracle."""
+    req_ids = list(req_ids)
+    pools, bts = [], []
+    for pool, bt in zip(case.pools, case.block_tables):
+        rows = bt[req_ids]
+        ids = sorted({int(x) for x in rows.ravel() if x >= 0})
+        remap = {x: i for i, x in enumerate(ids)}
+        idx = torch.tensor(ids if ids else [0], dtype=torch.long, device=pool.device)
+        sub = pool[layer:layer + 1].index_select(1, idx).cpu().view(torch.int16).numpy().view(np.uint16)
+        nbt = np.vectorize(lambda x: remap.get(int(x), -1))(rows).astype(np.int32) if ids else rows
+        pools.append(np.ascontiguousarray(sub))
+        bts.append(np.ascontiguousarray(nbt))
+    q = case.q[layer, req_ids].cpu().view(torch.int16).numpy().view(np.uint16)
+    return pools, bts, np.ascontiguousarray(case.kv_split[req_ids]), np.ascontiguousarray(q)
+
+
 def default_scale(d: int) -> float:
     """Reading R-A2: scale = 1/sqrt(d) rounded to fp32, passed to both sides."""
     return float(np.float32(1.0 / math.sqrt(d)))

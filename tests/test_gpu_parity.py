@@ -1,0 +1,277 @@
+"""GPU parity: every kernel behind the C-ABI against the fp64 oracle on the same seeded
+inputs.
+
+Tolerances (BASELINE.json north_star, reading R-A15):
+  migration                  bit-exact (byte equality of whole pools)
+  merged attention output    max |d| <= 2e-2 and per-row max|d| / max|ref| <= 1e-2 (bf16 out)
+  merged / per-shard lse     |d| <= 1e-4 (natural log)
+  per-shard o~ (fp32)        |d| <= 1e-3 (reported tighter than the bar; fp32 accumulate)
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+ABS_TOL, ROW_REL_TOL, LSE_TOL, PART_TOL = 2e-2, 1e-2, 1e-4, 1e-3
+
+
+@pytest.fixture(scope="module")
+def bs():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_2510_13223_b200 as m
+    m.lib()
+    return m
+
+
+def dev_bf16(a: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).view(torch.bfloat16).cuda()
+
+
+def dev_i32(a) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).cuda()
+
+
+def host_u16(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().view(torch.int16).numpy().view(np.uint16)
+
+
+def gpu_pools(bs, shape, shard_pools):
+    pools = []
+    for sp in shard_pools:
+        L, nb = sp.shape[0], sp.shape[1]
+        p = bs.KVPool(L, nb, shape.hkv, shape.d)
+        p.data.copy_(dev_bf16(sp))
+        pools.append(p)
+    return pools
+
+
+def run_split_attention(bs, shape, pools, block_tables, kv_split, q, layer, scale):
+    """All shards through bs_split_decode_attention, then bs_merge_partials."""
+    B, hq, d = q.shape
+    ks = dev_i32(kv_split)
+    qd = q if isinstance(q, torch.Tensor) else dev_bf16(q)
+    parts = []
+    for j, (pool, bt) in enumerate(zip(pools, block_tables)):
+        btd = dev_i32(bt)
+        o = torch.full((B, hq, d), float("nan"), device="cuda")
+        m = torch.full((B, hq), float("nan"), device="cuda")
+        l = torch.full((B, hq), float("nan"), device="cuda")
+        ws_n = bs.split_decode_attention_workspace_size(pool, B, hq, bt.shape[1])
+        ws = torch.zeros(max(ws_n, 16), dtype=torch.uint8, device="cuda")
+        bs.split_decode_attention(pool, layer, qd, btd, ks, j, scale, o, m, l, ws)
+        parts.append((o, m, l, ws))
+    out = torch.full((B, hq, d), float("nan"), dtype=torch.bfloat16, device="cuda")
+    lse = torch.full((B, hq), float("nan"), device="cuda")
+    bs.merge_partials([p[0] for p in parts], [p[1] for p in parts], [p[2] for p in parts], out, lse)
+    torch.cuda.synchronize()
+    return parts, out, lse
+
+
+def check_against_oracle(shape, shard_pools, block_tables, kv_split, q_u16, layer, scale, parts,
+                         out, lse):
+    ref_parts = [oracle.attention_shard(p, layer, q_u16, bt, kv_split, j, scale)
+                 for j, (p, bt) in enumerate(zip(shard_pools, block_tables))]
+    for (o, m, l, _), (ro, rm, rl) in zip(parts, ref_parts):
+        o, m, l = o.cpu().double().numpy(), m.cpu().double().numpy(), l.cpu().double().numpy()
+        empty = rl == 0
+        assert np.array_equal(l == 0, empty), "empty-shard rows disagree"
+        assert np.all(np.isneginf(m[empty])) and np.all(o[empty] == 0)
+        ne = ~empty
+        if ne.any():
+            assert np.abs((m + np.log(l))[ne] - (rm + np.log(rl))[ne]).max() <= LSE_TOL
+            assert np.abs(o[ne] - ro[ne]).max() <= PART_TOL
+    ref_o, ref_lse = oracle.merge_partials([p[0] for p in ref_parts], [p[1] for p in ref_parts],
+                                           [p[2] for p in ref_parts])
+    got = out.float().cpu().double().numpy()
+    gl = lse.cpu().double().numpy()
+    fin = np.isfinite(ref_lse)
+    assert np.array_equal(np.isneginf(gl), ~fin)
+    assert np.all(got[~fin] == 0)
+    err = np.abs(got - ref_o)
+    assert err.max() <= ABS_TOL, err.max()
+    rowmax = np.abs(ref_o).max(axis=-1)
+    rel = err.max(axis=-1)[fin] / np.maximum(rowmax[fin], 1e-30)
+    assert rel.max() <= ROW_REL_TOL, rel.max()
+    if fin.any():
+        assert np.abs(gl[fin] - ref_lse[fin]).max() <= LSE_TOL
+    return err.max()
+
+
+# ---------------------------------------------------------------------------- attention
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_toy_config_split_attention(bs, seed):
+    dense, ks, shards = synth.toy_case(seed)
+    shape = synth.TOY
+    pools = gpu_pools(bs, shape, [s.pool for s in shards])
+    sc = synth.default_scale(shape.d)
+    bts = [s.block_tables for s in shards]
+    parts, out, lse = run_split_attention(bs, shape, pools, bts, ks, dense.q[0], 0, sc)
+    check_against_oracle(shape, [s.pool for s in shards], bts, ks, dense.q[0], 0, sc, parts, out, lse)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_shapes_ragged_unaligned_empty_shards(bs, d, G):
+    shape = synth.Shape(2, 2 * G, 2, d)
+    lens = (0, 1, 15, 16, 17, 100, 333, 64)
+    dense = synth.gen_dense(shape, lens, seed=G * 10 + d)
+    ks = synth.random_split(lens, 3, seed=G + d)
+    ks[6] = [0, 0, 333, 333]              # empty first and last shard
+    ks[7] = [0, 16, 48, 64]               # block-aligned
+    shards = synth.place_shards(dense, ks, seed=G)
+    pools = gpu_pools(bs, shape, [s.pool for s in shards])
+    sc = synth.default_scale(d)
+    bts = [s.block_tables for s in shards]
+    for layer in range(2):
+        parts, out, lse = run_split_attention(bs, shape, pools, bts, ks, dense.q[layer], layer, sc)
+        check_against_oracle(shape, [s.pool for s in shards], bts, ks, dense.q[layer], layer, sc,
+                             parts, out, lse)
+
+
+@pytest.mark.parametrize("n_shards", [1, 8])
+def test_many_shards_and_split_k(bs, n_shards):
+    """B=1 long context forces the intra-GPU split-K (workspace + last-CTA merge)."""
+    shape = synth.Shape(1, 8, 2, 128)
+    lens = (5003,)
+    dense = synth.gen_dense(shape, lens, seed=77)
+    ks = synth.block_aligned_split(lens, n_shards)
+    shards = synth.place_shards(dense, ks, seed=5)
+    pools = gpu_pools(bs, shape, [s.pool for s in shards])
+    bts = [s.block_tables for s in shards]
+    sc = synth.default_scale(128)
+    assert bs.split_decode_attention_workspace_size(pools[0], 1, 8, bts[0].shape[1]) > 0
+    parts, out, lse = run_split_attention(bs, shape, pools, bts, ks, dense.q[0], 0, sc)
+    check_against_oracle(shape, [s.pool for s in shards], bts, ks, dense.q[0], 0, sc, parts, out, lse)
+    # second call reuses the workspace (counters re-armed) and is bitwise deterministic
+    parts2, out2, lse2 = run_split_attention(bs, shape, pools, bts, ks, dense.q[0], 0, sc)
+    assert torch.equal(out.view(torch.int16), out2.view(torch.int16))
+    assert torch.equal(lse, lse2)
+
+
+def test_llama3_8b_gqa_four_way(bs):
+    """C3-like shape (Hq 32 / Hkv 8, d 128) at reduced length, 4-way token split."""
+    shape = synth.Shape(1, 32, 8, 128)
+    lens = (8192, 3000, 17, 1)
+    dense = synth.gen_dense(shape, lens, seed=3)
+    ks = synth.block_aligned_split(lens, 4)
+    shards = synth.place_shards(dense, ks, seed=3)
+    pools = gpu_pools(bs, shape, [s.pool for s in shards])
+    bts = [s.block_tables for s in shards]
+    sc = synth.default_scale(128)
+    parts, out, lse = run_split_attention(bs, shape, pools, bts, ks, dense.q[0], 0, sc)
+    check_against_oracle(shape, [s.pool for s in shards], bts, ks, dense.q[0], 0, sc, parts, out, lse)
+
+
+def test_full_size_c2_layer_sampled(bs):
+    """BASELINE config C2 (Llama-2-7B shape, B=64 x 2048, 2-way split between the decode
+    and prefill pools) at full size for one layer, in the bench's launch configuration;
+    the oracle recomputes a sample of requests one by one."""
+    shape = synth.LLAMA2_7B
+    B, S = 64, 2048
+    lens = np.full(B, S)
+    ks = synth.block_aligned_split(lens, 2)
+    case = synth.device_shards(shape, lens, ks, seed=11, device="cuda", layers=1)
+    pools = []
+    for pt in case.pools:
+        p = bs.KVPool(1, pt.shape[1], shape.hkv, shape.d, base=pt.reshape(-1))
+        pools.append(p)
+    sc = synth.default_scale(128)
+    parts, out, lse = run_split_attention(bs, shape, pools, case.block_tables, ks, case.q[0], 0, sc)
+    sample = [0, 17, 63]
+    sp, sbt, sks, sq = synth.extract_requests(case, sample, 0)
+    sparts = [(o[sample], m[sample], l[sample], None) for (o, m, l, _) in parts]
+    check_against_oracle(shape, sp, sbt, sks, sq, 0, sc, sparts, out[sample], lse[sample])
+
+
+# ---------------------------------------------------------------------------- migration
+
+def random_pool(shape, nb, L, seed):
+    g = torch.Generator().manual_seed(seed)
+    return torch.randint(0, 65536, (L, nb, 2, shape.hkv, shape.bs, shape.d), generator=g,
+                         dtype=torch.int32).to(torch.int16).numpy().view(np.uint16)
+
+
+@pytest.mark.parametrize("method", [0, 1, 2])
+def test_toy_migration_bit_exact(bs, method):
+    dense, ks, shards = synth.toy_case(0)
+    shape = synth.TOY
+    src = shards[1]
+    nb_dst = 40
+    dst_np = np.full((1, nb_dst) + src.pool.shape[2:], synth.DST_SENTINEL, dtype=np.uint16)
+    src_g = gpu_pools(bs, shape, [src.pool])[0]
+    dst_g = gpu_pools(bs, shape, [dst_np])[0]
+    ref_alloc = oracle.Allocator(nb_dst)
+    assert dst_g.alloc(5) == list(ref_alloc.alloc(5))      # a tenant holds blocks 0..4
+    src_ids, new_bt = [], np.full_like(src.block_tables, -1)
+    dst_ids = []
+    for b in range(4):
+        row = [int(x) for x in src.block_tables[b] if x >= 0]
+        got = dst_g.alloc(len(row))
+        assert got == list(ref_alloc.alloc(len(row)))       # same allocator policy
+        new_bt[b, :len(row)] = got
+        src_ids += row
+        dst_ids += got
+    bs.kv_migrate_layer(src_g, dst_g, 0, dev_i32(src_ids), dev_i32(dst_ids), method=method)
+    torch.cuda.synchronize()
+    ref = dst_np.copy()
+    oracle.migrate_layer(src.pool, ref, 0, src_ids, dst_ids)
+    assert np.array_equal(host_u16(dst_g.data), ref)
+    # eq. 5: attention through the migrated blocks equals attention through the source, bitwise
+    sc = synth.default_scale(64)
+    q = dev_bf16(dense.q[0])
+    outs = []
+    for pool, bt in ((src_g, src.block_tables), (dst_g, new_bt)):
+        o = torch.empty(4, 4, 64, device="cuda")
+        m = torch.empty(4, 4, device="cuda")
+        l = torch.empty(4, 4, device="cuda")
+        bs.split_decode_attention(pool, 0, q, dev_i32(bt), dev_i32(ks), 1, sc, o, m, l)
+        outs.append((o, m, l))
+    torch.cuda.synchronize()
+    for x, y in zip(*outs):
+        assert torch.equal(x.nan_to_num(), y.nan_to_num())
+
+
+@pytest.mark.parametrize("method", [1, 2])
+@pytest.mark.parametrize("d,hkv", [(128, 8), (64, 4), (128, 32)])
+def test_migration_random_pairs_bit_exact(bs, method, d, hkv):
+    shape = synth.Shape(3, hkv, hkv, d)
+    nb_src, nb_dst = 300, 280
+    src_np = random_pool(shape, nb_src, 3, seed=d + hkv)
+    dst_np = np.full((3, nb_dst, 2, hkv, 16, d), synth.DST_SENTINEL, dtype=np.uint16)
+    src_g, dst_g = gpu_pools(bs, shape, [src_np, dst_np])
+    rng = np.random.default_rng(d * hkv)
+    ref = dst_np.copy()
+    for layer, n in ((0, 257), (1, 1), (2, 0), (2, 280)):
+        s = rng.integers(0, nb_src, size=n).astype(np.int32)
+        t = rng.permutation(nb_dst)[:n].astype(np.int32)
+        bs.kv_migrate_layer(src_g, dst_g, layer, dev_i32(s), dev_i32(t), method=method)
+        oracle.migrate_layer(src_np, ref, layer, s, t)
+    torch.cuda.synchronize()
+    assert np.array_equal(host_u16(dst_g.data), ref)
+
+
+def test_gather_scatter_roundtrip_equals_migrate(bs):
+    """The two-sided transport halves (pack -> [send/recv] -> unpack) are the same copy."""
+    shape = synth.Shape(2, 8, 8, 128)
+    src_np = random_pool(shape, 50, 2, seed=1)
+    dst_np = np.full((2, 60, 2, 8, 16, 128), synth.DST_SENTINEL, dtype=np.uint16)
+    src_g, dst_g = gpu_pools(bs, shape, [src_np, dst_np])
+    s = np.array([3, 49, 0, 7, 7], dtype=np.int32)
+    t = np.array([59, 0, 1, 30, 31], dtype=np.int32)
+    staging = torch.empty(len(s) * src_g.chunk_bytes, dtype=torch.uint8, device="cuda")
+    bs.kv_gather_layer(src_g, 1, dev_i32(s), staging)
+    bs.kv_scatter_layer(dst_g, 1, dev_i32(t), staging)
+    torch.cuda.synchronize()
+    ref = dst_np.copy()
+    oracle.migrate_layer(src_np, ref, 1, s, t)
+    assert np.array_equal(host_u16(dst_g.data), ref)
+    # staging holds the chunks in pair order
+    st = staging.cpu().numpy().view(np.uint16).reshape(len(s), -1)
+    for i, x in enumerate(s):
+        assert np.array_equal(st[i], src_np[1, x].ravel())

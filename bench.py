@@ -48,6 +48,13 @@ WORKLOAD = ("C2: Llama-2-7B shape (L=32, Hq=Hkv=32, d=128, bf16 KV), decode B=64
 FALLBACK_HBM_GBS = 6650.0
 
 
+def omp_threads() -> int:
+    """Threads the OpenMP oracle actually uses (OMP_NUM_THREADS, else the CPU affinity)."""
+    if os.environ.get("OMP_NUM_THREADS"):
+        return int(os.environ["OMP_NUM_THREADS"])
+    return len(os.sched_getaffinity(0))
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -329,7 +336,7 @@ def time_oracle_sample(sample, scale):
     return ta, tm
 
 
-def cpu_baseline(case, budget_s=12.0, reqs_per_sample=8):
+def cpu_baseline(case, budget_s=12.0, reqs_per_sample=32):
     """Time the oracle (as it stands) on sampled (request, layer) units until ~budget_s of
     CPU work, then extrapolate to the full step: T = L*(B/r * t_attn + H/h * t_mig)."""
     import oracle
@@ -339,21 +346,22 @@ def cpu_baseline(case, budget_s=12.0, reqs_per_sample=8):
     ta_tot = tm_tot = 0.0
     layers = 0
     t_start = time.perf_counter()
-    for layer in range(SHAPE.n_layers):
-        req = [(layer * reqs_per_sample + i) % BATCH for i in range(reqs_per_sample)]
+    for it in range(4 * SHAPE.n_layers):
+        layer = it % SHAPE.n_layers
+        req = [(it * reqs_per_sample + i) % BATCH for i in range(reqs_per_sample)]
         s = oracle_sample(case, req, layer, handoff_chunks)
         ta, tm = time_oracle_sample(s, scale)
         ta_tot += ta
         tm_tot += tm
         layers += 1
-        if time.perf_counter() - t_start > budget_s:
+        if ta_tot + tm_tot > budget_s or time.perf_counter() - t_start > 3 * budget_s:
             break
     t_attn = ta_tot / layers * (BATCH / reqs_per_sample)
     t_mig = tm_tot / layers * N_HANDOFF
     t_step = SHAPE.n_layers * (t_attn + t_mig)
     return {"value": round(BATCH / t_step, 4), "unit": "tokens/s", "kind": "oracle",
-            "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count())),
-            "sample": (f"{layers} layers x {reqs_per_sample} requests (both shards + merge) + "
+            "cores": omp_threads(),
+            "sample": (f"{layers} (layer, {reqs_per_sample}-request) units (both shards + merge) + "
                        f"1 hand-off request's chunks per layer, fp64 C oracle; extrapolated "
                        f"linearly to B={BATCH}, {N_HANDOFF} hand-offs, {SHAPE.n_layers} layers"),
             "measured_seconds": round(ta_tot + tm_tot, 3)}
@@ -387,7 +395,7 @@ def run_reference(args, rank, world, device):
     wall = time.perf_counter() - t0
     t_step = SHAPE.n_layers * (ta / args.steps * BATCH / reqs + tm / args.steps * N_HANDOFF)
     v = BATCH / t_step
-    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
+    cores = omp_threads()
     sample = (f"per step: 1 layer x {reqs} requests (both shards + merge) + 1 hand-off request's "
               f"chunks, fp64 C oracle; extrapolated to B={BATCH}, {N_HANDOFF} hand-offs, "
               f"{SHAPE.n_layers} layers")

@@ -1,0 +1,133 @@
+#!/usr/bin/env python
+"""Per-kernel microbenchmarks (device time via CUDA events, warm, inputs > L2).
+
+    python scripts/microbench.py [--only attn|mig] [--json out.json]
+
+attention: one bs_split_decode_attention launch per iteration, one shard, shapes of the
+BASELINE configs (C2 MHA, C3 GQA-4 long context, C4 GQA-8 mixed lengths); GB/s =
+algorithmic bytes (KV + q + partials + block table) / event time.
+migration: bs_kv_migrate_layer local copies (VEC16 vs BULK), payload GB/s (HBM traffic
+is 2x).  Profiling hook: --ncu-attn / --ncu-mig run a few launches of one case only.
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2510_13223_b200 as bs  # noqa: E402
+import synth  # noqa: E402
+
+
+def attn_case(name, shape, lens, iters=20, warm=5):
+    dev = torch.device("cuda")
+    lens = np.asarray(lens, dtype=np.int64)
+    ks = np.stack([np.zeros_like(lens), lens], 1).astype(np.int32)
+    case = synth.device_shards(shape, lens, ks, seed=1, device=dev, layers=1)
+    pt, bt = case.pools[0], case.block_tables[0]
+    pool = bs.KVPool(1, pt.shape[1], shape.hkv, shape.d, base=pt.reshape(-1))
+    B = len(lens)
+    q = case.q[0]
+    btd = torch.from_numpy(bt).to(dev)
+    ksd = torch.from_numpy(ks).to(dev)
+    o = torch.empty(B, shape.hq, shape.d, device=dev)
+    m = torch.empty(B, shape.hq, device=dev)
+    l = torch.empty(B, shape.hq, device=dev)
+    ws = torch.zeros(max(16, bs.split_decode_attention_workspace_size(pool, B, shape.hq, bt.shape[1])),
+                     dtype=torch.uint8, device=dev)
+    sc = synth.default_scale(shape.d)
+    for _ in range(warm):
+        bs.split_decode_attention(pool, 0, q, btd, ksd, 0, sc, o, m, l, ws)
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+    for a, b in evs:
+        a.record()
+        bs.split_decode_attention(pool, 0, q, btd, ksd, 0, sc, o, m, l, ws)
+        b.record()
+    torch.cuda.synchronize()
+    t = sorted(a.elapsed_time(b) for a, b in evs)
+    med = t[len(t) // 2]
+    kv = int(lens.sum()) * 2 * shape.hkv * shape.d * 2
+    alg = kv + B * shape.hq * shape.d * 2 + B * shape.hq * (shape.d + 2) * 4 + 4 * int(
+        sum(synth.ceil_div(int(x), 16) for x in lens))
+    return {"case": name, "B": B, "G": shape.group, "tokens": int(lens.sum()), "us": round(med * 1e3, 2),
+            "GBps": round(alg / (med * 1e-3) / 1e9, 1), "bytes": alg,
+            "ws": ws.numel() > 16}
+
+
+def mig_case(name, shape, n_pairs, method, iters=20, warm=5):
+    dev = torch.device("cuda")
+    nb = n_pairs + 64
+    src = bs.KVPool(1, nb, shape.hkv, shape.d)
+    dst = bs.KVPool(1, nb, shape.hkv, shape.d)
+    src.data.normal_()
+    g = torch.Generator().manual_seed(0)
+    s = torch.randperm(nb, generator=g)[:n_pairs].to(torch.int32).to(dev)
+    d = torch.randperm(nb, generator=g)[:n_pairs].to(torch.int32).to(dev)
+    for _ in range(warm):
+        bs.kv_migrate_layer(src, dst, 0, s, d, method=method)
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+    for a, b in evs:
+        a.record()
+        bs.kv_migrate_layer(src, dst, 0, s, d, method=method)
+        b.record()
+    torch.cuda.synchronize()
+    t = sorted(a.elapsed_time(b) for a, b in evs)
+    med = t[len(t) // 2]
+    by = n_pairs * src.chunk_bytes
+    return {"case": name, "method": ["auto", "vec16", "bulk"][method], "pairs": n_pairs,
+            "MiB": round(by / 2**20, 1), "us": round(med * 1e3, 2),
+            "payload_GBps": round(by / (med * 1e-3) / 1e9, 1),
+            "hbm_GBps": round(2 * by / (med * 1e-3) / 1e9, 1)}
+
+
+ATTN = {
+    "C2_mha_B64_2048": (synth.LLAMA2_7B, [2048] * 64),
+    "C2_shard_B64_1024": (synth.LLAMA2_7B, [1024] * 64),
+    "C3_gqa4_B8_8192": (synth.LLAMA3_8B, [8192] * 8),
+    "C3_gqa4_B1_8192": (synth.LLAMA3_8B, [8192] * 1),
+    "C3_gqa4_B32_8192": (synth.LLAMA3_8B, [8192] * 32),
+    "C3_gqa4_B8_32768_1gpu": (synth.LLAMA3_8B, [32768] * 8),
+    "C4_gqa8_mixed_B256": (synth.LLAMA2_70B, list(synth.mixed_lengths(256, seed=0) // 8)),
+}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", choices=["attn", "mig"])
+    ap.add_argument("--case")
+    ap.add_argument("--json")
+    ap.add_argument("--iters", type=int, default=20)
+    args = ap.parse_args()
+    res = []
+    if args.only in (None, "attn"):
+        for name, (shape, lens) in ATTN.items():
+            if args.case and args.case != name:
+                continue
+            r = attn_case(name, shape, lens, iters=args.iters)
+            print(json.dumps(r), flush=True)
+            res.append(r)
+    if args.only in (None, "mig"):
+        for name, shape, n in (("C2_chunk256K_384", synth.LLAMA2_7B, 384),
+                               ("C2_chunk256K_8192", synth.LLAMA2_7B, 8192),
+                               ("C4_chunk64K_512", synth.LLAMA3_8B, 512),
+                               ("C4_chunk64K_8192", synth.LLAMA3_8B, 8192)):
+            if args.case and args.case != name:
+                continue
+            for method in (1, 2):
+                r = mig_case(name, shape, n, method, iters=args.iters)
+                print(json.dumps(r), flush=True)
+                res.append(r)
+    if args.json:
+        with open(args.json, "w") as f:
+            json.dump(res, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 #include "ptx.cuh"
@@ -82,37 +83,23 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
   return __ffma2_rn(a, b, c);
 }
 
-// Sum 16 per-lane partials over the 32 lanes; lane pair (2t, 2t+1) returns token t's total.
-__device__ __forceinline__ float reduce_scatter16(float (&v)[16], int lane) {
-  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+// Sum 16 per-lane partials over the 32 lanes.  Slot i of lane L holds token i ^ (L >> 1)
+// (the K rows are loaded in that lane-permuted order), so every butterfly step keeps the
+// low half of its slots and sends the high half -- no per-lane selects -- and lane pair
+// (2t, 2t+1) ends with token t's total.
+__device__ __forceinline__ float reduce_scatter16(float (&v)[16]) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const float send = b4 ? v[i] : v[i + 8];
-    const float keep = b4 ? v[i + 8] : v[i];
-    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-  }
+  for (int i = 0; i < 8; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i + 8], 16);
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float send = b3 ? v[i] : v[i + 4];
-    const float keep = b3 ? v[i + 4] : v[i];
-    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-  }
+  for (int i = 0; i < 4; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i + 4], 8);
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const float send = b2 ? v[i] : v[i + 2];
-    const float keep = b2 ? v[i + 2] : v[i];
-    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-  }
-  {
-    const float send = b1 ? v[0] : v[1];
-    const float keep = b1 ? v[1] : v[0];
-    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-  }
+  for (int i = 0; i < 2; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i + 2], 4);
+  v[0] += __shfl_xor_sync(0xffffffffu, v[1], 2);
   return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
-template <int D, int G, int STAGES>
-__global__ void __launch_bounds__(kWarps * 32, 2) split_decode_attn(const AttnParams p) {
+template <int D, int G, int STAGES, int MINB>
+__global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const AttnParams p) {
   using S = Smem<D, G, STAGES>;
   constexpr int DPL = D / 32;  // head dims per lane (4 or 2)
   constexpr int DP2 = DPL / 2;
@@ -196,15 +183,17 @@ __global__ void __launch_bounds__(kWarps * 32, 2) split_decode_attn(const AttnPa
     const int nvalid = min(16, len - blk * 16);
 
     // ---- scores: s_t = <q_h, k_t> (log2 units) -------------------------------------
-    float2 kf[16][DP2];
+    float2 kf[16][DP2];  // slot i = token i ^ (lane >> 1)
+    const uint32_t kswz = (uint32_t)((lane >> 1) & 15) * (D * 2);
 #pragma unroll
     for (int t = 0; t < 16; ++t) {
+      const uint8_t* row = sk + ((uint32_t)(t * D * 2) ^ kswz);
       if constexpr (DPL == 4) {
-        const uint2 w = *reinterpret_cast<const uint2*>(sk + t * D * 2 + lane * 8);
+        const uint2 w = *reinterpret_cast<const uint2*>(row + lane * 8);
         kf[t][0] = bf2_to_f2(w.x);
         kf[t][1] = bf2_to_f2(w.y);
       } else {
-        const uint32_t w = *reinterpret_cast<const uint32_t*>(sk + t * D * 2 + lane * 4);
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(row + lane * 4);
         kf[t][0] = bf2_to_f2(w);
       }
     }
@@ -220,7 +209,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) split_decode_attn(const AttnPa
         for (int e = 0; e < DP2; ++e) a = ffma2(qv[h][e], kf[t][e], a);
         v[t] = a.x + a.y;
       }
-      float sc = reduce_scatter16(v, lane);
+      float sc = reduce_scatter16(v);
       sc = valid ? sc : -INFINITY;
       float mb = sc;
       mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 2));
@@ -379,34 +368,66 @@ __global__ void __launch_bounds__(kWarps * 32, 2) split_decode_attn(const AttnPa
   }
 }
 
+// Pipeline depth / residency per (head_dim, group): STAGES blocks (K+V pages) per warp in
+// flight, MINB CTAs per SM.  G <= 2 fits 3 CTAs/SM (registers <= 168) with a 2-deep ring
+// (d=128); G >= 4 needs more registers and keeps 2 CTAs/SM with a 3-deep ring.  Both give
+// ~192 KiB of KV in flight per SM.
+struct Variant {
+  int stages, minb;
+};
+
+int alt_variant() {
+  static int v = [] {
+    const char* e = getenv("BS_ATTN_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+Variant variant_for(int d, int G) {
+  if (alt_variant() == 1) return d == 128 ? Variant{3, 2} : Variant{6, 2};
+  if (d == 128) return G <= 2 ? Variant{2, 3} : Variant{3, 2};
+  return G <= 2 ? Variant{4, 3} : Variant{6, 2};
+}
+
 struct Plan {
   int nsplit, bps;
   size_t ws_bytes, off_ml, off_cnt;
 };
 
+// Split-K planning: pick the number of CTAs per (request, kv-head) that minimises
+// waves x blocks-per-CTA (+ a fixed per-CTA cost), i.e. fills all SM slots evenly.
 bs_status make_plan(int batch, int hq, int hkv, int d, int max_blocks, Plan* out) {
   const int sms = sm_count(current_device());
+  const int G = hq / std::max(hkv, 1);
+  const int64_t slots = (int64_t)sms * variant_for(d, G).minb;
   const int64_t base = (int64_t)batch * hkv;
-  const int64_t target = (int64_t)sms * 2 * 2;  // two waves of 2 CTAs/SM
-  int nsplit = 1;
-  if (base < target) nsplit = (int)((target + base - 1) / base);
-  const int min_bps = kWarps * 2;
-  nsplit = std::min(nsplit, kMaxSplit);
-  nsplit = std::min(nsplit, std::max(1, (max_blocks + min_bps - 1) / min_bps));
-  int bps = std::max(1, (max_blocks + nsplit - 1) / nsplit);
-  bps = std::max(bps, (max_blocks + kMaxSplit - 1) / kMaxSplit);
-  if (bps > kBtMax) {
-    bps = kBtMax;
-    if ((max_blocks + bps - 1) / bps > kMaxSplit)
-      return set_error(BS_ERR_UNSUPPORTED, "max_blocks %d exceeds %d", max_blocks,
-                       kBtMax * kMaxSplit);
+  const int min_bps = kWarps;
+  const int max_ns = std::min(kMaxSplit, std::max(1, (max_blocks + min_bps - 1) / min_bps));
+  int best_ns = 1;
+  double best = 1e300;
+  for (int ns = 1; ns <= max_ns; ++ns) {
+    const int bps = (max_blocks + ns - 1) / ns;
+    if (bps > kBtMax) continue;
+    const int real_ns = (max_blocks + bps - 1) / bps;
+    if (real_ns != ns) continue;
+    const int64_t ctas = base * ns;
+    const int64_t waves = (ctas + slots - 1) / slots;
+    // cost in block-times per SM slot: per-warp blocks, plus CTA prologue/epilogue and
+    // (for ns > 1) the partial write + last-CTA merge
+    const double cost = (double)waves * ((double)bps / kWarps + 2.0 + (ns > 1 ? 1.0 : 0.0));
+    if (cost < best - 1e-9) {
+      best = cost;
+      best_ns = ns;
+    }
   }
-  nsplit = std::max(1, (max_blocks + bps - 1) / bps);
+  if (best == 1e300)
+    return set_error(BS_ERR_UNSUPPORTED, "max_blocks %d exceeds %d", max_blocks, kBtMax * kMaxSplit);
   Plan pl{};
-  pl.nsplit = nsplit;
-  pl.bps = bps;
-  if (nsplit > 1) {
-    const size_t parts = (size_t)batch * hq * nsplit;
+  pl.nsplit = best_ns;
+  pl.bps = (max_blocks + best_ns - 1) / best_ns;
+  if (best_ns > 1) {
+    const size_t parts = (size_t)batch * hq * best_ns;
     pl.off_ml = parts * d * 4;
     pl.off_cnt = pl.off_ml + parts * 2 * 4;
     pl.ws_bytes = pl.off_cnt + (size_t)batch * hkv * 4;
@@ -415,20 +436,31 @@ bs_status make_plan(int batch, int hq, int hkv, int d, int max_blocks, Plan* out
   return BS_OK;
 }
 
-template <int D, int G>
-bs_status launch_attn_t(const AttnParams& p, int batch, cudaStream_t stream) {
-  constexpr int STAGES = D == 128 ? 3 : 6;
+template <int D, int G, int STAGES, int MINB>
+bs_status launch_attn_v(const AttnParams& p, int batch, cudaStream_t stream) {
   using S = Smem<D, G, STAGES>;
   static int configured_dev = -1;
   const int dev = current_device();
   if (configured_dev != dev) {
-    cudaFuncSetAttribute(split_decode_attn<D, G, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         S::kTotal);
+    cudaFuncSetAttribute(split_decode_attn<D, G, STAGES, MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
     configured_dev = dev;
   }
   dim3 grid(p.nsplit, p.hkv, batch);
-  split_decode_attn<D, G, STAGES><<<grid, kWarps * 32, S::kTotal, stream>>>(p);
+  split_decode_attn<D, G, STAGES, MINB><<<grid, kWarps * 32, S::kTotal, stream>>>(p);
   return check_launch("split_decode_attn");
+}
+
+template <int D, int G>
+bs_status launch_attn_t(const AttnParams& p, int batch, cudaStream_t stream) {
+  const Variant v = variant_for(D, G);
+  if constexpr (D == 128) {
+    if (v.stages == 2) return launch_attn_v<D, G, 2, 3>(p, batch, stream);
+    return launch_attn_v<D, G, 3, 2>(p, batch, stream);
+  } else {
+    if (v.stages == 4) return launch_attn_v<D, G, 4, 3>(p, batch, stream);
+    return launch_attn_v<D, G, 6, 2>(p, batch, stream);
+  }
 }
 
 template <int D>

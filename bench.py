@@ -16,8 +16,10 @@ layers of: migrate(l) || [split attention on D, on P -> LSE merge -> bf16 O].
 value = decode tokens/s of the step (B / step time), inputs resident in HBM; pools are
 70 GiB >> 126 MB L2, so no L2 flush is needed.  e2e = the same through host buffers
 (q H2D from pinned memory and O/lse D2H every step).  The CPU oracle is timed beside
-it on a bounded sample (cpu_baseline).  N>1 (torchrun): independent replicas per GPU
-(weak scaling); see DESIGN.md §Multi-GPU.
+it on a bounded sample (cpu_baseline).  N>1 (torchrun): a ring of instances, one per GPU
+-- rank r is home for its 64 requests and cold instance of rank r-1 (holds their shard 1
+and their hand-off KV); q, partials and hand-off chunks cross NVLink via NCCL P2P every
+layer (weak scaling: per-GPU work is fixed).  See DESIGN.md §8.
 """
 from __future__ import annotations
 
@@ -133,35 +135,46 @@ class ClockSampler:
 # the workload on the device
 # --------------------------------------------------------------------------------------
 
-def build_workload(bs, device, seed=0, layers=None):
-    from paper_2510_13223_b200.pipeline import LayerwiseDecodeStep, MigrationJob, Shard
+def build_workload(bs, device, rank=0, world=1, layers=None):
+    """Rank r's share of the ring (paper_2510_13223_b200/ring.py): home pool = shard 0 of
+    its own 64 requests + free blocks for hand-offs; cold pool = shard 1 of rank r-1's
+    requests + the KV handed off to r-1.  At N=1 the ring closes on itself."""
+    import torch.distributed as dist
+    from paper_2510_13223_b200.ring import CudaExec, CudaOps, ShardedDecodeStep
 
     L = SHAPE.n_layers if layers is None else layers
+    prev = (rank - 1) % world
     lens = np.full(BATCH, SEQ, dtype=np.int64)
     ks = synth.block_aligned_split(lens, N_SHARDS)
     handoff_blocks = N_HANDOFF * synth.ceil_div(SEQ, SHAPE.bs)
-    case = synth.device_shards(SHAPE, lens, ks, seed=seed, device=device,
-                               spare_blocks=handoff_blocks, layers=L)
+    home_t, home_bt = synth.device_pool(SHAPE, ks[:, 1] - ks[:, 0], synth.shard_seed(rank, 0),
+                                        device, spare_blocks=handoff_blocks, layers=L)
+    cold_t, cold_bt = synth.device_pool(SHAPE, ks[:, 2] - ks[:, 1], synth.shard_seed(prev, 1),
+                                        device, spare_blocks=handoff_blocks, layers=L)
+    q = synth.device_q(SHAPE, BATCH, rank, device, L)
+    case = synth.DeviceShards(SHAPE, lens, ks, [home_t, cold_t], [home_bt, cold_bt], q)
     pools = []
-    for pt, bt in zip(case.pools, case.block_tables):
+    for pt, bt in ((home_t, home_bt), (cold_t, cold_bt)):
         pool = bs.KVPool(L, pt.shape[1], SHAPE.hkv, SHAPE.d, base=pt.reshape(-1))
         # register the placement with the allocator: take everything, return the free ids
         pool.alloc(pool.num_blocks)
         used = set(int(x) for x in bt.ravel() if x >= 0)
         pool.free(sorted(set(range(pool.num_blocks)) - used))
         pools.append(pool)
-    D, P = pools
-    # hand-off requests: their KV sits in P's spare blocks; D allocates destinations
-    src_ids = P.alloc(handoff_blocks)
+    home, cold = pools
+    # hand-off requests: their KV sits in the cold pool's spare blocks; home allocates
+    src_ids = cold.alloc(handoff_blocks)
     assert src_ids == handoff_src_ids(case, handoff_blocks)
-    dst_ids = D.alloc(handoff_blocks)
-    shards = [Shard(pool, torch.from_numpy(bt).to(device), j)
-              for j, (pool, bt) in enumerate(zip(pools, case.block_tables))]
-    job = MigrationJob(P, D, torch.tensor(src_ids, dtype=torch.int32, device=device),
-                       torch.tensor(dst_ids, dtype=torch.int32, device=device))
-    step = LayerwiseDecodeStep(shards, torch.from_numpy(ks).to(device), SHAPE.hq, L,
-                               synth.default_scale(SHAPE.d), migrations=[job], lookahead=1)
-    return case, pools, shards, job, step, ks
+    dst_ids = home.alloc(handoff_blocks)
+    i32 = lambda x: torch.as_tensor(np.asarray(x), dtype=torch.int32).to(device)
+    step = ShardedDecodeStep(
+        CudaOps(synth.default_scale(SHAPE.d)), CudaExec(device), rank, world, home, i32(home_bt),
+        cold, i32(cold_bt), i32(ks), SHAPE.hq, L, SHAPE.d, handoff_src_ids=i32(src_ids),
+        handoff_dst_ids=i32(dst_ids), chunk_bytes=home.chunk_bytes,
+        pg_attn=dist.group.WORLD if world > 1 else None,
+        pg_mig=dist.new_group(list(range(world))) if world > 1 else None,
+        lookahead=1, device=device)
+    return case, pools, step, ks
 
 
 def handoff_src_ids(case, n):
@@ -188,7 +201,7 @@ def run_ours(args, rank, world, device):
     import paper_2510_13223_b200 as bs
 
     torch.cuda.set_device(device)
-    case, pools, shards, job, step, ks = build_workload(bs, device, seed=rank)
+    case, pools, step, ks = build_workload(bs, device, rank, world)
     L = SHAPE.n_layers
     q = case.q
     out = torch.empty((L, BATCH, SHAPE.hq, SHAPE.d), dtype=torch.bfloat16, device=device)
@@ -255,7 +268,7 @@ def run_ours(args, rank, world, device):
 
     # ---- derived numbers ----------------------------------------------------------------
     a_bytes = attn_bytes_per_layer(ks)
-    mig_bytes = job.src_ids.numel() * pools[0].chunk_bytes  # per layer, counted once
+    mig_bytes = step.n_handoff * pools[0].chunk_bytes  # per layer, counted once
     attn_avg_ms = statistics.fmean(attn_ms)
     mig_avg_ms = statistics.fmean(mig_ms)
     attn_gbs = a_bytes / (attn_avg_ms * 1e-3) / 1e9
@@ -280,7 +293,8 @@ def run_ours(args, rank, world, device):
             "workload": WORKLOAD,
             "layers": L, "batch": BATCH, "seq_len": SEQ, "num_q_heads": SHAPE.hq,
             "num_kv_heads": SHAPE.hkv, "head_dim": SHAPE.d, "kv_shards": N_SHARDS,
-            "handoff_requests_per_step": N_HANDOFF, "parallelism": f"replicas{world}" if world > 1 else "1 GPU, 2 virtual instances",
+            "handoff_requests_per_step": N_HANDOFF, "parallelism": (f"ring of {world} instances (home + cold per GPU), NCCL P2P" if world > 1
+                            else "1 GPU, 2 virtual instances"),
             "l2": "no flush: resident pools 70 GiB >> 126 MB L2",
         },
         "attn_hbm_gbs": round(attn_gbs, 1),
@@ -288,7 +302,8 @@ def run_ours(args, rank, world, device):
         "migrate_gbs": round(mig_gbs, 1),
         "migrate_ms_per_layer": round(mig_avg_ms, 5),
         "migrate_bytes_per_layer": mig_bytes,
-        "migrate_transport": "local HBM copy (N=1: both instances on GPU 0; NVLink needs N>=2)",
+        "migrate_transport": ("fused copy kernel, local HBM (N=1: both instances on GPU 0)" if world == 1
+                              else "gather -> NCCL send/recv over NVLink -> scatter"),
         "roofline": {
             "bound": "hbm", "kernel": "split_decode_attn (2 shard launches per layer)",
             "achieved": round(attn_gbs, 1), "peak": peak, "peak_source": peak_src,
@@ -303,7 +318,7 @@ def run_ours(args, rank, world, device):
                 "d2h_bytes_per_step": out.numel() * out.element_size() + lse.numel() * lse.element_size()},
         "clocks": clk.summary(),
     }
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline(case, budget_s=args.cpu_seconds)
     return res
 
@@ -381,8 +396,8 @@ def run_reference(args, rank, world, device):
     case = synth.device_shards(SHAPE, lens, ks, seed=0, device=gen_dev,
                                spare_blocks=N_HANDOFF * handoff_chunks, layers=nl)
     scale = synth.default_scale(SHAPE.d)
-    reqs = 2
-    samples = [oracle_sample(case, [(2 * i) % BATCH, (2 * i + 1) % BATCH], i % nl,
+    reqs = 8
+    samples = [oracle_sample(case, [(reqs * i + r) % BATCH for r in range(reqs)], i % nl,
                              handoff_chunks) for i in range(2)]
     for i in range(args.warmup):
         time_oracle_sample(samples[i % 2], scale)

@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "internal.h"
 #include "ptx.cuh"
@@ -86,14 +87,31 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
 // Sum 16 per-lane partials over the 32 lanes.  Slot i of lane L holds token i ^ (L >> 1)
 // (the K rows are loaded in that lane-permuted order), so every butterfly step keeps the
 // low half of its slots and sends the high half -- no per-lane selects -- and lane pair
-// (2t, 2t+1) ends with token t's total.
+// (2t, 2t+1) ends with token t's total.  Adds are packed (FADD2) on slot pairs.
 __device__ __forceinline__ float reduce_scatter16(float (&v)[16]) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i + 8], 16);
+  for (int i = 0; i < 8; i += 2) {
+    const float2 r = make_float2(__shfl_xor_sync(0xffffffffu, v[i + 8], 16),
+                                 __shfl_xor_sync(0xffffffffu, v[i + 9], 16));
+    const float2 x = __fadd2_rn(make_float2(v[i], v[i + 1]), r);
+    v[i] = x.x;
+    v[i + 1] = x.y;
+  }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i + 4], 8);
-#pragma unroll
-  for (int i = 0; i < 2; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i + 2], 4);
+  for (int i = 0; i < 4; i += 2) {
+    const float2 r = make_float2(__shfl_xor_sync(0xffffffffu, v[i + 4], 8),
+                                 __shfl_xor_sync(0xffffffffu, v[i + 5], 8));
+    const float2 x = __fadd2_rn(make_float2(v[i], v[i + 1]), r);
+    v[i] = x.x;
+    v[i + 1] = x.y;
+  }
+  {
+    const float2 r = make_float2(__shfl_xor_sync(0xffffffffu, v[2], 4),
+                                 __shfl_xor_sync(0xffffffffu, v[3], 4));
+    const float2 x = __fadd2_rn(make_float2(v[0], v[1]), r);
+    v[0] = x.x;
+    v[1] = x.y;
+  }
   v[0] += __shfl_xor_sync(0xffffffffu, v[1], 2);
   return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
@@ -145,34 +163,54 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
     for (int k = 0; k < min(STAGES, nmine); ++k) issue(k);
   }
 
-  // q for the G heads of this group, this lane's dims, pre-scaled into log2 units
-  float2 qv[G][DP2];
+  // q for the G heads of this group, this lane's dims, pre-scaled into log2 units and
+  // duplicated into both halves of a packed pair ({q_e, q_e}) for token-pair FFMA2
+  float2 qq[G][DPL];
   {
     const __nv_bfloat16* qp = p.q + ((int64_t)b * p.hq + g * G) * D + lane * DPL;
 #pragma unroll
     for (int h = 0; h < G; ++h) {
+      float qf[DPL];
       if constexpr (DPL == 4) {
         const uint2 w = *reinterpret_cast<const uint2*>(qp + h * D);
-        float2 a = bf2_to_f2(w.x), c = bf2_to_f2(w.y);
-        qv[h][0] = make_float2(a.x * p.scale_log2, a.y * p.scale_log2);
-        qv[h][1] = make_float2(c.x * p.scale_log2, c.y * p.scale_log2);
+        const float2 a = bf2_to_f2(w.x), c = bf2_to_f2(w.y);
+        qf[0] = a.x; qf[1] = a.y; qf[2] = c.x; qf[3] = c.y;
       } else {
-        const uint32_t w = *reinterpret_cast<const uint32_t*>(qp + h * D);
-        float2 a = bf2_to_f2(w);
-        qv[h][0] = make_float2(a.x * p.scale_log2, a.y * p.scale_log2);
+        const float2 a = bf2_to_f2(*reinterpret_cast<const uint32_t*>(qp + h * D));
+        qf[0] = a.x; qf[1] = a.y;
       }
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) qq[h][e] = make_float2(qf[e] * p.scale_log2, qf[e] * p.scale_log2);
     }
   }
 
+  // running state; acc[h][e] = {sum over even tokens, sum over odd tokens} for dim e
   float m_run[G], l_run[G];
-  float2 acc[G][DP2];
+  float2 acc[G][DPL];
 #pragma unroll
   for (int h = 0; h < G; ++h) {
     m_run[h] = -INFINITY;
     l_run[h] = 0.f;
 #pragma unroll
-    for (int e = 0; e < DP2; ++e) acc[h][e] = make_float2(0.f, 0.f);
+    for (int e = 0; e < DPL; ++e) acc[h][e] = make_float2(0.f, 0.f);
   }
+
+  // two rows (tokens) of a page, this lane's DPL dims -> DPL packed {row0, row1} pairs
+  auto load_pair = [&](const uint8_t* r0, const uint8_t* r1, float2 (&out)[DPL]) {
+    if constexpr (DPL == 4) {
+      const uint2 w0 = *reinterpret_cast<const uint2*>(r0 + lane * 8);
+      const uint2 w1 = *reinterpret_cast<const uint2*>(r1 + lane * 8);
+      out[0] = make_float2(__uint_as_float(w0.x << 16), __uint_as_float(w1.x << 16));
+      out[1] = make_float2(__uint_as_float(w0.x & 0xffff0000u), __uint_as_float(w1.x & 0xffff0000u));
+      out[2] = make_float2(__uint_as_float(w0.y << 16), __uint_as_float(w1.y << 16));
+      out[3] = make_float2(__uint_as_float(w0.y & 0xffff0000u), __uint_as_float(w1.y & 0xffff0000u));
+    } else {
+      const uint32_t w0 = *reinterpret_cast<const uint32_t*>(r0 + lane * 4);
+      const uint32_t w1 = *reinterpret_cast<const uint32_t*>(r1 + lane * 4);
+      out[0] = make_float2(__uint_as_float(w0 << 16), __uint_as_float(w1 << 16));
+      out[1] = make_float2(__uint_as_float(w0 & 0xffff0000u), __uint_as_float(w1 & 0xffff0000u));
+    }
+  };
 
   for (int k = 0; k < nmine; ++k) {
     const int s = k % STAGES;
@@ -183,31 +221,25 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
     const int nvalid = min(16, len - blk * 16);
 
     // ---- scores: s_t = <q_h, k_t> (log2 units) -------------------------------------
-    float2 kf[16][DP2];  // slot i = token i ^ (lane >> 1)
+    // slot i holds token i ^ (lane >> 1) (see reduce_scatter16); slots paired (2j, 2j+1)
+    float2 kp[8][DPL];
     const uint32_t kswz = (uint32_t)((lane >> 1) & 15) * (D * 2);
 #pragma unroll
-    for (int t = 0; t < 16; ++t) {
-      const uint8_t* row = sk + ((uint32_t)(t * D * 2) ^ kswz);
-      if constexpr (DPL == 4) {
-        const uint2 w = *reinterpret_cast<const uint2*>(row + lane * 8);
-        kf[t][0] = bf2_to_f2(w.x);
-        kf[t][1] = bf2_to_f2(w.y);
-      } else {
-        const uint32_t w = *reinterpret_cast<const uint32_t*>(row + lane * 4);
-        kf[t][0] = bf2_to_f2(w);
-      }
-    }
+    for (int j = 0; j < 8; ++j)
+      load_pair(sk + ((uint32_t)(2 * j * D * 2) ^ kswz), sk + ((uint32_t)((2 * j + 1) * D * 2) ^ kswz),
+                kp[j]);
     const bool valid = (lane >> 1) < nvalid;
     float alpha[G];
 #pragma unroll
     for (int h = 0; h < G; ++h) {
       float v[16];
 #pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        float2 a = make_float2(0.f, 0.f);
+      for (int j = 0; j < 8; ++j) {
+        float2 a = __fmul2_rn(qq[h][0], kp[j][0]);
 #pragma unroll
-        for (int e = 0; e < DP2; ++e) a = ffma2(qv[h][e], kf[t][e], a);
-        v[t] = a.x + a.y;
+        for (int e = 1; e < DPL; ++e) a = ffma2(qq[h][e], kp[j][e], a);
+        v[2 * j] = a.x;
+        v[2 * j + 1] = a.y;
       }
       float sc = reduce_scatter16(v);
       sc = valid ? sc : -INFINITY;
@@ -225,39 +257,41 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
     }
     __syncwarp();
 
-    // ---- o = alpha * o + sum_t p_t v_t ----------------------------------------------
+    // ---- o = alpha * o + sum_t p_t v_t  (token pairs: {p_2j, p_2j+1} x {v_2j, v_2j+1})
 #pragma unroll
-    for (int h = 0; h < G; ++h)
+    for (int h = 0; h < G; ++h) {
+      const float2 a2 = make_float2(alpha[h], alpha[h]);
 #pragma unroll
-      for (int e = 0; e < DP2; ++e) acc[h][e] = make_float2(acc[h][e].x * alpha[h], acc[h][e].y * alpha[h]);
+      for (int e = 0; e < DPL; ++e) acc[h][e] = __fmul2_rn(acc[h][e], a2);
+    }
+    auto pv = [&](auto full) {
 #pragma unroll
-    for (int t4 = 0; t4 < 16; t4 += 4) {
-      float4 pp[G];
+      for (int j4 = 0; j4 < 4; ++j4) {  // 4 tokens per float4 of p
+        float4 pp[G];
 #pragma unroll
-      for (int h = 0; h < G; ++h) pp[h] = *reinterpret_cast<const float4*>(s_p + h * 16 + t4);
+        for (int h = 0; h < G; ++h) pp[h] = *reinterpret_cast<const float4*>(s_p + h * 16 + 4 * j4);
 #pragma unroll
-      for (int tt = 0; tt < 4; ++tt) {
-        const int t = t4 + tt;
-        if (t < nvalid) {  // pad slots hold garbage (NaN-poisoned in tests): skip, don't scale
-          float2 vf[DP2];
-          if constexpr (DPL == 4) {
-            const uint2 w = *reinterpret_cast<const uint2*>(sv + t * D * 2 + lane * 8);
-            vf[0] = bf2_to_f2(w.x);
-            vf[1] = bf2_to_f2(w.y);
-          } else {
-            const uint32_t w = *reinterpret_cast<const uint32_t*>(sv + t * D * 2 + lane * 4);
-            vf[0] = bf2_to_f2(w);
+        for (int half = 0; half < 2; ++half) {
+          const int t0 = 4 * j4 + 2 * half;
+          if (!decltype(full)::value && t0 >= nvalid) continue;
+          float2 vp[DPL];
+          load_pair(sv + t0 * D * 2, sv + (t0 + 1) * D * 2, vp);
+          if (!decltype(full)::value && t0 + 1 >= nvalid) {  // odd token is a pad slot
+#pragma unroll
+            for (int e = 0; e < DPL; ++e) vp[e].y = 0.f;
           }
 #pragma unroll
           for (int h = 0; h < G; ++h) {
-            const float pt = tt == 0 ? pp[h].x : tt == 1 ? pp[h].y : tt == 2 ? pp[h].z : pp[h].w;
-            const float2 p2 = make_float2(pt, pt);
+            const float2 p2 = half == 0 ? make_float2(pp[h].x, pp[h].y) : make_float2(pp[h].z, pp[h].w);
 #pragma unroll
-            for (int e = 0; e < DP2; ++e) acc[h][e] = ffma2(p2, vf[e], acc[h][e]);
+            for (int e = 0; e < DPL; ++e) acc[h][e] = ffma2(p2, vp[e], acc[h][e]);
           }
         }
       }
-    }
+    };
+    // pad slots hold garbage (NaN-poisoned in tests): the partial last block masks V too
+    if (nvalid == 16) pv(std::true_type{});
+    else pv(std::false_type{});
     __syncwarp();
     if (lane == 0 && k + STAGES < nmine) {
       ptx::fence_proxy_async_smem();
@@ -285,7 +319,8 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
   for (int h = 0; h < G; ++h) {
 #pragma unroll
     for (int e = 0; e < DP2; ++e)
-      *reinterpret_cast<float2*>(s_acc + (warp * G + h) * D + lane * DPL + 2 * e) = acc[h][e];
+      *reinterpret_cast<float2*>(s_acc + (warp * G + h) * D + lane * DPL + 2 * e) =
+          make_float2(acc[h][2 * e].x + acc[h][2 * e].y, acc[h][2 * e + 1].x + acc[h][2 * e + 1].y);
     if (lane == 0) {
       s_ml[(warp * G + h) * 2] = m_run[h];
       s_ml[(warp * G + h) * 2 + 1] = l_run[h];
@@ -369,9 +404,9 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
 }
 
 // Pipeline depth / residency per (head_dim, group): STAGES blocks (K+V pages) per warp in
-// flight, MINB CTAs per SM.  G <= 2 fits 3 CTAs/SM (registers <= 168) with a 2-deep ring
-// (d=128); G >= 4 needs more registers and keeps 2 CTAs/SM with a 3-deep ring.  Both give
-// ~192 KiB of KV in flight per SM.
+// flight, MINB CTAs per SM.  G <= 4 fits 3 CTAs/SM (registers <= 168) with a 2-deep ring
+// (d=128); G = 8 needs more registers and keeps 2 CTAs/SM with a 3-deep ring.  Both give
+// ~192 KiB of KV in flight per SM.  BS_ATTN_VARIANT=1 forces the 2-CTA/3-deep variant.
 struct Variant {
   int stages, minb;
 };
@@ -386,8 +421,8 @@ int alt_variant() {
 
 Variant variant_for(int d, int G) {
   if (alt_variant() == 1) return d == 128 ? Variant{3, 2} : Variant{6, 2};
-  if (d == 128) return G <= 2 ? Variant{2, 3} : Variant{3, 2};
-  return G <= 2 ? Variant{4, 3} : Variant{6, 2};
+  if (d == 128) return G <= 4 ? Variant{2, 3} : Variant{3, 2};
+  return G <= 4 ? Variant{4, 3} : Variant{6, 2};
 }
 
 struct Plan {

@@ -1,0 +1,251 @@
+"""Multi-instance decode step: attention-level migration across a ring of GPUs.
+
+Rank r is the *home* (decode) instance of its own batch and the *cold* instance of
+rank prev = r-1 (mod N) (Fig. 4: KV2 "offloaded to a cold GPU"):
+
+  home pool  (rank r): shard 0 of r's requests   + free blocks receiving hand-offs
+  cold pool  (rank r): shard 1 of prev's requests + KV being handed off to prev
+
+Per layer l (every exchange is point-to-point, NCCL via torch.distributed on GPUs):
+  migration  : cold pool --gather--> send to prev ; recv from next --scatter--> home pool
+               (H2 two-sided transport; at N=1 the fused copy kernel P -> D)
+  q exchange : send q_l of my requests to next (their cold instance); recv prev's q_l
+               (issued for all layers at the start of the step)
+  attention  : shard 0 of my requests over the home pool               (H4)
+               shard 1 of prev's requests over the cold pool (prev's q) (H4)
+  exchange   : send prev's partial (o~, m, l) to prev; recv mine from next  (H5,
+               PAPER.md:237 "O^(1) (or E^(2)) is sent back")
+  merge      : LSE merge of my two partials -> bf16 O, fp32 lse           (H6)
+Streams: compute, copy (migration, high priority) and comm (q / partial exchange +
+merge), ordered by events; the attention of layer l waits for layer l's migration
+(layer-wise overlap, Fig. 6).  At N=1 the ring closes on itself: no
+exchange, prev = next = self.
+
+The protocol is written against two small interfaces -- ``ops`` (the kernels) and
+``ex`` (streams/events) -- so the identical code runs on GPUs with libbanaserve.so and
+on CPU under gloo in the tests (where ``ops`` is test infrastructure).
+"""
+from __future__ import annotations
+
+import contextlib
+
+import torch
+import torch.distributed as dist
+
+
+class CudaExec:
+    """Streams and events on the current CUDA device."""
+
+    def __init__(self, device):
+        self.device = device
+        self.compute = torch.cuda.Stream(device=device)
+        self.copy = torch.cuda.Stream(device=device, priority=-1)
+        self.comm = torch.cuda.Stream(device=device)
+
+    def use(self, s):
+        return torch.cuda.stream(s)
+
+    def event(self):
+        return torch.cuda.Event()
+
+    def record(self, ev, s):
+        ev.record(s)
+
+    def wait(self, s, ev):
+        s.wait_event(ev)
+
+    def begin(self):
+        cur = torch.cuda.current_stream()
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        for s in (self.compute, self.copy, self.comm):
+            s.wait_event(ev)
+
+    def end(self):
+        cur = torch.cuda.current_stream()
+        for s in (self.compute, self.copy, self.comm):
+            cur.wait_stream(s)
+
+
+class CpuExec:
+    """Sequential execution (gloo tests): streams and events are no-ops."""
+    compute = copy = comm = None
+
+    def use(self, s):
+        return contextlib.nullcontext()
+
+    def event(self):
+        return None
+
+    def record(self, ev, s):
+        pass
+
+    def wait(self, s, ev):
+        pass
+
+    def begin(self):
+        pass
+
+    def end(self):
+        pass
+
+
+class CudaOps:
+    """The kernels: C-ABI calls into libbanaserve.so on the current stream."""
+
+    def __init__(self, scale: float):
+        from . import (kv_gather_layer, kv_migrate_layer, kv_scatter_layer, merge_partials,
+                       split_decode_attention)
+        self._att, self._merge = split_decode_attention, merge_partials
+        self._mig, self._gather, self._scatter = kv_migrate_layer, kv_gather_layer, kv_scatter_layer
+        self.scale = scale
+
+    def attention(self, pool, layer, q, block_tables, kv_split, shard_id, part):
+        o, m, l, ws = part[:4]
+        self._att(pool, layer, q, block_tables, kv_split, shard_id, self.scale, o, m, l, ws)
+
+    def merge(self, parts, out, lse):
+        self._merge([p[0] for p in parts], [p[1] for p in parts], [p[2] for p in parts], out, lse)
+
+    def migrate_local(self, src, dst, layer, src_ids, dst_ids):
+        self._mig(src, dst, layer, src_ids, dst_ids)
+
+    def gather(self, pool, layer, ids, staging):
+        self._gather(pool, layer, ids, staging)
+
+    def scatter(self, pool, layer, ids, staging):
+        self._scatter(pool, layer, ids, staging)
+
+    def partial_buffers(self, pool, batch, hq, head_dim, max_blocks, device):
+        from . import split_decode_attention_workspace_size
+        flat = torch.empty(batch * hq * (head_dim + 2), dtype=torch.float32, device=device)
+        ws_n = split_decode_attention_workspace_size(pool, batch, hq, max_blocks)
+        ws = torch.zeros(max(ws_n, 16), dtype=torch.uint8, device=device)
+        return split_partial(flat, batch, hq, head_dim) + (ws, flat)
+
+
+def split_partial(flat: torch.Tensor, batch: int, hq: int, d: int):
+    """One contiguous fp32 buffer [o (B*Hq*d) | m (B*Hq) | l (B*Hq)] -> (o, m, l) views, so
+    a partial crosses the wire as a single message."""
+    n = batch * hq
+    o = flat[: n * d].view(batch, hq, d)
+    m = flat[n * d: n * d + n].view(batch, hq)
+    l = flat[n * d + n: n * d + 2 * n].view(batch, hq)
+    return o, m, l
+
+
+def _sendrecv(pg, send: torch.Tensor, to: int, recv: torch.Tensor, frm: int):
+    """One grouped send+recv (ring neighbours; symmetric on every rank => no deadlock)."""
+    s = send.reshape(-1).view(torch.uint8)   # bytes on the wire (any dtype, any backend)
+    r = recv.reshape(-1).view(torch.uint8)
+    ops = [dist.P2POp(dist.isend, s, to, group=pg), dist.P2POp(dist.irecv, r, frm, group=pg)]
+    for w in dist.batch_isend_irecv(ops):
+        w.wait()
+
+
+class ShardedDecodeStep:
+    def __init__(self, ops, ex, rank: int, world: int, home_pool, home_bt, cold_pool, cold_bt,
+                 kv_split, num_q_heads: int, num_layers: int, head_dim: int,
+                 handoff_src_ids=None, handoff_dst_ids=None, chunk_bytes: int = 0,
+                 pg_attn=None, pg_mig=None, lookahead: int = 1, device=None):
+        self.ops, self.ex = ops, ex
+        self.rank, self.world = rank, world
+        self.prev, self.next = (rank - 1) % world, (rank + 1) % world
+        self.home, self.home_bt = home_pool, home_bt
+        self.cold, self.cold_bt = cold_pool, cold_bt
+        self.kv_split = kv_split
+        self.L, self.hq, self.d = num_layers, num_q_heads, head_dim
+        self.B = kv_split.shape[0]
+        self.src_ids, self.dst_ids = handoff_src_ids, handoff_dst_ids
+        self.n_handoff = 0 if handoff_src_ids is None else int(handoff_src_ids.numel())
+        self.pg_attn, self.pg_mig = pg_attn, pg_mig
+        self.lookahead = lookahead
+        dev = device
+        mk = lambda pool, bt: ops.partial_buffers(pool, self.B, self.hq, self.d, bt.shape[1], dev)
+        # per-layer partial buffers: the merge of layer l may trail the attention of l+1
+        self.part_own = [mk(home_pool, home_bt) for _ in range(num_layers)]
+        self.part_cold = [mk(cold_pool, cold_bt) for _ in range(num_layers)]
+        self.part_recv = self.part_cold if world == 1 else [
+            self._recv_buffer(p[4]) for p in self.part_cold]
+        self.q_prev = None
+        if world > 1:
+            self.q_prev = None  # allocated lazily with q's shape/dtype
+            nbytes = self.n_handoff * chunk_bytes
+            self.stage_send = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
+            self.stage_recv = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
+        self.ev = {k: [ex.event() for _ in range(num_layers)]
+                   for k in ("mig_done", "layer_start", "q_ready", "part_ready")}
+
+    def _recv_buffer(self, like: torch.Tensor):
+        flat = torch.empty_like(like)
+        return split_partial(flat, self.B, self.hq, self.d) + (None, flat)
+
+    @property
+    def launches_per_step(self) -> int:
+        """Our kernels per step: 2 attention + 1 merge (+ 1 fused copy at N=1, or
+        gather + scatter at N>1, when hand-offs are present) per layer."""
+        mig = 0 if self.n_handoff == 0 else (1 if self.world == 1 else 2)
+        return self.L * (3 + mig)
+
+    def enqueue(self, q: torch.Tensor, out: torch.Tensor, lse: torch.Tensor | None = None,
+                timers=None) -> None:
+        """q [L][B][Hq][d] bf16 of this rank's requests -> out [L][B][Hq][d] bf16 and
+        lse [L][B][Hq] fp32.  ``timers[l]`` = (attn_start, attn_end, mig_start, mig_end)
+        events recorded on the launching streams (CUDA only)."""
+        ex, ops, E = self.ex, self.ops, self.ev
+        if self.world > 1 and (self.q_prev is None or self.q_prev.shape != q.shape):
+            self.q_prev = torch.empty_like(q)
+        ex.begin()
+        if self.world > 1:
+            # q of my requests to their cold instance (next), prev's q from prev: issued
+            # up front in layer order; attention on the cold pool waits per layer
+            with ex.use(ex.comm):
+                for layer in range(self.L):
+                    _sendrecv(self.pg_attn, q[layer], self.next, self.q_prev[layer], self.prev)
+                    ex.record(E["q_ready"][layer], ex.comm)
+        for layer in range(self.L):
+            # ---- H2/H3: migration channel ---------------------------------------------
+            with ex.use(ex.copy):
+                if self.lookahead >= 0 and layer - self.lookahead >= 0:
+                    ex.wait(ex.copy, E["layer_start"][layer - self.lookahead])
+                if timers is not None:
+                    timers[layer][2].record(ex.copy)
+                if self.n_handoff:
+                    if self.world == 1:
+                        ops.migrate_local(self.cold, self.home, layer, self.src_ids, self.dst_ids)
+                    else:
+                        ops.gather(self.cold, layer, self.src_ids, self.stage_send)
+                        _sendrecv(self.pg_mig, self.stage_send, self.prev, self.stage_recv, self.next)
+                        ops.scatter(self.home, layer, self.dst_ids, self.stage_recv)
+                if timers is not None:
+                    timers[layer][3].record(ex.copy)
+                ex.record(E["mig_done"][layer], ex.copy)
+            # ---- H4: attention over both pools -------------------------------------------
+            with ex.use(ex.compute):
+                ex.record(E["layer_start"][layer], ex.compute)
+                ex.wait(ex.compute, E["mig_done"][layer])
+                if timers is not None:
+                    timers[layer][0].record(ex.compute)
+                ops.attention(self.home, layer, q[layer], self.home_bt, self.kv_split, 0,
+                              self.part_own[layer])
+                if self.world > 1:
+                    ex.wait(ex.compute, E["q_ready"][layer])
+                qc = q[layer] if self.world == 1 else self.q_prev[layer]
+                ops.attention(self.cold, layer, qc, self.cold_bt, self.kv_split, 1,
+                              self.part_cold[layer])
+                if timers is not None:
+                    timers[layer][1].record(ex.compute)
+                ex.record(E["part_ready"][layer], ex.compute)
+            # ---- H5 exchange + H6 merge -------------------------------------------------
+            if self.world == 1:
+                with ex.use(ex.compute):
+                    ops.merge([self.part_own[layer], self.part_cold[layer]], out[layer],
+                              None if lse is None else lse[layer])
+            else:
+                with ex.use(ex.comm):
+                    ex.wait(ex.comm, E["part_ready"][layer])
+                    _sendrecv(self.pg_attn, self.part_cold[layer][4], self.prev,
+                              self.part_recv[layer][4], self.next)
+                    ops.merge([self.part_own[layer], self.part_recv[layer]], out[layer],
+                              None if lse is None else lse[layer])
+        ex.end()

@@ -236,37 +236,58 @@ class DeviceShards:
     q: "torch.Tensor"
 
 
-def device_shards(shape: Shape, seq_lens, kv_split: np.ndarray, seed: int, device,
-                  spare_blocks: int = 0, layers: int | None = None) -> DeviceShards:
-    """Seeded N(0,1) bf16 K/V (+ per-channel V bias) and q generated on ``device`` with a
-    torch CUDA generator; block placement from a seeded CPU permutation (fragmented
-    pool).  Pad slots keep their random values (attention must mask them)."""
+def device_pool(shape: Shape, shard_lens, seed: int, device, spare_blocks: int = 0,
+                layers: int | None = None):
+    """One paged pool holding one shard of every request (shard-local token order):
+    seeded N(0,1) bf16 K, N(0,1) + per-channel bias V, generated on ``device`` with a torch
+    generator; block placement from a seeded CPU permutation (a fragmented pool).  Pad
+    slots keep random values (attention must mask them).  Returns (pool, block_table)."""
     L = shape.n_layers if layers is None else layers
     gd = torch.Generator(device=device)
     gd.manual_seed(int(seed))
-    gc = _gen(seed + 104729)
+    gc = _gen(int(seed) + 104729)
+    lens = np.asarray(shard_lens, dtype=np.int64)
+    B = len(lens)
+    nblk = [ceil_div(int(x), shape.bs) for x in lens]
+    nb = max(int(sum(nblk)) + spare_blocks, 1)
+    perm = torch.randperm(nb, generator=gc).numpy()
+    pool = torch.randn((L, nb, 2, shape.hkv, shape.bs, shape.d), generator=gd, device=device,
+                       dtype=torch.bfloat16)
+    bias = (torch.rand((L, shape.hkv, 1, shape.d), generator=gd, device=device) * 2 - 1)
+    pool[:, :, 1] += bias.to(torch.bfloat16)[:, None]
+    bt = np.full((B, max(1, max(nblk) if nblk else 1)), -1, dtype=np.int32)
+    nxt = 0
+    for b in range(B):
+        bt[b, :nblk[b]] = perm[nxt:nxt + nblk[b]]
+        nxt += nblk[b]
+    return pool, bt
+
+
+def device_q(shape: Shape, batch: int, seed: int, device, layers: int | None = None):
+    L = shape.n_layers if layers is None else layers
+    gd = torch.Generator(device=device)
+    gd.manual_seed(int(seed) * 7919 + 17)
+    return torch.randn((L, batch, shape.hq, shape.d), generator=gd, device=device,
+                       dtype=torch.bfloat16)
+
+
+def shard_seed(request_seed: int, shard: int) -> int:
+    return int(request_seed) * 1000 + int(shard) + 1
+
+
+def device_shards(shape: Shape, seq_lens, kv_split: np.ndarray, seed: int, device,
+                  spare_blocks: int = 0, layers: int | None = None) -> DeviceShards:
+    """Full-size case generated directly in device memory: one pool per shard
+    (``device_pool`` with seed ``shard_seed(seed, j)``) and q (``device_q``)."""
     B = len(seq_lens)
     n = kv_split.shape[1] - 1
     pools, bts = [], []
     for j in range(n):
         lens = (kv_split[:, j + 1] - kv_split[:, j]).astype(np.int64)
-        nblk = [ceil_div(int(x), shape.bs) for x in lens]
-        nb = int(sum(nblk)) + spare_blocks
-        nb = max(nb, 1)
-        perm = torch.randperm(nb, generator=gc).numpy()
-        pool = torch.randn((L, nb, 2, shape.hkv, shape.bs, shape.d), generator=gd, device=device,
-                           dtype=torch.bfloat16)
-        bias = (torch.rand((L, shape.hkv, 1, shape.d), generator=gd, device=device) * 2 - 1)
-        pool[:, :, 1] += bias.to(torch.bfloat16)[:, None]
-        mb = max(1, max(nblk))
-        bt = np.full((B, mb), -1, dtype=np.int32)
-        nxt = 0
-        for b in range(B):
-            bt[b, :nblk[b]] = perm[nxt:nxt + nblk[b]]
-            nxt += nblk[b]
+        pool, bt = device_pool(shape, lens, shard_seed(seed, j), device, spare_blocks, layers)
         pools.append(pool)
         bts.append(bt)
-    q = torch.randn((L, B, shape.hq, shape.d), generator=gd, device=device, dtype=torch.bfloat16)
+    q = device_q(shape, B, seed, device, layers)
     return DeviceShards(shape, np.asarray(seq_lens), kv_split, pools, bts, q)
 
 

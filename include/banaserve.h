@@ -163,6 +163,52 @@ bs_status bs_merge_partials(int32_t n_parts, const float* const* o_parts,
                             int32_t batch, int32_t num_q_heads, int32_t head_dim, void* out,
                             float* lse_out, void* stream);
 
+/* ------------------------------------------------------------------------------ */
+/* Cross-instance transports (reading D6; PAPER.md:197 names NVLink / InfiniBand).   */
+/*                                                                                  */
+/* (a) Two-sided NCCL (resolved at run time: dlopen "libnccl.so.2" or               */
+/*     $BS_NCCL_LIBRARY; without NCCL these return BS_ERR_NCCL).  A bs_comm wraps an */
+/*     ncclComm_t built from a unique id the harness broadcasts.  Every call is     */
+/*     enqueued on `stream`; send/recv pairs must be issued in the same order on    */
+/*     both peers (NCCL rules).  A peer may be the caller itself (loopback).        */
+/* ------------------------------------------------------------------------------ */
+typedef struct bs_comm bs_comm;
+
+/* Size of an NCCL unique id (128). */
+size_t bs_nccl_unique_id_bytes(void);
+/* Rank 0 creates the id into `out` (host, bs_nccl_unique_id_bytes bytes). */
+bs_status bs_nccl_get_unique_id(void* out);
+/* Collective over the nranks processes; the current CUDA device is this rank's GPU. */
+bs_status bs_comm_init(const void* nccl_unique_id, int32_t nranks, int32_t rank, bs_comm** out);
+bs_status bs_comm_destroy(bs_comm* comm);
+/* One grouped ncclSend(sendbuf -> send_peer) + ncclRecv(recvbuf <- recv_peer) of raw
+ * bytes (DEVICE buffers).  A negative peer or zero size skips that half.  This is the
+ * H5 partial exchange: a partial is one contiguous fp32 buffer [o~ | m | l]. */
+bs_status bs_sendrecv(bs_comm* comm, const void* sendbuf, size_t send_bytes, int32_t send_peer,
+                      void* recvbuf, size_t recv_bytes, int32_t recv_peer, void* stream);
+/* H2 over NCCL: gather chunk(layer, src_ids[i]) into staging (n * chunk bytes, DEVICE)
+ * and send it to `peer`; the peer's bs_kv_recv_layer receives into its staging and
+ * scatters to chunk(layer, dst_ids[i]).  Bit-exact, same pair order on both sides. */
+bs_status bs_kv_send_layer(const bs_kv_pool* src, int32_t layer, const int32_t* src_ids, int32_t n,
+                           int32_t peer, bs_comm* comm, void* staging, void* stream);
+bs_status bs_kv_recv_layer(bs_kv_pool* dst, int32_t layer, const int32_t* dst_ids, int32_t n,
+                           int32_t peer, bs_comm* comm, void* staging, void* stream);
+/* Both halves in one NCCL group (ring neighbours: send to one peer, receive from
+ * another without deadlock).  n_send or n_recv may be 0. */
+bs_status bs_kv_sendrecv_layer(bs_comm* comm, const bs_kv_pool* src, const int32_t* src_ids,
+                               int32_t n_send, int32_t send_peer, void* send_staging,
+                               bs_kv_pool* dst, const int32_t* dst_ids, int32_t n_recv,
+                               int32_t recv_peer, void* recv_staging, int32_t layer, void* stream);
+
+/* (b) CUDA IPC: export a device pointer (possibly interior to an allocation) as a
+ * handle + offset; another process imports it as a device pointer usable as the `base`
+ * of a remote-view pool, so bs_kv_migrate_layer pushes chunks over NVLink (P2P push).
+ * handle: host buffer of bs_ipc_handle_bytes() bytes.  bs_ipc_close undoes an import. */
+size_t bs_ipc_handle_bytes(void);
+bs_status bs_ipc_export(const void* dev_ptr, void* handle_out, size_t* offset_out);
+bs_status bs_ipc_import(const void* handle, size_t offset, void** dev_ptr_out);
+bs_status bs_ipc_close(void* dev_ptr, size_t offset);
+
 #ifdef __cplusplus
 }
 #endif

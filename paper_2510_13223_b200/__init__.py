@@ -29,7 +29,10 @@ EXPORTED_SYMBOLS = (
     "bs_kv_pool_create", "bs_kv_pool_destroy", "bs_kv_pool_alloc", "bs_kv_pool_free",
     "bs_kv_pool_num_free", "bs_kv_migrate_layer", "bs_kv_migrate_layer_ex",
     "bs_kv_gather_layer", "bs_kv_scatter_layer", "bs_split_decode_attention_workspace_size",
-    "bs_split_decode_attention", "bs_merge_partials",
+    "bs_split_decode_attention", "bs_merge_partials", "bs_nccl_unique_id_bytes",
+    "bs_nccl_get_unique_id", "bs_comm_init", "bs_comm_destroy", "bs_sendrecv", "bs_kv_send_layer",
+    "bs_kv_recv_layer", "bs_kv_sendrecv_layer", "bs_ipc_handle_bytes", "bs_ipc_export",
+    "bs_ipc_import", "bs_ipc_close",
 )
 
 
@@ -83,6 +86,18 @@ def lib():
         "bs_split_decode_attention": ([_p, _i32, _p, _i32, _i32, _p, _i32, _p, _i32, _i32, _f32,
                                        _p, _p, _p, _p, _sz, _p], _i32),
         "bs_merge_partials": ([_i32, _p, _p, _p, _i32, _i32, _i32, _p, _p, _p], _i32),
+        "bs_nccl_unique_id_bytes": ([], _sz),
+        "bs_nccl_get_unique_id": ([_p], _i32),
+        "bs_comm_init": ([_p, _i32, _i32, ctypes.POINTER(_p)], _i32),
+        "bs_comm_destroy": ([_p], _i32),
+        "bs_sendrecv": ([_p, _p, _sz, _i32, _p, _sz, _i32, _p], _i32),
+        "bs_kv_send_layer": ([_p, _i32, _p, _i32, _i32, _p, _p, _p], _i32),
+        "bs_kv_recv_layer": ([_p, _i32, _p, _i32, _i32, _p, _p, _p], _i32),
+        "bs_kv_sendrecv_layer": ([_p, _p, _p, _i32, _i32, _p, _p, _p, _i32, _i32, _p, _i32, _p], _i32),
+        "bs_ipc_handle_bytes": ([], _sz),
+        "bs_ipc_export": ([_p, _p, ctypes.POINTER(_sz)], _i32),
+        "bs_ipc_import": ([_p, _sz, ctypes.POINTER(_p)], _i32),
+        "bs_ipc_close": ([_p, _sz], _i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -235,3 +250,80 @@ def merge_partials(o_parts, m_parts, l_parts, out: torch.Tensor, lse: torch.Tens
     _check(lib().bs_merge_partials(n, o_arr, m_arr, l_arr, B, hq, d, _dptr(out, torch.bfloat16),
                                    _dptr(lse, torch.float32) if lse is not None else None,
                                    _stream(stream)))
+
+
+# ---------------------------------------------------------------------------------------
+# transports: NCCL (two-sided) and CUDA IPC (peer-mapped remote views for P2P push)
+# ---------------------------------------------------------------------------------------
+
+class Comm:
+    """NCCL communicator owned by the library (``bs_comm``).  ``unique_id`` (bytes) is
+    created by rank 0 with :func:`nccl_unique_id` and broadcast by the harness."""
+
+    def __init__(self, unique_id: bytes, nranks: int, rank: int):
+        h = _p()
+        buf = ctypes.create_string_buffer(unique_id, len(unique_id))
+        _check(lib().bs_comm_init(buf, nranks, rank, ctypes.byref(h)))
+        self.handle, self.nranks, self.rank = h, nranks, rank
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().bs_comm_destroy(self.handle)
+            self.handle = None
+
+    def sendrecv(self, send: torch.Tensor | None, send_peer: int, recv: torch.Tensor | None,
+                 recv_peer: int, stream=None) -> None:
+        sb = 0 if send is None else send.numel() * send.element_size()
+        rb = 0 if recv is None else recv.numel() * recv.element_size()
+        _check(lib().bs_sendrecv(self.handle, _dptr(send), sb, send_peer if send is not None else -1,
+                                 _dptr(recv), rb, recv_peer if recv is not None else -1,
+                                 _stream(stream)))
+
+
+def nccl_unique_id() -> bytes:
+    n = lib().bs_nccl_unique_id_bytes()
+    buf = ctypes.create_string_buffer(n)
+    _check(lib().bs_nccl_get_unique_id(buf))
+    return buf.raw
+
+
+def kv_send_layer(src: KVPool, layer: int, ids: torch.Tensor, peer: int, comm: Comm,
+                  staging: torch.Tensor, stream=None) -> None:
+    _check(lib().bs_kv_send_layer(src.handle, layer, _dptr(ids, torch.int32), ids.numel(), peer,
+                                  comm.handle, _dptr(staging), _stream(stream)))
+
+
+def kv_recv_layer(dst: KVPool, layer: int, ids: torch.Tensor, peer: int, comm: Comm,
+                  staging: torch.Tensor, stream=None) -> None:
+    _check(lib().bs_kv_recv_layer(dst.handle, layer, _dptr(ids, torch.int32), ids.numel(), peer,
+                                  comm.handle, _dptr(staging), _stream(stream)))
+
+
+def kv_sendrecv_layer(comm: Comm, src: KVPool, src_ids: torch.Tensor, send_peer: int,
+                      send_staging: torch.Tensor, dst: KVPool, dst_ids: torch.Tensor,
+                      recv_peer: int, recv_staging: torch.Tensor, layer: int, stream=None) -> None:
+    _check(lib().bs_kv_sendrecv_layer(
+        comm.handle, src.handle, _dptr(src_ids, torch.int32), src_ids.numel(), send_peer,
+        _dptr(send_staging), dst.handle, _dptr(dst_ids, torch.int32), dst_ids.numel(), recv_peer,
+        _dptr(recv_staging), layer, _stream(stream)))
+
+
+def ipc_export(t: torch.Tensor):
+    """(handle bytes, offset) naming ``t``'s device memory for another process."""
+    n = lib().bs_ipc_handle_bytes()
+    buf = ctypes.create_string_buffer(n)
+    off = _sz()
+    _check(lib().bs_ipc_export(_dptr(t), buf, ctypes.byref(off)))
+    return buf.raw, off.value
+
+
+def ipc_import(handle: bytes, offset: int) -> int:
+    """Device address (int) of an exported allocation + offset, mapped in this process."""
+    out = _p()
+    buf = ctypes.create_string_buffer(handle, len(handle))
+    _check(lib().bs_ipc_import(buf, offset, ctypes.byref(out)))
+    return out.value
+
+
+def ipc_close(ptr: int, offset: int) -> None:
+    _check(lib().bs_ipc_close(ptr, offset))

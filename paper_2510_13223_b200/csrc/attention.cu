@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
   if (lane == 0) {
     for (int k = 0; k < min(STAGES, nmine); ++k) issue(k);
   }
+  __syncwarp();
 
   // q for the G heads of this group, this lane's dims, pre-scaled into log2 units and
   // duplicated into both halves of a packed pair ({q_e, q_e}) for token-pair FFMA2
@@ -215,6 +216,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
   for (int k = 0; k < nmine; ++k) {
     const int s = k % STAGES;
     ptx::mbar_wait(&bars[s], (uint32_t)((k / STAGES) & 1));
+    __syncwarp();
     const uint8_t* sk = ring + s * S::kStage;
     const uint8_t* sv = sk + S::kPage;
     const int blk = blo + warp + k * kWarps;  // block index within the shard
@@ -297,6 +299,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
       ptx::fence_proxy_async_smem();
       issue(k + STAGES);
     }
+    __syncwarp();
   }
 
   // ---- merge the 4 warp states in shared memory ------------------------------------

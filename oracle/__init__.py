@@ -66,6 +66,9 @@ def lib():
         L.or_pool_free.restype = _i32
         L.or_migrate_layer.argtypes = [_p, _i32, _p, _i32, _i32, _i32, _i32, _i32, _p, _p, _i32]
         L.or_migrate_layer.restype = None
+        L.or_migrate_heads_layer.argtypes = [_p, _i32, _i32, _p, _i32, _i32, _i32, _i32, _i32, _p,
+                                             _p, _i32, _i32, _i32, _i32]
+        L.or_migrate_heads_layer.restype = None
         L.or_attention_shard.argtypes = [_p, _i32, _i32, _i32, _i32, _i32, _p, _i32, _i32, _p,
                                          _i32, _p, _i32, _i32, _f32, _p, _p, _p]
         L.or_attention_shard.restype = None
@@ -156,6 +159,23 @@ def migrate_layer(src_pool: np.ndarray, dst_pool: np.ndarray, layer: int, src_id
         return
     lib().or_migrate_layer(_ptr(src_pool), nbs, _ptr(dst_pool), dst_pool.shape[1], hkv, bs, d,
                            layer, _ptr(s), _ptr(t), int(s.size))
+
+
+def migrate_heads_layer(src_pool: np.ndarray, dst_pool: np.ndarray, layer: int, src_ids, dst_ids,
+                        src_head_lo: int, dst_head_lo: int, n_heads: int) -> None:
+    """NEXT F2: K/V pages of n_heads kv-heads, in place on dst_pool."""
+    assert src_pool.dtype == np.uint16 and dst_pool.dtype == np.uint16
+    _, nbs, _, shkv, bs, d = src_pool.shape
+    _, nbd, _, dhkv, bs2, d2 = dst_pool.shape
+    assert (bs, d) == (bs2, d2)
+    assert 0 <= src_head_lo and src_head_lo + n_heads <= shkv
+    assert 0 <= dst_head_lo and dst_head_lo + n_heads <= dhkv
+    s = _c(src_ids, np.int32)
+    t = _c(dst_ids, np.int32)
+    if s.size == 0:
+        return
+    lib().or_migrate_heads_layer(_ptr(src_pool), nbs, shkv, _ptr(dst_pool), nbd, dhkv, bs, d, layer,
+                                 _ptr(s), _ptr(t), int(s.size), src_head_lo, dst_head_lo, n_heads)
 
 
 # --- H4 attention over one shard -------------------------------------------------------

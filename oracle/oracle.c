@@ -21,6 +21,9 @@
  *   or_chained_two_shard         -> equals dense attention and the LSE merge       [pinned]
  *   or_migrate_layer             -> byte identity through block tables, sentinel
  *                                   preservation outside dst ids                   [pinned]
+ *   or_migrate_heads_layer       -> page identity, untouched heads/blocks, head-
+ *                                   split attention == full-pool heads; concat of
+ *                                   the head groups == torch SDPA (NEXT F2)        [pinned]
  *   or_pool_alloc / or_pool_free -> brute-force enumeration of the stated policy
  *                                   (R-A12 is a policy choice: "parity unpinned"
  *                                   for the choice itself, pinned for the policy)
@@ -150,6 +153,33 @@ void or_migrate_layer(const uint16_t* src_pool, int32_t src_blocks, uint16_t* ds
     uint16_t* t = dst_pool + ((int64_t)layer * dst_blocks + dst_ids[i]) * chunk;
     memcpy(t, s, (size_t)chunk * sizeof(uint16_t));
   }
+}
+
+/* ------------------------------------------------------------------------- */
+/* NEXT F2: head-granular attention-level migration -- the paper's literal text: */
+/* "partition the KV Cache along the attention head dimension and selectively  */
+/* migrate only the KV states of certain heads" (Alg. 1 */
+/* MigrateKVHeads, :411).  For every pair i, both K and V pages of kv-heads     */
+/* [src_head_lo, src_head_lo + n_heads) of block src_ids[i] go to heads         */
+/* [dst_head_lo, ...) of block dst_ids[i]; pools may have different Hkv (the    */
+/* cold pool keeps only the migrated heads).                                    */
+/* ------------------------------------------------------------------------- */
+
+void or_migrate_heads_layer(const uint16_t* src_pool, int32_t src_blocks, int32_t src_hkv,
+                            uint16_t* dst_pool, int32_t dst_blocks, int32_t dst_hkv, int32_t bs,
+                            int32_t d, int32_t layer, const int32_t* src_ids,
+                            const int32_t* dst_ids, int32_t n, int32_t src_head_lo,
+                            int32_t dst_head_lo, int32_t n_heads) {
+  const int64_t page = (int64_t)bs * d;
+  for (int32_t i = 0; i < n; ++i)
+    for (int32_t kv = 0; kv < 2; ++kv)
+      for (int32_t h = 0; h < n_heads; ++h) {
+        const uint16_t* s =
+            src_pool + elem_index(src_blocks, src_hkv, bs, d, layer, src_ids[i], kv, src_head_lo + h, 0, 0);
+        uint16_t* t =
+            dst_pool + elem_index(dst_blocks, dst_hkv, bs, d, layer, dst_ids[i], kv, dst_head_lo + h, 0, 0);
+        memcpy(t, s, (size_t)page * sizeof(uint16_t));
+      }
 }
 
 /* ------------------------------------------------------------------------- */

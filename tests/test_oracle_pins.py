@@ -311,3 +311,36 @@ def test_toy_brute_force_all_aligned_two_way_splits():
         if count >= 120:
             break
     assert count >= 100
+
+
+# ---------------------------------------------------------------------------- NEXT F2
+
+def test_migrate_heads_pages_and_head_split_attention():
+    """Head-granular migration: moved pages are byte-identical, other
+    heads and blocks keep their sentinel, and attention for the migrated kv-heads read
+    from the compact cold pool equals the same heads read from the full pool (eq. 5);
+    concatenating the two head groups reproduces full attention (torch SDPA)."""
+    shape = synth.Shape(1, 8, 4, 64)                      # G = 2
+    lens = (37, 70)
+    dense, ks, shards = unsplit_case(shape, lens, seed=12)
+    home = shards[0]
+    c0, nh = 3, 1                                         # migrate kv-head 3 only
+    nb = home.pool.shape[1]
+    cold = np.full((1, nb, 2, nh, 16, 64), synth.DST_SENTINEL, dtype=np.uint16)
+    ids = np.array([x for x in home.block_tables.ravel() if x >= 0], dtype=np.int32)
+    oracle.migrate_heads_layer(home.pool, cold, 0, ids, ids, c0, 0, nh)
+    for x in range(nb):
+        if x in set(ids.tolist()):
+            assert np.array_equal(cold[0, x, :, 0], home.pool[0, x, :, c0])
+        else:
+            assert np.all(cold[0, x] == synth.DST_SENTINEL)
+    sc = synth.default_scale(64)
+    o_full, m_full, l_full = oracle.attention_shard(home.pool, 0, dense.q[0], home.block_tables, ks, 0, sc)
+    G = 2
+    q_cold = np.ascontiguousarray(dense.q[0][:, c0 * G:(c0 + nh) * G])
+    o_c, m_c, l_c = oracle.attention_shard(cold, 0, q_cold, home.block_tables, ks, 0, sc)
+    assert np.array_equal(o_c, o_full[:, c0 * G:(c0 + nh) * G])
+    assert np.array_equal(m_c, m_full[:, c0 * G:(c0 + nh) * G])
+    ref, _ = sdpa_reference(dense, 0, sc)
+    cat = np.concatenate([o_full[:, :c0 * G], o_c], axis=1)   # merge = concat for a head split
+    assert np.abs(cat - ref).max() < 1e-12

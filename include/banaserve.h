@@ -41,6 +41,9 @@ typedef enum {
 } bs_status;
 
 enum { BS_DTYPE_BF16 = 0 };
+/* bs_kv_pool_desc.device value for a host-tier pool (page-locked, UVA-mapped host
+ * memory: the Global KV Cache Store's CPU tier, Fig. 5). */
+#define BS_DEVICE_HOST (-1)
 
 /* Thread-local text for the most recent non-OK status on this thread. */
 const char* bs_last_error(void);
@@ -65,7 +68,8 @@ typedef struct {
   int32_t num_kv_heads;  /* Hkv >= 1                                  */
   int32_t head_dim;      /* 64 or 128                                 */
   int32_t dtype;         /* BS_DTYPE_BF16                             */
-  int32_t device;        /* CUDA ordinal that owns the memory         */
+  int32_t device;        /* CUDA ordinal that owns the memory, or     */
+                         /* BS_DEVICE_HOST for a host-tier pool       */
 } bs_kv_pool_desc;
 
 typedef struct bs_kv_pool bs_kv_pool; /* opaque host handle */
@@ -77,7 +81,10 @@ size_t bs_kv_chunk_bytes(const bs_kv_pool_desc* desc);
 
 /* Describe caller-owned device memory `base` (>= bs_kv_pool_bytes, 256-B aligned) as a
  * pool.  All blocks start free.  `base` may be a peer-mapped pointer to another GPU's
- * pool (a "remote view"): migrate calls then write over NVLink (P2P push). */
+ * pool (a "remote view"): migrate calls then write over NVLink (P2P push).  With
+ * device = BS_DEVICE_HOST, `base` is page-locked host memory (cudaHostAlloc / torch
+ * pin_memory): migrate / gather / scatter to or from it are the store's fetch (HtoD)
+ * and store (DtoH) legs, done by a few CTAs over PCIe; attention never reads it. */
 bs_status bs_kv_pool_create(const bs_kv_pool_desc* desc, void* base, bs_kv_pool** out);
 /* Free the host handle (never the device memory). NULL is a no-op. */
 bs_status bs_kv_pool_destroy(bs_kv_pool* pool);
@@ -111,6 +118,14 @@ bs_status bs_kv_migrate_layer(const bs_kv_pool* src, bs_kv_pool* dst, int32_t la
 bs_status bs_kv_migrate_layer_ex(const bs_kv_pool* src, bs_kv_pool* dst, int32_t layer,
                                  const int32_t* src_ids, const int32_t* dst_ids, int32_t n,
                                  int32_t method, void* stream);
+
+/* Copy-engine variant (DMA, no SM time -- for the host tier's fetch / store legs, which
+ * should not compete with attention for SMs): HOST int32 id arrays (validated), runs of
+ * consecutive ids coalesced, one cudaMemcpyBatchAsync per call on a non-NULL stream
+ * (per-copy cudaMemcpyAsync otherwise).  Same semantics as bs_kv_migrate_layer. */
+bs_status bs_kv_migrate_layer_ce(const bs_kv_pool* src, bs_kv_pool* dst, int32_t layer,
+                                 const int32_t* src_ids, const int32_t* dst_ids, int32_t n,
+                                 void* stream);
 
 /* Two-sided transport halves (pack / unpack), for a send/recv transport (NCCL) that
  * moves one contiguous staging buffer per layer: staging[i] = chunk(layer, ids[i]).
@@ -149,6 +164,41 @@ bs_status bs_split_decode_attention(const bs_kv_pool* pool, int32_t layer, const
                                     const int32_t* kv_split, int32_t n_shards, int32_t shard_id,
                                     float scale, float* o_part, float* m, float* l,
                                     void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------ */
+/* NEXT F2: head-granular attention-level migration -- the paper's literal text       */
+/* ("partition the KV Cache along the attention head dimension and selectively      */
+/* migrate only the KV states of certain heads"; Alg. 1      */
+/* MigrateKVHeads).  For every pair i, the K and V pages of kv-heads   */
+/* [src_head_lo, src_head_lo+n_heads) of chunk(layer, src_ids[i]) are copied to      */
+/* heads [dst_head_lo, ...) of chunk(layer, dst_ids[i]).  The pools must agree on    */
+/* num_layers / head_dim and may differ in num_kv_heads (a cold pool can hold just   */
+/* the migrated heads).  Bit-exact; ids are DEVICE int32 [n].                        */
+/* ------------------------------------------------------------------------------ */
+bs_status bs_kv_migrate_heads_layer(const bs_kv_pool* src, bs_kv_pool* dst, int32_t layer,
+                                    const int32_t* src_ids, const int32_t* dst_ids, int32_t n,
+                                    int32_t src_head_lo, int32_t dst_head_lo, int32_t n_heads,
+                                    void* stream);
+/* H4 restricted to n_kv_heads kv-heads: pool heads [pool_head_lo, +n) are the model's
+ * kv-heads [model_head_lo, +n); G = num_q_heads / num_kv_heads_total.  q, o_part, m, l
+ * keep the MODEL's full layouts ([batch][num_q_heads]...): only the rows of q-heads
+ * [model_head_lo*G, (model_head_lo+n)*G) are read / written, so the home and the cold
+ * instance write disjoint rows of one buffer and the head-split "merge" is a concat.
+ * Everything else as bs_split_decode_attention. */
+bs_status bs_split_decode_attention_heads_workspace_size(const bs_kv_pool* pool, int32_t batch,
+                                                         int32_t n_kv_heads,
+                                                         int32_t num_kv_heads_total,
+                                                         int32_t num_q_heads, int32_t max_blocks,
+                                                         size_t* bytes);
+bs_status bs_split_decode_attention_heads(const bs_kv_pool* pool, int32_t layer,
+                                          int32_t pool_head_lo, int32_t model_head_lo,
+                                          int32_t n_kv_heads, int32_t num_kv_heads_total,
+                                          const void* q, int32_t batch, int32_t num_q_heads,
+                                          const int32_t* block_tables, int32_t max_blocks,
+                                          const int32_t* kv_split, int32_t n_shards,
+                                          int32_t shard_id, float scale, float* o_part, float* m,
+                                          float* l, void* workspace, size_t workspace_bytes,
+                                          void* stream);
 
 /* ------------------------------------------------------------------------------ */
 /* H6: exact LSE merge of n shard partials (eq. 10, R-A4, R-A14):   */

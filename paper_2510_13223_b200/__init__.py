@@ -27,12 +27,13 @@ BS_OK, BS_ERR_INVALID_ARG, BS_ERR_OUT_OF_BLOCKS, BS_ERR_UNSUPPORTED, BS_ERR_CUDA
 EXPORTED_SYMBOLS = (
     "bs_last_error", "bs_abi_version", "bs_kv_pool_bytes", "bs_kv_chunk_bytes",
     "bs_kv_pool_create", "bs_kv_pool_destroy", "bs_kv_pool_alloc", "bs_kv_pool_free",
-    "bs_kv_pool_num_free", "bs_kv_migrate_layer", "bs_kv_migrate_layer_ex",
+    "bs_kv_pool_num_free", "bs_kv_migrate_layer", "bs_kv_migrate_layer_ex", "bs_kv_migrate_layer_ce",
     "bs_kv_gather_layer", "bs_kv_scatter_layer", "bs_split_decode_attention_workspace_size",
     "bs_split_decode_attention", "bs_merge_partials", "bs_nccl_unique_id_bytes",
     "bs_nccl_get_unique_id", "bs_comm_init", "bs_comm_destroy", "bs_sendrecv", "bs_kv_send_layer",
     "bs_kv_recv_layer", "bs_kv_sendrecv_layer", "bs_ipc_handle_bytes", "bs_ipc_export",
-    "bs_ipc_import", "bs_ipc_close",
+    "bs_ipc_import", "bs_ipc_close", "bs_kv_migrate_heads_layer",
+    "bs_split_decode_attention_heads_workspace_size", "bs_split_decode_attention_heads",
 )
 
 
@@ -80,6 +81,7 @@ def lib():
         "bs_kv_pool_num_free": ([_p], _i32),
         "bs_kv_migrate_layer": ([_p, _p, _i32, _p, _p, _i32, _p], _i32),
         "bs_kv_migrate_layer_ex": ([_p, _p, _i32, _p, _p, _i32, _i32, _p], _i32),
+        "bs_kv_migrate_layer_ce": ([_p, _p, _i32, _p, _p, _i32, _p], _i32),
         "bs_kv_gather_layer": ([_p, _i32, _p, _i32, _p, _p], _i32),
         "bs_kv_scatter_layer": ([_p, _i32, _p, _i32, _p, _p], _i32),
         "bs_split_decode_attention_workspace_size": ([_p, _i32, _i32, _i32, ctypes.POINTER(_sz)], _i32),
@@ -98,6 +100,12 @@ def lib():
         "bs_ipc_export": ([_p, _p, ctypes.POINTER(_sz)], _i32),
         "bs_ipc_import": ([_p, _sz, ctypes.POINTER(_p)], _i32),
         "bs_ipc_close": ([_p, _sz], _i32),
+        "bs_kv_migrate_heads_layer": ([_p, _p, _i32, _p, _p, _i32, _i32, _i32, _i32, _p], _i32),
+        "bs_split_decode_attention_heads_workspace_size": ([_p, _i32, _i32, _i32, _i32, _i32,
+                                                            ctypes.POINTER(_sz)], _i32),
+        "bs_split_decode_attention_heads": ([_p, _i32, _i32, _i32, _i32, _i32, _p, _i32, _i32, _p,
+                                             _i32, _p, _i32, _i32, _f32, _p, _p, _p, _p, _sz, _p],
+                                            _i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -140,23 +148,36 @@ class KVPool:
     """
 
     def __init__(self, num_layers: int, num_blocks: int, num_kv_heads: int, head_dim: int,
-                 device=None, base: torch.Tensor | None = None, block_size: int = 16):
-        device = torch.device(device if device is not None else "cuda")
-        if device.index is None:
-            device = torch.device("cuda", torch.cuda.current_device())
-        self.desc = _Desc(num_layers, num_blocks, block_size, num_kv_heads, head_dim, 0, device.index)
+                 device=None, base: torch.Tensor | None = None, block_size: int = 16,
+                 host: bool = False):
+        """``host=True``: a Global KV Cache Store tier pool in page-locked host memory
+        (PAPER.md:248-254); only migrate / gather / scatter touch it."""
+        if host:
+            device = torch.device("cpu")
+            dev_index = -1
+        else:
+            device = torch.device(device if device is not None else "cuda")
+            if device.index is None:
+                device = torch.device("cuda", torch.cuda.current_device())
+            dev_index = device.index
+        self.desc = _Desc(num_layers, num_blocks, block_size, num_kv_heads, head_dim, 0, dev_index)
         nbytes = lib().bs_kv_pool_bytes(ctypes.byref(self.desc))
         if nbytes == 0:
             raise BSError(BS_ERR_UNSUPPORTED, "unsupported pool geometry")
         if base is None:
-            base = torch.empty(nbytes // 2, dtype=torch.bfloat16, device=device)
+            base = (torch.empty(nbytes // 2, dtype=torch.bfloat16, pin_memory=True) if host else
+                    torch.empty(nbytes // 2, dtype=torch.bfloat16, device=device))
         if base.numel() * base.element_size() < nbytes:
             raise ValueError("base tensor too small")
+        if host and not base.is_pinned():
+            raise ValueError("host pools need page-locked (pinned) memory")
         self.base = base
+        self.host = host
         self.data = base.view(torch.bfloat16).reshape(-1)[: nbytes // 2].view(
             num_layers, num_blocks, 2, num_kv_heads, block_size, head_dim)
         h = _p()
-        _check(lib().bs_kv_pool_create(ctypes.byref(self.desc), _dptr(base), ctypes.byref(h)))
+        _check(lib().bs_kv_pool_create(ctypes.byref(self.desc), base.data_ptr() if host else _dptr(base),
+                                       ctypes.byref(h)))
         self.handle = h
         self.num_layers, self.num_blocks = num_layers, num_blocks
         self.num_kv_heads, self.head_dim, self.block_size = num_kv_heads, head_dim, block_size
@@ -199,6 +220,18 @@ def kv_migrate_layer(src: KVPool, dst: KVPool, layer: int, src_ids: torch.Tensor
     _check(lib().bs_kv_migrate_layer_ex(src.handle, dst.handle, layer,
                                         _dptr(src_ids, torch.int32), _dptr(dst_ids, torch.int32),
                                         n, method, _stream(stream)))
+
+
+def kv_migrate_layer_ce(src: KVPool, dst: KVPool, layer: int, src_ids, dst_ids, stream=None) -> None:
+    """H2 on the copy engines (DMA): host id lists; for the host-tier fetch / store legs."""
+    s = [int(x) for x in src_ids]
+    d = [int(x) for x in dst_ids]
+    if len(s) != len(d):
+        raise ValueError("src_ids / dst_ids length mismatch")
+    n = len(s)
+    sa = (ctypes.c_int32 * max(n, 1))(*s)
+    da = (ctypes.c_int32 * max(n, 1))(*d)
+    _check(lib().bs_kv_migrate_layer_ce(src.handle, dst.handle, layer, sa, da, n, _stream(stream)))
 
 
 def kv_gather_layer(src: KVPool, layer: int, ids: torch.Tensor, staging: torch.Tensor,
@@ -327,3 +360,40 @@ def ipc_import(handle: bytes, offset: int) -> int:
 
 def ipc_close(ptr: int, offset: int) -> None:
     _check(lib().bs_ipc_close(ptr, offset))
+
+
+# ---------------------------------------------------------------------------------------
+# NEXT F2: head-granular migration + attention over a kv-head range
+# ---------------------------------------------------------------------------------------
+
+def kv_migrate_heads_layer(src: KVPool, dst: KVPool, layer: int, src_ids: torch.Tensor,
+                           dst_ids: torch.Tensor, src_head_lo: int, dst_head_lo: int, n_heads: int,
+                           stream=None) -> None:
+    _check(lib().bs_kv_migrate_heads_layer(src.handle, dst.handle, layer,
+                                           _dptr(src_ids, torch.int32), _dptr(dst_ids, torch.int32),
+                                           src_ids.numel(), src_head_lo, dst_head_lo, n_heads,
+                                           _stream(stream)))
+
+
+def split_decode_attention_heads_workspace_size(pool: KVPool, batch: int, n_kv_heads: int,
+                                                num_kv_heads_total: int, num_q_heads: int,
+                                                max_blocks: int) -> int:
+    out = _sz()
+    _check(lib().bs_split_decode_attention_heads_workspace_size(
+        pool.handle, batch, n_kv_heads, num_kv_heads_total, num_q_heads, max_blocks, ctypes.byref(out)))
+    return out.value
+
+
+def split_decode_attention_heads(pool: KVPool, layer: int, pool_head_lo: int, model_head_lo: int,
+                                 n_kv_heads: int, num_kv_heads_total: int, q: torch.Tensor,
+                                 block_tables: torch.Tensor, kv_split: torch.Tensor, shard_id: int,
+                                 scale: float, o: torch.Tensor, m: torch.Tensor, l: torch.Tensor,
+                                 workspace: torch.Tensor | None = None, stream=None) -> None:
+    B, hq, d = q.shape
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check(lib().bs_split_decode_attention_heads(
+        pool.handle, layer, pool_head_lo, model_head_lo, n_kv_heads, num_kv_heads_total,
+        _dptr(q, torch.bfloat16), B, hq, _dptr(block_tables, torch.int32), block_tables.shape[1],
+        _dptr(kv_split, torch.int32), kv_split.shape[1] - 1, shard_id, float(scale),
+        _dptr(o, torch.float32), _dptr(m, torch.float32), _dptr(l, torch.float32),
+        _dptr(workspace), ws_bytes, _stream(stream)))

@@ -51,7 +51,9 @@ struct AttnParams {
   const int32_t* kv_split;
   int32_t n_shards, shard_id;
   float scale_log2;
-  int32_t hq, hkv;
+  int32_t hq, hkv;          // hq: q heads of the MODEL (row stride); hkv: kv heads in this launch
+  int32_t pool_head_lo;      // first kv head of this launch inside the pool
+  int32_t model_head_lo;     // ... and inside the model (selects q / output rows)
   int32_t nsplit, bps;
   float* o;
   float* m;
@@ -147,7 +149,8 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
   __syncthreads();
 
   const int nmine = nb_cta > warp ? (nb_cta - warp + kWarps - 1) / kWarps : 0;
-  const uint8_t* kv_head = p.kv + (int64_t)g * S::kPage;
+  const uint8_t* kv_head = p.kv + (int64_t)(p.pool_head_lo + g) * S::kPage;
+  const int gm = p.model_head_lo + g;  // kv head index in the model
   uint64_t policy = 0;
   if (lane == 0) policy = ptx::policy_evict_first();
   auto issue = [&](int k) {
@@ -168,7 +171,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
   // duplicated into both halves of a packed pair ({q_e, q_e}) for token-pair FFMA2
   float2 qq[G][DPL];
   {
-    const __nv_bfloat16* qp = p.q + ((int64_t)b * p.hq + g * G) * D + lane * DPL;
+    const __nv_bfloat16* qp = p.q + ((int64_t)b * p.hq + gm * G) * D + lane * DPL;
 #pragma unroll
     for (int h = 0; h < G; ++h) {
       float qf[DPL];
@@ -346,7 +349,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
         O += s_acc[(w * G + h) * D + x] * f;
       }
     }
-    const int64_t row = (int64_t)b * p.hq + g * G + h;
+    const int64_t row = (int64_t)b * p.hq + gm * G + h;
     const bool any = L > 0.f;
     if (p.nsplit == 1) {
       p.o[row * D + x] = any ? O / L : 0.f;
@@ -380,7 +383,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
   __threadfence();
   if (threadIdx.x < G) {  // per-head weights w_j = l_j 2^(m_j - M) / L, fixed order
     const int h = threadIdx.x;
-    const int64_t row = (int64_t)b * p.hq + g * G + h;
+    const int64_t row = (int64_t)b * p.hq + gm * G + h;
     const float* ml = p.ws_ml + row * p.nsplit * 2;
     float M = -INFINITY;
     for (int j = 0; j < p.nsplit; ++j) M = fmaxf(M, __ldcg(ml + 2 * j));
@@ -398,7 +401,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
   __syncthreads();
   for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
     const int h = idx / D, x = idx - h * D;
-    const int64_t row = (int64_t)b * p.hq + g * G + h;
+    const int64_t row = (int64_t)b * p.hq + gm * G + h;
     const float* po = p.ws_o + row * p.nsplit * D + x;
     float O = 0.f;
     for (int j = 0; j < p.nsplit; ++j) O += s_w[h * kMaxSplit + j] * __ldcg(po + (int64_t)j * D);
@@ -435,9 +438,9 @@ struct Plan {
 
 // Split-K planning: pick the number of CTAs per (request, kv-head) that minimises
 // waves x blocks-per-CTA (+ a fixed per-CTA cost), i.e. fills all SM slots evenly.
-bs_status make_plan(int batch, int hq, int hkv, int d, int max_blocks, Plan* out) {
+// hkv: kv heads handled by the launch (grid.y); hq: q heads of the model (partial rows)
+bs_status make_plan(int batch, int G, int hq, int hkv, int d, int max_blocks, Plan* out) {
   const int sms = sm_count(current_device());
-  const int G = hq / std::max(hkv, 1);
   const int64_t slots = (int64_t)sms * variant_for(d, G).minb;
   const int64_t base = (int64_t)batch * hkv;
   const int min_bps = kWarps;
@@ -515,36 +518,28 @@ bs_status launch_attn_d(const AttnParams& p, int G, int batch, cudaStream_t stre
 }  // namespace
 }  // namespace bs
 
-extern "C" {
-
-bs_status bs_split_decode_attention_workspace_size(const bs_kv_pool* pool, int32_t batch,
-                                                   int32_t num_q_heads, int32_t max_blocks,
-                                                   size_t* bytes) {
-  BS_REQUIRE(pool && bytes, "bs_split_decode_attention_workspace_size: NULL argument");
-  BS_REQUIRE(batch >= 0 && max_blocks >= 1 && num_q_heads >= 1,
-             "bs_split_decode_attention_workspace_size: bad batch/max_blocks/heads");
-  bs::Plan pl;
-  bs_status st = bs::make_plan(batch, num_q_heads, pool->desc.num_kv_heads, pool->desc.head_dim,
-                               max_blocks, &pl);
-  if (st != BS_OK) return st;
-  *bytes = pl.ws_bytes;
-  return BS_OK;
-}
-
-bs_status bs_split_decode_attention(const bs_kv_pool* pool, int32_t layer, const void* q,
-                                    int32_t batch, int32_t num_q_heads,
-                                    const int32_t* block_tables, int32_t max_blocks,
-                                    const int32_t* kv_split, int32_t n_shards, int32_t shard_id,
-                                    float scale, float* o_part, float* m, float* l,
-                                    void* workspace, size_t workspace_bytes, void* stream) {
+static bs_status attention_impl(const bs_kv_pool* pool, int32_t layer, int32_t pool_head_lo,
+                                int32_t model_head_lo, int32_t n_kv_heads, int32_t num_kv_heads_total,
+                                const void* q, int32_t batch, int32_t num_q_heads,
+                                const int32_t* block_tables, int32_t max_blocks,
+                                const int32_t* kv_split, int32_t n_shards, int32_t shard_id,
+                                float scale, float* o_part, float* m, float* l, void* workspace,
+                                size_t workspace_bytes, void* stream) {
   BS_REQUIRE(pool, "bs_split_decode_attention: NULL pool");
-  const int hkv = pool->desc.num_kv_heads, d = pool->desc.head_dim;
+  BS_REQUIRE(!pool->host, "bs_split_decode_attention: host-tier pools are fetched first, not read");
+  const int d = pool->desc.head_dim;
   BS_REQUIRE(layer >= 0 && layer < pool->desc.num_layers, "bs_split_decode_attention: layer %d out of range",
              layer);
   BS_REQUIRE(batch >= 0, "bs_split_decode_attention: batch < 0");
+  BS_REQUIRE(num_kv_heads_total >= 1 && num_q_heads >= num_kv_heads_total &&
+                 num_q_heads % num_kv_heads_total == 0,
+             "bs_split_decode_attention: num_q_heads %d not a multiple of Hkv %d", num_q_heads,
+             num_kv_heads_total);
+  BS_REQUIRE(n_kv_heads >= 1 && pool_head_lo >= 0 && pool_head_lo + n_kv_heads <= pool->desc.num_kv_heads &&
+                 model_head_lo >= 0 && model_head_lo + n_kv_heads <= num_kv_heads_total,
+             "bs_split_decode_attention: head range [%d,+%d) (model %d) outside pool (%d) / model (%d)",
+             pool_head_lo, n_kv_heads, model_head_lo, pool->desc.num_kv_heads, num_kv_heads_total);
   if (batch == 0) return BS_OK;
-  BS_REQUIRE(num_q_heads >= hkv && num_q_heads % hkv == 0,
-             "bs_split_decode_attention: num_q_heads %d not a multiple of Hkv %d", num_q_heads, hkv);
   BS_REQUIRE(max_blocks >= 1, "bs_split_decode_attention: max_blocks < 1");
   BS_REQUIRE(n_shards >= 1 && shard_id >= 0 && shard_id < n_shards,
              "bs_split_decode_attention: shard %d of %d", shard_id, n_shards);
@@ -553,8 +548,11 @@ bs_status bs_split_decode_attention(const bs_kv_pool* pool, int32_t layer, const
   BS_REQUIRE(((uintptr_t)q & 15) == 0 && ((uintptr_t)o_part & 15) == 0,
              "bs_split_decode_attention: q/o_part must be 16-B aligned");
   BS_REQUIRE(scale > 0.f && scale == scale, "bs_split_decode_attention: bad scale");
+  const int G = num_q_heads / num_kv_heads_total;
+  if (G != 1 && G != 2 && G != 4 && G != 8)
+    return bs::set_error(BS_ERR_UNSUPPORTED, "query group G=%d not in {1,2,4,8}", G);
   bs::Plan pl;
-  bs_status st = bs::make_plan(batch, num_q_heads, hkv, d, max_blocks, &pl);
+  bs_status st = bs::make_plan(batch, G, num_q_heads, n_kv_heads, d, max_blocks, &pl);
   if (st != BS_OK) return st;
   BS_REQUIRE(pl.ws_bytes == 0 || (workspace && workspace_bytes >= pl.ws_bytes &&
                                   ((uintptr_t)workspace & 15) == 0),
@@ -563,7 +561,7 @@ bs_status bs_split_decode_attention(const bs_kv_pool* pool, int32_t layer, const
   bs::AttnParams p{};
   p.kv = pool->base + (size_t)layer * pool->layer_bytes;
   p.chunk_bytes = (int64_t)pool->chunk_bytes;
-  p.v_off = (int64_t)hkv * pool->page_bytes;
+  p.v_off = (int64_t)pool->desc.num_kv_heads * pool->page_bytes;
   p.q = static_cast<const __nv_bfloat16*>(q);
   p.bt = block_tables;
   p.max_blocks = max_blocks;
@@ -572,7 +570,9 @@ bs_status bs_split_decode_attention(const bs_kv_pool* pool, int32_t layer, const
   p.shard_id = shard_id;
   p.scale_log2 = scale * bs::kLog2e;
   p.hq = num_q_heads;
-  p.hkv = hkv;
+  p.hkv = n_kv_heads;
+  p.pool_head_lo = pool_head_lo;
+  p.model_head_lo = model_head_lo;
   p.nsplit = pl.nsplit;
   p.bps = pl.bps;
   p.o = o_part;
@@ -584,10 +584,69 @@ bs_status bs_split_decode_attention(const bs_kv_pool* pool, int32_t layer, const
     p.ws_ml = reinterpret_cast<float*>(ws + pl.off_ml);
     p.ws_cnt = reinterpret_cast<int32_t*>(ws + pl.off_cnt);
   }
-  const int G = num_q_heads / hkv;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (d == 128) return bs::launch_attn_d<128>(p, G, batch, s);
   return bs::launch_attn_d<64>(p, G, batch, s);
+}
+
+static bs_status workspace_impl(const bs_kv_pool* pool, int32_t batch, int32_t n_kv_heads,
+                                int32_t num_kv_heads_total, int32_t num_q_heads, int32_t max_blocks,
+                                size_t* bytes) {
+  BS_REQUIRE(pool && bytes, "bs_split_decode_attention_workspace_size: NULL argument");
+  BS_REQUIRE(batch >= 0 && max_blocks >= 1 && n_kv_heads >= 1 && num_kv_heads_total >= 1 &&
+                 num_q_heads >= num_kv_heads_total && num_q_heads % num_kv_heads_total == 0,
+             "bs_split_decode_attention_workspace_size: bad batch/max_blocks/heads");
+  bs::Plan pl;
+  bs_status st = bs::make_plan(batch, num_q_heads / num_kv_heads_total, num_q_heads, n_kv_heads,
+                               pool->desc.head_dim, max_blocks, &pl);
+  if (st != BS_OK) return st;
+  *bytes = pl.ws_bytes;
+  return BS_OK;
+}
+
+extern "C" {
+
+bs_status bs_split_decode_attention_workspace_size(const bs_kv_pool* pool, int32_t batch,
+                                                   int32_t num_q_heads, int32_t max_blocks,
+                                                   size_t* bytes) {
+  BS_REQUIRE(pool, "bs_split_decode_attention_workspace_size: NULL pool");
+  return workspace_impl(pool, batch, pool->desc.num_kv_heads, pool->desc.num_kv_heads, num_q_heads,
+                        max_blocks, bytes);
+}
+
+bs_status bs_split_decode_attention(const bs_kv_pool* pool, int32_t layer, const void* q,
+                                    int32_t batch, int32_t num_q_heads,
+                                    const int32_t* block_tables, int32_t max_blocks,
+                                    const int32_t* kv_split, int32_t n_shards, int32_t shard_id,
+                                    float scale, float* o_part, float* m, float* l,
+                                    void* workspace, size_t workspace_bytes, void* stream) {
+  BS_REQUIRE(pool, "bs_split_decode_attention: NULL pool");
+  const int hkv = pool->desc.num_kv_heads;
+  return attention_impl(pool, layer, 0, 0, hkv, hkv, q, batch, num_q_heads, block_tables,
+                        max_blocks, kv_split, n_shards, shard_id, scale, o_part, m, l, workspace,
+                        workspace_bytes, stream);
+}
+
+bs_status bs_split_decode_attention_heads_workspace_size(const bs_kv_pool* pool, int32_t batch,
+                                                         int32_t n_kv_heads,
+                                                         int32_t num_kv_heads_total,
+                                                         int32_t num_q_heads, int32_t max_blocks,
+                                                         size_t* bytes) {
+  return workspace_impl(pool, batch, n_kv_heads, num_kv_heads_total, num_q_heads, max_blocks, bytes);
+}
+
+bs_status bs_split_decode_attention_heads(const bs_kv_pool* pool, int32_t layer,
+                                          int32_t pool_head_lo, int32_t model_head_lo,
+                                          int32_t n_kv_heads, int32_t num_kv_heads_total,
+                                          const void* q, int32_t batch, int32_t num_q_heads,
+                                          const int32_t* block_tables, int32_t max_blocks,
+                                          const int32_t* kv_split, int32_t n_shards,
+                                          int32_t shard_id, float scale, float* o_part, float* m,
+                                          float* l, void* workspace, size_t workspace_bytes,
+                                          void* stream) {
+  return attention_impl(pool, layer, pool_head_lo, model_head_lo, n_kv_heads, num_kv_heads_total,
+                        q, batch, num_q_heads, block_tables, max_blocks, kv_split, n_shards,
+                        shard_id, scale, o_part, m, l, workspace, workspace_bytes, stream);
 }
 
 }  // extern "C"

@@ -14,7 +14,8 @@
 
 struct bs_kv_pool {
   bs_kv_pool_desc desc;
-  uint8_t* base = nullptr;
+  uint8_t* base = nullptr;  // device-visible address (host pools: the UVA mapping)
+  bool host = false;        // pinned host memory (Global KV Cache Store tier)
   size_t chunk_bytes = 0;   // one (layer, block): K+V pages of all heads
   size_t page_bytes = 0;    // one (layer, block, K|V, head)
   size_t layer_bytes = 0;   // num_blocks * chunk_bytes
@@ -34,7 +35,8 @@ inline bs_status ok() { return BS_OK; }
 // Launchers (defined in the .cu files).
 bs_status launch_copy_chunks(const uint8_t* src_base, const int32_t* src_ids, uint8_t* dst_base,
                              const int32_t* dst_ids, int32_t n, size_t chunk_bytes,
-                             size_t page_bytes, int method, cudaStream_t stream);
+                             size_t page_bytes, int method, cudaStream_t stream,
+                             int max_ctas = 0);
 
 }  // namespace bs
 

@@ -14,6 +14,9 @@
 //     cp.async.bulk shared->global in bulk groups); no registers touch the payload.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <vector>
+
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -59,6 +62,37 @@ __global__ void __launch_bounds__(256) copy_pages_vec16(const uint8_t* __restric
     for (int v = 0; v < V; ++v) r[v] = ld_stream(s + v * 32);
 #pragma unroll
     for (int v = 0; v < V; ++v) st_stream(d + v * 32, r[v]);
+  }
+}
+
+// NEXT F2: head-granular pages (K and V of n_heads kv-heads of each pair), between pools
+// whose kv-head counts may differ (a cold pool can keep only the migrated heads).
+template <int PAGE_BYTES>
+__global__ void __launch_bounds__(256) copy_head_pages_vec16(
+    const uint8_t* __restrict__ src_base, const int32_t* __restrict__ src_ids, int64_t src_chunk,
+    int32_t src_hkv, int32_t src_head_lo, uint8_t* __restrict__ dst_base,
+    const int32_t* __restrict__ dst_ids, int64_t dst_chunk, int32_t dst_hkv, int32_t dst_head_lo,
+    int32_t n, int32_t n_heads) {
+  constexpr int V = PAGE_BYTES / (16 * 32);
+  const int lane = threadIdx.x & 31;
+  const int wpc = blockDim.x >> 5;
+  const int32_t ppp = 2 * n_heads;  // pages per pair
+  const int64_t total = (int64_t)n * ppp;
+  for (int64_t p = (int64_t)blockIdx.x * wpc + (threadIdx.x >> 5); p < total;
+       p += (int64_t)gridDim.x * wpc) {
+    const int32_t i = (int32_t)(p / ppp);
+    const int32_t r = (int32_t)(p - (int64_t)i * ppp);
+    const int32_t kv = r / n_heads, h = r - kv * n_heads;
+    const int4* s = reinterpret_cast<const int4*>(
+        src_base + (int64_t)__ldg(src_ids + i) * src_chunk +
+        (int64_t)(kv * src_hkv + src_head_lo + h) * PAGE_BYTES) + lane;
+    int4* d = reinterpret_cast<int4*>(dst_base + (int64_t)__ldg(dst_ids + i) * dst_chunk +
+                                      (int64_t)(kv * dst_hkv + dst_head_lo + h) * PAGE_BYTES) + lane;
+    int4 rg[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) rg[v] = ld_stream(s + v * 32);
+#pragma unroll
+    for (int v = 0; v < V; ++v) st_stream(d + v * 32, rg[v]);
   }
 }
 
@@ -145,7 +179,7 @@ __global__ void __launch_bounds__(32) copy_pages_bulk(const uint8_t* __restrict_
 template <int PAGE_BYTES>
 bs_status launch_copy_t(const uint8_t* src_base, const int32_t* src_ids, uint8_t* dst_base,
                         const int32_t* dst_ids, int32_t n, int32_t ppc, int64_t chunk, int method,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, int max_ctas) {
   const int64_t total = (int64_t)n * ppc;
   const int sms = sm_count(current_device());
   if (method == BS_MIGRATE_BULK) {
@@ -157,12 +191,14 @@ bs_status launch_copy_t(const uint8_t* src_base, const int32_t* src_ids, uint8_t
       configured = true;
     }
     int64_t grid = std::min<int64_t>(total, (int64_t)sms * 3);
+    if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
     copy_pages_bulk<PAGE_BYTES><<<(unsigned)grid, 32, smem, stream>>>(
         src_base, src_ids, dst_base, dst_ids, n, ppc, chunk);
     return check_launch("copy_pages_bulk");
   }
   const int wpc = 8;
   int64_t grid = std::min<int64_t>((total + wpc - 1) / wpc, (int64_t)sms * 8);
+  if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
   copy_pages_vec16<PAGE_BYTES><<<(unsigned)grid, wpc * 32, 0, stream>>>(
       src_base, src_ids, dst_base, dst_ids, n, ppc, chunk);
   return check_launch("copy_pages_vec16");
@@ -172,20 +208,32 @@ bs_status launch_copy_t(const uint8_t* src_base, const int32_t* src_ids, uint8_t
 
 bs_status launch_copy_chunks(const uint8_t* src_base, const int32_t* src_ids, uint8_t* dst_base,
                              const int32_t* dst_ids, int32_t n, size_t chunk_bytes,
-                             size_t page_bytes, int method, cudaStream_t stream) {
+                             size_t page_bytes, int method, cudaStream_t stream, int max_ctas) {
   if (n == 0) return BS_OK;
   const int32_t ppc = (int32_t)(chunk_bytes / page_bytes);
   if (method == BS_MIGRATE_AUTO) method = BS_MIGRATE_VEC16;
   if (page_bytes == 4096)
     return launch_copy_t<4096>(src_base, src_ids, dst_base, dst_ids, n, ppc, (int64_t)chunk_bytes,
-                               method, stream);
+                               method, stream, max_ctas);
   if (page_bytes == 2048)
     return launch_copy_t<2048>(src_base, src_ids, dst_base, dst_ids, n, ppc, (int64_t)chunk_bytes,
-                               method, stream);
+                               method, stream, max_ctas);
   return set_error(BS_ERR_UNSUPPORTED, "page size %zu", page_bytes);
 }
 
 }  // namespace bs
+
+// CTAs for a copy that touches a host-tier pool: ~8 x 8 warps x 4 KiB in flight covers
+// PCIe latency x bandwidth (~2 us x 55 GB/s); the other SMs keep the layer's compute.
+static int host_copy_ctas() {
+  static int v = [] {
+    const char* e = getenv("BS_HOST_COPY_CTAS");
+    int x = e ? atoi(e) : 8;
+    return x > 0 ? x : 8;
+  }();
+  return v;
+}
+#define kHostCopyCtas host_copy_ctas()
 
 static bool same_geometry(const bs_kv_pool* a, const bs_kv_pool* b) {
   return a->desc.num_layers == b->desc.num_layers && a->desc.num_kv_heads == b->desc.num_kv_heads &&
@@ -206,16 +254,100 @@ bs_status bs_kv_migrate_layer_ex(const bs_kv_pool* src, bs_kv_pool* dst, int32_t
   BS_REQUIRE(n == 0 || (src_ids && dst_ids), "bs_kv_migrate_layer: NULL ids");
   BS_REQUIRE(method >= BS_MIGRATE_AUTO && method <= BS_MIGRATE_BULK,
              "bs_kv_migrate_layer: bad method %d", method);
+  // a host-tier pool is behind PCIe / C2C: a few CTAs keep it saturated, the rest of the
+  // SMs stay with the layer's compute (three-stage pipeline, Fig. 6)
+  const int max_ctas = (src->host || dst->host) ? kHostCopyCtas : 0;
   return bs::launch_copy_chunks(src->base + (size_t)layer * src->layer_bytes, src_ids,
                                 dst->base + (size_t)layer * dst->layer_bytes, dst_ids, n,
                                 src->chunk_bytes, src->page_bytes, method,
-                                static_cast<cudaStream_t>(stream));
+                                static_cast<cudaStream_t>(stream), max_ctas);
 }
 
 bs_status bs_kv_migrate_layer(const bs_kv_pool* src, bs_kv_pool* dst, int32_t layer,
                               const int32_t* src_ids, const int32_t* dst_ids, int32_t n,
                               void* stream) {
   return bs_kv_migrate_layer_ex(src, dst, layer, src_ids, dst_ids, n, BS_MIGRATE_AUTO, stream);
+}
+
+bs_status bs_kv_migrate_layer_ce(const bs_kv_pool* src, bs_kv_pool* dst, int32_t layer,
+                                 const int32_t* src_ids, const int32_t* dst_ids, int32_t n,
+                                 void* stream) {
+  BS_REQUIRE(src && dst, "bs_kv_migrate_layer_ce: NULL pool");
+  BS_REQUIRE(same_geometry(src, dst), "bs_kv_migrate_layer_ce: src/dst geometry differs");
+  BS_REQUIRE(layer >= 0 && layer < src->desc.num_layers, "bs_kv_migrate_layer_ce: layer out of range");
+  BS_REQUIRE(n >= 0, "bs_kv_migrate_layer_ce: n < 0");
+  if (n == 0) return BS_OK;
+  BS_REQUIRE(src_ids && dst_ids, "bs_kv_migrate_layer_ce: NULL ids");
+  const size_t chunk = src->chunk_bytes;
+  std::vector<void*> dsts, srcs;
+  std::vector<size_t> sizes;
+  dsts.reserve(n);
+  srcs.reserve(n);
+  sizes.reserve(n);
+  for (int32_t i = 0; i < n;) {
+    const int32_t s0 = src_ids[i], d0 = dst_ids[i];
+    BS_REQUIRE(s0 >= 0 && s0 < src->desc.num_blocks && d0 >= 0 && d0 < dst->desc.num_blocks,
+               "bs_kv_migrate_layer_ce: pair %d (%d -> %d) out of range", i, s0, d0);
+    int32_t run = 1;  // coalesce runs of consecutive ids on both sides into one copy
+    while (i + run < n && src_ids[i + run] == s0 + run && dst_ids[i + run] == d0 + run &&
+           s0 + run < src->desc.num_blocks && d0 + run < dst->desc.num_blocks)
+      ++run;
+    srcs.push_back(src->base + (size_t)layer * src->layer_bytes + (size_t)s0 * chunk);
+    dsts.push_back(dst->base + (size_t)layer * dst->layer_bytes + (size_t)d0 * chunk);
+    sizes.push_back((size_t)run * chunk);
+    i += run;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaSuccess;
+  if (s != nullptr) {
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    size_t attr_idx = 0, fail = 0;
+    e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), sizes.size(), &attr, &attr_idx,
+                             1, &fail, s);
+  }
+  if (s == nullptr || e != cudaSuccess) {  // legacy stream / older driver: one copy each
+    cudaGetLastError();
+    for (size_t k = 0; k < sizes.size(); ++k) {
+      e = cudaMemcpyAsync(dsts[k], srcs[k], sizes[k], cudaMemcpyDefault, s);
+      if (e != cudaSuccess) break;
+    }
+  }
+  if (e != cudaSuccess) return bs::set_error(BS_ERR_CUDA, "bs_kv_migrate_layer_ce: %s", cudaGetErrorString(e));
+  return BS_OK;
+}
+
+bs_status bs_kv_migrate_heads_layer(const bs_kv_pool* src, bs_kv_pool* dst, int32_t layer,
+                                    const int32_t* src_ids, const int32_t* dst_ids, int32_t n,
+                                    int32_t src_head_lo, int32_t dst_head_lo, int32_t n_heads,
+                                    void* stream) {
+  BS_REQUIRE(src && dst, "bs_kv_migrate_heads_layer: NULL pool");
+  BS_REQUIRE(src->desc.num_layers == dst->desc.num_layers && src->desc.head_dim == dst->desc.head_dim,
+             "bs_kv_migrate_heads_layer: layers / head_dim differ");
+  BS_REQUIRE(layer >= 0 && layer < src->desc.num_layers, "bs_kv_migrate_heads_layer: layer out of range");
+  BS_REQUIRE(n_heads >= 1 && src_head_lo >= 0 && src_head_lo + n_heads <= src->desc.num_kv_heads &&
+                 dst_head_lo >= 0 && dst_head_lo + n_heads <= dst->desc.num_kv_heads,
+             "bs_kv_migrate_heads_layer: head range outside a pool");
+  BS_REQUIRE(n >= 0, "bs_kv_migrate_heads_layer: n < 0");
+  if (n == 0) return BS_OK;
+  BS_REQUIRE(src_ids && dst_ids, "bs_kv_migrate_heads_layer: NULL ids");
+  const int sms = bs::sm_count(bs::current_device());
+  const int64_t total = (int64_t)n * 2 * n_heads;
+  const int wpc = 8;
+  int64_t grid = std::min<int64_t>((total + wpc - 1) / wpc, (int64_t)sms * 8);
+  if (src->host || dst->host) grid = std::min<int64_t>(grid, kHostCopyCtas);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint8_t* sb = src->base + (size_t)layer * src->layer_bytes;
+  uint8_t* db = dst->base + (size_t)layer * dst->layer_bytes;
+  if (src->page_bytes == 4096)
+    bs::copy_head_pages_vec16<4096><<<(unsigned)grid, wpc * 32, 0, s>>>(
+        sb, src_ids, (int64_t)src->chunk_bytes, src->desc.num_kv_heads, src_head_lo, db, dst_ids,
+        (int64_t)dst->chunk_bytes, dst->desc.num_kv_heads, dst_head_lo, n, n_heads);
+  else
+    bs::copy_head_pages_vec16<2048><<<(unsigned)grid, wpc * 32, 0, s>>>(
+        sb, src_ids, (int64_t)src->chunk_bytes, src->desc.num_kv_heads, src_head_lo, db, dst_ids,
+        (int64_t)dst->chunk_bytes, dst->desc.num_kv_heads, dst_head_lo, n, n_heads);
+  return bs::check_launch("copy_head_pages_vec16");
 }
 
 bs_status bs_kv_gather_layer(const bs_kv_pool* src, int32_t layer, const int32_t* ids, int32_t n,
@@ -227,7 +359,8 @@ bs_status bs_kv_gather_layer(const bs_kv_pool* src, int32_t layer, const int32_t
   BS_REQUIRE(((uintptr_t)staging & 15) == 0, "bs_kv_gather_layer: staging not 16-B aligned");
   return bs::launch_copy_chunks(src->base + (size_t)layer * src->layer_bytes, ids,
                                 static_cast<uint8_t*>(staging), nullptr, n, src->chunk_bytes,
-                                src->page_bytes, BS_MIGRATE_AUTO, static_cast<cudaStream_t>(stream));
+                                src->page_bytes, BS_MIGRATE_AUTO, static_cast<cudaStream_t>(stream),
+                                src->host ? kHostCopyCtas : 0);
 }
 
 bs_status bs_kv_scatter_layer(bs_kv_pool* dst, int32_t layer, const int32_t* ids, int32_t n,
@@ -240,7 +373,7 @@ bs_status bs_kv_scatter_layer(bs_kv_pool* dst, int32_t layer, const int32_t* ids
   return bs::launch_copy_chunks(static_cast<const uint8_t*>(staging), nullptr,
                                 dst->base + (size_t)layer * dst->layer_bytes, ids, n,
                                 dst->chunk_bytes, dst->page_bytes, BS_MIGRATE_AUTO,
-                                static_cast<cudaStream_t>(stream));
+                                static_cast<cudaStream_t>(stream), dst->host ? kHostCopyCtas : 0);
 }
 
 }  // extern "C"

@@ -50,7 +50,7 @@ int sm_count(int device) {
 static bool desc_ok(const bs_kv_pool_desc* d) {
   return d && d->num_layers >= 1 && d->num_blocks >= 1 && d->block_size == 16 &&
          d->num_kv_heads >= 1 && (d->head_dim == 64 || d->head_dim == 128) &&
-         d->dtype == BS_DTYPE_BF16 && d->device >= 0;
+         d->dtype == BS_DTYPE_BF16 && (d->device >= 0 || d->device == BS_DEVICE_HOST);
 }
 
 extern "C" {
@@ -83,10 +83,24 @@ bs_status bs_kv_pool_create(const bs_kv_pool_desc* desc, void* base, bs_kv_pool*
              desc->num_layers, desc->num_blocks, desc->num_kv_heads, desc->device);
   BS_REQUIRE(base != nullptr, "bs_kv_pool_create: base is NULL");
   BS_REQUIRE(((uintptr_t)base & 255) == 0, "bs_kv_pool_create: base must be 256-byte aligned");
+  uint8_t* dbase = static_cast<uint8_t*>(base);
+  if (desc->device == BS_DEVICE_HOST) {
+    // Global KV Cache Store tier: page-locked host memory, reached by the copy kernels
+    // through its UVA device mapping (zero-copy over PCIe / C2C)
+    cudaPointerAttributes attr{};
+    cudaError_t e = cudaPointerGetAttributes(&attr, base);
+    if (e != cudaSuccess || attr.type != cudaMemoryTypeHost || !attr.devicePointer) {
+      cudaGetLastError();
+      return bs::set_error(BS_ERR_INVALID_ARG,
+                           "bs_kv_pool_create: host pool base must be page-locked, mapped memory");
+    }
+    dbase = static_cast<uint8_t*>(attr.devicePointer);
+  }
   bs_kv_pool* p = new (std::nothrow) bs_kv_pool();
   if (!p) return bs::set_error(BS_ERR_INVALID_ARG, "bs_kv_pool_create: host OOM");
   p->desc = *desc;
-  p->base = static_cast<uint8_t*>(base);
+  p->base = dbase;
+  p->host = desc->device == BS_DEVICE_HOST;
   p->chunk_bytes = bs_kv_chunk_bytes(desc);
   p->page_bytes = (size_t)desc->block_size * desc->head_dim * 2;
   p->layer_bytes = (size_t)desc->num_blocks * p->chunk_bytes;

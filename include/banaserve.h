@@ -259,6 +259,31 @@ bs_status bs_ipc_export(const void* dev_ptr, void* handle_out, size_t* offset_ou
 bs_status bs_ipc_import(const void* handle, size_t offset, void** dev_ptr_out);
 bs_status bs_ipc_close(void* dev_ptr, size_t offset);
 
+/* ------------------------------------------------------------------------------ */
+/* NEXT F4: control plane (host only; §4.4).  Readings R-F4a..g in */
+/* DESIGN.md.  Loads are normalised utilisations U = C/C_max + M/M_max (eq. 32/37).  */
+/* ------------------------------------------------------------------------------ */
+double bs_utilization(double c, double c_max, double m, double m_max);
+/* Alg. 2: dispatch n_req requests (est_load[r] each, in queue order) over n_inst
+ * prefill instances.  load / q_len (HOST arrays [n_inst]) are read and updated in
+ * place; assign_out[r] = chosen instance.  Least-loaded (load, q_len, index) if its load
+ * < delta_l (then load += est_load), else lowest-queue (q_len, load, index); q_len += 1
+ * on every assignment. */
+bs_status bs_dispatch_requests(int32_t n_inst, double* load, int32_t* q_len, int32_t n_req,
+                               const double* est_load, double delta_l, int32_t* assign_out);
+/* Alg. 1, one control cycle over n_dev devices (HOST arrays [n_dev]; load, n_layers,
+ * n_heads updated in place).  While an overloaded (load - min > delta) and another
+ * underloaded (max - load > delta) device exist: d_o = most loaded overloaded, d_u =
+ * least loaded underloaded; if the gap >= delta try a layer move (supports_layer,
+ * n_layers > 0) then a KV-head move (supports_attn, n_heads > 0), each executed only if
+ * (gap - |gap after|) / cost >= rho (eq. 35).  Stops when no move passes or after
+ * max_moves.  moves_out[3k..3k+2] = (kind 0 layer | 1 heads, from, to). */
+bs_status bs_plan_migrations(int32_t n_dev, double* load, int32_t* n_layers, const double* layer_load,
+                             const double* layer_cost, int32_t* n_heads, const double* head_load,
+                             const double* head_cost, const uint8_t* supports_layer,
+                             const uint8_t* supports_attn, double delta, double rho,
+                             int32_t max_moves, int32_t* moves_out, int32_t* n_moves_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -34,6 +34,7 @@ EXPORTED_SYMBOLS = (
     "bs_kv_recv_layer", "bs_kv_sendrecv_layer", "bs_ipc_handle_bytes", "bs_ipc_export",
     "bs_ipc_import", "bs_ipc_close", "bs_kv_migrate_heads_layer",
     "bs_split_decode_attention_heads_workspace_size", "bs_split_decode_attention_heads",
+    "bs_utilization", "bs_dispatch_requests", "bs_plan_migrations",
 )
 
 
@@ -106,6 +107,10 @@ def lib():
         "bs_split_decode_attention_heads": ([_p, _i32, _i32, _i32, _i32, _i32, _p, _i32, _i32, _p,
                                              _i32, _p, _i32, _i32, _f32, _p, _p, _p, _p, _sz, _p],
                                             _i32),
+        "bs_utilization": ([ctypes.c_double] * 4, ctypes.c_double),
+        "bs_dispatch_requests": ([_i32, _p, _p, _i32, _p, ctypes.c_double, _p], _i32),
+        "bs_plan_migrations": ([_i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, ctypes.c_double,
+                                ctypes.c_double, _i32, _p, ctypes.POINTER(_i32)], _i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

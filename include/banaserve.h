@@ -166,6 +166,18 @@ bs_status bs_split_decode_attention(const bs_kv_pool* pool, int32_t layer, const
                                     void* workspace, size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------------------ */
+/* NEXT F3: layer-level migration (Fig. 3, eqs. 3-5): a contiguous  */
+/* set of layers moves with its weights W_l and its KV_l.  bs_kv_migrate_layers is    */
+/* bs_kv_migrate_layer for layers [layer_lo, layer_lo + n_layers) in ONE launch (the  */
+/* same pairs every layer: block ids are shared by all layers).  bs_copy_bytes moves a */
+/* weight tensor (DEVICE / peer / pinned-host pointers; copy engine).                 */
+/* ------------------------------------------------------------------------------ */
+bs_status bs_kv_migrate_layers(const bs_kv_pool* src, bs_kv_pool* dst, int32_t layer_lo,
+                               int32_t n_layers, const int32_t* src_ids, const int32_t* dst_ids,
+                               int32_t n, void* stream);
+bs_status bs_copy_bytes(void* dst, const void* src, size_t bytes, void* stream);
+
+/* ------------------------------------------------------------------------------ */
 /* NEXT F2: head-granular attention-level migration -- the paper's literal text       */
 /* ("partition the KV Cache along the attention head dimension and selectively      */
 /* migrate only the KV states of certain heads"; Alg. 1      */

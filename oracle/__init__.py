@@ -56,6 +56,10 @@ def lib():
         L.or_t_f_layer_ms.restype = _f64
         L.or_t_kv_ms.argtypes = [_f64, _f64, _f64, _f64]
         L.or_t_kv_ms.restype = _f64
+        L.or_layer_payload_bytes.argtypes = [_f64, _f64]
+        L.or_layer_payload_bytes.restype = _f64
+        L.or_t_layer_s.argtypes = [_f64, _f64, _f64]
+        L.or_t_layer_s.restype = _f64
         L.or_chunk_elems.argtypes = [_i32, _i32, _i32]
         L.or_chunk_elems.restype = _i64
         L.or_pool_bytes.argtypes = [_i32, _i32, _i32, _i32, _i32]
@@ -110,6 +114,22 @@ def t_f_layer_ms(t_f_ms: float, r: float, n_layers: int) -> float:
 def t_kv_ms(s_kv_bytes: float, l_tokens: float, r: float, b_gbps: float) -> float:
     """eq. 13, units per reading R-A17."""
     return lib().or_t_kv_ms(s_kv_bytes, l_tokens, r, b_gbps)
+
+
+def layer_payload_bytes(s_w: float, s_kv: float) -> float:
+    """eq. 3 (PAPER.md:187-190)."""
+    return lib().or_layer_payload_bytes(s_w, s_kv)
+
+
+def t_layer_s(s_total: float, b_net: float, t_sync: float) -> float:
+    """eq. 4; parity unpinned: the paper prints no worked example."""
+    return lib().or_t_layer_s(s_total, b_net, t_sync)
+
+
+def migrate_layers(src_pool, dst_pool, layer_lo, n_layers, src_ids, dst_ids) -> None:
+    """NEXT F3: migrate_layer for each layer of the range, in order."""
+    for layer in range(layer_lo, layer_lo + n_layers):
+        migrate_layer(src_pool, dst_pool, layer, src_ids, dst_ids)
 
 
 # --- pool geometry and allocator (H0) ------------------------------------------------

@@ -76,6 +76,12 @@ double or_t_kv_ms(double s_kv_bytes, double l_tokens, double r, double b_gbps) {
   return s_kv_bytes * l_tokens * r / bytes_per_s * 1e3;
 }
 
+/* eq. 3: layer-level migration payload S_total = S_w + S_kv. */
+double or_layer_payload_bytes(double s_w, double s_kv) { return s_w + s_kv; }
+
+/* eq. 4: T_layer ~= S_total / B_net + T_sync (seconds, bytes/s). */
+double or_t_layer_s(double s_total, double b_net, double t_sync) { return s_total / b_net + t_sync; }
+
 /* ------------------------------------------------------------------------- */
 /* Paged pool geometry (R-A: layout D4; vLLM PagedAttention blocks PAPER.md:126) */
 /*   pool[layer][block][kv(0=K,1=V)][kv_head][slot][dim], bf16                   */

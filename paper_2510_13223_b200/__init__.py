@@ -34,7 +34,8 @@ EXPORTED_SYMBOLS = (
     "bs_kv_recv_layer", "bs_kv_sendrecv_layer", "bs_ipc_handle_bytes", "bs_ipc_export",
     "bs_ipc_import", "bs_ipc_close", "bs_kv_migrate_heads_layer",
     "bs_split_decode_attention_heads_workspace_size", "bs_split_decode_attention_heads",
-    "bs_utilization", "bs_dispatch_requests", "bs_plan_migrations",
+    "bs_utilization", "bs_dispatch_requests", "bs_plan_migrations", "bs_kv_migrate_layers",
+    "bs_copy_bytes",
 )
 
 
@@ -108,6 +109,8 @@ def lib():
                                              _i32, _p, _i32, _i32, _f32, _p, _p, _p, _p, _sz, _p],
                                             _i32),
         "bs_utilization": ([ctypes.c_double] * 4, ctypes.c_double),
+        "bs_kv_migrate_layers": ([_p, _p, _i32, _i32, _p, _p, _i32, _p], _i32),
+        "bs_copy_bytes": ([_p, _p, _sz, _p], _i32),
         "bs_dispatch_requests": ([_i32, _p, _p, _i32, _p, ctypes.c_double, _p], _i32),
         "bs_plan_migrations": ([_i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, ctypes.c_double,
                                 ctypes.c_double, _i32, _p, ctypes.POINTER(_i32)], _i32),
@@ -402,3 +405,39 @@ def split_decode_attention_heads(pool: KVPool, layer: int, pool_head_lo: int, mo
         _dptr(kv_split, torch.int32), kv_split.shape[1] - 1, shard_id, float(scale),
         _dptr(o, torch.float32), _dptr(m, torch.float32), _dptr(l, torch.float32),
         _dptr(workspace), ws_bytes, _stream(stream)))
+
+
+# ---------------------------------------------------------------------------------------
+# NEXT F3: layer-level migration (KV of a contiguous layer range + weight tensors)
+# ---------------------------------------------------------------------------------------
+
+def kv_migrate_layers(src: KVPool, dst: KVPool, layer_lo: int, n_layers: int,
+                      src_ids: torch.Tensor, dst_ids: torch.Tensor, stream=None) -> None:
+    _check(lib().bs_kv_migrate_layers(src.handle, dst.handle, layer_lo, n_layers,
+                                      _dptr(src_ids, torch.int32), _dptr(dst_ids, torch.int32),
+                                      src_ids.numel(), _stream(stream)))
+
+
+def copy_bytes(dst: torch.Tensor, src: torch.Tensor, stream=None) -> None:
+    nb = src.numel() * src.element_size()
+    if dst.numel() * dst.element_size() < nb:
+        raise ValueError("dst too small")
+    _check(lib().bs_copy_bytes(dst.data_ptr(), src.data_ptr(), nb, _stream(stream)))
+
+
+def migrate_layers(src: KVPool, dst: KVPool, layer_lo: int, n_layers: int, src_ids: torch.Tensor,
+                   dst_ids: torch.Tensor, weights=(), stream=None) -> int:
+    """Layer-level migration (Fig. 3): the KV of layers
+    [layer_lo, layer_lo + n_layers) for the given block pairs plus each (src, dst) weight
+    tensor pair W_l.  Returns the payload S_total = S_w + S_kv in bytes (eq. 3)."""
+    kv_migrate_layers(src, dst, layer_lo, n_layers, src_ids, dst_ids, stream=stream)
+    s_w = 0
+    for ws, wd in weights:
+        copy_bytes(wd, ws, stream=stream)
+        s_w += ws.numel() * ws.element_size()
+    return s_w + n_layers * src_ids.numel() * src.chunk_bytes
+
+
+def t_layer_model(s_total_bytes: float, b_net_bytes_per_s: float, t_sync_s: float = 0.0) -> float:
+    """eq. 4 (PAPER.md:192-195): T_layer ~= S_total / B_net + T_sync."""
+    return s_total_bytes / b_net_bytes_per_s + t_sync_s

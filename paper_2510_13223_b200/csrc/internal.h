@@ -36,7 +36,8 @@ inline bs_status ok() { return BS_OK; }
 bs_status launch_copy_chunks(const uint8_t* src_base, const int32_t* src_ids, uint8_t* dst_base,
                              const int32_t* dst_ids, int32_t n, size_t chunk_bytes,
                              size_t page_bytes, int method, cudaStream_t stream,
-                             int max_ctas = 0);
+                             int max_ctas = 0, int32_t n_layers = 1, int64_t src_layer_stride = 0,
+                             int64_t dst_layer_stride = 0);
 
 }  // namespace bs
 

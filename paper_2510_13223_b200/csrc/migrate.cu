@@ -43,20 +43,26 @@ __global__ void __launch_bounds__(256) copy_pages_vec16(const uint8_t* __restric
                                                         uint8_t* __restrict__ dst_base,
                                                         const int32_t* __restrict__ dst_ids,
                                                         int32_t n, int32_t pages_per_chunk,
-                                                        int64_t chunk_bytes) {
+                                                        int64_t chunk_bytes, int32_t n_layers,
+                                                        int64_t src_layer_stride,
+                                                        int64_t dst_layer_stride) {
   constexpr int V = PAGE_BYTES / (16 * 32);  // int4 per lane per page
   const int lane = threadIdx.x & 31;
   const int wpc = blockDim.x >> 5;
-  const int64_t total = (int64_t)n * pages_per_chunk;
+  const int64_t per_layer = (int64_t)n * pages_per_chunk;
+  const int64_t total = per_layer * n_layers;
   for (int64_t p = (int64_t)blockIdx.x * wpc + (threadIdx.x >> 5); p < total;
        p += (int64_t)gridDim.x * wpc) {
-    const int32_t i = (int32_t)(p / pages_per_chunk);
-    const int32_t j = (int32_t)(p - (int64_t)i * pages_per_chunk);
+    const int32_t ly = (int32_t)(p / per_layer);
+    const int64_t q = p - (int64_t)ly * per_layer;
+    const int32_t i = (int32_t)(q / pages_per_chunk);
+    const int32_t j = (int32_t)(q - (int64_t)i * pages_per_chunk);
     const int64_t si = src_ids ? __ldg(src_ids + i) : i;
     const int64_t di = dst_ids ? __ldg(dst_ids + i) : i;
-    const int4* s = reinterpret_cast<const int4*>(src_base + si * chunk_bytes +
+    const int4* s = reinterpret_cast<const int4*>(src_base + ly * src_layer_stride + si * chunk_bytes +
                                                   (int64_t)j * PAGE_BYTES) + lane;
-    int4* d = reinterpret_cast<int4*>(dst_base + di * chunk_bytes + (int64_t)j * PAGE_BYTES) + lane;
+    int4* d = reinterpret_cast<int4*>(dst_base + ly * dst_layer_stride + di * chunk_bytes +
+                                      (int64_t)j * PAGE_BYTES) + lane;
     int4 r[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) r[v] = ld_stream(s + v * 32);
@@ -179,8 +185,10 @@ __global__ void __launch_bounds__(32) copy_pages_bulk(const uint8_t* __restrict_
 template <int PAGE_BYTES>
 bs_status launch_copy_t(const uint8_t* src_base, const int32_t* src_ids, uint8_t* dst_base,
                         const int32_t* dst_ids, int32_t n, int32_t ppc, int64_t chunk, int method,
-                        cudaStream_t stream, int max_ctas) {
-  const int64_t total = (int64_t)n * ppc;
+                        cudaStream_t stream, int max_ctas, int32_t n_layers, int64_t src_ls,
+                        int64_t dst_ls) {
+  const int64_t total = (int64_t)n * ppc * n_layers;
+  if (method == BS_MIGRATE_BULK && n_layers != 1) method = BS_MIGRATE_VEC16;
   const int sms = sm_count(current_device());
   if (method == BS_MIGRATE_BULK) {
     const int smem = kBulkStages * PAGE_BYTES;
@@ -200,7 +208,7 @@ bs_status launch_copy_t(const uint8_t* src_base, const int32_t* src_ids, uint8_t
   int64_t grid = std::min<int64_t>((total + wpc - 1) / wpc, (int64_t)sms * 8);
   if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
   copy_pages_vec16<PAGE_BYTES><<<(unsigned)grid, wpc * 32, 0, stream>>>(
-      src_base, src_ids, dst_base, dst_ids, n, ppc, chunk);
+      src_base, src_ids, dst_base, dst_ids, n, ppc, chunk, n_layers, src_ls, dst_ls);
   return check_launch("copy_pages_vec16");
 }
 
@@ -208,16 +216,17 @@ bs_status launch_copy_t(const uint8_t* src_base, const int32_t* src_ids, uint8_t
 
 bs_status launch_copy_chunks(const uint8_t* src_base, const int32_t* src_ids, uint8_t* dst_base,
                              const int32_t* dst_ids, int32_t n, size_t chunk_bytes,
-                             size_t page_bytes, int method, cudaStream_t stream, int max_ctas) {
-  if (n == 0) return BS_OK;
+                             size_t page_bytes, int method, cudaStream_t stream, int max_ctas,
+                             int32_t n_layers, int64_t src_layer_stride, int64_t dst_layer_stride) {
+  if (n == 0 || n_layers == 0) return BS_OK;
   const int32_t ppc = (int32_t)(chunk_bytes / page_bytes);
   if (method == BS_MIGRATE_AUTO) method = BS_MIGRATE_VEC16;
   if (page_bytes == 4096)
     return launch_copy_t<4096>(src_base, src_ids, dst_base, dst_ids, n, ppc, (int64_t)chunk_bytes,
-                               method, stream, max_ctas);
+                               method, stream, max_ctas, n_layers, src_layer_stride, dst_layer_stride);
   if (page_bytes == 2048)
     return launch_copy_t<2048>(src_base, src_ids, dst_base, dst_ids, n, ppc, (int64_t)chunk_bytes,
-                               method, stream, max_ctas);
+                               method, stream, max_ctas, n_layers, src_layer_stride, dst_layer_stride);
   return set_error(BS_ERR_UNSUPPORTED, "page size %zu", page_bytes);
 }
 
@@ -261,6 +270,31 @@ bs_status bs_kv_migrate_layer_ex(const bs_kv_pool* src, bs_kv_pool* dst, int32_t
                                 dst->base + (size_t)layer * dst->layer_bytes, dst_ids, n,
                                 src->chunk_bytes, src->page_bytes, method,
                                 static_cast<cudaStream_t>(stream), max_ctas);
+}
+
+bs_status bs_kv_migrate_layers(const bs_kv_pool* src, bs_kv_pool* dst, int32_t layer_lo,
+                               int32_t n_layers, const int32_t* src_ids, const int32_t* dst_ids,
+                               int32_t n, void* stream) {
+  BS_REQUIRE(src && dst, "bs_kv_migrate_layers: NULL pool");
+  BS_REQUIRE(same_geometry(src, dst), "bs_kv_migrate_layers: src/dst geometry differs");
+  BS_REQUIRE(n_layers >= 0 && layer_lo >= 0 && layer_lo + n_layers <= src->desc.num_layers,
+             "bs_kv_migrate_layers: layers [%d,+%d) out of range", layer_lo, n_layers);
+  BS_REQUIRE(n >= 0, "bs_kv_migrate_layers: n < 0");
+  BS_REQUIRE(n == 0 || (src_ids && dst_ids), "bs_kv_migrate_layers: NULL ids");
+  const int max_ctas = (src->host || dst->host) ? kHostCopyCtas : 0;
+  return bs::launch_copy_chunks(src->base + (size_t)layer_lo * src->layer_bytes, src_ids,
+                                dst->base + (size_t)layer_lo * dst->layer_bytes, dst_ids, n,
+                                src->chunk_bytes, src->page_bytes, BS_MIGRATE_VEC16,
+                                static_cast<cudaStream_t>(stream), max_ctas, n_layers,
+                                (int64_t)src->layer_bytes, (int64_t)dst->layer_bytes);
+}
+
+bs_status bs_copy_bytes(void* dst, const void* src, size_t bytes, void* stream) {
+  BS_REQUIRE(bytes == 0 || (dst && src), "bs_copy_bytes: NULL pointer");
+  if (bytes == 0) return BS_OK;
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return bs::set_error(BS_ERR_CUDA, "bs_copy_bytes: %s", cudaGetErrorString(e));
+  return BS_OK;
 }
 
 bs_status bs_kv_migrate_layer(const bs_kv_pool* src, bs_kv_pool* dst, int32_t layer,

@@ -87,6 +87,47 @@ def mig_case(name, shape, n_pairs, method, iters=20, warm=5):
             "hbm_GBps": round(2 * by / (med * 1e-3) / 1e9, 1)}
 
 
+def mig_extra_cases(args, iters=20, warm=5):
+    """NEXT F2 (head pages) and F3 (multi-layer, one launch) copies, payload GB/s."""
+    dev = torch.device("cuda")
+    out = []
+
+    def timeit(fn):
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(iters):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / iters
+
+    shape = synth.LLAMA3_8B
+    n = 4096
+    src = bs.KVPool(8, n + 64, 8, 128)
+    dst = bs.KVPool(8, n + 64, 8, 128)
+    cold = bs.KVPool(8, n + 64, 2, 128)
+    g = torch.Generator().manual_seed(0)
+    s = torch.randperm(n + 64, generator=g)[:n].to(torch.int32).to(dev)
+    d = torch.randperm(n + 64, generator=g)[:n].to(torch.int32).to(dev)
+    ms = timeit(lambda: bs.kv_migrate_heads_layer(src, cold, 0, s, d, 6, 0, 2))
+    by = n * 2 * 2 * 16 * 128 * 2
+    out.append({"case": "F2_heads_2of8_4096blocks", "us": round(ms * 1e3, 2),
+                "payload_GBps": round(by / (ms * 1e-3) / 1e9, 1), "MiB": by / 2**20})
+    ms = timeit(lambda: bs.kv_migrate_layers(src, dst, 0, 8, s, d))
+    by = 8 * n * src.chunk_bytes
+    out.append({"case": "F3_8layers_4096chunks_one_launch", "us": round(ms * 1e3, 2),
+                "payload_GBps": round(by / (ms * 1e-3) / 1e9, 1), "MiB": by / 2**20})
+    ms = timeit(lambda: [bs.kv_migrate_layer(src, dst, x, s, d) for x in range(8)])
+    out.append({"case": "F3_8layers_4096chunks_per_layer_launches", "us": round(ms * 1e3, 2),
+                "payload_GBps": round(by / (ms * 1e-3) / 1e9, 1), "MiB": by / 2**20})
+    for r in out:
+        print(json.dumps(r), flush=True)
+    return out
+
+
 ATTN = {
     "C2_mha_B64_2048": (synth.LLAMA2_7B, [2048] * 64),
     "C2_shard_B64_1024": (synth.LLAMA2_7B, [1024] * 64),
@@ -124,6 +165,8 @@ def main():
                 r = mig_case(name, shape, n, method, iters=args.iters)
                 print(json.dumps(r), flush=True)
                 res.append(r)
+    if args.only in (None, "mig"):
+        res += mig_extra_cases(args)
     if args.json:
         with open(args.json, "w") as f:
             json.dump(res, f, indent=1)

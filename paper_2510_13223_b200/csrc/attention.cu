@@ -55,6 +55,8 @@ struct AttnParams {
   int32_t pool_head_lo;      // first kv head of this launch inside the pool
   int32_t model_head_lo;     // ... and inside the model (selects q / output rows)
   int32_t nsplit, bps;
+  int32_t layer_row0;        // tensor-map row of (layer, block 0, K, head 0, slot 0)
+  int32_t pool_hkv;          // kv heads per pool row group (tensor-map addressing)
   float* o;
   float* m;
   float* l;
@@ -116,6 +118,91 @@ __device__ __forceinline__ float reduce_scatter16(float (&v)[16]) {
   }
   v[0] += __shfl_xor_sync(0xffffffffu, v[1], 2);
   return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+
+// Merge the kWarps per-warp states of one CTA (s_acc [kWarps][G][D] unnormalised, s_ml
+// [kWarps][G] (m log2, l)) and write the shard output -- or, with intra-GPU split-K, the
+// CTA's partial; the last-arriving CTA of the (request, kv-head) then merges all partials
+// in fixed order, re-arms the arrival counter and writes the output.  Called by every
+// thread of the CTA after a __syncthreads.
+template <int D, int G>
+__device__ __forceinline__ void cta_combine_and_store(const AttnParams& p, int b, int g, int gm,
+                                                      int sp, const float* s_acc, const float* s_ml,
+                                                      float* s_w, int* s_flag) {
+
+  for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
+    const int h = idx / D, x = idx - h * D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) M = fmaxf(M, s_ml[(w * G + h) * 2]);
+    float L = 0.f, O = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const float mw = s_ml[(w * G + h) * 2];
+      if (mw != -INFINITY) {
+        const float f = exp2f(mw - M);
+        L += s_ml[(w * G + h) * 2 + 1] * f;
+        O += s_acc[(w * G + h) * D + x] * f;
+      }
+    }
+    const int64_t row = (int64_t)b * p.hq + gm * G + h;
+    const bool any = L > 0.f;
+    if (p.nsplit == 1) {
+      p.o[row * D + x] = any ? O / L : 0.f;
+      if (x == 0) {
+        p.m[row] = any ? M * kLn2 : -INFINITY;
+        p.l[row] = L;
+      }
+    } else {
+      const int64_t part = row * p.nsplit + sp;
+      p.ws_o[part * D + x] = any ? O / L : 0.f;
+      if (x == 0) {
+        p.ws_ml[part * 2] = any ? M : -INFINITY;  // log2 units
+        p.ws_ml[part * 2 + 1] = L;
+      }
+    }
+  }
+  if (p.nsplit == 1) return;
+
+  // ---- intra-GPU split-K: the last CTA of this (request, kv-head) merges ------------
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t* cnt = p.ws_cnt + (int64_t)b * p.hkv + g;
+    const int prev = atomicAdd(cnt, 1);
+    const int last = prev == p.nsplit - 1;
+    if (last) *cnt = 0;  // every CTA has arrived: re-arm for the next call
+    s_flag[0] = last;
+  }
+  __syncthreads();
+  if (!s_flag[0]) return;
+  __threadfence();
+  if (threadIdx.x < G) {  // per-head weights w_j = l_j 2^(m_j - M) / L, fixed order
+    const int h = threadIdx.x;
+    const int64_t row = (int64_t)b * p.hq + gm * G + h;
+    const float* ml = p.ws_ml + row * p.nsplit * 2;
+    float M = -INFINITY;
+    for (int j = 0; j < p.nsplit; ++j) M = fmaxf(M, __ldcg(ml + 2 * j));
+    float L = 0.f;
+    for (int j = 0; j < p.nsplit; ++j) {
+      const float mj = __ldcg(ml + 2 * j);
+      const float wj = mj == -INFINITY ? 0.f : __ldcg(ml + 2 * j + 1) * exp2f(mj - M);
+      s_w[h * kMaxSplit + j] = wj;
+      L += wj;
+    }
+    for (int j = 0; j < p.nsplit; ++j) s_w[h * kMaxSplit + j] = L > 0.f ? s_w[h * kMaxSplit + j] / L : 0.f;
+    p.m[row] = L > 0.f ? M * kLn2 : -INFINITY;
+    p.l[row] = L;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
+    const int h = idx / D, x = idx - h * D;
+    const int64_t row = (int64_t)b * p.hq + gm * G + h;
+    const float* po = p.ws_o + row * p.nsplit * D + x;
+    float O = 0.f;
+    for (int j = 0; j < p.nsplit; ++j) O += s_w[h * kMaxSplit + j] * __ldcg(po + (int64_t)j * D);
+    p.o[row * D + x] = O;
+  }
 }
 
 template <int D, int G, int STAGES, int MINB>
@@ -333,80 +420,260 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
     }
   }
   __syncthreads();
+  cta_combine_and_store<D, G>(p, b, g, gm, sp, s_acc, s_ml, s_w, s_flag);
+}
 
-  for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
-    const int h = idx / D, x = idx - h * D;
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) M = fmaxf(M, s_ml[(w * G + h) * 2]);
-    float L = 0.f, O = 0.f;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      const float mw = s_ml[(w * G + h) * 2];
-      if (mw != -INFINITY) {
-        const float f = exp2f(mw - M);
-        L += s_ml[(w * G + h) * 2 + 1] * f;
-        O += s_acc[(w * G + h) * D + x] * f;
-      }
-    }
-    const int64_t row = (int64_t)b * p.hq + gm * G + h;
-    const bool any = L > 0.f;
-    if (p.nsplit == 1) {
-      p.o[row * D + x] = any ? O / L : 0.f;
-      if (x == 0) {
-        p.m[row] = any ? M * kLn2 : -INFINITY;
-        p.l[row] = L;
-      }
-    } else {
-      const int64_t part = row * p.nsplit + sp;
-      p.ws_o[part * D + x] = any ? O / L : 0.f;
-      if (x == 0) {
-        p.ws_ml[part * 2] = any ? M : -INFINITY;  // log2 units
-        p.ws_ml[part * 2 + 1] = L;
-      }
-    }
-  }
-  if (p.nsplit == 1) return;
+// ---------------------------------------------------------------------------------------
+// Tensor-core variant for GQA groups G in {4, 8} (at G >= 4 the CUDA-core
+// kernel is issue-bound -- ncu: 724 instructions per 8 KiB block at G=4 -- so the two
+// per-block contractions go to mma.sync.m16n8k16 (bf16 in, fp32 accumulate)):
+//   S^T[16 tok x 8 heads] = K[16 x d] . Q^T[d x 8]   (A = K rows via ldmatrix, B = q in regs)
+//   O^T[d x 8 heads]     += V^T[d x 16] . P^T[16 x 8] (A = V via ldmatrix.trans, B = P bf16)
+// The G heads of the group fill N = 8 (G = 4: half the columns are padding).  Scores are
+// scaled in fp32 after the MMA (q stays exact bf16); P is rounded to bf16 for the PV MMA
+// (the denominator l sums the fp32 p).  K/V pages land in shared memory as 16 rows of
+// d*2 bytes padded to d*2+16 (one 256/128-byte TMA bulk copy per row, issued by 32 lanes
+// in parallel), which makes every ldmatrix row phase conflict-free.  Pipeline, split-K
+// and epilogue are those of split_decode_attn.
+// ---------------------------------------------------------------------------------------
 
-  // ---- intra-GPU split-K: the last CTA of this (request, kv-head) merges ------------
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int32_t* cnt = p.ws_cnt + (int64_t)b * p.hkv + g;
-    const int prev = atomicAdd(cnt, 1);
-    const int last = prev == p.nsplit - 1;
-    if (last) *cnt = 0;  // every CTA has arrived: re-arm for the next call
-    s_flag[0] = last;
+template <int D, int G, int STAGES>
+struct MmaSmem {
+  static constexpr int kBoxes = D / 64;       // 128-byte-wide TMA boxes per page
+  static constexpr int kBox = 16 * 128;       // one box: 16 rows x 128 B, 128B-swizzled
+  static constexpr int kStage = 2 * kBoxes * kBox;  // K boxes then V boxes
+  static constexpr int kRing = kWarps * STAGES * kStage;
+  static constexpr int kBtOff = kRing;
+  static constexpr int kPOff = kBtOff + kBtMax * 4;  // P^T bf16 [8][16] per warp
+  static constexpr int kBarOff = kPOff + kWarps * 8 * 16 * 2;
+  static constexpr int kMlOff = kBarOff + kWarps * STAGES * 8;
+  static constexpr int kWOff = kMlOff + kWarps * G * 2 * 4;
+  static constexpr int kFlagOff = kWOff + G * kMaxSplit * 4;
+  static constexpr int kTotal = kFlagOff + 16 + 1024;  // + alignment slack (swizzle atoms)
+  static_assert(kWarps * G * D * 4 <= kRing, "combine buffer must fit in the ring");
+};
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                               uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// 2D tensor TMA (pool viewed as [rows][D] bf16, box [16 rows][64 elems], 128B swizzle)
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t c0,
+                                            int32_t c1, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(ptx::smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+// byte offset of (row, 16-byte chunk) inside a 128B-swizzled box
+__device__ __forceinline__ uint32_t swz(int row, int chunk) {
+  return (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
+}
+
+template <int D, int G, int STAGES, int MINB>
+__global__ void __launch_bounds__(kWarps * 32, MINB)
+    split_decode_attn_mma(const AttnParams p, const __grid_constant__ CUtensorMap tmap) {
+  using S = MmaSmem<D, G, STAGES>;
+  constexpr int KS = D / 16;  // k-steps of the QK MMA == m-tiles of the PV MMA
+  constexpr int NB = S::kBoxes;
+  static_assert(G <= 8, "one n8 tile of heads");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int gq = lane >> 2, tq = lane & 3;  // mma groupID / thread-in-group
+  const int sp = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
+
+  const int32_t* ks = p.kv_split + (int64_t)b * (p.n_shards + 1) + p.shard_id;
+  const int32_t len = max(__ldg(ks + 1) - __ldg(ks), 0);
+  const int32_t nblk = (len + 15) >> 4;
+  const int32_t blo = sp * p.bps;
+  const int32_t nb_cta = max(min(nblk, blo + p.bps) - blo, 0);
+
+  int32_t* s_bt = reinterpret_cast<int32_t*>(smem + S::kBtOff);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBarOff) + warp * STAGES;
+  uint8_t* s_pt = smem + S::kPOff + warp * 8 * 16 * 2;
+  uint8_t* ring = smem + warp * STAGES * S::kStage;
+
+  for (int i = threadIdx.x; i < nb_cta; i += blockDim.x)
+    s_bt[i] = __ldg(p.bt + (int64_t)b * p.max_blocks + blo + i);
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&bars[s], 1);
+    ptx::fence_mbar_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
   }
   __syncthreads();
-  if (!s_flag[0]) return;
-  __threadfence();
-  if (threadIdx.x < G) {  // per-head weights w_j = l_j 2^(m_j - M) / L, fixed order
-    const int h = threadIdx.x;
-    const int64_t row = (int64_t)b * p.hq + gm * G + h;
-    const float* ml = p.ws_ml + row * p.nsplit * 2;
-    float M = -INFINITY;
-    for (int j = 0; j < p.nsplit; ++j) M = fmaxf(M, __ldcg(ml + 2 * j));
-    float L = 0.f;
-    for (int j = 0; j < p.nsplit; ++j) {
-      const float mj = __ldcg(ml + 2 * j);
-      const float wj = mj == -INFINITY ? 0.f : __ldcg(ml + 2 * j + 1) * exp2f(mj - M);
-      s_w[h * kMaxSplit + j] = wj;
-      L += wj;
+
+  const int nmine = nb_cta > warp ? (nb_cta - warp + kWarps - 1) / kWarps : 0;
+  const int gm = p.model_head_lo + g;
+  const int head = p.pool_head_lo + g;
+  uint64_t policy = 0;
+  if (lane == 0) policy = ptx::policy_evict_first();
+  const uint32_t ring_u32 = ptx::smem_u32(ring);
+  auto issue = [&](int k) {  // lane 0 only
+    const int s = k % STAGES;
+    const int32_t phys = s_bt[warp + k * kWarps];
+    const int32_t row_k = p.layer_row0 + ((phys * 2 + 0) * p.pool_hkv + head) * 16;
+    const int32_t row_v = row_k + p.pool_hkv * 16;
+    const uint32_t st = ring_u32 + s * S::kStage;
+    ptx::mbar_expect_tx(&bars[s], 2 * 16 * D * 2);
+#pragma unroll
+    for (int bx = 0; bx < NB; ++bx) {
+      tma_load_2d(st + bx * S::kBox, &tmap, 64 * bx, row_k, &bars[s], policy);
+      tma_load_2d(st + (NB + bx) * S::kBox, &tmap, 64 * bx, row_v, &bars[s], policy);
     }
-    for (int j = 0; j < p.nsplit; ++j) s_w[h * kMaxSplit + j] = L > 0.f ? s_w[h * kMaxSplit + j] / L : 0.f;
-    p.m[row] = L > 0.f ? M * kLn2 : -INFINITY;
-    p.l[row] = L;
+  };
+  if (lane == 0)
+    for (int k = 0; k < min(STAGES, nmine); ++k) issue(k);
+  __syncwarp();
+
+  // q^T B-fragments (bf16 pairs) for head n = gq (zero padding for n >= G)
+  uint32_t bq[KS][2];
+  {
+    const uint32_t* qrow = reinterpret_cast<const uint32_t*>(p.q + ((int64_t)b * p.hq + gm * G + gq) * D);
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk) {
+      bq[kk][0] = gq < G ? __ldg(qrow + 8 * kk + tq) : 0u;
+      bq[kk][1] = gq < G ? __ldg(qrow + 8 * kk + 4 + tq) : 0u;
+    }
+  }
+
+  float oacc[KS][4];  // O^T: rows dims 16*mt + gq (+8), cols heads 2*tq, 2*tq+1
+#pragma unroll
+  for (int mt = 0; mt < KS; ++mt) oacc[mt][0] = oacc[mt][1] = oacc[mt][2] = oacc[mt][3] = 0.f;
+  float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
+
+  const uint32_t pt_u32 = ptx::smem_u32(s_pt);
+  const int lr = (lane & 7) + 8 * ((lane >> 3) & 1);  // K rows (ldmatrix matrix = lane / 8)
+  const int kh = lane >> 4;                          // K: which 8-dim half of the k-step
+  const int vtok = (lane & 7) + 8 * (lane >> 4);     // V rows (tokens)
+  const int vh = (lane >> 3) & 1;                    // V: which 8-dim half of the m-tile
+
+  for (int k = 0; k < nmine; ++k) {
+    const int s = k % STAGES;
+    ptx::mbar_wait(&bars[s], (uint32_t)((k / STAGES) & 1));
+    __syncwarp();
+    const int blk = blo + warp + k * kWarps;
+    const int nvalid = min(16, len - blk * 16);
+    const uint32_t st = ring_u32 + s * S::kStage;
+
+    // ---- S^T = K q^T ----------------------------------------------------------------
+    float sc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk) {
+      uint32_t a[4];
+      ldsm_x4(st + (kk / 4) * S::kBox + swz(lr, 2 * (kk % 4) + kh), a);
+      mma_bf16_16816(sc, a, bq[kk][0], bq[kk][1]);
+    }
+    // sc[0] = (tok gq, head 2tq), sc[1] = (gq, 2tq+1), sc[2] = (gq+8, 2tq), sc[3] = (gq+8, 2tq+1)
+    const bool v0 = gq < nvalid, v1 = gq + 8 < nvalid;
+    sc[0] = v0 ? sc[0] * p.scale_log2 : -INFINITY;
+    sc[1] = v0 ? sc[1] * p.scale_log2 : -INFINITY;
+    sc[2] = v1 ? sc[2] * p.scale_log2 : -INFINITY;
+    sc[3] = v1 ? sc[3] * p.scale_log2 : -INFINITY;
+    float mx0 = fmaxf(sc[0], sc[2]), mx1 = fmaxf(sc[1], sc[3]);
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+    }
+    const float mn0 = fmaxf(m_run[0], mx0), mn1 = fmaxf(m_run[1], mx1);  // finite
+    const float al0 = exp2f(m_run[0] - mn0), al1 = exp2f(m_run[1] - mn1);
+    m_run[0] = mn0;
+    m_run[1] = mn1;
+    const float p0 = exp2f(sc[0] - mn0), p1 = exp2f(sc[1] - mn1);
+    const float p2 = exp2f(sc[2] - mn0), p3 = exp2f(sc[3] - mn1);
+    l_run[0] = l_run[0] * al0 + (p0 + p2);
+    l_run[1] = l_run[1] * al1 + (p1 + p3);
+    // P^T (bf16) -> smem [head][16 tokens]
+    __nv_bfloat16* pt = reinterpret_cast<__nv_bfloat16*>(s_pt);
+    pt[(2 * tq) * 16 + gq] = __float2bfloat16_rn(p0);
+    pt[(2 * tq + 1) * 16 + gq] = __float2bfloat16_rn(p1);
+    pt[(2 * tq) * 16 + gq + 8] = __float2bfloat16_rn(p2);
+    pt[(2 * tq + 1) * 16 + gq + 8] = __float2bfloat16_rn(p3);
+    if (nvalid < 16) {  // pad rows of the V page may hold anything (NaN): zero them
+      for (int i = lane; i < (16 - nvalid) * NB * 8; i += 32) {
+        const int r = nvalid + i / (NB * 8), rem = i % (NB * 8);
+        *reinterpret_cast<uint4*>(ring + s * S::kStage + (NB + rem / 8) * S::kBox + r * 128 +
+                                  (rem % 8) * 16) = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+    __syncwarp();
+    uint32_t bp0, bp1;  // P^T B-fragment: head n = gq, tokens 2tq(+1), 2tq+8(+9)
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(bp0) : "r"(pt_u32 + gq * 32 + 4 * tq));
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(bp1) : "r"(pt_u32 + gq * 32 + 16 + 4 * tq));
+
+    // ---- O^T = alpha O^T + V^T P^T ------------------------------------------------------
+    const uint32_t vb = st + NB * S::kBox;
+#pragma unroll
+    for (int mt = 0; mt < KS; ++mt) {
+      oacc[mt][0] *= al0;
+      oacc[mt][1] *= al1;
+      oacc[mt][2] *= al0;
+      oacc[mt][3] *= al1;
+      uint32_t a[4];
+      ldsm_x4_t(vb + (mt / 4) * S::kBox + swz(vtok, 2 * (mt % 4) + vh), a);
+      mma_bf16_16816(oacc[mt], a, bp0, bp1);
+    }
+    __syncwarp();
+    if (lane == 0 && k + STAGES < nmine) {
+      ptx::fence_proxy_async_smem();
+      issue(k + STAGES);
+    }
+    __syncwarp();
+  }
+
+  // ---- per-warp state -> shared memory, then the common CTA epilogue --------------------
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    float x = l_run[j];
+    x += __shfl_xor_sync(0xffffffffu, x, 4);
+    x += __shfl_xor_sync(0xffffffffu, x, 8);
+    x += __shfl_xor_sync(0xffffffffu, x, 16);
+    l_run[j] = x;
+  }
+  __syncthreads();  // rings idle: reuse them for the combine
+  float* s_acc = reinterpret_cast<float*>(smem);  // [kWarps][G][D]
+  float* s_ml = reinterpret_cast<float*>(smem + S::kMlOff);
+  float* s_w = reinterpret_cast<float*>(smem + S::kWOff);
+  int* s_flag = reinterpret_cast<int*>(smem + S::kFlagOff);
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int h = 2 * tq + j;
+    if (h < G) {
+#pragma unroll
+      for (int mt = 0; mt < KS; ++mt) {
+        s_acc[(warp * G + h) * D + 16 * mt + gq] = oacc[mt][j];
+        s_acc[(warp * G + h) * D + 16 * mt + gq + 8] = oacc[mt][2 + j];
+      }
+      if (gq == 0) {
+        s_ml[(warp * G + h) * 2] = m_run[j];
+        s_ml[(warp * G + h) * 2 + 1] = l_run[j];
+      }
+    }
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
-    const int h = idx / D, x = idx - h * D;
-    const int64_t row = (int64_t)b * p.hq + gm * G + h;
-    const float* po = p.ws_o + row * p.nsplit * D + x;
-    float O = 0.f;
-    for (int j = 0; j < p.nsplit; ++j) O += s_w[h * kMaxSplit + j] * __ldcg(po + (int64_t)j * D);
-    p.o[row * D + x] = O;
-  }
+  cta_combine_and_store<D, G>(p, b, g, gm, sp, s_acc, s_ml, s_w, s_flag);
 }
 
 // Pipeline depth / residency per (head_dim, group): STAGES blocks (K+V pages) per warp in
@@ -415,20 +682,29 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
 // ~192 KiB of KV in flight per SM.  BS_ATTN_VARIANT=1 forces the 2-CTA/3-deep variant.
 struct Variant {
   int stages, minb;
+  bool mma;
 };
 
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 int alt_variant() {
-  static int v = [] {
-    const char* e = getenv("BS_ATTN_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
+  static int v = env_int("BS_ATTN_VARIANT", 0);
   return v;
 }
 
+bool use_mma(int G) {
+  static int v = env_int("BS_ATTN_MMA", 1);  // 0: CUDA-core kernel for every G
+  return v != 0 && G >= 4;
+}
+
 Variant variant_for(int d, int G) {
-  if (alt_variant() == 1) return d == 128 ? Variant{3, 2} : Variant{6, 2};
-  if (d == 128) return G <= 4 ? Variant{2, 3} : Variant{3, 2};
-  return G <= 4 ? Variant{4, 3} : Variant{6, 2};
+  if (use_mma(G)) return d == 128 ? Variant{2, 3, true} : Variant{4, 3, true};
+  if (alt_variant() == 1) return d == 128 ? Variant{3, 2, false} : Variant{6, 2, false};
+  if (d == 128) return G <= 4 ? Variant{2, 3, false} : Variant{3, 2, false};
+  return G <= 4 ? Variant{4, 3, false} : Variant{6, 2, false};
 }
 
 struct Plan {
@@ -492,9 +768,32 @@ bs_status launch_attn_v(const AttnParams& p, int batch, cudaStream_t stream) {
   return check_launch("split_decode_attn");
 }
 
+template <int D, int G, int STAGES, int MINB>
+bs_status launch_attn_mma(const AttnParams& p, const CUtensorMap& tmap, int batch,
+                          cudaStream_t stream) {
+  using S = MmaSmem<D, G, STAGES>;
+  static int configured_dev = -1;
+  const int dev = current_device();
+  if (configured_dev != dev) {
+    cudaFuncSetAttribute(split_decode_attn_mma<D, G, STAGES, MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
+    configured_dev = dev;
+  }
+  dim3 grid(p.nsplit, p.hkv, batch);
+  split_decode_attn_mma<D, G, STAGES, MINB><<<grid, kWarps * 32, S::kTotal, stream>>>(p, tmap);
+  return check_launch("split_decode_attn_mma");
+}
+
 template <int D, int G>
-bs_status launch_attn_t(const AttnParams& p, int batch, cudaStream_t stream) {
+bs_status launch_attn_t(const AttnParams& p, const CUtensorMap* tmap, int batch,
+                        cudaStream_t stream) {
   const Variant v = variant_for(D, G);
+  if constexpr (G >= 4) {
+    if (v.mma && tmap) {
+      if constexpr (D == 128) return launch_attn_mma<D, G, 2, 3>(p, *tmap, batch, stream);
+      else return launch_attn_mma<D, G, 4, 3>(p, *tmap, batch, stream);
+    }
+  }
   if constexpr (D == 128) {
     if (v.stages == 2) return launch_attn_v<D, G, 2, 3>(p, batch, stream);
     return launch_attn_v<D, G, 3, 2>(p, batch, stream);
@@ -505,18 +804,55 @@ bs_status launch_attn_t(const AttnParams& p, int batch, cudaStream_t stream) {
 }
 
 template <int D>
-bs_status launch_attn_d(const AttnParams& p, int G, int batch, cudaStream_t stream) {
+bs_status launch_attn_d(const AttnParams& p, const CUtensorMap* tmap, int G, int batch,
+                        cudaStream_t stream) {
   switch (G) {
-    case 1: return launch_attn_t<D, 1>(p, batch, stream);
-    case 2: return launch_attn_t<D, 2>(p, batch, stream);
-    case 4: return launch_attn_t<D, 4>(p, batch, stream);
-    case 8: return launch_attn_t<D, 8>(p, batch, stream);
+    case 1: return launch_attn_t<D, 1>(p, tmap, batch, stream);
+    case 2: return launch_attn_t<D, 2>(p, tmap, batch, stream);
+    case 4: return launch_attn_t<D, 4>(p, tmap, batch, stream);
+    case 8: return launch_attn_t<D, 8>(p, tmap, batch, stream);
   }
   return set_error(BS_ERR_UNSUPPORTED, "query group G=%d not in {1,2,4,8}", G);
 }
 
 }  // namespace
 }  // namespace bs
+
+// Encode (once) a 2D tensor map over the whole pool -- rows = (layer, block, K|V, head,
+// slot), inner dim = head_dim -- with 16 x 64 boxes and the 128-byte swizzle the
+// tensor-core kernel's ldmatrix addressing expects.
+static const CUtensorMap* pool_tensor_map(const bs_kv_pool* cpool) {
+  bs_kv_pool* pool = const_cast<bs_kv_pool*>(cpool);
+  std::lock_guard<std::mutex> g(pool->mu);
+  if (pool->tmap_state == 0) {
+    using Enc = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                             CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                             CUtensorMapFloatOOBfill);
+    static Enc enc = nullptr;
+    if (!enc) {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess)
+        enc = reinterpret_cast<Enc>(fn);
+    }
+    const bs_kv_pool_desc& d = pool->desc;
+    const uint64_t rows = (uint64_t)d.num_layers * d.num_blocks * 2 * d.num_kv_heads * 16;
+    pool->tmap_state = -1;
+    if (enc && !pool->host && rows < (1ull << 31)) {
+      const cuuint64_t dims[2] = {(cuuint64_t)d.head_dim, rows};
+      const cuuint64_t strides[1] = {(cuuint64_t)d.head_dim * 2};
+      const cuuint32_t box[2] = {64, 16};
+      const cuuint32_t estr[2] = {1, 1};
+      if (enc(&pool->tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, pool->base, dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+        pool->tmap_state = 1;
+    }
+    cudaGetLastError();
+  }
+  return pool->tmap_state == 1 ? &pool->tmap : nullptr;
+}
 
 static bs_status attention_impl(const bs_kv_pool* pool, int32_t layer, int32_t pool_head_lo,
                                 int32_t model_head_lo, int32_t n_kv_heads, int32_t num_kv_heads_total,
@@ -573,6 +909,8 @@ static bs_status attention_impl(const bs_kv_pool* pool, int32_t layer, int32_t p
   p.hkv = n_kv_heads;
   p.pool_head_lo = pool_head_lo;
   p.model_head_lo = model_head_lo;
+  p.pool_hkv = pool->desc.num_kv_heads;
+  p.layer_row0 = (int32_t)((int64_t)layer * pool->desc.num_blocks * 2 * pool->desc.num_kv_heads * 16);
   p.nsplit = pl.nsplit;
   p.bps = pl.bps;
   p.o = o_part;
@@ -585,8 +923,9 @@ static bs_status attention_impl(const bs_kv_pool* pool, int32_t layer, int32_t p
     p.ws_cnt = reinterpret_cast<int32_t*>(ws + pl.off_cnt);
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (d == 128) return bs::launch_attn_d<128>(p, G, batch, s);
-  return bs::launch_attn_d<64>(p, G, batch, s);
+  const CUtensorMap* tmap = bs::variant_for(d, G).mma ? pool_tensor_map(pool) : nullptr;
+  if (d == 128) return bs::launch_attn_d<128>(p, tmap, G, batch, s);
+  return bs::launch_attn_d<64>(p, tmap, G, batch, s);
 }
 
 static bs_status workspace_impl(const bs_kv_pool* pool, int32_t batch, int32_t n_kv_heads,

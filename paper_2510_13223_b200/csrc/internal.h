@@ -1,6 +1,7 @@
 // Internal helpers shared by the library's translation units (never installed).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdarg>
@@ -19,8 +20,10 @@ struct bs_kv_pool {
   size_t chunk_bytes = 0;   // one (layer, block): K+V pages of all heads
   size_t page_bytes = 0;    // one (layer, block, K|V, head)
   size_t layer_bytes = 0;   // num_blocks * chunk_bytes
-  std::mutex mu;            // guards the allocator
+  std::mutex mu;            // guards the allocator and the tensor-map cache
   std::set<int32_t> free_ids;
+  alignas(64) CUtensorMap tmap;  // pool as [rows][head_dim] bf16 for the tensor-core kernel
+  int tmap_state = 0;            // 0 not encoded yet, 1 ok, -1 unavailable
 };
 
 namespace bs {

@@ -5,7 +5,8 @@ Tolerances (BASELINE.json north_star, reading R-A15):
   migration                  bit-exact (byte equality of whole pools)
   merged attention output    max |d| <= 2e-2 and per-row max|d| / max|ref| <= 1e-2 (bf16 out)
   merged / per-shard lse     |d| <= 1e-4 (natural log)
-  per-shard o~ (fp32)        |d| <= 1e-3 (reported tighter than the bar; fp32 accumulate)
+  per-shard o~ (fp32)        |d| <= 5e-3 (tighter than the bar; the tensor-core variant for
+                             G >= 4 rounds p to bf16 for the PV product: 2^-9 relative)
 """
 import numpy as np
 import pytest
@@ -16,7 +17,7 @@ import synth
 
 pytestmark = pytest.mark.gpu
 
-ABS_TOL, ROW_REL_TOL, LSE_TOL, PART_TOL = 2e-2, 1e-2, 1e-4, 1e-3
+ABS_TOL, ROW_REL_TOL, LSE_TOL, PART_TOL = 2e-2, 1e-2, 1e-4, 5e-3
 
 
 @pytest.fixture(scope="module")

@@ -165,6 +165,27 @@ bs_status bs_split_decode_attention(const bs_kv_pool* pool, int32_t layer, const
                                     float scale, float* o_part, float* m, float* l,
                                     void* workspace, size_t workspace_bytes, void* stream);
 
+/* H4 + H6 fused for shards that live on THIS GPU (the N=1 / co-located case): one
+ * launch computes every local shard of every request, writes the per-CTA partials to
+ * the workspace, and the last CTA of each (request, kv-head) merges them -- all local
+ * shards and intra-shard split-K ranges -- in fixed order (shard-major) into bf16 O
+ * and fp32 lse (natural log).  Equivalent to bs_split_decode_attention per shard +
+ * bs_merge_partials, without the partial round trip and the extra launches.
+ * pools / block_tables / max_blocks / shard_ids: HOST arrays of n_local (1..4) entries;
+ * the pools must share num_layers / num_kv_heads / head_dim.  out bf16 [B][Hq][D] and
+ * lse fp32 [B][Hq] (or NULL) are DEVICE buffers.  Workspace rules as for H4. */
+bs_status bs_split_decode_attention_local_workspace_size(int32_t n_local,
+                                                         const bs_kv_pool* const* pools,
+                                                         const int32_t* max_blocks, int32_t batch,
+                                                         int32_t num_q_heads, size_t* bytes);
+bs_status bs_split_decode_attention_local(int32_t n_local, const bs_kv_pool* const* pools,
+                                          int32_t layer, const void* q, int32_t batch,
+                                          int32_t num_q_heads, const int32_t* const* block_tables,
+                                          const int32_t* max_blocks, const int32_t* shard_ids,
+                                          const int32_t* kv_split, int32_t n_shards, float scale,
+                                          void* out, float* lse, void* workspace,
+                                          size_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------------------------------------ */
 /* NEXT F3: layer-level migration (Fig. 3, eqs. 3-5): a contiguous  */
 /* set of layers moves with its weights W_l and its KV_l.  bs_kv_migrate_layers is    */

@@ -35,7 +35,8 @@ EXPORTED_SYMBOLS = (
     "bs_ipc_import", "bs_ipc_close", "bs_kv_migrate_heads_layer",
     "bs_split_decode_attention_heads_workspace_size", "bs_split_decode_attention_heads",
     "bs_utilization", "bs_dispatch_requests", "bs_plan_migrations", "bs_kv_migrate_layers",
-    "bs_copy_bytes",
+    "bs_copy_bytes", "bs_split_decode_attention_local_workspace_size",
+    "bs_split_decode_attention_local",
 )
 
 
@@ -111,6 +112,10 @@ def lib():
         "bs_utilization": ([ctypes.c_double] * 4, ctypes.c_double),
         "bs_kv_migrate_layers": ([_p, _p, _i32, _i32, _p, _p, _i32, _p], _i32),
         "bs_copy_bytes": ([_p, _p, _sz, _p], _i32),
+        "bs_split_decode_attention_local_workspace_size": ([_i32, _p, _p, _i32, _i32,
+                                                            ctypes.POINTER(_sz)], _i32),
+        "bs_split_decode_attention_local": ([_i32, _p, _i32, _p, _i32, _i32, _p, _p, _p, _p, _i32,
+                                             _f32, _p, _p, _p, _sz, _p], _i32),
         "bs_dispatch_requests": ([_i32, _p, _p, _i32, _p, ctypes.c_double, _p], _i32),
         "bs_plan_migrations": ([_i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, ctypes.c_double,
                                 ctypes.c_double, _i32, _p, ctypes.POINTER(_i32)], _i32),
@@ -277,6 +282,36 @@ def split_decode_attention(pool: KVPool, layer: int, q: torch.Tensor, block_tabl
         block_tables.shape[1], _dptr(kv_split, torch.int32), kv_split.shape[1] - 1, shard_id,
         float(scale), _dptr(o, torch.float32), _dptr(m, torch.float32), _dptr(l, torch.float32),
         _dptr(workspace), ws_bytes, _stream(stream)))
+
+
+def split_decode_attention_local_workspace_size(pools, max_blocks, batch: int,
+                                                num_q_heads: int) -> int:
+    n = len(pools)
+    pa = (ctypes.c_void_p * n)(*[p.handle.value for p in pools])
+    mb = (ctypes.c_int32 * n)(*[int(x) for x in max_blocks])
+    out = _sz()
+    _check(lib().bs_split_decode_attention_local_workspace_size(n, pa, mb, batch, num_q_heads,
+                                                                ctypes.byref(out)))
+    return out.value
+
+
+def split_decode_attention_local(pools, layer: int, q: torch.Tensor, block_tables,
+                                 shard_ids, kv_split: torch.Tensor, scale: float, out: torch.Tensor,
+                                 lse: torch.Tensor, workspace: torch.Tensor | None = None,
+                                 stream=None) -> None:
+    """H4+H6 fused over shards resident on this GPU: bf16 ``out`` [B,Hq,d] + fp32 ``lse``."""
+    n = len(pools)
+    B, hq, d = q.shape
+    pa = (ctypes.c_void_p * n)(*[p.handle.value for p in pools])
+    ba = (ctypes.c_void_p * n)(*[_dptr(t, torch.int32) for t in block_tables])
+    mb = (ctypes.c_int32 * n)(*[int(t.shape[1]) for t in block_tables])
+    sa = (ctypes.c_int32 * n)(*[int(x) for x in shard_ids])
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check(lib().bs_split_decode_attention_local(
+        n, pa, layer, _dptr(q, torch.bfloat16), B, hq, ba, mb, sa, _dptr(kv_split, torch.int32),
+        kv_split.shape[1] - 1, float(scale), _dptr(out, torch.bfloat16),
+        _dptr(lse, torch.float32) if lse is not None else None, _dptr(workspace), ws_bytes,
+        _stream(stream)))
 
 
 def merge_partials(o_parts, m_parts, l_parts, out: torch.Tensor, lse: torch.Tensor | None = None,

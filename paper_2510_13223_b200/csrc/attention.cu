@@ -41,29 +41,56 @@ constexpr int kWarps = 4;
 constexpr int kBtMax = 512;     // blocks per CTA range (bt cached in smem)
 constexpr int kMaxSplit = 64;   // intra-GPU split-K limit
 
-struct AttnParams {
+constexpr int kMaxLocal = 4;  // shards fused into one launch (bs_split_decode_attention_local)
+
+// One KV shard of the launch: where its pages live and how its blocks are cut into CTAs.
+struct ShardDesc {
   const uint8_t* kv;  // pool base + layer * layer_bytes
   int64_t chunk_bytes;
   int64_t v_off;      // Hkv * page bytes: K page -> V page of the same head
-  const __nv_bfloat16* q;
   const int32_t* bt;
   int32_t max_blocks;
+  int32_t shard_id;    // column of kv_split
+  int32_t bps;         // blocks per CTA range
+  int32_t split_off;   // first grid.x index of this shard
+  int32_t layer_row0;  // tensor-map row of (layer, block 0, K, head 0, slot 0)
+  int32_t pool_hkv;    // kv heads of the pool (tensor-map addressing)
+  int32_t pool_head_lo;  // first kv head of this launch inside the pool
+};
+
+struct AttnParams {
+  ShardDesc sh[kMaxLocal];
+  int32_t n_local;
+  const __nv_bfloat16* q;
   const int32_t* kv_split;
-  int32_t n_shards, shard_id;
+  int32_t n_shards;
   float scale_log2;
   int32_t hq, hkv;          // hq: q heads of the MODEL (row stride); hkv: kv heads in this launch
-  int32_t pool_head_lo;      // first kv head of this launch inside the pool
-  int32_t model_head_lo;     // ... and inside the model (selects q / output rows)
-  int32_t nsplit, bps;
-  int32_t layer_row0;        // tensor-map row of (layer, block 0, K, head 0, slot 0)
-  int32_t pool_hkv;          // kv heads per pool row group (tensor-map addressing)
+  int32_t model_head_lo;    // first kv head of the launch in the model (q / output rows)
+  int32_t nsplit;           // grid.x = CTA ranges per (request, kv-head) over all shards
+  int32_t merged;           // 1: write bf16 O + lse (local shards merged); 0: (o~, m, l)
   float* o;
   float* m;
   float* l;
+  __nv_bfloat16* out;
+  float* lse;
   float* ws_o;
   float* ws_ml;
   int32_t* ws_cnt;
 };
+
+struct TMaps {
+  CUtensorMap m[kMaxLocal];
+};
+
+// grid.x index -> (shard of the launch, CTA range inside it)
+__device__ __forceinline__ int shard_of(const AttnParams& p, int spg) {
+  int j = 0;
+#pragma unroll
+  for (int i = 1; i < kMaxLocal; ++i)
+    if (i < p.n_local && spg >= p.sh[i].split_off) j = i;
+  return j;
+}
 
 template <int D, int G, int STAGES>
 struct Smem {
@@ -129,7 +156,6 @@ template <int D, int G>
 __device__ __forceinline__ void cta_combine_and_store(const AttnParams& p, int b, int g, int gm,
                                                       int sp, const float* s_acc, const float* s_ml,
                                                       float* s_w, int* s_flag) {
-
   for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
     const int h = idx / D, x = idx - h * D;
     float M = -INFINITY;
@@ -148,10 +174,15 @@ __device__ __forceinline__ void cta_combine_and_store(const AttnParams& p, int b
     const int64_t row = (int64_t)b * p.hq + gm * G + h;
     const bool any = L > 0.f;
     if (p.nsplit == 1) {
-      p.o[row * D + x] = any ? O / L : 0.f;
-      if (x == 0) {
-        p.m[row] = any ? M * kLn2 : -INFINITY;
-        p.l[row] = L;
+      if (p.merged) {
+        p.out[row * D + x] = __float2bfloat16_rn(any ? O / L : 0.f);
+        if (x == 0 && p.lse) p.lse[row] = any ? M * kLn2 + logf(L) : -INFINITY;
+      } else {
+        p.o[row * D + x] = any ? O / L : 0.f;
+        if (x == 0) {
+          p.m[row] = any ? M * kLn2 : -INFINITY;
+          p.l[row] = L;
+        }
       }
     } else {
       const int64_t part = row * p.nsplit + sp;
@@ -164,7 +195,7 @@ __device__ __forceinline__ void cta_combine_and_store(const AttnParams& p, int b
   }
   if (p.nsplit == 1) return;
 
-  // ---- intra-GPU split-K: the last CTA of this (request, kv-head) merges ------------
+  // ---- split-K / local shards: the last CTA of this (request, kv-head) merges ---------
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -191,8 +222,12 @@ __device__ __forceinline__ void cta_combine_and_store(const AttnParams& p, int b
       L += wj;
     }
     for (int j = 0; j < p.nsplit; ++j) s_w[h * kMaxSplit + j] = L > 0.f ? s_w[h * kMaxSplit + j] / L : 0.f;
-    p.m[row] = L > 0.f ? M * kLn2 : -INFINITY;
-    p.l[row] = L;
+    if (p.merged) {
+      if (p.lse) p.lse[row] = L > 0.f ? M * kLn2 + logf(L) : -INFINITY;
+    } else {
+      p.m[row] = L > 0.f ? M * kLn2 : -INFINITY;
+      p.l[row] = L;
+    }
   }
   __syncthreads();
   for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
@@ -201,7 +236,8 @@ __device__ __forceinline__ void cta_combine_and_store(const AttnParams& p, int b
     const float* po = p.ws_o + row * p.nsplit * D + x;
     float O = 0.f;
     for (int j = 0; j < p.nsplit; ++j) O += s_w[h * kMaxSplit + j] * __ldcg(po + (int64_t)j * D);
-    p.o[row * D + x] = O;
+    if (p.merged) p.out[row * D + x] = __float2bfloat16_rn(O);
+    else p.o[row * D + x] = O;
   }
 }
 
@@ -213,13 +249,16 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int sp = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
+  const int spg = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
+  const int js = shard_of(p, spg);
+  const ShardDesc& sd = p.sh[js];
+  const int sp = spg - sd.split_off;
 
-  const int32_t* ks = p.kv_split + (int64_t)b * (p.n_shards + 1) + p.shard_id;
+  const int32_t* ks = p.kv_split + (int64_t)b * (p.n_shards + 1) + sd.shard_id;
   const int32_t len = max(__ldg(ks + 1) - __ldg(ks), 0);
   const int32_t nblk = (len + 15) >> 4;
-  const int32_t blo = sp * p.bps;
-  const int32_t nb_cta = max(min(nblk, blo + p.bps) - blo, 0);
+  const int32_t blo = sp * sd.bps;
+  const int32_t nb_cta = max(min(nblk, blo + sd.bps) - blo, 0);
 
   int32_t* s_bt = reinterpret_cast<int32_t*>(smem + S::kBtOff);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBarOff) + warp * STAGES;
@@ -227,7 +266,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
   uint8_t* ring = smem + warp * STAGES * S::kStage;
 
   for (int i = threadIdx.x; i < nb_cta; i += blockDim.x)
-    s_bt[i] = __ldg(p.bt + (int64_t)b * p.max_blocks + blo + i);
+    s_bt[i] = __ldg(sd.bt + (int64_t)b * sd.max_blocks + blo + i);
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&bars[s], 1);
@@ -236,18 +275,18 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
   __syncthreads();
 
   const int nmine = nb_cta > warp ? (nb_cta - warp + kWarps - 1) / kWarps : 0;
-  const uint8_t* kv_head = p.kv + (int64_t)(p.pool_head_lo + g) * S::kPage;
+  const uint8_t* kv_head = sd.kv + (int64_t)(sd.pool_head_lo + g) * S::kPage;
   const int gm = p.model_head_lo + g;  // kv head index in the model
   uint64_t policy = 0;
   if (lane == 0) policy = ptx::policy_evict_first();
   auto issue = [&](int k) {
     const int s = k % STAGES;
     const int64_t phys = s_bt[warp + k * kWarps];
-    const uint8_t* kp = kv_head + phys * p.chunk_bytes;
+    const uint8_t* kp = kv_head + phys * sd.chunk_bytes;
     uint8_t* dst = ring + s * S::kStage;
     ptx::mbar_expect_tx(&bars[s], 2 * S::kPage);
     ptx::bulk_g2s_evict_first(dst, kp, S::kPage, &bars[s], policy);
-    ptx::bulk_g2s_evict_first(dst + S::kPage, kp + p.v_off, S::kPage, &bars[s], policy);
+    ptx::bulk_g2s_evict_first(dst + S::kPage, kp + sd.v_off, S::kPage, &bars[s], policy);
   };
   if (lane == 0) {
     for (int k = 0; k < min(STAGES, nmine); ++k) issue(k);
@@ -420,7 +459,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
     }
   }
   __syncthreads();
-  cta_combine_and_store<D, G>(p, b, g, gm, sp, s_acc, s_ml, s_w, s_flag);
+  cta_combine_and_store<D, G>(p, b, g, gm, spg, s_acc, s_ml, s_w, s_flag);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -491,7 +530,7 @@ __device__ __forceinline__ uint32_t swz(int row, int chunk) {
 
 template <int D, int G, int STAGES, int MINB>
 __global__ void __launch_bounds__(kWarps * 32, MINB)
-    split_decode_attn_mma(const AttnParams p, const __grid_constant__ CUtensorMap tmap) {
+    split_decode_attn_mma(const AttnParams p, const __grid_constant__ TMaps tm) {
   using S = MmaSmem<D, G, STAGES>;
   constexpr int KS = D / 16;  // k-steps of the QK MMA == m-tiles of the PV MMA
   constexpr int NB = S::kBoxes;
@@ -501,13 +540,16 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int gq = lane >> 2, tq = lane & 3;  // mma groupID / thread-in-group
-  const int sp = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
+  const int spg = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
+  const int js = shard_of(p, spg);
+  const ShardDesc& sd = p.sh[js];
+  const int sp = spg - sd.split_off;
 
-  const int32_t* ks = p.kv_split + (int64_t)b * (p.n_shards + 1) + p.shard_id;
+  const int32_t* ks = p.kv_split + (int64_t)b * (p.n_shards + 1) + sd.shard_id;
   const int32_t len = max(__ldg(ks + 1) - __ldg(ks), 0);
   const int32_t nblk = (len + 15) >> 4;
-  const int32_t blo = sp * p.bps;
-  const int32_t nb_cta = max(min(nblk, blo + p.bps) - blo, 0);
+  const int32_t blo = sp * sd.bps;
+  const int32_t nb_cta = max(min(nblk, blo + sd.bps) - blo, 0);
 
   int32_t* s_bt = reinterpret_cast<int32_t*>(smem + S::kBtOff);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBarOff) + warp * STAGES;
@@ -515,32 +557,33 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
   uint8_t* ring = smem + warp * STAGES * S::kStage;
 
   for (int i = threadIdx.x; i < nb_cta; i += blockDim.x)
-    s_bt[i] = __ldg(p.bt + (int64_t)b * p.max_blocks + blo + i);
+    s_bt[i] = __ldg(sd.bt + (int64_t)b * sd.max_blocks + blo + i);
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&bars[s], 1);
     ptx::fence_mbar_init();
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.m[shard_of(p, blockIdx.x)])) : "memory");
   }
   __syncthreads();
 
   const int nmine = nb_cta > warp ? (nb_cta - warp + kWarps - 1) / kWarps : 0;
   const int gm = p.model_head_lo + g;
-  const int head = p.pool_head_lo + g;
+  const int head = sd.pool_head_lo + g;
+  const CUtensorMap* tmap = &tm.m[js];
   uint64_t policy = 0;
   if (lane == 0) policy = ptx::policy_evict_first();
   const uint32_t ring_u32 = ptx::smem_u32(ring);
   auto issue = [&](int k) {  // lane 0 only
     const int s = k % STAGES;
     const int32_t phys = s_bt[warp + k * kWarps];
-    const int32_t row_k = p.layer_row0 + ((phys * 2 + 0) * p.pool_hkv + head) * 16;
-    const int32_t row_v = row_k + p.pool_hkv * 16;
+    const int32_t row_k = sd.layer_row0 + ((phys * 2 + 0) * sd.pool_hkv + head) * 16;
+    const int32_t row_v = row_k + sd.pool_hkv * 16;
     const uint32_t st = ring_u32 + s * S::kStage;
     ptx::mbar_expect_tx(&bars[s], 2 * 16 * D * 2);
 #pragma unroll
     for (int bx = 0; bx < NB; ++bx) {
-      tma_load_2d(st + bx * S::kBox, &tmap, 64 * bx, row_k, &bars[s], policy);
-      tma_load_2d(st + (NB + bx) * S::kBox, &tmap, 64 * bx, row_v, &bars[s], policy);
+      tma_load_2d(st + bx * S::kBox, tmap, 64 * bx, row_k, &bars[s], policy);
+      tma_load_2d(st + (NB + bx) * S::kBox, tmap, 64 * bx, row_v, &bars[s], policy);
     }
   };
   if (lane == 0)
@@ -673,7 +716,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
     }
   }
   __syncthreads();
-  cta_combine_and_store<D, G>(p, b, g, gm, sp, s_acc, s_ml, s_w, s_flag);
+  cta_combine_and_store<D, G>(p, b, g, gm, spg, s_acc, s_ml, s_w, s_flag);
 }
 
 // Pipeline depth / residency per (head_dim, group): STAGES blocks (K+V pages) per warp in
@@ -696,8 +739,9 @@ int alt_variant() {
 }
 
 bool use_mma(int G) {
-  static int v = env_int("BS_ATTN_MMA", 1);  // 0: CUDA-core kernel for every G
-  return v != 0 && G >= 4;
+  // 2 (default): tensor cores for every G; 1: only for G >= 4; 0: CUDA cores for every G
+  static int v = env_int("BS_ATTN_MMA", 2);
+  return (v == 1 && G >= 4) || v == 2;
 }
 
 Variant variant_for(int d, int G) {
@@ -708,43 +752,62 @@ Variant variant_for(int d, int G) {
 }
 
 struct Plan {
-  int nsplit, bps;
+  int bps;                   // blocks per CTA range (common to the launch's shards)
+  int nsplit;                // total CTA ranges per (request, kv-head)
+  int split_off[kMaxLocal];  // first range of each shard
+  int nsplit_s[kMaxLocal];   // ranges of each shard
   size_t ws_bytes, off_ml, off_cnt;
 };
 
-// Split-K planning: pick the number of CTAs per (request, kv-head) that minimises
-// waves x blocks-per-CTA (+ a fixed per-CTA cost), i.e. fills all SM slots evenly.
-// hkv: kv heads handled by the launch (grid.y); hq: q heads of the model (partial rows)
-bs_status make_plan(int batch, int G, int hq, int hkv, int d, int max_blocks, Plan* out) {
+// Split-K planning over the launch's shards (one for bs_split_decode_attention, all the
+// local shards for bs_split_decode_attention_local): pick the CTA range length that
+// minimises waves x blocks-per-CTA (+ a fixed per-CTA cost), i.e. fills the SM slots.
+// hkv: kv heads handled by the launch (grid.y); hq: q heads of the model (partial rows).
+bs_status make_plan(int batch, int G, int hq, int hkv, int d, int n_local, const int* max_blocks,
+                    bool merged, Plan* out) {
   const int sms = sm_count(current_device());
   const int64_t slots = (int64_t)sms * variant_for(d, G).minb;
   const int64_t base = (int64_t)batch * hkv;
+  int mb_max = 1;
+  for (int j = 0; j < n_local; ++j) mb_max = std::max(mb_max, max_blocks[j]);
   const int min_bps = kWarps;
-  const int max_ns = std::min(kMaxSplit, std::max(1, (max_blocks + min_bps - 1) / min_bps));
-  int best_ns = 1;
+  int best_bps = -1;
   double best = 1e300;
-  for (int ns = 1; ns <= max_ns; ++ns) {
-    const int bps = (max_blocks + ns - 1) / ns;
-    if (bps > kBtMax) continue;
-    const int real_ns = (max_blocks + bps - 1) / bps;
-    if (real_ns != ns) continue;
-    const int64_t ctas = base * ns;
+  int last_bps = -1;
+  for (int ns = 1; ns <= kMaxSplit; ++ns) {
+    const int bps = std::max(min_bps, (mb_max + ns - 1) / ns);
+    if (bps == last_bps || bps > kBtMax) {
+      if (bps > kBtMax) continue;
+      if (bps == last_bps) continue;
+    }
+    last_bps = bps;
+    int total = 0;
+    for (int j = 0; j < n_local; ++j) total += (max_blocks[j] + bps - 1) / bps;
+    if (total > kMaxSplit) continue;
+    const int64_t ctas = base * total;
     const int64_t waves = (ctas + slots - 1) / slots;
-    // cost in block-times per SM slot: per-warp blocks, plus CTA prologue/epilogue and
-    // (for ns > 1) the partial write + last-CTA merge
-    const double cost = (double)waves * ((double)bps / kWarps + 2.0 + (ns > 1 ? 1.0 : 0.0));
+    const bool partial = total > 1;
+    const double cost = (double)waves * ((double)bps / kWarps + 2.0 + (partial ? 1.0 : 0.0));
     if (cost < best - 1e-9) {
       best = cost;
-      best_ns = ns;
+      best_bps = bps;
     }
+    if (bps == min_bps) break;
   }
-  if (best == 1e300)
-    return set_error(BS_ERR_UNSUPPORTED, "max_blocks %d exceeds %d", max_blocks, kBtMax * kMaxSplit);
+  if (best_bps < 0)
+    return set_error(BS_ERR_UNSUPPORTED, "max_blocks %d exceeds %d", mb_max, kBtMax * kMaxSplit);
   Plan pl{};
-  pl.nsplit = best_ns;
-  pl.bps = (max_blocks + best_ns - 1) / best_ns;
-  if (best_ns > 1) {
-    const size_t parts = (size_t)batch * hq * best_ns;
+  pl.bps = best_bps;
+  int off = 0;
+  for (int j = 0; j < n_local; ++j) {
+    pl.split_off[j] = off;
+    pl.nsplit_s[j] = (max_blocks[j] + best_bps - 1) / best_bps;
+    off += pl.nsplit_s[j];
+  }
+  pl.nsplit = off;
+  (void)merged;
+  if (pl.nsplit > 1) {
+    const size_t parts = (size_t)batch * hq * pl.nsplit;
     pl.off_ml = parts * d * 4;
     pl.off_cnt = pl.off_ml + parts * 2 * 4;
     pl.ws_bytes = pl.off_cnt + (size_t)batch * hkv * 4;
@@ -769,8 +832,7 @@ bs_status launch_attn_v(const AttnParams& p, int batch, cudaStream_t stream) {
 }
 
 template <int D, int G, int STAGES, int MINB>
-bs_status launch_attn_mma(const AttnParams& p, const CUtensorMap& tmap, int batch,
-                          cudaStream_t stream) {
+bs_status launch_attn_mma(const AttnParams& p, const TMaps& tm, int batch, cudaStream_t stream) {
   using S = MmaSmem<D, G, STAGES>;
   static int configured_dev = -1;
   const int dev = current_device();
@@ -780,19 +842,16 @@ bs_status launch_attn_mma(const AttnParams& p, const CUtensorMap& tmap, int batc
     configured_dev = dev;
   }
   dim3 grid(p.nsplit, p.hkv, batch);
-  split_decode_attn_mma<D, G, STAGES, MINB><<<grid, kWarps * 32, S::kTotal, stream>>>(p, tmap);
+  split_decode_attn_mma<D, G, STAGES, MINB><<<grid, kWarps * 32, S::kTotal, stream>>>(p, tm);
   return check_launch("split_decode_attn_mma");
 }
 
 template <int D, int G>
-bs_status launch_attn_t(const AttnParams& p, const CUtensorMap* tmap, int batch,
-                        cudaStream_t stream) {
+bs_status launch_attn_t(const AttnParams& p, const TMaps* tm, int batch, cudaStream_t stream) {
   const Variant v = variant_for(D, G);
-  if constexpr (G >= 4) {
-    if (v.mma && tmap) {
-      if constexpr (D == 128) return launch_attn_mma<D, G, 2, 3>(p, *tmap, batch, stream);
-      else return launch_attn_mma<D, G, 4, 3>(p, *tmap, batch, stream);
-    }
+  if (v.mma && tm) {
+    if constexpr (D == 128) return launch_attn_mma<D, G, 2, 3>(p, *tm, batch, stream);
+    else return launch_attn_mma<D, G, 4, 3>(p, *tm, batch, stream);
   }
   if constexpr (D == 128) {
     if (v.stages == 2) return launch_attn_v<D, G, 2, 3>(p, batch, stream);
@@ -804,13 +863,12 @@ bs_status launch_attn_t(const AttnParams& p, const CUtensorMap* tmap, int batch,
 }
 
 template <int D>
-bs_status launch_attn_d(const AttnParams& p, const CUtensorMap* tmap, int G, int batch,
-                        cudaStream_t stream) {
+bs_status launch_attn_d(const AttnParams& p, const TMaps* tm, int G, int batch, cudaStream_t stream) {
   switch (G) {
-    case 1: return launch_attn_t<D, 1>(p, tmap, batch, stream);
-    case 2: return launch_attn_t<D, 2>(p, tmap, batch, stream);
-    case 4: return launch_attn_t<D, 4>(p, tmap, batch, stream);
-    case 8: return launch_attn_t<D, 8>(p, tmap, batch, stream);
+    case 1: return launch_attn_t<D, 1>(p, tm, batch, stream);
+    case 2: return launch_attn_t<D, 2>(p, tm, batch, stream);
+    case 4: return launch_attn_t<D, 4>(p, tm, batch, stream);
+    case 8: return launch_attn_t<D, 8>(p, tm, batch, stream);
   }
   return set_error(BS_ERR_UNSUPPORTED, "query group G=%d not in {1,2,4,8}", G);
 }
@@ -854,94 +912,151 @@ static const CUtensorMap* pool_tensor_map(const bs_kv_pool* cpool) {
   return pool->tmap_state == 1 ? &pool->tmap : nullptr;
 }
 
-static bs_status attention_impl(const bs_kv_pool* pool, int32_t layer, int32_t pool_head_lo,
-                                int32_t model_head_lo, int32_t n_kv_heads, int32_t num_kv_heads_total,
-                                const void* q, int32_t batch, int32_t num_q_heads,
-                                const int32_t* block_tables, int32_t max_blocks,
-                                const int32_t* kv_split, int32_t n_shards, int32_t shard_id,
-                                float scale, float* o_part, float* m, float* l, void* workspace,
-                                size_t workspace_bytes, void* stream) {
-  BS_REQUIRE(pool, "bs_split_decode_attention: NULL pool");
-  BS_REQUIRE(!pool->host, "bs_split_decode_attention: host-tier pools are fetched first, not read");
-  const int d = pool->desc.head_dim;
-  BS_REQUIRE(layer >= 0 && layer < pool->desc.num_layers, "bs_split_decode_attention: layer %d out of range",
-             layer);
-  BS_REQUIRE(batch >= 0, "bs_split_decode_attention: batch < 0");
-  BS_REQUIRE(num_kv_heads_total >= 1 && num_q_heads >= num_kv_heads_total &&
-                 num_q_heads % num_kv_heads_total == 0,
-             "bs_split_decode_attention: num_q_heads %d not a multiple of Hkv %d", num_q_heads,
-             num_kv_heads_total);
-  BS_REQUIRE(n_kv_heads >= 1 && pool_head_lo >= 0 && pool_head_lo + n_kv_heads <= pool->desc.num_kv_heads &&
-                 model_head_lo >= 0 && model_head_lo + n_kv_heads <= num_kv_heads_total,
-             "bs_split_decode_attention: head range [%d,+%d) (model %d) outside pool (%d) / model (%d)",
-             pool_head_lo, n_kv_heads, model_head_lo, pool->desc.num_kv_heads, num_kv_heads_total);
-  if (batch == 0) return BS_OK;
-  BS_REQUIRE(max_blocks >= 1, "bs_split_decode_attention: max_blocks < 1");
-  BS_REQUIRE(n_shards >= 1 && shard_id >= 0 && shard_id < n_shards,
-             "bs_split_decode_attention: shard %d of %d", shard_id, n_shards);
-  BS_REQUIRE(q && block_tables && kv_split && o_part && m && l,
-             "bs_split_decode_attention: NULL device pointer");
-  BS_REQUIRE(((uintptr_t)q & 15) == 0 && ((uintptr_t)o_part & 15) == 0,
-             "bs_split_decode_attention: q/o_part must be 16-B aligned");
-  BS_REQUIRE(scale > 0.f && scale == scale, "bs_split_decode_attention: bad scale");
-  const int G = num_q_heads / num_kv_heads_total;
+namespace {
+
+struct LaunchArgs {
+  int n_local;
+  const bs_kv_pool* pools[bs::kMaxLocal];
+  const int32_t* bts[bs::kMaxLocal];
+  int32_t max_blocks[bs::kMaxLocal];
+  int32_t shard_ids[bs::kMaxLocal];
+  int32_t pool_head_lo, model_head_lo, n_kv_heads, num_kv_heads_total;
+  int32_t layer, batch, num_q_heads, n_shards;
+  const void* q;
+  const int32_t* kv_split;
+  float scale;
+  bool merged;
+  float *o, *m, *l;
+  void* out;
+  float* lse;
+  void* workspace;
+  size_t workspace_bytes;
+  void* stream;
+};
+
+bs_status validate_common(const LaunchArgs& a, int* G_out) {
+  BS_REQUIRE(a.n_local >= 1 && a.n_local <= bs::kMaxLocal, "attention: %d local shards (1..%d)",
+             a.n_local, bs::kMaxLocal);
+  const bs_kv_pool* p0 = a.pools[0];
+  for (int j = 0; j < a.n_local; ++j) {
+    const bs_kv_pool* pj = a.pools[j];
+    BS_REQUIRE(pj, "attention: NULL pool");
+    BS_REQUIRE(!pj->host, "attention: host-tier pools are fetched first, not read");
+    BS_REQUIRE(pj->desc.head_dim == p0->desc.head_dim && pj->desc.num_layers == p0->desc.num_layers,
+               "attention: local shards must share head_dim / num_layers");
+    BS_REQUIRE(a.pool_head_lo >= 0 && a.pool_head_lo + a.n_kv_heads <= pj->desc.num_kv_heads,
+               "attention: head range [%d,+%d) outside pool (%d)", a.pool_head_lo, a.n_kv_heads,
+               pj->desc.num_kv_heads);
+    BS_REQUIRE(a.max_blocks[j] >= 1, "attention: max_blocks < 1");
+    BS_REQUIRE(a.shard_ids[j] >= 0 && a.shard_ids[j] < a.n_shards, "attention: shard %d of %d",
+               a.shard_ids[j], a.n_shards);
+  }
+  BS_REQUIRE(a.layer >= 0 && a.layer < p0->desc.num_layers, "attention: layer %d out of range", a.layer);
+  BS_REQUIRE(a.batch >= 0, "attention: batch < 0");
+  BS_REQUIRE(a.num_kv_heads_total >= 1 && a.num_q_heads >= a.num_kv_heads_total &&
+                 a.num_q_heads % a.num_kv_heads_total == 0,
+             "attention: num_q_heads %d not a multiple of Hkv %d", a.num_q_heads, a.num_kv_heads_total);
+  BS_REQUIRE(a.n_kv_heads >= 1 && a.model_head_lo >= 0 &&
+                 a.model_head_lo + a.n_kv_heads <= a.num_kv_heads_total,
+             "attention: model head range [%d,+%d) outside %d", a.model_head_lo, a.n_kv_heads,
+             a.num_kv_heads_total);
+  BS_REQUIRE(a.n_shards >= 1, "attention: n_shards < 1");
+  BS_REQUIRE(a.scale > 0.f && a.scale == a.scale, "attention: bad scale");
+  const int G = a.num_q_heads / a.num_kv_heads_total;
   if (G != 1 && G != 2 && G != 4 && G != 8)
     return bs::set_error(BS_ERR_UNSUPPORTED, "query group G=%d not in {1,2,4,8}", G);
-  bs::Plan pl;
-  bs_status st = bs::make_plan(batch, G, num_q_heads, n_kv_heads, d, max_blocks, &pl);
+  *G_out = G;
+  return BS_OK;
+}
+
+bs_status run_attention(const LaunchArgs& a) {
+  int G = 0;
+  bs_status st = validate_common(a, &G);
   if (st != BS_OK) return st;
-  BS_REQUIRE(pl.ws_bytes == 0 || (workspace && workspace_bytes >= pl.ws_bytes &&
-                                  ((uintptr_t)workspace & 15) == 0),
-             "bs_split_decode_attention: workspace needs %zu bytes (got %zu)", pl.ws_bytes,
-             workspace_bytes);
+  if (a.batch == 0) return BS_OK;
+  BS_REQUIRE(a.q && a.kv_split, "attention: NULL q / kv_split");
+  for (int j = 0; j < a.n_local; ++j) BS_REQUIRE(a.bts[j], "attention: NULL block table");
+  if (a.merged) BS_REQUIRE(a.out, "attention: NULL out");
+  else BS_REQUIRE(a.o && a.m && a.l, "attention: NULL o / m / l");
+  BS_REQUIRE(((uintptr_t)a.q & 15) == 0 && ((uintptr_t)(a.merged ? a.out : (void*)a.o) & 15) == 0,
+             "attention: q / output must be 16-B aligned");
+  const int d = a.pools[0]->desc.head_dim;
+  bs::Plan pl;
+  st = bs::make_plan(a.batch, G, a.num_q_heads, a.n_kv_heads, d, a.n_local, a.max_blocks, a.merged, &pl);
+  if (st != BS_OK) return st;
+  BS_REQUIRE(pl.ws_bytes == 0 || (a.workspace && a.workspace_bytes >= pl.ws_bytes &&
+                                  ((uintptr_t)a.workspace & 15) == 0),
+             "attention: workspace needs %zu bytes (got %zu)", pl.ws_bytes, a.workspace_bytes);
   bs::AttnParams p{};
-  p.kv = pool->base + (size_t)layer * pool->layer_bytes;
-  p.chunk_bytes = (int64_t)pool->chunk_bytes;
-  p.v_off = (int64_t)pool->desc.num_kv_heads * pool->page_bytes;
-  p.q = static_cast<const __nv_bfloat16*>(q);
-  p.bt = block_tables;
-  p.max_blocks = max_blocks;
-  p.kv_split = kv_split;
-  p.n_shards = n_shards;
-  p.shard_id = shard_id;
-  p.scale_log2 = scale * bs::kLog2e;
-  p.hq = num_q_heads;
-  p.hkv = n_kv_heads;
-  p.pool_head_lo = pool_head_lo;
-  p.model_head_lo = model_head_lo;
-  p.pool_hkv = pool->desc.num_kv_heads;
-  p.layer_row0 = (int32_t)((int64_t)layer * pool->desc.num_blocks * 2 * pool->desc.num_kv_heads * 16);
+  p.n_local = a.n_local;
+  bs::TMaps tm;
+  bool have_maps = bs::variant_for(d, G).mma;
+  for (int j = 0; j < a.n_local; ++j) {
+    const bs_kv_pool* pool = a.pools[j];
+    bs::ShardDesc& sd = p.sh[j];
+    sd.kv = pool->base + (size_t)a.layer * pool->layer_bytes;
+    sd.chunk_bytes = (int64_t)pool->chunk_bytes;
+    sd.v_off = (int64_t)pool->desc.num_kv_heads * pool->page_bytes;
+    sd.bt = a.bts[j];
+    sd.max_blocks = a.max_blocks[j];
+    sd.shard_id = a.shard_ids[j];
+    sd.bps = pl.bps;
+    sd.split_off = pl.split_off[j];
+    sd.pool_hkv = pool->desc.num_kv_heads;
+    sd.pool_head_lo = a.pool_head_lo;
+    sd.layer_row0 =
+        (int32_t)((int64_t)a.layer * pool->desc.num_blocks * 2 * pool->desc.num_kv_heads * 16);
+    if (have_maps) {
+      const CUtensorMap* m = pool_tensor_map(pool);
+      if (m) tm.m[j] = *m;
+      else have_maps = false;
+    }
+  }
+  p.q = static_cast<const __nv_bfloat16*>(a.q);
+  p.kv_split = a.kv_split;
+  p.n_shards = a.n_shards;
+  p.scale_log2 = a.scale * bs::kLog2e;
+  p.hq = a.num_q_heads;
+  p.hkv = a.n_kv_heads;
+  p.model_head_lo = a.model_head_lo;
   p.nsplit = pl.nsplit;
-  p.bps = pl.bps;
-  p.o = o_part;
-  p.m = m;
-  p.l = l;
+  p.merged = a.merged ? 1 : 0;
+  p.o = a.o;
+  p.m = a.m;
+  p.l = a.l;
+  p.out = static_cast<__nv_bfloat16*>(a.out);
+  p.lse = a.lse;
   if (pl.ws_bytes) {
-    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    uint8_t* ws = static_cast<uint8_t*>(a.workspace);
     p.ws_o = reinterpret_cast<float*>(ws);
     p.ws_ml = reinterpret_cast<float*>(ws + pl.off_ml);
     p.ws_cnt = reinterpret_cast<int32_t*>(ws + pl.off_cnt);
   }
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const CUtensorMap* tmap = bs::variant_for(d, G).mma ? pool_tensor_map(pool) : nullptr;
-  if (d == 128) return bs::launch_attn_d<128>(p, tmap, G, batch, s);
-  return bs::launch_attn_d<64>(p, tmap, G, batch, s);
+  cudaStream_t s = static_cast<cudaStream_t>(a.stream);
+  const bs::TMaps* tmp = have_maps ? &tm : nullptr;
+  if (d == 128) return bs::launch_attn_d<128>(p, tmp, G, a.batch, s);
+  return bs::launch_attn_d<64>(p, tmp, G, a.batch, s);
 }
 
-static bs_status workspace_impl(const bs_kv_pool* pool, int32_t batch, int32_t n_kv_heads,
-                                int32_t num_kv_heads_total, int32_t num_q_heads, int32_t max_blocks,
-                                size_t* bytes) {
-  BS_REQUIRE(pool && bytes, "bs_split_decode_attention_workspace_size: NULL argument");
-  BS_REQUIRE(batch >= 0 && max_blocks >= 1 && n_kv_heads >= 1 && num_kv_heads_total >= 1 &&
+bs_status workspace_impl(int n_local, const bs_kv_pool* const* pools, const int32_t* max_blocks,
+                         int32_t batch, int32_t n_kv_heads, int32_t num_kv_heads_total,
+                         int32_t num_q_heads, bool merged, size_t* bytes) {
+  BS_REQUIRE(pools && bytes && max_blocks, "attention workspace size: NULL argument");
+  BS_REQUIRE(n_local >= 1 && n_local <= bs::kMaxLocal, "attention workspace size: %d shards", n_local);
+  for (int j = 0; j < n_local; ++j)
+    BS_REQUIRE(pools[j] && max_blocks[j] >= 1, "attention workspace size: bad pool / max_blocks");
+  BS_REQUIRE(batch >= 0 && n_kv_heads >= 1 && num_kv_heads_total >= 1 &&
                  num_q_heads >= num_kv_heads_total && num_q_heads % num_kv_heads_total == 0,
-             "bs_split_decode_attention_workspace_size: bad batch/max_blocks/heads");
+             "attention workspace size: bad batch / heads");
   bs::Plan pl;
   bs_status st = bs::make_plan(batch, num_q_heads / num_kv_heads_total, num_q_heads, n_kv_heads,
-                               pool->desc.head_dim, max_blocks, &pl);
+                               pools[0]->desc.head_dim, n_local, max_blocks, merged, &pl);
   if (st != BS_OK) return st;
   *bytes = pl.ws_bytes;
   return BS_OK;
 }
+
+}  // namespace
 
 extern "C" {
 
@@ -949,8 +1064,8 @@ bs_status bs_split_decode_attention_workspace_size(const bs_kv_pool* pool, int32
                                                    int32_t num_q_heads, int32_t max_blocks,
                                                    size_t* bytes) {
   BS_REQUIRE(pool, "bs_split_decode_attention_workspace_size: NULL pool");
-  return workspace_impl(pool, batch, pool->desc.num_kv_heads, pool->desc.num_kv_heads, num_q_heads,
-                        max_blocks, bytes);
+  return workspace_impl(1, &pool, &max_blocks, batch, pool->desc.num_kv_heads,
+                        pool->desc.num_kv_heads, num_q_heads, false, bytes);
 }
 
 bs_status bs_split_decode_attention(const bs_kv_pool* pool, int32_t layer, const void* q,
@@ -960,10 +1075,31 @@ bs_status bs_split_decode_attention(const bs_kv_pool* pool, int32_t layer, const
                                     float scale, float* o_part, float* m, float* l,
                                     void* workspace, size_t workspace_bytes, void* stream) {
   BS_REQUIRE(pool, "bs_split_decode_attention: NULL pool");
-  const int hkv = pool->desc.num_kv_heads;
-  return attention_impl(pool, layer, 0, 0, hkv, hkv, q, batch, num_q_heads, block_tables,
-                        max_blocks, kv_split, n_shards, shard_id, scale, o_part, m, l, workspace,
-                        workspace_bytes, stream);
+  LaunchArgs a{};
+  a.n_local = 1;
+  a.pools[0] = pool;
+  a.bts[0] = block_tables;
+  a.max_blocks[0] = max_blocks;
+  a.shard_ids[0] = shard_id;
+  a.pool_head_lo = 0;
+  a.model_head_lo = 0;
+  a.n_kv_heads = pool->desc.num_kv_heads;
+  a.num_kv_heads_total = pool->desc.num_kv_heads;
+  a.layer = layer;
+  a.batch = batch;
+  a.num_q_heads = num_q_heads;
+  a.n_shards = n_shards;
+  a.q = q;
+  a.kv_split = kv_split;
+  a.scale = scale;
+  a.merged = false;
+  a.o = o_part;
+  a.m = m;
+  a.l = l;
+  a.workspace = workspace;
+  a.workspace_bytes = workspace_bytes;
+  a.stream = stream;
+  return run_attention(a);
 }
 
 bs_status bs_split_decode_attention_heads_workspace_size(const bs_kv_pool* pool, int32_t batch,
@@ -971,7 +1107,8 @@ bs_status bs_split_decode_attention_heads_workspace_size(const bs_kv_pool* pool,
                                                          int32_t num_kv_heads_total,
                                                          int32_t num_q_heads, int32_t max_blocks,
                                                          size_t* bytes) {
-  return workspace_impl(pool, batch, n_kv_heads, num_kv_heads_total, num_q_heads, max_blocks, bytes);
+  return workspace_impl(1, &pool, &max_blocks, batch, n_kv_heads, num_kv_heads_total, num_q_heads,
+                        false, bytes);
 }
 
 bs_status bs_split_decode_attention_heads(const bs_kv_pool* pool, int32_t layer,
@@ -983,9 +1120,82 @@ bs_status bs_split_decode_attention_heads(const bs_kv_pool* pool, int32_t layer,
                                           int32_t shard_id, float scale, float* o_part, float* m,
                                           float* l, void* workspace, size_t workspace_bytes,
                                           void* stream) {
-  return attention_impl(pool, layer, pool_head_lo, model_head_lo, n_kv_heads, num_kv_heads_total,
-                        q, batch, num_q_heads, block_tables, max_blocks, kv_split, n_shards,
-                        shard_id, scale, o_part, m, l, workspace, workspace_bytes, stream);
+  LaunchArgs a{};
+  a.n_local = 1;
+  a.pools[0] = pool;
+  a.bts[0] = block_tables;
+  a.max_blocks[0] = max_blocks;
+  a.shard_ids[0] = shard_id;
+  a.pool_head_lo = pool_head_lo;
+  a.model_head_lo = model_head_lo;
+  a.n_kv_heads = n_kv_heads;
+  a.num_kv_heads_total = num_kv_heads_total;
+  a.layer = layer;
+  a.batch = batch;
+  a.num_q_heads = num_q_heads;
+  a.n_shards = n_shards;
+  a.q = q;
+  a.kv_split = kv_split;
+  a.scale = scale;
+  a.merged = false;
+  a.o = o_part;
+  a.m = m;
+  a.l = l;
+  a.workspace = workspace;
+  a.workspace_bytes = workspace_bytes;
+  a.stream = stream;
+  return run_attention(a);
+}
+
+bs_status bs_split_decode_attention_local_workspace_size(int32_t n_local,
+                                                         const bs_kv_pool* const* pools,
+                                                         const int32_t* max_blocks, int32_t batch,
+                                                         int32_t num_q_heads, size_t* bytes) {
+  BS_REQUIRE(pools && pools[0], "bs_split_decode_attention_local_workspace_size: NULL pool");
+  const int hkv = pools[0]->desc.num_kv_heads;
+  return workspace_impl(n_local, pools, max_blocks, batch, hkv, hkv, num_q_heads, true, bytes);
+}
+
+bs_status bs_split_decode_attention_local(int32_t n_local, const bs_kv_pool* const* pools,
+                                          int32_t layer, const void* q, int32_t batch,
+                                          int32_t num_q_heads, const int32_t* const* block_tables,
+                                          const int32_t* max_blocks, const int32_t* shard_ids,
+                                          const int32_t* kv_split, int32_t n_shards, float scale,
+                                          void* out, float* lse, void* workspace,
+                                          size_t workspace_bytes, void* stream) {
+  BS_REQUIRE(pools && block_tables && max_blocks && shard_ids,
+             "bs_split_decode_attention_local: NULL array");
+  BS_REQUIRE(n_local >= 1 && n_local <= bs::kMaxLocal, "bs_split_decode_attention_local: %d shards",
+             n_local);
+  BS_REQUIRE(pools[0], "bs_split_decode_attention_local: NULL pool");
+  LaunchArgs a{};
+  a.n_local = n_local;
+  for (int j = 0; j < n_local; ++j) {
+    a.pools[j] = pools[j];
+    a.bts[j] = block_tables[j];
+    a.max_blocks[j] = max_blocks[j];
+    a.shard_ids[j] = shard_ids[j];
+    BS_REQUIRE(pools[j] && pools[j]->desc.num_kv_heads == pools[0]->desc.num_kv_heads,
+               "bs_split_decode_attention_local: shards must share num_kv_heads");
+  }
+  a.pool_head_lo = 0;
+  a.model_head_lo = 0;
+  a.n_kv_heads = pools[0]->desc.num_kv_heads;
+  a.num_kv_heads_total = a.n_kv_heads;
+  a.layer = layer;
+  a.batch = batch;
+  a.num_q_heads = num_q_heads;
+  a.n_shards = n_shards;
+  a.q = q;
+  a.kv_split = kv_split;
+  a.scale = scale;
+  a.merged = true;
+  a.out = out;
+  a.lse = lse;
+  a.workspace = workspace;
+  a.workspace_bytes = workspace_bytes;
+  a.stream = stream;
+  return run_attention(a);
 }
 
 }  // extern "C"

@@ -19,7 +19,8 @@ Per layer l (every exchange is point-to-point, NCCL via torch.distributed on GPU
 Streams: compute, copy (migration, high priority) and comm (q / partial exchange +
 merge), ordered by events; the attention of layer l waits for layer l's migration
 (layer-wise overlap, Fig. 6).  At N=1 the ring closes on itself: no
-exchange, prev = next = self.
+exchange, prev = next = self, and both shards being local, attention over both pools and
+the LSE merge run as ONE fused launch (bs_split_decode_attention_local).
 
 The protocol is written against two small interfaces -- ``ops`` (the kernels) and
 ``ex`` (streams/events) -- so the identical code runs on GPUs with libbanaserve.so and
@@ -107,6 +108,18 @@ class CudaOps:
     def merge(self, parts, out, lse):
         self._merge([p[0] for p in parts], [p[1] for p in parts], [p[2] for p in parts], out, lse)
 
+    def attention_local(self, pools, layer, q, block_tables, shard_ids, kv_split, out, lse, ws):
+        """H4 + H6 fused over shards resident on this GPU (one launch)."""
+        from . import split_decode_attention_local
+        split_decode_attention_local(pools, layer, q, block_tables, shard_ids, kv_split,
+                                     self.scale, out, lse, ws)
+
+    def local_workspace(self, pools, block_tables, batch, hq, device):
+        from . import split_decode_attention_local_workspace_size
+        n = split_decode_attention_local_workspace_size(pools, [t.shape[1] for t in block_tables],
+                                                        batch, hq)
+        return torch.zeros(max(n, 16), dtype=torch.uint8, device=device)
+
     def migrate_local(self, src, dst, layer, src_ids, dst_ids):
         self._mig(src, dst, layer, src_ids, dst_ids)
 
@@ -147,7 +160,8 @@ class ShardedDecodeStep:
     def __init__(self, ops, ex, rank: int, world: int, home_pool, home_bt, cold_pool, cold_bt,
                  kv_split, num_q_heads: int, num_layers: int, head_dim: int,
                  handoff_src_ids=None, handoff_dst_ids=None, chunk_bytes: int = 0,
-                 pg_attn=None, pg_mig=None, lookahead: int = 1, device=None):
+                 pg_attn=None, pg_mig=None, lookahead: int = 1, device=None,
+                 fuse_local: bool = True):
         self.ops, self.ex = ops, ex
         self.rank, self.world = rank, world
         self.prev, self.next = (rank - 1) % world, (rank + 1) % world
@@ -173,6 +187,11 @@ class ShardedDecodeStep:
             nbytes = self.n_handoff * chunk_bytes
             self.stage_send = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
             self.stage_recv = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
+        # N=1: both shards are local -> one fused attention + merge launch per layer
+        self.fuse_local = fuse_local and world == 1 and hasattr(ops, "attention_local")
+        if self.fuse_local:
+            self.local_ws = ops.local_workspace([home_pool, cold_pool], [home_bt, cold_bt], self.B,
+                                                self.hq, dev)
         self.ev = {k: [ex.event() for _ in range(num_layers)]
                    for k in ("mig_done", "layer_start", "q_ready", "part_ready")}
 
@@ -185,7 +204,8 @@ class ShardedDecodeStep:
         """Our kernels per step: 2 attention + 1 merge (+ 1 fused copy at N=1, or
         gather + scatter at N>1, when hand-offs are present) per layer."""
         mig = 0 if self.n_handoff == 0 else (1 if self.world == 1 else 2)
-        return self.L * (3 + mig)
+        attn = 1 if self.fuse_local else 3
+        return self.L * (attn + mig)
 
     def enqueue(self, q: torch.Tensor, out: torch.Tensor, lse: torch.Tensor | None = None,
                 timers=None) -> None:
@@ -226,6 +246,14 @@ class ShardedDecodeStep:
                 ex.wait(ex.compute, E["mig_done"][layer])
                 if timers is not None:
                     timers[layer][0].record(ex.compute)
+                if self.fuse_local:
+                    ops.attention_local([self.home, self.cold], layer, q[layer],
+                                        [self.home_bt, self.cold_bt], [0, 1], self.kv_split,
+                                        out[layer], None if lse is None else lse[layer],
+                                        self.local_ws)
+                    if timers is not None:
+                        timers[layer][1].record(ex.compute)
+                    continue
                 ops.attention(self.home, layer, q[layer], self.home_bt, self.kv_split, 0,
                               self.part_own[layer])
                 if self.world > 1:

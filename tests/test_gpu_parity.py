@@ -278,3 +278,45 @@ def test_gather_scatter_roundtrip_equals_migrate(bs):
     st = staging.cpu().numpy().view(np.uint16).reshape(len(s), -1)
     for i, x in enumerate(s):
         assert np.array_equal(st[i], src_np[1, x].ravel())
+
+
+# ---------------------------------------------------------------------------- fused local
+
+@pytest.mark.parametrize("d,G,n_local", [(64, 2, 2), (128, 1, 2), (128, 4, 3), (128, 8, 2), (64, 8, 4)])
+def test_fused_local_shards_attention_and_merge(bs, d, G, n_local):
+    """bs_split_decode_attention_local (H4+H6 in one launch over co-located shards) equals
+    the oracle's per-shard attention + LSE merge, incl. empty and unaligned shards."""
+    shape = synth.Shape(1, 2 * G, 2, d)
+    lens = (0, 1, 17, 100, 700, 2000)
+    dense = synth.gen_dense(shape, lens, seed=d + G + n_local)
+    ks = synth.random_split(lens, n_local, seed=n_local)
+    ks[5] = synth.block_aligned_split([2000], n_local)[0]
+    shards = synth.place_shards(dense, ks, seed=G)
+    pools = gpu_pools(bs, shape, [s.pool for s in shards])
+    bts = [dev_i32(s.block_tables) for s in shards]
+    sc = synth.default_scale(d)
+    B, hq = len(lens), shape.hq
+    q = dev_bf16(dense.q[0])
+    ksd = dev_i32(ks)
+    ws_n = bs.split_decode_attention_local_workspace_size(pools, [t.shape[1] for t in bts], B, hq)
+    ws = torch.zeros(max(ws_n, 16), dtype=torch.uint8, device="cuda")
+    out = torch.full((B, hq, d), float("nan"), dtype=torch.bfloat16, device="cuda")
+    lse = torch.full((B, hq), float("nan"), device="cuda")
+    bs.split_decode_attention_local(pools, 0, q, bts, list(range(n_local)), ksd, sc, out, lse, ws)
+    torch.cuda.synchronize()
+    ref_o, ref_lse = oracle.attention_full([s.pool for s in shards], [s.block_tables for s in shards],
+                                           0, dense.q[0], ks, sc)
+    got = out.float().cpu().double().numpy()
+    gl = lse.cpu().double().numpy()
+    fin = np.isfinite(ref_lse)
+    assert np.array_equal(np.isneginf(gl), ~fin) and np.all(got[~fin] == 0)
+    err = np.abs(got - ref_o)
+    assert err.max() <= ABS_TOL
+    rel = err.max(-1)[fin] / np.abs(ref_o).max(-1)[fin]
+    assert rel.max() <= ROW_REL_TOL
+    assert np.abs(gl[fin] - ref_lse[fin]).max() <= LSE_TOL
+    # second call: counters re-armed, bitwise deterministic
+    out2 = torch.empty_like(out)
+    bs.split_decode_attention_local(pools, 0, q, bts, list(range(n_local)), ksd, sc, out2, None, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int16), out2.view(torch.int16))

@@ -184,16 +184,19 @@ def handoff_src_ids(case, n):
     return [i for i in range(case.pools[1].shape[1]) if i not in used][:n]
 
 
-def attn_bytes_per_layer(ks):
-    """Algorithmic bytes of the attention launches of one layer:
-    per (request, shard): len*2*Hkv*d*2 (KV) + Hq*d*2 (q) + Hq*(d+2)*4 (partials)
-    + 4*ceil(len/16) (block table)."""
+def attn_bytes_per_layer(ks, fused: bool = True):
+    """Algorithmic bytes of one layer's attention: per (request, shard)
+    len*2*Hkv*d*2 (KV) + 4*ceil(len/16) (block table); per request Hq*d*2 (q) and, with
+    the fused local launch (N=1), the merged bf16 O + fp32 lse (Hq*(d*2+4)) -- without it,
+    each shard's fp32 partial Hq*(d+2)*4 instead."""
     tot = 0
-    for j in range(ks.shape[1] - 1):
-        for n in (ks[:, j + 1] - ks[:, j]):
-            n = int(n)
-            tot += n * 2 * SHAPE.hkv * SHAPE.d * 2 + SHAPE.hq * SHAPE.d * 2 + \
-                SHAPE.hq * (SHAPE.d + 2) * 4 + 4 * synth.ceil_div(n, SHAPE.bs)
+    n_sh = ks.shape[1] - 1
+    for b in range(ks.shape[0]):
+        tot += SHAPE.hq * SHAPE.d * 2
+        tot += SHAPE.hq * (SHAPE.d * 2 + 4) if fused else n_sh * SHAPE.hq * (SHAPE.d + 2) * 4
+        for j in range(n_sh):
+            n = int(ks[b, j + 1] - ks[b, j])
+            tot += n * 2 * SHAPE.hkv * SHAPE.d * 2 + 4 * synth.ceil_div(n, SHAPE.bs)
     return tot
 
 
@@ -267,7 +270,7 @@ def run_ours(args, rank, world, device):
     e2e_ms = float(e2e_ms.item())
 
     # ---- derived numbers ----------------------------------------------------------------
-    a_bytes = attn_bytes_per_layer(ks)
+    a_bytes = attn_bytes_per_layer(ks, fused=step.fuse_local)
     mig_bytes = step.n_handoff * pools[0].chunk_bytes  # per layer, counted once
     attn_avg_ms = statistics.fmean(attn_ms)
     mig_avg_ms = statistics.fmean(mig_ms)
@@ -305,7 +308,9 @@ def run_ours(args, rank, world, device):
         "migrate_transport": ("fused copy kernel, local HBM (N=1: both instances on GPU 0)" if world == 1
                               else "gather -> NCCL send/recv over NVLink -> scatter"),
         "roofline": {
-            "bound": "hbm", "kernel": "split_decode_attn (2 shard launches per layer)",
+            "bound": "hbm",
+            "kernel": ("split_decode_attn_mma, fused local shards + LSE merge (1 launch per layer)"
+                       if step.fuse_local else "split_decode_attn_mma (2 shard launches per layer)"),
             "achieved": round(attn_gbs, 1), "peak": peak, "peak_source": peak_src,
             "unit": "GB/s", "frac": round(attn_gbs / peak, 4),
             "traffic": traffic, "traffic_source": traffic_src,

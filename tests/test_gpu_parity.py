@@ -320,3 +320,57 @@ def test_fused_local_shards_attention_and_merge(bs, d, G, n_local):
     bs.split_decode_attention_local(pools, 0, q, bts, list(range(n_local)), ksd, sc, out2, None, ws)
     torch.cuda.synchronize()
     assert torch.equal(out.view(torch.int16), out2.view(torch.int16))
+
+
+# ---------------------------------------------------------------------------- full sizes
+
+def _sampled_check(bs, shape, lens, ks, sample, seed, fused):
+    case = synth.device_shards(shape, np.asarray(lens), ks, seed=seed, device="cuda", layers=1)
+    pools = [bs.KVPool(1, pt.shape[1], shape.hkv, shape.d, base=pt.reshape(-1)) for pt in case.pools]
+    sc = synth.default_scale(shape.d)
+    B = len(lens)
+    bts = [dev_i32(bt) for bt in case.block_tables]
+    ksd = dev_i32(ks)
+    sp, sbt, sks, sq = synth.extract_requests(case, sample, 0)
+    ref_o, ref_lse = oracle.attention_full(sp, sbt, 0, sq, sks, sc)
+    if fused:
+        n = len(pools)
+        ws = torch.zeros(max(16, bs.split_decode_attention_local_workspace_size(
+            pools, [t.shape[1] for t in bts], B, shape.hq)), dtype=torch.uint8, device="cuda")
+        out = torch.empty(B, shape.hq, shape.d, dtype=torch.bfloat16, device="cuda")
+        lse = torch.empty(B, shape.hq, device="cuda")
+        bs.split_decode_attention_local(pools, 0, case.q[0], bts, list(range(n)), ksd, sc, out, lse, ws)
+    else:
+        parts, out, lse = run_split_attention(bs, shape, pools, case.block_tables, ks, case.q[0], 0, sc)
+    torch.cuda.synchronize()
+    got = out[sample].float().cpu().double().numpy()
+    gl = lse[sample].cpu().double().numpy()
+    fin = np.isfinite(ref_lse)
+    err = np.abs(got - ref_o)
+    assert err.max() <= ABS_TOL
+    assert (err.max(-1)[fin] / np.abs(ref_o).max(-1)[fin]).max() <= ROW_REL_TOL
+    assert np.abs(gl[fin] - ref_lse[fin]).max() <= LSE_TOL
+    assert np.array_equal(np.isneginf(gl), ~fin)
+
+
+def test_full_size_c3_llama3_8b_32k_4way_sampled(bs):
+    """BASELINE config C3 at full size: Llama-3-8B GQA (32/8 heads, d 128), 32k context,
+    4-way token split, B = 8 -- all four shards on one GPU (the 1-GPU split-K baseline),
+    fused launch; the oracle recomputes 2 sampled requests."""
+    shape = synth.Shape(1, 32, 8, 128)
+    lens = [32768] * 8
+    ks = synth.block_aligned_split(lens, 4)
+    _sampled_check(bs, shape, lens, ks, [0, 5], seed=31, fused=True)
+
+
+def test_full_size_c4_llama70b_mixed_8way_sampled(bs):
+    """BASELINE config C4 at full size for one layer: Llama-2-70B GQA (64/8 heads),
+    B = 256 mixed prompt/generation lengths (Fig. 7 recipe), 8-way block-aligned
+    split (short requests leave empty shards) -- per-shard launches + LSE merge; the
+    oracle recomputes sampled short and long requests."""
+    shape = synth.Shape(1, 64, 8, 128)
+    lens = synth.mixed_lengths(256, seed=0)
+    ks = synth.block_aligned_split(lens, 8)
+    longest = int(np.argmax(lens))
+    shortest = int(np.argmin(lens))
+    _sampled_check(bs, shape, list(lens), ks, [shortest, longest, 7], seed=47, fused=False)

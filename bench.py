@@ -356,34 +356,36 @@ def time_oracle_sample(sample, scale):
     return ta, tm
 
 
-def cpu_baseline(case, budget_s=12.0, reqs_per_sample=32):
-    """Time the oracle (as it stands) on sampled (request, layer) units until ~budget_s of
-    CPU work, then extrapolate to the full step: T = L*(B/r * t_attn + H/h * t_mig)."""
+def cpu_baseline(case, budget_s=12.0, reqs_per_sample=32, n_samples=4):
+    """Time the oracle (as it stands) on sampled (layer, 32-request) units -- extracted
+    once, then re-timed round-robin until ~budget_s of oracle CPU time -- and extrapolate
+    linearly to the full step: T = L * (B/r * t_attn + H * t_mig)."""
     import oracle
     oracle.lib()
     scale = synth.default_scale(SHAPE.d)
     handoff_chunks = synth.ceil_div(SEQ, SHAPE.bs)  # one hand-off request's chunks
+    L = case.pools[0].shape[0]
+    samples = []
+    for i in range(n_samples):
+        layer = (i * 7) % L
+        req = [(i * reqs_per_sample + r) % BATCH for r in range(reqs_per_sample)]
+        samples.append(oracle_sample(case, req, layer, handoff_chunks))
     ta_tot = tm_tot = 0.0
-    layers = 0
-    t_start = time.perf_counter()
-    for it in range(4 * SHAPE.n_layers):
-        layer = it % SHAPE.n_layers
-        req = [(it * reqs_per_sample + i) % BATCH for i in range(reqs_per_sample)]
-        s = oracle_sample(case, req, layer, handoff_chunks)
-        ta, tm = time_oracle_sample(s, scale)
+    units = 0
+    while units < 1000 and ta_tot + tm_tot < budget_s:
+        ta, tm = time_oracle_sample(samples[units % n_samples], scale)
         ta_tot += ta
         tm_tot += tm
-        layers += 1
-        if ta_tot + tm_tot > budget_s or time.perf_counter() - t_start > 3 * budget_s:
-            break
-    t_attn = ta_tot / layers * (BATCH / reqs_per_sample)
-    t_mig = tm_tot / layers * N_HANDOFF
+        units += 1
+    t_attn = ta_tot / units * (BATCH / reqs_per_sample)
+    t_mig = tm_tot / units * N_HANDOFF
     t_step = SHAPE.n_layers * (t_attn + t_mig)
     return {"value": round(BATCH / t_step, 4), "unit": "tokens/s", "kind": "oracle",
             "cores": omp_threads(),
-            "sample": (f"{layers} (layer, {reqs_per_sample}-request) units (both shards + merge) + "
-                       f"1 hand-off request's chunks per layer, fp64 C oracle; extrapolated "
-                       f"linearly to B={BATCH}, {N_HANDOFF} hand-offs, {SHAPE.n_layers} layers"),
+            "sample": (f"{units} timed (layer, {reqs_per_sample}-request) units from {n_samples} "
+                       f"extracted samples (both shards + LSE merge) + 1 hand-off request's "
+                       f"chunks each, fp64 C oracle; extrapolated linearly to B={BATCH}, "
+                       f"{N_HANDOFF} hand-offs, {SHAPE.n_layers} layers"),
             "measured_seconds": round(ta_tot + tm_tot, 3)}
 
 
@@ -434,7 +436,7 @@ def run_reference(args, rank, world, device):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -244,6 +244,18 @@ static int host_copy_ctas() {
 }
 #define kHostCopyCtas host_copy_ctas()
 
+// Optional cap on the CTAs of a device-side migration (BS_MIGRATE_MAX_CTAS, 0 = none): a
+// hand-off that runs beside attention only needs ~96 MiB per layer, so a few dozen CTAs
+// keep it on time while leaving the SM slots to the attention launch.
+static int dev_copy_ctas() {
+  static int v = [] {
+    const char* e = getenv("BS_MIGRATE_MAX_CTAS");
+    int x = e ? atoi(e) : 0;
+    return x > 0 ? x : 0;
+  }();
+  return v;
+}
+
 static bool same_geometry(const bs_kv_pool* a, const bs_kv_pool* b) {
   return a->desc.num_layers == b->desc.num_layers && a->desc.num_kv_heads == b->desc.num_kv_heads &&
          a->desc.head_dim == b->desc.head_dim && a->desc.block_size == b->desc.block_size &&
@@ -265,7 +277,7 @@ bs_status bs_kv_migrate_layer_ex(const bs_kv_pool* src, bs_kv_pool* dst, int32_t
              "bs_kv_migrate_layer: bad method %d", method);
   // a host-tier pool is behind PCIe / C2C: a few CTAs keep it saturated, the rest of the
   // SMs stay with the layer's compute (three-stage pipeline, Fig. 6)
-  const int max_ctas = (src->host || dst->host) ? kHostCopyCtas : 0;
+  const int max_ctas = (src->host || dst->host) ? kHostCopyCtas : dev_copy_ctas();
   return bs::launch_copy_chunks(src->base + (size_t)layer * src->layer_bytes, src_ids,
                                 dst->base + (size_t)layer * dst->layer_bytes, dst_ids, n,
                                 src->chunk_bytes, src->page_bytes, method,

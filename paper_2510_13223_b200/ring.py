@@ -120,8 +120,14 @@ class CudaOps:
                                                         batch, hq)
         return torch.zeros(max(n, 16), dtype=torch.uint8, device=device)
 
-    def migrate_local(self, src, dst, layer, src_ids, dst_ids):
-        self._mig(src, dst, layer, src_ids, dst_ids)
+    def migrate_local(self, src, dst, layer, src_ids, dst_ids, host_ids=None):
+        """Local hand-off copy: the copy kernel (SMs) or, with host id lists, the copy
+        engines (DMA, no SM time -- the attention launch keeps every SM)."""
+        if host_ids is not None:
+            from . import kv_migrate_layer_ce
+            kv_migrate_layer_ce(src, dst, layer, host_ids[0], host_ids[1])
+        else:
+            self._mig(src, dst, layer, src_ids, dst_ids)
 
     def gather(self, pool, layer, ids, staging):
         self._gather(pool, layer, ids, staging)
@@ -161,7 +167,7 @@ class ShardedDecodeStep:
                  kv_split, num_q_heads: int, num_layers: int, head_dim: int,
                  handoff_src_ids=None, handoff_dst_ids=None, chunk_bytes: int = 0,
                  pg_attn=None, pg_mig=None, lookahead: int = 1, device=None,
-                 fuse_local: bool = True):
+                 fuse_local: bool = True, copy_engine: bool = False):
         self.ops, self.ex = ops, ex
         self.rank, self.world = rank, world
         self.prev, self.next = (rank - 1) % world, (rank + 1) % world
@@ -172,6 +178,10 @@ class ShardedDecodeStep:
         self.B = kv_split.shape[0]
         self.src_ids, self.dst_ids = handoff_src_ids, handoff_dst_ids
         self.n_handoff = 0 if handoff_src_ids is None else int(handoff_src_ids.numel())
+        # N=1 hand-off on the copy engines (host id lists) instead of the copy kernel
+        self.ce_ids = None
+        if copy_engine and world == 1 and self.n_handoff:
+            self.ce_ids = (handoff_src_ids.cpu().tolist(), handoff_dst_ids.cpu().tolist())
         self.pg_attn, self.pg_mig = pg_attn, pg_mig
         self.lookahead = lookahead
         dev = device
@@ -194,6 +204,7 @@ class ShardedDecodeStep:
                                                 self.hq, dev)
         self.ev = {k: [ex.event() for _ in range(num_layers)]
                    for k in ("mig_done", "layer_start", "q_ready", "part_ready")}
+        self.out_ready = [ex.event() for _ in range(num_layers)]
 
     def _recv_buffer(self, like: torch.Tensor):
         flat = torch.empty_like(like)
@@ -203,15 +214,17 @@ class ShardedDecodeStep:
     def launches_per_step(self) -> int:
         """Our kernels per step: 2 attention + 1 merge (+ 1 fused copy at N=1, or
         gather + scatter at N>1, when hand-offs are present) per layer."""
-        mig = 0 if self.n_handoff == 0 else (1 if self.world == 1 else 2)
+        mig = 0 if self.n_handoff == 0 or self.ce_ids is not None else (1 if self.world == 1 else 2)
         attn = 1 if self.fuse_local else 3
         return self.L * (attn + mig)
 
     def enqueue(self, q: torch.Tensor, out: torch.Tensor, lse: torch.Tensor | None = None,
-                timers=None) -> None:
+                timers=None, inputs_ready=None) -> None:
         """q [L][B][Hq][d] bf16 of this rank's requests -> out [L][B][Hq][d] bf16 and
         lse [L][B][Hq] fp32.  ``timers[l]`` = (attn_start, attn_end, mig_start, mig_end)
-        events recorded on the launching streams (CUDA only)."""
+        events recorded on the launching streams (CUDA only).  ``inputs_ready[l]``: an
+        event the step waits for before reading q[l] (e.g. its H2D copy); after the call,
+        ``self.out_ready[l]`` is recorded once out[l] / lse[l] are final (per-layer D2H)."""
         ex, ops, E = self.ex, self.ops, self.ev
         if self.world > 1 and (self.q_prev is None or self.q_prev.shape != q.shape):
             self.q_prev = torch.empty_like(q)
@@ -221,6 +234,8 @@ class ShardedDecodeStep:
             # up front in layer order; attention on the cold pool waits per layer
             with ex.use(ex.comm):
                 for layer in range(self.L):
+                    if inputs_ready is not None:
+                        ex.wait(ex.comm, inputs_ready[layer])
                     _sendrecv(self.pg_attn, q[layer], self.next, self.q_prev[layer], self.prev)
                     ex.record(E["q_ready"][layer], ex.comm)
         for layer in range(self.L):
@@ -232,7 +247,8 @@ class ShardedDecodeStep:
                     timers[layer][2].record(ex.copy)
                 if self.n_handoff:
                     if self.world == 1:
-                        ops.migrate_local(self.cold, self.home, layer, self.src_ids, self.dst_ids)
+                        ops.migrate_local(self.cold, self.home, layer, self.src_ids, self.dst_ids,
+                                          self.ce_ids)
                     else:
                         ops.gather(self.cold, layer, self.src_ids, self.stage_send)
                         _sendrecv(self.pg_mig, self.stage_send, self.prev, self.stage_recv, self.next)
@@ -244,6 +260,8 @@ class ShardedDecodeStep:
             with ex.use(ex.compute):
                 ex.record(E["layer_start"][layer], ex.compute)
                 ex.wait(ex.compute, E["mig_done"][layer])
+                if inputs_ready is not None:
+                    ex.wait(ex.compute, inputs_ready[layer])
                 if timers is not None:
                     timers[layer][0].record(ex.compute)
                 if self.fuse_local:
@@ -253,6 +271,7 @@ class ShardedDecodeStep:
                                         self.local_ws)
                     if timers is not None:
                         timers[layer][1].record(ex.compute)
+                    ex.record(self.out_ready[layer], ex.compute)
                     continue
                 ops.attention(self.home, layer, q[layer], self.home_bt, self.kv_split, 0,
                               self.part_own[layer])
@@ -269,6 +288,7 @@ class ShardedDecodeStep:
                 with ex.use(ex.compute):
                     ops.merge([self.part_own[layer], self.part_cold[layer]], out[layer],
                               None if lse is None else lse[layer])
+                    ex.record(self.out_ready[layer], ex.compute)
             else:
                 with ex.use(ex.comm):
                     ex.wait(ex.comm, E["part_ready"][layer])
@@ -276,4 +296,5 @@ class ShardedDecodeStep:
                               self.part_recv[layer][4], self.next)
                     ops.merge([self.part_own[layer], self.part_recv[layer]], out[layer],
                               None if lse is None else lse[layer])
+                    ex.record(self.out_ready[layer], ex.comm)
         ex.end()

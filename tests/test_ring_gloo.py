@@ -50,7 +50,7 @@ class OracleOps:
         out.copy_(torch.from_numpy(o).to(torch.bfloat16))
         lse.copy_(torch.from_numpy(x))
 
-    def migrate_local(self, src, dst, layer, s, d):
+    def migrate_local(self, src, dst, layer, s, d, host_ids=None):
         oracle.migrate_layer(src.data, dst.data, layer, s.numpy(), d.numpy())
 
     def gather(self, pool, layer, ids, staging):

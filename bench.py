@@ -135,7 +135,7 @@ class ClockSampler:
 # the workload on the device
 # --------------------------------------------------------------------------------------
 
-def build_workload(bs, device, rank=0, world=1, layers=None):
+def build_workload(bs, device, rank=0, world=1, layers=None, transport="p2p"):
     """Rank r's share of the ring (paper_2510_13223_b200/ring.py): home pool = shard 0 of
     its own 64 requests + free blocks for hand-offs; cold pool = shard 1 of rank r-1's
     requests + the KV handed off to r-1.  At N=1 the ring closes on itself."""
@@ -173,7 +173,8 @@ def build_workload(bs, device, rank=0, world=1, layers=None):
         handoff_dst_ids=i32(dst_ids), chunk_bytes=home.chunk_bytes,
         pg_attn=dist.group.WORLD if world > 1 else None,
         pg_mig=dist.new_group(list(range(world))) if world > 1 else None,
-        lookahead=1, device=device, copy_engine=os.environ.get("BS_HANDOFF_CE", "0") == "1")
+        lookahead=1, device=device, copy_engine=os.environ.get("BS_HANDOFF_CE", "0") == "1",
+        transport=transport)
     return case, pools, step, ks
 
 
@@ -200,11 +201,21 @@ def attn_bytes_per_layer(ks, fused: bool = True):
     return tot
 
 
+def _allreduce_max(t):
+    """Max over ranks (gloo needs CPU tensors, NCCL device tensors)."""
+    if torch.distributed.get_backend() == "gloo":
+        c = t.cpu()
+        torch.distributed.all_reduce(c, op=torch.distributed.ReduceOp.MAX)
+        return c
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return t
+
+
 def run_ours(args, rank, world, device):
     import paper_2510_13223_b200 as bs
 
     torch.cuda.set_device(device)
-    case, pools, step, ks = build_workload(bs, device, rank, world)
+    case, pools, step, ks = build_workload(bs, device, rank, world, transport=args.transport)
     L = SHAPE.n_layers
     q = case.q
     out = torch.empty((L, BATCH, SHAPE.hq, SHAPE.d), dtype=torch.bfloat16, device=device)
@@ -233,12 +244,14 @@ def run_ours(args, rank, world, device):
         t1.record()
         torch.cuda.synchronize()
     barrier()
+    if step.links is not None:
+        step.links.check()
     ms = t0.elapsed_time(t1) / K
     attn_ms = [a.elapsed_time(b) for tk in timers for (a, b, _, _) in tk]
     mig_ms = [c.elapsed_time(d) for tk in timers for (_, _, c, d) in tk]
     ms_t = torch.tensor([ms], device=device)
     if world > 1:
-        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
+        ms_t = _allreduce_max(ms_t)
     ms_max = float(ms_t.item())
 
     # ---- e2e: same step through host buffers ----------------------------------------
@@ -281,7 +294,7 @@ def run_ours(args, rank, world, device):
     torch.cuda.synchronize()
     e2e_ms = torch.tensor([e0.elapsed_time(e1) / K], device=device)
     if world > 1:
-        torch.distributed.all_reduce(e2e_ms, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = _allreduce_max(e2e_ms)
     e2e_ms = float(e2e_ms.item())
     assert torch.equal(out_host.view(torch.int16), out.cpu().view(torch.int16))
 
@@ -322,7 +335,9 @@ def run_ours(args, rank, world, device):
         "migrate_ms_per_layer": round(mig_avg_ms, 5),
         "migrate_bytes_per_layer": mig_bytes,
         "migrate_transport": ("fused copy kernel, local HBM (N=1: both instances on GPU 0)" if world == 1
-                              else "gather -> NCCL send/recv over NVLink -> scatter"),
+                              else ("copy kernel pushing into the peer's IPC-mapped pool (P2P, NVLink)"
+                                    if args.transport == "p2p" else
+                                    "gather -> NCCL send/recv over NVLink -> scatter")),
         "roofline": {
             "bound": "hbm",
             "kernel": ("split_decode_attn_mma, fused local shards + LSE merge (1 launch per layer)"
@@ -457,6 +472,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--transport", choices=["p2p", "nccl"], default=os.environ.get("BS_TRANSPORT", "p2p"),
+                    help="N>1 exchange: CUDA-IPC pushes + flags (p2p) or torch.distributed NCCL P2P")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: --warmup < 3 violates the timing rules; using 3")
@@ -465,14 +482,21 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    device = torch.device("cuda", local)
+    # functional check of the N>1 path on a 1-GPU box: every rank on cuda:0 (time-sliced,
+    # numbers meaningless), gloo for the host plumbing, P2P transport
+    same_gpu = os.environ.get("BS_RING_SAME_GPU", "0") == "1"
+    device = torch.device("cuda", 0 if same_gpu else local)
     if args.impl == "reference":  # rank 0 alone runs it; other ranks exit without work
         if rank == 0:
             print(json.dumps(run_reference(args, rank, world, device)), flush=True)
         return
     if world > 1:
         torch.cuda.set_device(device)
-        torch.distributed.init_process_group("nccl", device_id=device)
+        if same_gpu:
+            args.transport = "p2p"
+            torch.distributed.init_process_group("gloo")
+        else:
+            torch.distributed.init_process_group("nccl", device_id=device)
     try:
         res = run_ours(args, rank, world, device)
         if rank == 0:

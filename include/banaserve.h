@@ -288,6 +288,14 @@ bs_status bs_kv_sendrecv_layer(bs_comm* comm, const bs_kv_pool* src, const int32
  * of a remote-view pool, so bs_kv_migrate_layer pushes chunks over NVLink (P2P push).
  * handle: host buffer of bs_ipc_handle_bytes() bytes.  bs_ipc_close undoes an import. */
 size_t bs_ipc_handle_bytes(void);
+/* Signalling for pushes into peer memory: bs_signal enqueues "all prior work on `stream`
+ * is complete and visible system-wide, then *flag = value" (flag may be peer-mapped);
+ * bs_wait_signal enqueues "wait until *flag >= value" (flag local or peer) -- epochs only
+ * grow, so flags are never reset.  A wait gives up after timeout_ns (0 = never) and sets
+ * *err = 1 (err DEVICE int32, may be NULL) rather than hang the stream. */
+bs_status bs_signal(int32_t* flag, int32_t value, void* stream);
+bs_status bs_wait_signal(const int32_t* flag, int32_t value, uint64_t timeout_ns, int32_t* err,
+                         void* stream);
 bs_status bs_ipc_export(const void* dev_ptr, void* handle_out, size_t* offset_out);
 bs_status bs_ipc_import(const void* handle, size_t offset, void** dev_ptr_out);
 bs_status bs_ipc_close(void* dev_ptr, size_t offset);

@@ -36,7 +36,7 @@ EXPORTED_SYMBOLS = (
     "bs_split_decode_attention_heads_workspace_size", "bs_split_decode_attention_heads",
     "bs_utilization", "bs_dispatch_requests", "bs_plan_migrations", "bs_kv_migrate_layers",
     "bs_copy_bytes", "bs_split_decode_attention_local_workspace_size",
-    "bs_split_decode_attention_local",
+    "bs_split_decode_attention_local", "bs_signal", "bs_wait_signal",
 )
 
 
@@ -112,6 +112,8 @@ def lib():
         "bs_utilization": ([ctypes.c_double] * 4, ctypes.c_double),
         "bs_kv_migrate_layers": ([_p, _p, _i32, _i32, _p, _p, _i32, _p], _i32),
         "bs_copy_bytes": ([_p, _p, _sz, _p], _i32),
+        "bs_signal": ([_p, _i32, _p], _i32),
+        "bs_wait_signal": ([_p, _i32, ctypes.c_uint64, _p, _p], _i32),
         "bs_split_decode_attention_local_workspace_size": ([_i32, _p, _p, _i32, _i32,
                                                             ctypes.POINTER(_sz)], _i32),
         "bs_split_decode_attention_local": ([_i32, _p, _i32, _p, _i32, _i32, _p, _p, _p, _p, _i32,
@@ -476,3 +478,36 @@ def migrate_layers(src: KVPool, dst: KVPool, layer_lo: int, n_layers: int, src_i
 def t_layer_model(s_total_bytes: float, b_net_bytes_per_s: float, t_sync_s: float = 0.0) -> float:
     """eq. 4 (PAPER.md:192-195): T_layer ~= S_total / B_net + T_sync."""
     return s_total_bytes / b_net_bytes_per_s + t_sync_s
+
+
+def signal(flag_ptr: int, value: int, stream=None) -> None:
+    """After all prior work on the stream: *flag = value (flag may be peer-mapped)."""
+    _check(lib().bs_signal(flag_ptr, int(value), _stream(stream)))
+
+
+def wait_signal(flag_ptr: int, value: int, timeout_ns: int = 0, err_ptr: int | None = None,
+                stream=None) -> None:
+    """The stream waits until *flag >= value (gives up after timeout_ns, setting *err)."""
+    _check(lib().bs_wait_signal(flag_ptr, int(value), int(timeout_ns), err_ptr, _stream(stream)))
+
+
+def copy_ptr(dst_ptr: int, src_ptr: int, nbytes: int, stream=None) -> None:
+    """Raw device / peer / host copy by address (copy engine)."""
+    _check(lib().bs_copy_bytes(dst_ptr, src_ptr, nbytes, _stream(stream)))
+
+
+def pool_view(num_layers: int, num_blocks: int, num_kv_heads: int, head_dim: int, ptr: int,
+              device_index: int):
+    """A pool handle over raw (e.g. peer-mapped) memory: the remote view a P2P push
+    writes into.  Returns an object with ``.handle`` usable by the migrate calls."""
+    desc = _Desc(num_layers, num_blocks, 16, num_kv_heads, head_dim, 0, device_index)
+    h = _p()
+    _check(lib().bs_kv_pool_create(ctypes.byref(desc), ptr, ctypes.byref(h)))
+
+    class _View:
+        pass
+    v = _View()
+    v.handle, v.desc = h, desc
+    v.num_layers, v.num_blocks, v.num_kv_heads, v.head_dim = num_layers, num_blocks, num_kv_heads, head_dim
+    v.chunk_bytes = lib().bs_kv_chunk_bytes(ctypes.byref(desc))
+    return v

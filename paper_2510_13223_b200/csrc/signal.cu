@@ -1,0 +1,58 @@
+// Cross-instance signalling for the P2P transport: a producer pushes data
+// straight into a peer-mapped buffer (remote-view pool, q or partial buffer) and then
+// raises a flag in the consumer's memory; the consumer's stream waits on its local flag.
+// Flags carry a monotonically increasing epoch (the decode step), so they never need
+// resetting.  A waiter gives up after `timeout_ns` and records the failure in `err`
+// instead of hanging the GPU.
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace bs {
+namespace {
+
+__global__ void signal_kernel(int32_t* flag, int32_t value) {
+  // every write enqueued before this kernel on the stream is complete (kernel boundary);
+  // make it visible system-wide, then publish the flag with release semantics
+  __threadfence_system();
+  asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
+}
+
+__global__ void wait_kernel(const int32_t* flag, int32_t value, uint64_t timeout_ns, int32_t* err) {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  unsigned ns = 32;
+  while (true) {
+    int32_t v;
+    asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (v >= value) break;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (timeout_ns && t - t0 > timeout_ns) {
+      if (err) atomicExch(err, 1);
+      break;
+    }
+    __nanosleep(ns);
+    if (ns < 4096) ns <<= 1;
+  }
+}
+
+}  // namespace
+}  // namespace bs
+
+extern "C" {
+
+bs_status bs_signal(int32_t* flag, int32_t value, void* stream) {
+  BS_REQUIRE(flag, "bs_signal: NULL flag");
+  bs::signal_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(flag, value);
+  return bs::check_launch("signal_kernel");
+}
+
+bs_status bs_wait_signal(const int32_t* flag, int32_t value, uint64_t timeout_ns, int32_t* err,
+                         void* stream) {
+  BS_REQUIRE(flag, "bs_wait_signal: NULL flag");
+  bs::wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(flag, value, timeout_ns, err);
+  return bs::check_launch("wait_kernel");
+}
+
+}  // extern "C"

@@ -162,12 +162,79 @@ def _sendrecv(pg, send: torch.Tensor, to: int, recv: torch.Tensor, frm: int):
         w.wait()
 
 
+class P2PLinks:
+    """CUDA-IPC links to the two ring neighbours for the P2P transport: this rank's
+    receive buffers and flags are exported; the neighbours' are mapped into this process.
+
+    Pushes (all on this rank's streams, straight into peer memory -- no staging):
+      my q[l]                      -> next.q_prev[l]       then next.flag(q, l) = epoch
+      prev's shard-1 partial [l]   -> prev.part_recv[l]    then prev.flag(part, l) = epoch
+      hand-off chunks (cold pool)  -> prev.home pool (the copy kernel writes the remote
+                                      view directly)       then prev.flag(mig, l) = epoch
+    Acks (back-pressure before a buffer is reused next step): q_ack, part_ack."""
+    KINDS = ("mig", "q", "part", "q_ack", "part_ack")
+
+    def __init__(self, rank, world, num_layers, home_pool, q_like, part_numel, handoff_dst_ids,
+                 device, group, timeout_ms=20000):
+        from . import ipc_export, ipc_import, pool_view
+        self.L = num_layers
+        self.flags = torch.zeros(len(self.KINDS) * num_layers, dtype=torch.int32, device=device)
+        self.err = torch.zeros(1, dtype=torch.int32, device=device)
+        self.q_prev = torch.empty_like(q_like)
+        self.part_recv = torch.empty((num_layers, part_numel), dtype=torch.float32, device=device)
+        self.timeout_ns = int(timeout_ms) * 1_000_000
+        mine = {"flags": ipc_export(self.flags), "q_prev": ipc_export(self.q_prev),
+                "part_recv": ipc_export(self.part_recv), "home": ipc_export(home_pool.data),
+                "home_blocks": home_pool.num_blocks,
+                "handoff_dst": [int(x) for x in handoff_dst_ids.cpu().tolist()]}
+        everyone = [None] * world
+        dist.all_gather_object(everyone, mine, group=group)
+        prev, nxt = (rank - 1) % world, (rank + 1) % world
+        self._opened = {}
+
+        def open_(who, name):
+            key = (who, name)
+            if key not in self._opened:
+                h, off = everyone[who][name]
+                self._opened[key] = (ipc_import(h, off), off)
+            return self._opened[key][0]
+        self.next_q_prev = open_(nxt, "q_prev")
+        self.next_flags = open_(nxt, "flags")
+        self.prev_part_recv = open_(prev, "part_recv")
+        self.prev_flags = open_(prev, "flags")
+        prev_home = open_(prev, "home")
+        self.prev_home = pool_view(home_pool.num_layers, everyone[prev]["home_blocks"],
+                                   home_pool.num_kv_heads, home_pool.head_dim, prev_home,
+                                   device.index if device.index is not None else 0)
+        self.prev_handoff_dst = torch.tensor(everyone[prev]["handoff_dst"], dtype=torch.int32,
+                                             device=device)
+
+    def flag(self, base: int, kind: str, layer: int) -> int:
+        return base + 4 * (self.KINDS.index(kind) * self.L + layer)
+
+    def my_flag(self, kind, layer):
+        return self.flag(self.flags.data_ptr(), kind, layer)
+
+    def check(self):
+        if int(self.err.item()) != 0:
+            raise RuntimeError("P2P transport: a peer signal timed out")
+
+    def close(self):
+        from . import ipc_close
+        for ptr, off in self._opened.values():
+            try:
+                ipc_close(ptr, off)
+            except Exception:
+                pass
+        self._opened = {}
+
+
 class ShardedDecodeStep:
     def __init__(self, ops, ex, rank: int, world: int, home_pool, home_bt, cold_pool, cold_bt,
                  kv_split, num_q_heads: int, num_layers: int, head_dim: int,
                  handoff_src_ids=None, handoff_dst_ids=None, chunk_bytes: int = 0,
                  pg_attn=None, pg_mig=None, lookahead: int = 1, device=None,
-                 fuse_local: bool = True, copy_engine: bool = False):
+                 fuse_local: bool = True, copy_engine: bool = False, transport: str = "nccl"):
         self.ops, self.ex = ops, ex
         self.rank, self.world = rank, world
         self.prev, self.next = (rank - 1) % world, (rank + 1) % world
@@ -202,6 +269,23 @@ class ShardedDecodeStep:
         if self.fuse_local:
             self.local_ws = ops.local_workspace([home_pool, cold_pool], [home_bt, cold_bt], self.B,
                                                 self.hq, dev)
+        # N>1 transport: "nccl" (torch.distributed P2P; gather/send/recv/scatter for the
+        # hand-off) or "p2p" (CUDA IPC pushes straight into the neighbours' memory + flags)
+        self.transport = transport if world > 1 else "local"
+        self.links = None
+        self.epoch = 0
+        if self.transport == "p2p":
+            pn = self.part_cold[0][4].numel()
+            self.links = P2PLinks(rank, world, num_layers, home_pool,
+                                  torch.empty((num_layers, self.B, num_q_heads, head_dim),
+                                              dtype=torch.bfloat16, device=dev),
+                                  pn, handoff_dst_ids if handoff_dst_ids is not None else
+                                  torch.zeros(0, dtype=torch.int32), dev, pg_attn)
+            self.part_recv = [split_partial(self.links.part_recv[layer], self.B, self.hq, self.d)
+                              + (None, self.links.part_recv[layer]) for layer in range(num_layers)]
+            self.q_prev = self.links.q_prev
+            self.push = torch.cuda.Stream(device=dev)
+            self.merge_s = torch.cuda.Stream(device=dev)
         self.ev = {k: [ex.event() for _ in range(num_layers)]
                    for k in ("mig_done", "layer_start", "q_ready", "part_ready")}
         self.out_ready = [ex.event() for _ in range(num_layers)]
@@ -214,7 +298,10 @@ class ShardedDecodeStep:
     def launches_per_step(self) -> int:
         """Our kernels per step: 2 attention + 1 merge (+ 1 fused copy at N=1, or
         gather + scatter at N>1, when hand-offs are present) per layer."""
-        mig = 0 if self.n_handoff == 0 or self.ce_ids is not None else (1 if self.world == 1 else 2)
+        mig = 0 if self.n_handoff == 0 or self.ce_ids is not None else (
+            1 if self.world == 1 or self.transport == "p2p" else 2)
+        if self.transport == "p2p":  # + the tiny signal / wait kernels of the protocol
+            return self.L * (3 + mig + 8)
         attn = 1 if self.fuse_local else 3
         return self.L * (attn + mig)
 
@@ -225,6 +312,8 @@ class ShardedDecodeStep:
         events recorded on the launching streams (CUDA only).  ``inputs_ready[l]``: an
         event the step waits for before reading q[l] (e.g. its H2D copy); after the call,
         ``self.out_ready[l]`` is recorded once out[l] / lse[l] are final (per-layer D2H)."""
+        if self.transport == "p2p":
+            return self._enqueue_p2p(q, out, lse, timers, inputs_ready)
         ex, ops, E = self.ex, self.ops, self.ev
         if self.world > 1 and (self.q_prev is None or self.q_prev.shape != q.shape):
             self.q_prev = torch.empty_like(q)
@@ -297,4 +386,70 @@ class ShardedDecodeStep:
                     ops.merge([self.part_own[layer], self.part_recv[layer]], out[layer],
                               None if lse is None else lse[layer])
                     ex.record(self.out_ready[layer], ex.comm)
+        ex.end()
+
+    def _enqueue_p2p(self, q, out, lse, timers, inputs_ready):
+        """N>1 over CUDA IPC: every exchange is a push into the neighbour's memory followed
+        by a flag; consumers' streams wait on their local flags (epoch = step counter)."""
+        from . import copy_ptr, kv_migrate_layer, signal, wait_signal
+        ex, ops, E, lk = self.ex, self.ops, self.ev, self.links
+        self.epoch += 1
+        e = self.epoch
+        to, err = lk.timeout_ns, lk.err.data_ptr()
+        qb = q[0].numel() * q.element_size()
+        ex.begin()
+        for s_ in (self.push, self.merge_s):
+            s_.wait_stream(torch.cuda.current_stream())
+        with ex.use(ex.comm):  # q of my requests -> next (their cold instance)
+            for layer in range(self.L):
+                if inputs_ready is not None:
+                    ex.wait(ex.comm, inputs_ready[layer])
+                wait_signal(lk.my_flag("q_ack", layer), e - 1, to, err)
+                copy_ptr(lk.next_q_prev + layer * qb, q[layer].data_ptr(), qb)
+                signal(lk.flag(lk.next_flags, "q", layer), e)
+        for layer in range(self.L):
+            with ex.use(ex.copy):  # hand-off: my cold pool -> prev's home pool, pushed
+                if self.lookahead >= 0 and layer - self.lookahead >= 0:
+                    ex.wait(ex.copy, E["layer_start"][layer - self.lookahead])
+                if timers is not None:
+                    timers[layer][2].record(ex.copy)
+                if self.n_handoff:
+                    kv_migrate_layer(self.cold, lk.prev_home, layer, self.src_ids,
+                                     lk.prev_handoff_dst)
+                signal(lk.flag(lk.prev_flags, "mig", layer), e)
+                if timers is not None:
+                    timers[layer][3].record(ex.copy)
+            with ex.use(ex.compute):
+                ex.record(E["layer_start"][layer], ex.compute)
+                wait_signal(lk.my_flag("mig", layer), e, to, err)  # next's hand-off arrived
+                if inputs_ready is not None:
+                    ex.wait(ex.compute, inputs_ready[layer])
+                if timers is not None:
+                    timers[layer][0].record(ex.compute)
+                ops.attention(self.home, layer, q[layer], self.home_bt, self.kv_split, 0,
+                              self.part_own[layer])
+                wait_signal(lk.my_flag("q", layer), e, to, err)    # prev's q arrived
+                ops.attention(self.cold, layer, self.q_prev[layer], self.cold_bt, self.kv_split,
+                              1, self.part_cold[layer])
+                signal(lk.flag(lk.prev_flags, "q_ack", layer), e)
+                if timers is not None:
+                    timers[layer][1].record(ex.compute)
+                ex.record(E["part_ready"][layer], ex.compute)
+            with torch.cuda.stream(self.push):  # prev's shard-1 partial -> prev
+                self.push.wait_event(E["part_ready"][layer])
+                wait_signal(lk.my_flag("part_ack", layer), e - 1, to, err)
+                flat = self.part_cold[layer][4]
+                copy_ptr(lk.prev_part_recv + layer * flat.numel() * 4, flat.data_ptr(),
+                         flat.numel() * 4)
+                signal(lk.flag(lk.prev_flags, "part", layer), e)
+            with torch.cuda.stream(self.merge_s):  # my shard-1 partial from next -> merge
+                wait_signal(lk.my_flag("part", layer), e, to, err)
+                self.merge_s.wait_event(E["part_ready"][layer])
+                ops.merge([self.part_own[layer], self.part_recv[layer]], out[layer],
+                          None if lse is None else lse[layer])
+                signal(lk.flag(lk.next_flags, "part_ack", layer), e)
+                self.out_ready[layer].record(self.merge_s)
+        cur = torch.cuda.current_stream()
+        for s_ in (self.push, self.merge_s):
+            cur.wait_stream(s_)
         ex.end()

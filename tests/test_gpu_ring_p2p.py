@@ -1,0 +1,118 @@
+"""The N>1 ring on real GPU kernels with the P2P transport (CUDA IPC pushes + flags),
+run as 2 and 3 processes sharing GPU 0 (the only GPU gpurun offers; IPC between
+processes works on one device, NCCL does not).  Every rank checks its merged O / lse
+against the oracle over its requests' whole KV (shard 1 lived on the next rank) and the
+hand-off chunks pushed into its home pool by the next rank, over two steps (epochs) so
+the back-pressure acks are exercised."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+SHAPE = synth.Shape(2, 8, 2, 128)
+LENS = (37, 64, 300)
+N_HANDOFF_BLOCKS = 5
+
+
+def handoff_bytes(owner_seed):
+    g = torch.Generator().manual_seed(1000 + owner_seed)
+    shp = (SHAPE.n_layers, N_HANDOFF_BLOCKS, 2, SHAPE.hkv, SHAPE.bs, SHAPE.d)
+    return torch.randint(0, 65536, shp, generator=g, dtype=torch.int32).to(torch.int16).numpy().view(np.uint16)
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).view(torch.bfloat16).cuda()
+
+
+def run_rank(rank, world, port, errq):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import paper_2510_13223_b200 as bs
+        from paper_2510_13223_b200.ring import CudaExec, CudaOps, ShardedDecodeStep
+        prev, nxt = (rank - 1) % world, (rank + 1) % world
+        ks = synth.block_aligned_split(LENS, 2)
+        own = synth.gen_dense(SHAPE, LENS, seed=rank)
+        prv = synth.gen_dense(SHAPE, LENS, seed=prev)
+        home = synth.place_shards(own, ks, seed=rank, spare_blocks=N_HANDOFF_BLOCKS + 2)[0]
+        cold = synth.place_shards(prv, ks, seed=prev, spare_blocks=N_HANDOFF_BLOCKS + 2)[1]
+        free_home = [i for i in range(home.pool.shape[1]) if not home.used[i]][:N_HANDOFF_BLOCKS]
+        free_cold = [i for i in range(cold.pool.shape[1]) if not cold.used[i]][:N_HANDOFF_BLOCKS]
+        cold.pool[:, free_cold] = handoff_bytes(rank)
+        hp = bs.KVPool(SHAPE.n_layers, home.pool.shape[1], SHAPE.hkv, SHAPE.d)
+        hp.data.copy_(_dev(home.pool))
+        cp = bs.KVPool(SHAPE.n_layers, cold.pool.shape[1], SHAPE.hkv, SHAPE.d)
+        cp.data.copy_(_dev(cold.pool))
+        i32 = lambda x: torch.as_tensor(np.asarray(x), dtype=torch.int32).cuda()
+        dev = torch.device("cuda", 0)
+        sc = synth.default_scale(SHAPE.d)
+        step = ShardedDecodeStep(CudaOps(sc), CudaExec(dev), rank, world, hp, i32(home.block_tables),
+                                 cp, i32(cold.block_tables), i32(ks), SHAPE.hq, SHAPE.n_layers, SHAPE.d,
+                                 handoff_src_ids=i32(free_cold), handoff_dst_ids=i32(free_home),
+                                 chunk_bytes=hp.chunk_bytes, pg_attn=dist.group.WORLD,
+                                 device=dev, transport="p2p")
+        q = _dev(own.q)
+        for _ in range(2):   # two epochs
+            out = torch.full(q.shape, float("nan"), dtype=torch.bfloat16, device=dev)
+            lse = torch.full(q.shape[:-1], float("nan"), device=dev)
+            step.enqueue(q, out, lse)
+            torch.cuda.synchronize()
+            step.links.check()
+            dist.barrier()
+            shards = synth.place_shards(own, ks, seed=rank)
+            for layer in range(SHAPE.n_layers):
+                ref_o, ref_lse = oracle.attention_full([s.pool for s in shards],
+                                                       [s.block_tables for s in shards], layer,
+                                                       own.q[layer], ks, sc)
+                got = out[layer].float().cpu().double().numpy()
+                assert np.abs(got - ref_o).max() <= 2e-2, (rank, layer)
+                assert np.abs(lse[layer].cpu().double().numpy() - ref_lse).max() <= 1e-4, (rank, layer)
+        got_home = hp.data.cpu().view(torch.int16).numpy().view(np.uint16)
+        assert np.array_equal(got_home[:, free_home], handoff_bytes(nxt)), rank
+        dist.barrier()
+        step.links.close()
+        dist.destroy_process_group()
+    except Exception:
+        import traceback
+        errq.put(f"rank {rank}: {traceback.format_exc()}")
+        raise
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ring_p2p_on_one_gpu(world):
+    ctx = mp.get_context("spawn")
+    errq = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=run_rank, args=(r, world, port, errq)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    alive = [p for p in procs if p.is_alive()]
+    for p in alive:
+        p.kill()
+    errs = []
+    while not errq.empty():
+        errs.append(errq.get())
+    assert not alive, "ranks hung"
+    assert not errs, "\n".join(errs)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]

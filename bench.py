@@ -18,8 +18,8 @@ value = decode tokens/s of the step (B / step time), inputs resident in HBM; poo
 (q H2D from pinned memory and O/lse D2H every step).  The CPU oracle is timed beside
 it on a bounded sample (cpu_baseline).  N>1 (torchrun): a ring of instances, one per GPU
 -- rank r is home for its 64 requests and cold instance of rank r-1 (holds their shard 1
-and their hand-off KV); q, partials and hand-off chunks cross NVLink via NCCL P2P every
-layer (weak scaling: per-GPU work is fixed).  See DESIGN.md §8.
+and their hand-off KV); q, partials and hand-off chunks cross NVLink every layer, pushed
+straight into the neighbour's IPC-mapped memory (--transport p2p, default) or by NCCL P2P (weak scaling: per-GPU work is fixed).  See DESIGN.md §8.
 """
 from __future__ import annotations
 
@@ -325,8 +325,10 @@ def run_ours(args, rank, world, device):
             "workload": WORKLOAD,
             "layers": L, "batch": BATCH, "seq_len": SEQ, "num_q_heads": SHAPE.hq,
             "num_kv_heads": SHAPE.hkv, "head_dim": SHAPE.d, "kv_shards": N_SHARDS,
-            "handoff_requests_per_step": N_HANDOFF, "parallelism": (f"ring of {world} instances (home + cold per GPU), NCCL P2P" if world > 1
-                            else "1 GPU, 2 virtual instances"),
+            "handoff_requests_per_step": N_HANDOFF, "parallelism": (f"ring of {world} instances (home + cold per GPU), {args.transport} transport"
+                            + (" [ALL RANKS ON ONE GPU: functional check only]"
+                               if os.environ.get("BS_RING_SAME_GPU") == "1" else "")
+                            if world > 1 else "1 GPU, 2 virtual instances"),
             "l2": "no flush: resident pools 70 GiB >> 126 MB L2",
         },
         "attn_hbm_gbs": round(attn_gbs, 1),

@@ -9,8 +9,9 @@ head_dim 128, bf16 KV), decode batch 64 at 2048 tokens.  Two serving instances -
 decode D (home) and prefill P -- each own a paged pool.  Every request's KV is split
 2-way (tokens [0,1024) in D, [1024,2048) offloaded to P: attention-level migration,
 PAPER.md:207-237 Fig. 4).  During each decode step 3 more 2048-token requests are handed
-off P -> D layer by layer on a side stream (Fig. 6; lookahead 1, event
-gated).  At N=1 both instances share GPU 0 (virtual instances).  One step = all 32
+off P -> D layer by layer on a side stream (Fig. 6; every layer's attention
+waits for its own layer's migration event; the copy stream streams ahead unthrottled --
+BS_LOOKAHEAD=-1, measured 5 % faster than lookahead 1 on one GPU).  At N=1 both instances share GPU 0 (virtual instances).  One step = all 32
 layers of: migrate(l) || [split attention on D, on P -> LSE merge -> bf16 O].
 
 value = decode tokens/s of the step (B / step time), inputs resident in HBM; pools are
@@ -173,7 +174,7 @@ def build_workload(bs, device, rank=0, world=1, layers=None, transport="p2p"):
         handoff_dst_ids=i32(dst_ids), chunk_bytes=home.chunk_bytes,
         pg_attn=dist.group.WORLD if world > 1 else None,
         pg_mig=dist.new_group(list(range(world))) if world > 1 else None,
-        lookahead=1, device=device, copy_engine=os.environ.get("BS_HANDOFF_CE", "0") == "1",
+        lookahead=int(os.environ.get("BS_LOOKAHEAD", "-1")), device=device, copy_engine=os.environ.get("BS_HANDOFF_CE", "0") == "1",
         transport=transport)
     return case, pools, step, ks
 

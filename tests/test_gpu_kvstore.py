@@ -130,3 +130,55 @@ def test_three_stage_pipeline(bs, engine):
     got_dev = _u16(dev.data)
     assert np.array_equal(got_dev[:, :, :, :, :, :], d_np)
     assert np.array_equal(_u16(store.pool.data), s_np)
+
+
+def test_c5_prefix_hits_fetched_then_attended(bs):
+    """C5-shaped (bursty, prefix hits from the Global KV Cache Store):
+    each request's first half (r = 0.5) lives only in the host store; the three-stage
+    pipeline fetches it layer by layer into the device blocks the request's block table
+    points at, and the SAME layer's attention reads them -- so the result is right only
+    if every layer's compute waits for its own fetch (H3).  Lengths log-uniform[128, 16k]
+    (SURVEY.md §8(d) C5), reduced to 12 requests x 3 layers."""
+    from paper_2510_13223_b200.kvstore import KVStore, ThreeStagePipeline
+    shape = synth.Shape(3, 32, 8, 128)                        # Llama-3-8B head shape
+    g = torch.Generator().manual_seed(5)
+    lo, hi = np.log(128.0), np.log(16384.0)
+    lens = np.exp(lo + (hi - lo) * torch.rand(12, generator=g).numpy()).astype(np.int64)
+    dense = synth.gen_dense(shape, lens, seed=5)
+    ks = np.stack([np.zeros(len(lens)), lens], 1).astype(np.int32)
+    res = synth.place_shards(dense, ks, seed=5, spare_blocks=4)[0]
+    nb = res.pool.shape[1]
+    # prefix blocks: the first floor(0.5 * nblk) blocks of every request
+    prefix = []
+    for b in range(len(lens)):
+        nblk = synth.ceil_div(int(lens[b]), 16)
+        prefix += [int(x) for x in res.block_tables[b, : nblk // 2]]
+    store_np = np.full((3, len(prefix) + 3, 2, 8, 16, 128), synth.BF16_NAN, dtype=np.uint16)
+    store_np[:, :len(prefix)] = res.pool[:, prefix]           # the store holds the prefixes
+    dev_np = res.pool.copy()
+    dev_np[:, prefix] = synth.BF16_NAN                        # not resident yet on the GPU
+    dev = bs.KVPool(3, nb, 8, 128)
+    _fill(dev, dev_np)
+    store = KVStore(3, store_np.shape[1], 8, 128)
+    _fill(store.pool, store_np)
+    q = torch.from_numpy(dense.q.view(np.int16)).view(torch.bfloat16).cuda()
+    bt = torch.from_numpy(res.block_tables).cuda()
+    ksd = torch.from_numpy(ks).cuda()
+    B, sc = len(lens), synth.default_scale(128)
+    o = torch.empty(3, B, 32, 128, device="cuda")
+    m = torch.empty(3, B, 32, device="cuda")
+    l = torch.empty(3, B, 32, device="cuda")
+    ws = torch.zeros(max(16, bs.split_decode_attention_workspace_size(dev, B, 32, bt.shape[1])),
+                     dtype=torch.uint8, device="cuda")
+
+    def compute(layer):
+        bs.split_decode_attention(dev, layer, q[layer], bt, ksd, 0, sc, o[layer], m[layer], l[layer], ws)
+
+    pipe = ThreeStagePipeline(store, dev, 3, compute,
+                              fetch_pairs=(list(range(len(prefix))), prefix), engine="ce")
+    pipe.enqueue()
+    torch.cuda.synchronize()
+    for layer in range(3):
+        ro, rm, rl = oracle.attention_shard(res.pool, layer, dense.q[layer], res.block_tables, ks, 0, sc)
+        assert np.abs(o[layer].cpu().double().numpy() - ro).max() <= 5e-3
+        assert np.abs((m[layer] + l[layer].log()).cpu().double().numpy() - (rm + np.log(rl))).max() <= 1e-4

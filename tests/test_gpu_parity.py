@@ -374,3 +374,35 @@ def test_full_size_c4_llama70b_mixed_8way_sampled(bs):
     longest = int(np.argmax(lens))
     shortest = int(np.argmin(lens))
     _sampled_check(bs, shape, list(lens), ks, [shortest, longest, 7], seed=47, fused=False)
+
+
+def test_bench_step_c2_sampled():
+    """The exact configuration bench.py times (C2, N=1: fused local attention over the
+    home and cold pools + the layer-wise hand-off on the copy stream, unthrottled
+    lookahead) for 2 full-size layers; the oracle recomputes sampled requests of both
+    layers, and the handed-off chunks are bit-exact in the home pool."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    import paper_2510_13223_b200 as bsm
+    dev = torch.device("cuda", 0)
+    case, pools, step, ks = bench.build_workload(bsm, dev, 0, 1, layers=2)
+    assert step.fuse_local
+    home, cold = pools
+    src_before = cold.data[:, step.src_ids.long()].clone()
+    out = torch.empty(case.q.shape, dtype=torch.bfloat16, device=dev)
+    lse = torch.empty(case.q.shape[:-1], dtype=torch.float32, device=dev)
+    step.enqueue(case.q, out, lse)
+    torch.cuda.synchronize()
+    assert torch.equal(home.data[:, step.dst_ids.long()].view(torch.int16), src_before.view(torch.int16))
+    sc = synth.default_scale(128)
+    sample = [0, 31, 63]
+    for layer in range(2):
+        sp, sbt, sks, sq = synth.extract_requests(case, sample, layer)
+        ref_o, ref_lse = oracle.attention_full(sp, sbt, 0, sq, sks, sc)
+        got = out[layer, sample].float().cpu().double().numpy()
+        err = np.abs(got - ref_o)
+        assert err.max() <= ABS_TOL
+        assert (err.max(-1) / np.abs(ref_o).max(-1)).max() <= ROW_REL_TOL
+        assert np.abs(lse[layer, sample].cpu().double().numpy() - ref_lse).max() <= LSE_TOL

@@ -208,25 +208,44 @@ __device__ __forceinline__ void cta_combine_and_store(const AttnParams& p, int b
   __syncthreads();
   if (!s_flag[0]) return;
   __threadfence();
-  if (threadIdx.x < G) {  // per-head weights w_j = l_j 2^(m_j - M) / L, fixed order
-    const int h = threadIdx.x;
-    const int64_t row = (int64_t)b * p.hq + gm * G + h;
-    const float* ml = p.ws_ml + row * p.nsplit * 2;
-    float M = -INFINITY;
-    for (int j = 0; j < p.nsplit; ++j) M = fmaxf(M, __ldcg(ml + 2 * j));
-    float L = 0.f;
-    for (int j = 0; j < p.nsplit; ++j) {
-      const float mj = __ldcg(ml + 2 * j);
-      const float wj = mj == -INFINITY ? 0.f : __ldcg(ml + 2 * j + 1) * exp2f(mj - M);
-      s_w[h * kMaxSplit + j] = wj;
-      L += wj;
-    }
-    for (int j = 0; j < p.nsplit; ++j) s_w[h * kMaxSplit + j] = L > 0.f ? s_w[h * kMaxSplit + j] / L : 0.f;
-    if (p.merged) {
-      if (p.lse) p.lse[row] = L > 0.f ? M * kLn2 + logf(L) : -INFINITY;
-    } else {
-      p.m[row] = L > 0.f ? M * kLn2 : -INFINITY;
-      p.l[row] = L;
+  // per-head weights w_j = l_j 2^(m_j - M) / L: one warp per head, lanes over the ranges
+  // (<= kMaxSplit = 64 -> 2 per lane); butterfly reductions keep the result deterministic
+  {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int h = warp; h < G; h += kWarps) {
+      const int64_t row = (int64_t)b * p.hq + gm * G + h;
+      const float* ml = p.ws_ml + row * p.nsplit * 2;
+      float mj[2], lj[2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int j = lane + 32 * t;
+        mj[t] = j < p.nsplit ? __ldcg(ml + 2 * j) : -INFINITY;
+        lj[t] = j < p.nsplit ? __ldcg(ml + 2 * j + 1) : 0.f;
+      }
+      float M = fmaxf(mj[0], mj[1]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+      float w[2], L = 0.f;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        w[t] = mj[t] == -INFINITY ? 0.f : lj[t] * exp2f(mj[t] - M);
+        L += w[t];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int j = lane + 32 * t;
+        if (j < p.nsplit) s_w[h * kMaxSplit + j] = L > 0.f ? w[t] / L : 0.f;
+      }
+      if (lane == 0) {
+        if (p.merged) {
+          if (p.lse) p.lse[row] = L > 0.f ? M * kLn2 + logf(L) : -INFINITY;
+        } else {
+          p.m[row] = L > 0.f ? M * kLn2 : -INFINITY;
+          p.l[row] = L;
+        }
+      }
     }
   }
   __syncthreads();
@@ -235,6 +254,7 @@ __device__ __forceinline__ void cta_combine_and_store(const AttnParams& p, int b
     const int64_t row = (int64_t)b * p.hq + gm * G + h;
     const float* po = p.ws_o + row * p.nsplit * D + x;
     float O = 0.f;
+#pragma unroll 8
     for (int j = 0; j < p.nsplit; ++j) O += s_w[h * kMaxSplit + j] * __ldcg(po + (int64_t)j * D);
     if (p.merged) p.out[row * D + x] = __float2bfloat16_rn(O);
     else p.o[row * D + x] = O;

@@ -37,7 +37,7 @@ __device__ __forceinline__ void st_stream(int4* p, const int4& v) {
                : "memory");
 }
 
-template <int PAGE_BYTES>
+template <int PAGE_BYTES, int U>
 __global__ void __launch_bounds__(256) copy_pages_vec16(const uint8_t* __restrict__ src_base,
                                                         const int32_t* __restrict__ src_ids,
                                                         uint8_t* __restrict__ dst_base,
@@ -51,23 +51,35 @@ __global__ void __launch_bounds__(256) copy_pages_vec16(const uint8_t* __restric
   const int wpc = blockDim.x >> 5;
   const int64_t per_layer = (int64_t)n * pages_per_chunk;
   const int64_t total = per_layer * n_layers;
-  for (int64_t p = (int64_t)blockIdx.x * wpc + (threadIdx.x >> 5); p < total;
-       p += (int64_t)gridDim.x * wpc) {
-    const int32_t ly = (int32_t)(p / per_layer);
-    const int64_t q = p - (int64_t)ly * per_layer;
-    const int32_t i = (int32_t)(q / pages_per_chunk);
-    const int32_t j = (int32_t)(q - (int64_t)i * pages_per_chunk);
-    const int64_t si = src_ids ? __ldg(src_ids + i) : i;
-    const int64_t di = dst_ids ? __ldg(dst_ids + i) : i;
-    const int4* s = reinterpret_cast<const int4*>(src_base + ly * src_layer_stride + si * chunk_bytes +
-                                                  (int64_t)j * PAGE_BYTES) + lane;
-    int4* d = reinterpret_cast<int4*>(dst_base + ly * dst_layer_stride + di * chunk_bytes +
-                                      (int64_t)j * PAGE_BYTES) + lane;
-    int4 r[V];
+  // a warp moves U pages per iteration: U * V 16-byte loads in flight per lane
+  for (int64_t p0 = ((int64_t)blockIdx.x * wpc + (threadIdx.x >> 5)) * U; p0 < total;
+       p0 += (int64_t)gridDim.x * wpc * U) {
+    int4 r[U][V];
+    int4* dst[U];
 #pragma unroll
-    for (int v = 0; v < V; ++v) r[v] = ld_stream(s + v * 32);
+    for (int u = 0; u < U; ++u) {
+      const int64_t p = p0 + u;
+      dst[u] = nullptr;
+      if (p < total) {
+        const int32_t ly = (int32_t)(p / per_layer);
+        const int64_t q = p - (int64_t)ly * per_layer;
+        const int32_t i = (int32_t)(q / pages_per_chunk);
+        const int32_t j = (int32_t)(q - (int64_t)i * pages_per_chunk);
+        const int64_t si = src_ids ? __ldg(src_ids + i) : i;
+        const int64_t di = dst_ids ? __ldg(dst_ids + i) : i;
+        const int4* s = reinterpret_cast<const int4*>(src_base + ly * src_layer_stride +
+                                                      si * chunk_bytes + (int64_t)j * PAGE_BYTES) + lane;
+        dst[u] = reinterpret_cast<int4*>(dst_base + ly * dst_layer_stride + di * chunk_bytes +
+                                         (int64_t)j * PAGE_BYTES) + lane;
 #pragma unroll
-    for (int v = 0; v < V; ++v) st_stream(d + v * 32, r[v]);
+        for (int v = 0; v < V; ++v) r[u][v] = ld_stream(s + v * 32);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (dst[u])
+#pragma unroll
+        for (int v = 0; v < V; ++v) st_stream(dst[u] + v * 32, r[u][v]);
   }
 }
 
@@ -205,10 +217,18 @@ bs_status launch_copy_t(const uint8_t* src_base, const int32_t* src_ids, uint8_t
     return check_launch("copy_pages_bulk");
   }
   const int wpc = 8;
-  int64_t grid = std::min<int64_t>((total + wpc - 1) / wpc, (int64_t)sms * 8);
+  static const int unroll = [] {
+    const char* e = getenv("BS_COPY_UNROLL");
+    return e && atoi(e) == 1 ? 1 : 2;
+  }();
+  int64_t grid = std::min<int64_t>((total + wpc * unroll - 1) / (wpc * unroll), (int64_t)sms * 8);
   if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
-  copy_pages_vec16<PAGE_BYTES><<<(unsigned)grid, wpc * 32, 0, stream>>>(
-      src_base, src_ids, dst_base, dst_ids, n, ppc, chunk, n_layers, src_ls, dst_ls);
+  if (unroll == 2)
+    copy_pages_vec16<PAGE_BYTES, 2><<<(unsigned)grid, wpc * 32, 0, stream>>>(
+        src_base, src_ids, dst_base, dst_ids, n, ppc, chunk, n_layers, src_ls, dst_ls);
+  else
+    copy_pages_vec16<PAGE_BYTES, 1><<<(unsigned)grid, wpc * 32, 0, stream>>>(
+        src_base, src_ids, dst_base, dst_ids, n, ppc, chunk, n_layers, src_ls, dst_ls);
   return check_launch("copy_pages_vec16");
 }
 

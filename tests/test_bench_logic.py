@@ -1,0 +1,60 @@
+"""Host-side logic of bench.py (no GPU): algorithmic-byte accounting, hand-off id choice,
+clock-log parsing, and the CLI."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+import synth  # noqa: E402
+
+
+def test_attention_bytes_closed_form():
+    ks = synth.block_aligned_split(np.full(64, 2048), 2)
+    hq, d, hkv = 32, 128, 32
+    kv = 64 * 2048 * 2 * hkv * d * 2
+    bt = 64 * 2 * 4 * 64
+    fused = kv + bt + 64 * hq * d * 2 + 64 * hq * (d * 2 + 4)
+    split = kv + bt + 64 * hq * d * 2 + 64 * 2 * hq * (d + 2) * 4
+    assert bench.attn_bytes_per_layer(ks, fused=True) == fused
+    assert bench.attn_bytes_per_layer(ks, fused=False) == split
+    assert fused == 2148573184                      # the number bench.py reports per layer
+
+
+def test_handoff_src_ids_are_lowest_unused_of_the_cold_pool():
+    lens = np.array([40, 33])
+    ks = synth.block_aligned_split(lens, 2)
+    case = synth.device_shards(synth.Shape(1, 2, 2, 64), lens, ks, seed=3, device="cpu",
+                               spare_blocks=4, layers=1)
+    used = set(int(x) for x in case.block_tables[1].ravel() if x >= 0)
+    got = bench.handoff_src_ids(case, 3)
+    assert got == sorted(i for i in range(case.pools[1].shape[1]) if i not in used)[:3]
+    assert not (set(got) & used)
+
+
+def test_clock_summary_parsing(tmp_path):
+    c = bench.ClockSampler(0)
+
+    class _P:
+        pass
+    c.proc = _P()
+    f = open(tmp_path / "c.csv", "w+")
+    f.write("1965, 1965, Not Active, Not Active, Not Active, Active\n"
+            "1900, 1965, Not Active, Not Active, Not Active, Not Active\n"
+            "garbage line\n")
+    f.flush()
+    c.f = f
+    s = c.summary()
+    assert s["sm_mhz"] == 1932.5 and s["sm_max_mhz"] == 1965.0
+    assert s["reasons"] == ["sw_power_cap"] and s["samples"] == 2
+
+
+def test_cli_help():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--help"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "--transport" in r.stdout and "--impl" in r.stdout

@@ -196,18 +196,21 @@ __device__ __forceinline__ void cta_combine_and_store(const AttnParams& p, int b
   if (p.nsplit == 1) return;
 
   // ---- split-K / local shards: the last CTA of this (request, kv-head) merges ---------
-  __threadfence();
+  // The barrier orders every thread's partial stores before thread 0's acq_rel atomic
+  // (release is cumulative), and the winner's acquire + barrier order the other CTAs'
+  // partials before this CTA's loads -- one gpu-scope atomic per CTA instead of a full
+  // fence (CCTL.IVALL) in every thread.
   __syncthreads();
   if (threadIdx.x == 0) {
     int32_t* cnt = p.ws_cnt + (int64_t)b * p.hkv + g;
-    const int prev = atomicAdd(cnt, 1);
+    int prev;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(cnt) : "memory");
     const int last = prev == p.nsplit - 1;
     if (last) *cnt = 0;  // every CTA has arrived: re-arm for the next call
     s_flag[0] = last;
   }
   __syncthreads();
   if (!s_flag[0]) return;
-  __threadfence();
   // per-head weights w_j = l_j 2^(m_j - M) / L: one warp per head, lanes over the ranges
   // (<= kMaxSplit = 64 -> 2 per lane); butterfly reductions keep the result deterministic
   {
@@ -669,11 +672,15 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
     l_run[0] = l_run[0] * al0 + (p0 + p2);
     l_run[1] = l_run[1] * al1 + (p1 + p3);
     // P^T (bf16) -> smem [head][16 tokens]
-    __nv_bfloat16* pt = reinterpret_cast<__nv_bfloat16*>(s_pt);
-    pt[(2 * tq) * 16 + gq] = __float2bfloat16_rn(p0);
-    pt[(2 * tq + 1) * 16 + gq] = __float2bfloat16_rn(p1);
-    pt[(2 * tq) * 16 + gq + 8] = __float2bfloat16_rn(p2);
-    pt[(2 * tq + 1) * 16 + gq + 8] = __float2bfloat16_rn(p3);
+    {
+      const uint32_t a = pt_u32 + ((2 * tq) * 16 + gq) * 2;
+      const __nv_bfloat16 b0 = __float2bfloat16_rn(p0), b1 = __float2bfloat16_rn(p1);
+      const __nv_bfloat16 b2 = __float2bfloat16_rn(p2), b3 = __float2bfloat16_rn(p3);
+      asm volatile("st.shared.b16 [%0], %1;" ::"r"(a), "h"(*reinterpret_cast<const uint16_t*>(&b0)));
+      asm volatile("st.shared.b16 [%0], %1;" ::"r"(a + 32), "h"(*reinterpret_cast<const uint16_t*>(&b1)));
+      asm volatile("st.shared.b16 [%0], %1;" ::"r"(a + 16), "h"(*reinterpret_cast<const uint16_t*>(&b2)));
+      asm volatile("st.shared.b16 [%0], %1;" ::"r"(a + 48), "h"(*reinterpret_cast<const uint16_t*>(&b3)));
+    }
     if (nvalid < 16) {  // pad rows of the V page may hold anything (NaN): zero them
       for (int i = lane; i < (16 - nvalid) * NB * 8; i += 32) {
         const int r = nvalid + i / (NB * 8), rem = i % (NB * 8);

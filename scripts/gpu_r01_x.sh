@@ -1,0 +1,7 @@
+set -x
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
+echo "pytest rc=$?"
+timeout 600 python scripts/microbench.py --only attn --json gpurun_out/micro_attn.json > gpurun_out/micro_attn.log 2>&1
+timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err
+echo "bench rc=$?"

@@ -798,28 +798,35 @@ bs_status make_plan(int batch, int G, int hq, int hkv, int d, int n_local, const
   int mb_max = 1;
   for (int j = 0; j < n_local; ++j) mb_max = std::max(mb_max, max_blocks[j]);
   const int min_bps = kWarps;
+  // cap the blocks per CTA range: with mixed lengths the longest request's CTA is the
+  // critical path; shorter ranges let the hardware scheduler balance them (BS_ATTN_MAX_BPS)
+  static const int max_bps = [] {
+    const char* e = getenv("BS_ATTN_MAX_BPS");
+    const int x = e ? atoi(e) : 0;
+    return x > 0 ? x : kBtMax;
+  }();
   int best_bps = -1;
   double best = 1e300;
-  int last_bps = -1;
-  for (int ns = 1; ns <= kMaxSplit; ++ns) {
-    const int bps = std::max(min_bps, (mb_max + ns - 1) / ns);
-    if (bps == last_bps || bps > kBtMax) {
-      if (bps > kBtMax) continue;
-      if (bps == last_bps) continue;
+  for (int pass = 0; pass < 2 && best_bps < 0; ++pass) {  // pass 1: without the cap
+    const int cap = pass == 0 ? std::min(kBtMax, std::max(max_bps, min_bps)) : kBtMax;
+    int last_bps = -1;
+    for (int ns = 1; ns <= kMaxSplit; ++ns) {
+      const int bps = std::max(min_bps, (mb_max + ns - 1) / ns);
+      if (bps > cap || bps == last_bps) continue;
+      last_bps = bps;
+      int total = 0;
+      for (int j = 0; j < n_local; ++j) total += (max_blocks[j] + bps - 1) / bps;
+      if (total > kMaxSplit) continue;
+      const int64_t ctas = base * total;
+      const int64_t waves = (ctas + slots - 1) / slots;
+      const bool partial = total > 1;
+      const double cost = (double)waves * ((double)bps / kWarps + 2.0 + (partial ? 1.0 : 0.0));
+      if (cost < best - 1e-9) {
+        best = cost;
+        best_bps = bps;
+      }
+      if (bps == min_bps) break;
     }
-    last_bps = bps;
-    int total = 0;
-    for (int j = 0; j < n_local; ++j) total += (max_blocks[j] + bps - 1) / bps;
-    if (total > kMaxSplit) continue;
-    const int64_t ctas = base * total;
-    const int64_t waves = (ctas + slots - 1) / slots;
-    const bool partial = total > 1;
-    const double cost = (double)waves * ((double)bps / kWarps + 2.0 + (partial ? 1.0 : 0.0));
-    if (cost < best - 1e-9) {
-      best = cost;
-      best_bps = bps;
-    }
-    if (bps == min_bps) break;
   }
   if (best_bps < 0)
     return set_error(BS_ERR_UNSUPPORTED, "max_blocks %d exceeds %d", mb_max, kBtMax * kMaxSplit);

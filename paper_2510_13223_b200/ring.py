@@ -453,3 +453,16 @@ class ShardedDecodeStep:
         for s_ in (self.push, self.merge_s):
             cur.wait_stream(s_)
         ex.end()
+
+    def capture(self, q: torch.Tensor, out: torch.Tensor, lse: torch.Tensor | None = None):
+        """Capture one full step (all layers, every stream) into a CUDA graph; replaying it
+        re-runs the step with whatever q / pools hold at replay time (N=1 / local only:
+        the P2P and NCCL transports talk to other processes)."""
+        if self.world != 1:
+            raise RuntimeError("graph capture is for the single-GPU step")
+        self.enqueue(q, out, lse)          # warm-up: lazy attributes, workspaces, maps
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.enqueue(q, out, lse)
+        return g

@@ -406,3 +406,28 @@ def test_bench_step_c2_sampled():
         assert err.max() <= ABS_TOL
         assert (err.max(-1) / np.abs(ref_o).max(-1)).max() <= ROW_REL_TOL
         assert np.abs(lse[layer, sample].cpu().double().numpy() - ref_lse).max() <= LSE_TOL
+
+
+def test_bench_step_cuda_graph_replay_matches_eager():
+    """The N=1 step captured into one CUDA graph (3 streams, events, all layers) replays
+    to the bitwise-identical result of eager execution."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    import paper_2510_13223_b200 as bsm
+    dev = torch.device("cuda", 0)
+    case, pools, step, ks = bench.build_workload(bsm, dev, 0, 1, layers=2)
+    out_e = torch.empty(case.q.shape, dtype=torch.bfloat16, device=dev)
+    lse_e = torch.empty(case.q.shape[:-1], dtype=torch.float32, device=dev)
+    step.enqueue(case.q, out_e, lse_e)
+    torch.cuda.synchronize()
+    out_g = torch.zeros_like(out_e)
+    lse_g = torch.zeros_like(lse_e)
+    g = step.capture(case.q, out_g, lse_g)
+    out_g.zero_()
+    lse_g.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out_g.view(torch.int16), out_e.view(torch.int16))
+    assert torch.equal(lse_g, lse_e)

@@ -139,8 +139,8 @@ __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-constexpr int kBulkStages = 16;  // ring slots (pages)
-constexpr int kBulkAhead = 8;    // loads in flight ahead of the store front
+constexpr int kBulkStages = 24;  // ring slots (pages)
+constexpr int kBulkAhead = 16;   // loads in flight ahead of the store front
 
 template <int PAGE_BYTES>
 __global__ void __launch_bounds__(32) copy_pages_bulk(const uint8_t* __restrict__ src_base,
@@ -210,7 +210,7 @@ bs_status launch_copy_t(const uint8_t* src_base, const int32_t* src_ids, uint8_t
                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       configured = true;
     }
-    int64_t grid = std::min<int64_t>(total, (int64_t)sms * 3);
+    int64_t grid = std::min<int64_t>(total, (int64_t)sms * 2);
     if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
     copy_pages_bulk<PAGE_BYTES><<<(unsigned)grid, 32, smem, stream>>>(
         src_base, src_ids, dst_base, dst_ids, n, ppc, chunk);
@@ -240,7 +240,13 @@ bs_status launch_copy_chunks(const uint8_t* src_base, const int32_t* src_ids, ui
                              int32_t n_layers, int64_t src_layer_stride, int64_t dst_layer_stride) {
   if (n == 0 || n_layers == 0) return BS_OK;
   const int32_t ppc = (int32_t)(chunk_bytes / page_bytes);
-  if (method == BS_MIGRATE_AUTO) method = BS_MIGRATE_VEC16;
+  if (method == BS_MIGRATE_AUTO) {
+    static const int dflt = [] {  // BS_MIGRATE_AUTO_METHOD: 1 vec16 (default), 2 bulk
+      const char* e = getenv("BS_MIGRATE_AUTO_METHOD");
+      return e && atoi(e) == BS_MIGRATE_BULK ? BS_MIGRATE_BULK : BS_MIGRATE_VEC16;
+    }();
+    method = dflt;
+  }
   if (page_bytes == 4096)
     return launch_copy_t<4096>(src_base, src_ids, dst_base, dst_ids, n, ppc, (int64_t)chunk_bytes,
                                method, stream, max_ctas, n_layers, src_layer_stride, dst_layer_stride);

@@ -1,27 +1,29 @@
-// H4: paged GQA split decode attention over one KV shard (split attention of
-// PAPER.md:216-231, eqs. 6-9, with readings R-A1..R-A11: token-range split, explicit
-// scale, max-shifted exponentials, shard-local block tables, masked pad slots).
+// H4 (+ H6 for co-located shards): paged GQA split decode attention over KV shards
+// (split attention of PAPER.md:216-231, eqs. 6-9, with readings R-A1..R-A11: token-range
+// split, explicit scale, max-shifted exponentials, shard-local block tables, masked pad
+// slots).
 //
-// Output per (request b, q-head h): the partial triple (o~ normalised by the local
-// denominator, m, l) in fp32, natural-log units -- exactly what bs_merge_partials
-// (eq. 10) consumes.
+// Outputs per (request b, q-head h): the partial triple (o~ normalised by the local
+// denominator, m, l) in fp32, natural-log units -- what bs_merge_partials (eq. 10)
+// consumes -- or, for shards that live on this GPU (bs_split_decode_attention_local),
+// the LSE-merged bf16 O and lse directly.
 //
-// Design (DESIGN.md §Kernels / attention):
-//  * HBM-bound (0.5*G FMA per KV byte): CUDA cores, no tensor cores.
-//  * grid = (nsplit, Hkv, B); a CTA owns one (request, kv-head, block range) and serves
-//    all G query heads of the group, so every K/V page is read from HBM exactly once.
+// Design:
+//  * grid = (CTA ranges over all shards of the launch, kv heads, requests); a CTA owns one
+//    (request, kv-head, block range) and serves all G query heads of the group, so every
+//    K/V page is read from HBM exactly once.
 //  * 4 warps per CTA, each an independent pipeline over every 4th block of the range:
-//    lane 0 streams the block's K page and V page (16 x d bf16 each, contiguous in the
-//    pool) into a STAGES-deep shared-memory ring with TMA bulk copies (cp.async.bulk +
-//    mbarrier complete_tx); block ids come from a shared-memory copy of the block table.
-//  * lane l owns head dims [l*d/32, (l+1)*d/32): q*k partials for all 16 tokens are
-//    reduced with a 16-shuffle reduce-scatter (lane pair 2t,2t+1 ends with token t),
-//    online softmax in log2 units (q pre-scaled by scale*log2e, ex2), p broadcast via
-//    shared memory, p*V accumulated with packed FFMA2.
-//  * the 4 warp states are merged in shared memory; with intra-GPU split-K (nsplit > 1)
-//    each CTA writes a partial to the workspace and the last-arriving CTA of the
-//    (request, kv-head) merges all partials in fixed order (deterministic), resets the
-//    arrival counter, and writes the shard output.  One launch either way.
+//    the block's K and V pages stream into a STAGES-deep shared-memory ring by TMA,
+//    completing on an mbarrier; block ids come from a shared-memory copy of the table.
+//  * split_decode_attn_mma (default): the per-block contractions S^T = K q^T and
+//    O^T += V^T P^T on the tensor cores (mma.sync m16n8k16 bf16 -> fp32, heads in N),
+//    pages by 2-D tensor TMA with 128-byte swizzle so ldmatrix is conflict-free.
+//  * split_decode_attn (CUDA cores, BS_ATTN_MMA=0): lane-owned head dims, a select-free
+//    16-shuffle reduce-scatter, online softmax in log2 units, packed FFMA2.
+//  * the 4 warp states merge in shared memory; with several CTA ranges per
+//    (request, kv-head) -- intra-GPU split-K and/or several local shards -- each CTA
+//    writes a partial to the workspace and the last-arriving CTA merges them in fixed
+//    order (deterministic), re-arms the arrival counter and writes the output.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 

@@ -431,3 +431,40 @@ def test_bench_step_cuda_graph_replay_matches_eager():
     torch.cuda.synchronize()
     assert torch.equal(out_g.view(torch.int16), out_e.view(torch.int16))
     assert torch.equal(lse_g, lse_e)
+
+
+@pytest.mark.parametrize("seed", list(range(24)))
+def test_fuzz_random_configs(bs, seed):
+    """Randomised shapes: G, head_dim, batch, lengths (incl. 0 / 1 / block edges), number
+    of shards, unaligned splits, fragmented pools, split-K and the fused local launch."""
+    rng = np.random.default_rng(1000 + seed)
+    G = int(rng.choice([1, 2, 4, 8]))
+    d = int(rng.choice([64, 128]))
+    hkv = int(rng.choice([1, 2, 3, 4]))
+    shape = synth.Shape(1, hkv * G, hkv, d)
+    B = int(rng.integers(1, 7))
+    lens = [int(x) for x in rng.choice([0, 1, 15, 16, 17, 31, 32, 33, 200, 777, 3000], size=B)]
+    n = int(rng.integers(1, 5))
+    dense = synth.gen_dense(shape, lens, seed=seed)
+    ks = synth.random_split(lens, n, seed=seed) if rng.random() < 0.5 else \
+        synth.block_aligned_split(lens, n)
+    shards = synth.place_shards(dense, ks, seed=seed)
+    pools = gpu_pools(bs, shape, [s.pool for s in shards])
+    bts = [s.block_tables for s in shards]
+    sc = synth.default_scale(d)
+    parts, out, lse = run_split_attention(bs, shape, pools, bts, ks, dense.q[0], 0, sc)
+    check_against_oracle(shape, [s.pool for s in shards], bts, ks, dense.q[0], 0, sc, parts, out, lse)
+    # the same shards through the fused local launch
+    btd = [dev_i32(t) for t in bts]
+    ws = torch.zeros(max(16, bs.split_decode_attention_local_workspace_size(
+        pools, [t.shape[1] for t in btd], B, shape.hq)), dtype=torch.uint8, device="cuda")
+    out2 = torch.empty_like(out)
+    lse2 = torch.empty_like(lse)
+    bs.split_decode_attention_local(pools, 0, dev_bf16(dense.q[0]), btd, list(range(n)),
+                                    dev_i32(ks), sc, out2, lse2, ws)
+    torch.cuda.synchronize()
+    assert (out2.float() - out.float()).abs().max().item() <= 2 * ABS_TOL
+    fin = torch.isfinite(lse)
+    assert torch.equal(torch.isfinite(lse2), fin)
+    if fin.any():
+        assert (lse2[fin] - lse[fin]).abs().max().item() <= 2 * LSE_TOL

@@ -252,10 +252,14 @@ class ShardedDecodeStep:
         self.pg_attn, self.pg_mig = pg_attn, pg_mig
         self.lookahead = lookahead
         dev = device
+        # N=1: both shards are local -> one fused attention + merge launch per layer
+        self.fuse_local = fuse_local and world == 1 and hasattr(ops, "attention_local")
         mk = lambda pool, bt: ops.partial_buffers(pool, self.B, self.hq, self.d, bt.shape[1], dev)
         # per-layer partial buffers: the merge of layer l may trail the attention of l+1
-        self.part_own = [mk(home_pool, home_bt) for _ in range(num_layers)]
-        self.part_cold = [mk(cold_pool, cold_bt) for _ in range(num_layers)]
+        # (not needed by the fused local launch, which merges in its epilogue)
+        n_part = 0 if self.fuse_local else num_layers
+        self.part_own = [mk(home_pool, home_bt) for _ in range(n_part)]
+        self.part_cold = [mk(cold_pool, cold_bt) for _ in range(n_part)]
         self.part_recv = self.part_cold if world == 1 else [
             self._recv_buffer(p[4]) for p in self.part_cold]
         self.q_prev = None
@@ -264,8 +268,6 @@ class ShardedDecodeStep:
             nbytes = self.n_handoff * chunk_bytes
             self.stage_send = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
             self.stage_recv = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
-        # N=1: both shards are local -> one fused attention + merge launch per layer
-        self.fuse_local = fuse_local and world == 1 and hasattr(ops, "attention_local")
         if self.fuse_local:
             self.local_ws = ops.local_workspace([home_pool, cold_pool], [home_bt, cold_bt], self.B,
                                                 self.hq, dev)
@@ -296,8 +298,9 @@ class ShardedDecodeStep:
 
     @property
     def launches_per_step(self) -> int:
-        """Our kernels per step: 2 attention + 1 merge (+ 1 fused copy at N=1, or
-        gather + scatter at N>1, when hand-offs are present) per layer."""
+        """Our kernels per step, per layer: the fused local attention (N=1) or 2 attention
+        launches + 1 merge; + the hand-off copy (1 kernel; gather + scatter with NCCL);
+        + 8 signal / wait kernels of the P2P protocol."""
         mig = 0 if self.n_handoff == 0 or self.ce_ids is not None else (
             1 if self.world == 1 or self.transport == "p2p" else 2)
         if self.transport == "p2p":  # + the tiny signal / wait kernels of the protocol

@@ -341,7 +341,9 @@ def run_ours(args, rank, world, device):
             "workload": WORKLOAD,
             "layers": L, "batch": BATCH, "seq_len": SEQ, "num_q_heads": SHAPE.hq,
             "num_kv_heads": SHAPE.hkv, "head_dim": SHAPE.d, "kv_shards": N_SHARDS,
-            "handoff_requests_per_step": N_HANDOFF, "parallelism": (f"ring of {world} instances (home + cold per GPU), {args.transport} transport"
+            "handoff_requests_per_step": N_HANDOFF, "parallelism": (f"ring of {world} instances (home + cold per GPU), {step.transport} transport"
+                            + (f" (p2p unavailable: {step.fallback_reason})"
+                               if getattr(step, "fallback_reason", None) else "")
                             + (" [ALL RANKS ON ONE GPU: functional check only]"
                                if os.environ.get("BS_RING_SAME_GPU") == "1" else "")
                             if world > 1 else "1 GPU, 2 virtual instances"),
@@ -354,7 +356,7 @@ def run_ours(args, rank, world, device):
         "migrate_bytes_per_layer": mig_bytes,
         "migrate_transport": ("fused copy kernel, local HBM (N=1: both instances on GPU 0)" if world == 1
                               else ("copy kernel pushing into the peer's IPC-mapped pool (P2P, NVLink)"
-                                    if args.transport == "p2p" else
+                                    if step.transport == "p2p" else
                                     "gather -> NCCL send/recv over NVLink -> scatter")),
         "roofline": {
             "bound": "hbm",

@@ -162,6 +162,15 @@ def _sendrecv(pg, send: torch.Tensor, to: int, recv: torch.Tensor, frm: int):
         w.wait()
 
 
+def _all_ranks_true(flag: bool, pg, device) -> bool:
+    """Logical AND over the ranks of pg (gloo: CPU tensor; NCCL: device tensor)."""
+    t = torch.tensor([1 if flag else 0], dtype=torch.int32)
+    if dist.get_backend(pg) != "gloo":
+        t = t.to(device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=pg)
+    return bool(int(t.item()))
+
+
 class P2PLinks:
     """CUDA-IPC links to the two ring neighbours for the P2P transport: this rank's
     receive buffers and flags are exported; the neighbours' are mapped into this process.
@@ -278,11 +287,23 @@ class ShardedDecodeStep:
         self.epoch = 0
         if self.transport == "p2p":
             pn = self.part_cold[0][4].numel()
-            self.links = P2PLinks(rank, world, num_layers, home_pool,
-                                  torch.empty((num_layers, self.B, num_q_heads, head_dim),
-                                              dtype=torch.bfloat16, device=dev),
-                                  pn, handoff_dst_ids if handoff_dst_ids is not None else
-                                  torch.zeros(0, dtype=torch.int32), dev, pg_attn)
+            ok, why = True, ""
+            try:
+                self.links = P2PLinks(rank, world, num_layers, home_pool,
+                                      torch.empty((num_layers, self.B, num_q_heads, head_dim),
+                                                  dtype=torch.bfloat16, device=dev),
+                                      pn, handoff_dst_ids if handoff_dst_ids is not None else
+                                      torch.zeros(0, dtype=torch.int32), dev, pg_attn)
+            except Exception as e:  # e.g. no peer access between these GPUs
+                ok, why = False, repr(e)
+            # every rank must take the same transport: fall back to NCCL unless all mapped
+            if not _all_ranks_true(ok, pg_attn, dev):
+                if self.links is not None:
+                    self.links.close()
+                self.links = None
+                self.transport = "nccl"
+                self.fallback_reason = why or "a peer could not map the IPC buffers"
+        if self.transport == "p2p":
             self.part_recv = [split_partial(self.links.part_recv[layer], self.B, self.hq, self.d)
                               + (None, self.links.part_recv[layer]) for layer in range(num_layers)]
             self.q_prev = self.links.q_prev

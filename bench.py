@@ -185,12 +185,14 @@ def handoff_src_ids(case, n):
     return [i for i in range(case.pools[1].shape[1]) if i not in used][:n]
 
 
-def attn_bytes_per_layer(ks, fused: bool = True):
+def attn_bytes_per_layer(ks, fused: bool = True, q_sets: int = 1):
     """Algorithmic bytes of one layer's attention: per (request, shard)
     len*2*Hkv*d*2 (KV) + 4*ceil(len/16) (block table); per request Hq*d*2 (q) and, with
-    the fused local launch (N=1), the merged bf16 O + fp32 lse (Hq*(d*2+4)) -- without it,
-    each shard's fp32 partial Hq*(d+2)*4 instead."""
-    tot = 0
+    the fused launches (local shards at N=1, fused exchange at N>1), the merged bf16 O +
+    fp32 lse (Hq*(d*2+4)) -- without them, each shard's fp32 partial Hq*(d+2)*4 instead.
+    q_sets = 2 at N>1: the launch serves its own requests' shard 0 and the predecessor's
+    shard 1, i.e. two sets of q."""
+    tot = (q_sets - 1) * ks.shape[0] * SHAPE.hq * SHAPE.d * 2
     n_sh = ks.shape[1] - 1
     for b in range(ks.shape[0]):
         tot += SHAPE.hq * SHAPE.d * 2
@@ -199,6 +201,21 @@ def attn_bytes_per_layer(ks, fused: bool = True):
             n = int(ks[b, j + 1] - ks[b, j])
             tot += n * 2 * SHAPE.hkv * SHAPE.d * 2 + 4 * synth.ceil_div(n, SHAPE.bs)
     return tot
+
+
+def step_stats(per_step):
+    """Median, spread and a 95 % CI of the mean over this rank's timed steps (rank 0's
+    steps; the headline ms_per_step is the max over ranks of the mean)."""
+    n = len(per_step)
+    if n == 0:
+        return None
+    mean = statistics.fmean(per_step)
+    sd = statistics.stdev(per_step) if n > 1 else 0.0
+    return {"median": round(statistics.median(per_step), 4), "min": round(per_step[0], 4),
+            "max": round(per_step[-1], 4), "mean": round(mean, 4),
+            "ci95": round(1.96 * sd / n ** 0.5, 4), "n": n,
+            "note": "per-step boundaries are events on the main stream; steps overlap a little "
+                    "(the copy stream runs ahead), the mean over K is the exact figure"}
 
 
 def _allreduce_max(t):
@@ -218,8 +235,12 @@ def run_ours(args, rank, world, device):
     case, pools, step, ks = build_workload(bs, device, rank, world, transport=args.transport)
     L = SHAPE.n_layers
     q = case.q
-    out = torch.empty((L, BATCH, SHAPE.hq, SHAPE.d), dtype=torch.bfloat16, device=device)
-    lse = torch.empty((L, BATCH, SHAPE.hq), dtype=torch.float32, device=device)
+    own = step.outputs()   # fused exchange: the buffers peers merge into (no copy)
+    if own is not None:
+        out, lse = own
+    else:
+        out = torch.empty((L, BATCH, SHAPE.hq, SHAPE.d), dtype=torch.bfloat16, device=device)
+        lse = torch.empty((L, BATCH, SHAPE.hq), dtype=torch.float32, device=device)
     torch.cuda.synchronize()
 
     def barrier():
@@ -237,16 +258,21 @@ def run_ours(args, rank, world, device):
     timers = [[tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in range(L)]
               for _ in range(K)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(K - 1)]
     with ClockSampler(torch.cuda.current_device()) as clk:
         t0.record()
         for k in range(K):
             step.enqueue(q, out, lse, timers=timers[k])
+            if k < K - 1:
+                step_ev[k].record()
         t1.record()
         torch.cuda.synchronize()
     barrier()
     if step.links is not None:
         step.links.check()
     ms = t0.elapsed_time(t1) / K
+    bounds = [t0] + step_ev + [t1]
+    per_step = sorted(a.elapsed_time(b) for a, b in zip(bounds[:-1], bounds[1:]))
     attn_ms = [a.elapsed_time(b) for tk in timers for (a, b, _, _) in tk]
     mig_ms = [c.elapsed_time(d) for tk in timers for (_, _, c, d) in tk]
     # ---- exposure of the migration: the same steps without hand-offs --
@@ -262,6 +288,22 @@ def run_ours(args, rank, world, device):
     c1.record()
     torch.cuda.synchronize()
     step.n_handoff = n_handoff
+    # ---- the hand-off alone (N=1: the same per-layer copy launches, nothing beside them)
+    ms_mig_only = None
+    if world == 1 and n_handoff:
+        def mig_only():
+            for layer in range(L):
+                step.ops.migrate_local(step.cold, step.home, layer, step.src_ids, step.dst_ids,
+                                       step.ce_ids)
+        mig_only()
+        torch.cuda.synchronize()
+        m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        m0.record()
+        for _ in range(K):
+            mig_only()
+        m1.record()
+        torch.cuda.synchronize()
+        ms_mig_only = m0.elapsed_time(m1) / K
     ms_compute = torch.tensor([c0.elapsed_time(c1) / K], device=device)
     ms_t = torch.tensor([ms], device=device)
     if world > 1:
@@ -315,7 +357,8 @@ def run_ours(args, rank, world, device):
     assert torch.equal(out_host.view(torch.int16), out.cpu().view(torch.int16))
 
     # ---- derived numbers ----------------------------------------------------------------
-    a_bytes = attn_bytes_per_layer(ks, fused=step.fuse_local)
+    a_bytes = attn_bytes_per_layer(ks, fused=step.fuse_local or step.fused_exchange,
+                                   q_sets=2 if world > 1 else 1)
     mig_bytes = step.n_handoff * pools[0].chunk_bytes  # per layer, counted once
     attn_avg_ms = statistics.fmean(attn_ms)
     mig_avg_ms = statistics.fmean(mig_ms)
@@ -332,6 +375,7 @@ def run_ours(args, rank, world, device):
         "steps": K,
         "warmup": args.warmup,
         "ms_per_step": round(ms_max, 4),
+        "step_ms_stats": step_stats(per_step),
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
@@ -342,6 +386,8 @@ def run_ours(args, rank, world, device):
             "layers": L, "batch": BATCH, "seq_len": SEQ, "num_q_heads": SHAPE.hq,
             "num_kv_heads": SHAPE.hkv, "head_dim": SHAPE.d, "kv_shards": N_SHARDS,
             "handoff_requests_per_step": N_HANDOFF, "parallelism": (f"ring of {world} instances (home + cold per GPU), {step.transport} transport"
+                            + (", fused exchange (partials stored into the home GPU's workspace, "
+                               "last-arriving CTA merges)" if step.fused_exchange else "")
                             + (f" (p2p unavailable: {step.fallback_reason})"
                                if getattr(step, "fallback_reason", None) else "")
                             + (" [ALL RANKS ON ONE GPU: functional check only]"
@@ -361,7 +407,10 @@ def run_ours(args, rank, world, device):
         "roofline": {
             "bound": "hbm",
             "kernel": ("split_decode_attn_mma, fused local shards + LSE merge (1 launch per layer)"
-                       if step.fuse_local else "split_decode_attn_mma (2 shard launches per layer)"),
+                       if step.fuse_local else
+                       "split_decode_attn_mma, own shard + predecessor's shard, partials into the "
+                       "home GPU's workspace, last-arriving CTA merges (1 launch per layer)"
+                       if step.fused_exchange else "split_decode_attn_mma (2 shard launches per layer)"),
             "achieved": round(attn_gbs, 1), "peak": peak, "peak_source": peak_src,
             "unit": "GB/s", "frac": round(attn_gbs / peak, 4),
             "traffic": traffic, "traffic_source": traffic_src,
@@ -369,6 +418,9 @@ def run_ours(args, rank, world, device):
         },
         "overlap": {"step_ms": round(ms_max, 4), "compute_only_ms": round(ms_compute, 4),
                     "exposure": round((ms_max - ms_compute) / ms_compute, 4),
+                    "migrate_only_ms": None if ms_mig_only is None else round(ms_mig_only, 4),
+                    "overlap_efficiency": (None if ms_mig_only is None else round(
+                        (ms_compute + ms_mig_only - ms_max) / min(ms_compute, ms_mig_only), 4)),
                     "migrate_bytes_per_step": mig_bytes * L,
                     "note": ("N=1: the hand-off and the attention share one GPU's HBM, so the "
                              "hand-off's bytes cannot be hidden; over NVLink (N>1) its write side "

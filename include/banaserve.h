@@ -186,6 +186,70 @@ bs_status bs_split_decode_attention_local(int32_t n_local, const bs_kv_pool* con
                                           void* out, float* lse, void* workspace,
                                           size_t workspace_bytes, void* stream);
 
+/* H4 + H5 + H6 fused across GPUs ("fused B200 variant"; PAPER.md:220,
+ * :233-237): an attention PROBLEM is a batch of requests whose KV shards may live on
+ * several GPUs.  Every launch that holds a shard of it writes that shard's per-range
+ * partials straight into the problem's workspace on the home GPU (peer-mapped, NVLink
+ * stores) and bumps the per-(request, kv-head) arrival counter there; whichever CTA
+ * arrives last -- on any GPU -- performs the eq. 10 merge over all ranges in fixed
+ * order (shard-major) and writes bf16 O + fp32 lse into the home GPU's buffers, then
+ * increments the problem's `done` counter.  No partial round trip, no merge launch, no
+ * collective call.  One launch may serve several problems (e.g. on GPU r of the ring:
+ * shard 0 of its own requests + shard 1 of its predecessor's).
+ *
+ * bs_attn_problem (identical on every GPU that serves the problem; pointers as seen
+ *   from the launching GPU, i.e. peer-mapped when the home is another GPU):
+ *   q          bf16 [batch][num_q_heads][head_dim] (readable by the launching GPU)
+ *   kv_split   DEVICE int32 [batch][n_shards+1] (the launching GPU's copy)
+ *   max_blocks HOST int32 [n_shards]: block-table width of EVERY shard of the problem
+ *              (n_shards <= 16); together with batch / heads / head_dim / the SM count it
+ *              fixes the range plan, so every GPU must pass the same values and be the
+ *              same GPU model
+ *   out, lse   home GPU bf16 [batch][num_q_heads][head_dim], fp32 [batch][num_q_heads]
+ *              (lse may be NULL)
+ *   workspace  home GPU scratch of bs_attention_problem_workspace_size bytes, zero-filled
+ *              once before first use (arrival counters re-arm themselves); a problem's
+ *              workspace may not be reused before its `done` reached the call's target
+ *   done       home GPU int32 counter or NULL: +batch*num_kv_heads per completed call,
+ *              with release semantics (system scope when cross_device) -- wait on it
+ *              (bs_wait_signal) before reading out / lse or reusing the workspace
+ *   cross_device 1 when the problem's shards run on more than one GPU
+ * bs_attn_task: one shard of one problem processed by THIS launch: pool (device-resident,
+ *   this GPU), block_tables DEVICE [batch][max_blocks[shard_id]], shard_id, problem index.
+ * 1 <= n_tasks <= 4, 1 <= n_problems <= 4; all tasks' pools share num_kv_heads / head_dim /
+ * num_layers; all problems have `batch` requests of num_q_heads heads.  The caller
+ * guarantees that every task of a problem is launched exactly once per call epoch.
+ * PAPER.md gives no fused variant; this is the B200 form of "E^(1) / O^(1) is sent back
+ * before the final summation" (:237) with the exchange folded into the producer. */
+typedef struct {
+  const void* q;
+  const int32_t* kv_split;
+  int32_t n_shards;
+  const int32_t* max_blocks;
+  void* out;
+  float* lse;
+  void* workspace;
+  size_t workspace_bytes;
+  int32_t* done;
+  int32_t cross_device;
+} bs_attn_problem;
+
+typedef struct {
+  const bs_kv_pool* pool;
+  const int32_t* block_tables;
+  int32_t shard_id;
+  int32_t problem;
+} bs_attn_task;
+
+bs_status bs_attention_problem_workspace_size(int32_t batch, int32_t num_q_heads,
+                                              int32_t num_kv_heads, int32_t head_dim,
+                                              int32_t n_shards, const int32_t* max_blocks,
+                                              size_t* bytes);
+bs_status bs_split_decode_attention_tasks(int32_t n_problems, const bs_attn_problem* problems,
+                                          int32_t n_tasks, const bs_attn_task* tasks,
+                                          int32_t layer, int32_t batch, int32_t num_q_heads,
+                                          float scale, void* stream);
+
 /* ------------------------------------------------------------------------------ */
 /* NEXT F3: layer-level migration (Fig. 3, eqs. 3-5): a contiguous  */
 /* set of layers moves with its weights W_l and its KV_l.  bs_kv_migrate_layers is    */
@@ -296,6 +360,10 @@ size_t bs_ipc_handle_bytes(void);
 bs_status bs_signal(int32_t* flag, int32_t value, void* stream);
 bs_status bs_wait_signal(const int32_t* flag, int32_t value, uint64_t timeout_ns, int32_t* err,
                          void* stream);
+/* Several waits in one launch: until *flags[i] >= values[i] for every i < n (1..8);
+ * flags / values are HOST arrays (of device pointers / values). */
+bs_status bs_wait_signals(int32_t n, const int32_t* const* flags, const int32_t* values,
+                          uint64_t timeout_ns, int32_t* err, void* stream);
 bs_status bs_ipc_export(const void* dev_ptr, void* handle_out, size_t* offset_out);
 bs_status bs_ipc_import(const void* handle, size_t offset, void** dev_ptr_out);
 bs_status bs_ipc_close(void* dev_ptr, size_t offset);

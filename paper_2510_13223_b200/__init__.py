@@ -37,6 +37,7 @@ EXPORTED_SYMBOLS = (
     "bs_utilization", "bs_dispatch_requests", "bs_plan_migrations", "bs_kv_migrate_layers",
     "bs_copy_bytes", "bs_split_decode_attention_local_workspace_size",
     "bs_split_decode_attention_local", "bs_signal", "bs_wait_signal",
+    "bs_attention_problem_workspace_size", "bs_split_decode_attention_tasks", "bs_wait_signals",
 )
 
 
@@ -114,10 +115,14 @@ def lib():
         "bs_copy_bytes": ([_p, _p, _sz, _p], _i32),
         "bs_signal": ([_p, _i32, _p], _i32),
         "bs_wait_signal": ([_p, _i32, ctypes.c_uint64, _p, _p], _i32),
+        "bs_wait_signals": ([_i32, _p, _p, ctypes.c_uint64, _p, _p], _i32),
         "bs_split_decode_attention_local_workspace_size": ([_i32, _p, _p, _i32, _i32,
                                                             ctypes.POINTER(_sz)], _i32),
         "bs_split_decode_attention_local": ([_i32, _p, _i32, _p, _i32, _i32, _p, _p, _p, _p, _i32,
                                              _f32, _p, _p, _p, _sz, _p], _i32),
+        "bs_attention_problem_workspace_size": ([_i32, _i32, _i32, _i32, _i32, _p,
+                                                 ctypes.POINTER(_sz)], _i32),
+        "bs_split_decode_attention_tasks": ([_i32, _p, _i32, _p, _i32, _i32, _i32, _f32, _p], _i32),
         "bs_dispatch_requests": ([_i32, _p, _p, _i32, _p, ctypes.c_double, _p], _i32),
         "bs_plan_migrations": ([_i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, ctypes.c_double,
                                 ctypes.c_double, _i32, _p, ctypes.POINTER(_i32)], _i32),
@@ -316,6 +321,59 @@ def split_decode_attention_local(pools, layer: int, q: torch.Tensor, block_table
         _stream(stream)))
 
 
+class _Problem(ctypes.Structure):
+    _fields_ = [("q", _p), ("kv_split", _p), ("n_shards", _i32), ("max_blocks", _p),
+                ("out", _p), ("lse", _p), ("workspace", _p), ("workspace_bytes", _sz),
+                ("done", _p), ("cross_device", _i32)]
+
+
+class _Task(ctypes.Structure):
+    _fields_ = [("pool", _p), ("block_tables", _p), ("shard_id", _i32), ("problem", _i32)]
+
+
+def _aptr(x, dtype=None):
+    """Device pointer of a tensor, or an int address as is (e.g. a peer mapping)."""
+    if x is None or isinstance(x, int):
+        return x
+    return _dptr(x, dtype)
+
+
+def attention_problem_workspace_size(batch: int, num_q_heads: int, num_kv_heads: int,
+                                     head_dim: int, max_blocks) -> int:
+    n = len(max_blocks)
+    mb = (ctypes.c_int32 * n)(*[int(x) for x in max_blocks])
+    out = _sz()
+    _check(lib().bs_attention_problem_workspace_size(batch, num_q_heads, num_kv_heads, head_dim, n,
+                                                     mb, ctypes.byref(out)))
+    return out.value
+
+
+def split_decode_attention_tasks(problems, tasks, layer: int, batch: int, num_q_heads: int,
+                                 scale: float, stream=None) -> None:
+    """H4+H5+H6 fused across launches / GPUs (bs_split_decode_attention_tasks).
+    ``problems``: dicts with q, kv_split, max_blocks (list), out, lse, workspace,
+    workspace_bytes, done, cross_device -- tensors, or int addresses for peer mappings.
+    ``tasks``: (pool, block_tables, shard_id, problem index) tuples."""
+    keep = []
+    pa = (_Problem * len(problems))()
+    for i, pr in enumerate(problems):
+        mb = (ctypes.c_int32 * len(pr["max_blocks"]))(*[int(x) for x in pr["max_blocks"]])
+        keep.append(mb)
+        ws = pr.get("workspace")
+        wsb = pr.get("workspace_bytes")
+        if wsb is None:
+            wsb = 0 if ws is None or isinstance(ws, int) else ws.numel() * ws.element_size()
+        pa[i] = _Problem(_aptr(pr["q"], torch.bfloat16), _aptr(pr["kv_split"], torch.int32),
+                         len(pr["max_blocks"]), ctypes.cast(mb, _p), _aptr(pr["out"], torch.bfloat16),
+                         _aptr(pr.get("lse"), torch.float32), _aptr(ws), wsb,
+                         _aptr(pr.get("done"), torch.int32), int(bool(pr.get("cross_device", False))))
+    ta = (_Task * len(tasks))()
+    for t, (pool, bt, shard, prob) in enumerate(tasks):
+        ta[t] = _Task(pool.handle.value, _dptr(bt, torch.int32), int(shard), int(prob))
+    _check(lib().bs_split_decode_attention_tasks(len(problems), pa, len(tasks), ta, layer, batch,
+                                                 num_q_heads, float(scale), _stream(stream)))
+
+
 def merge_partials(o_parts, m_parts, l_parts, out: torch.Tensor, lse: torch.Tensor | None = None,
                    stream=None) -> None:
     """H6: exact LSE merge of n partials into bf16 ``out`` [B,Hq,d] (+ fp32 lse [B,Hq])."""
@@ -489,6 +547,15 @@ def wait_signal(flag_ptr: int, value: int, timeout_ns: int = 0, err_ptr: int | N
                 stream=None) -> None:
     """The stream waits until *flag >= value (gives up after timeout_ns, setting *err)."""
     _check(lib().bs_wait_signal(flag_ptr, int(value), int(timeout_ns), err_ptr, _stream(stream)))
+
+
+def wait_signals(flag_ptrs, values, timeout_ns: int = 0, err_ptr: int | None = None,
+                 stream=None) -> None:
+    """One launch: the stream waits until *flag_ptrs[i] >= values[i] for every i (<= 8)."""
+    n = len(flag_ptrs)
+    fa = (ctypes.c_void_p * n)(*[int(f) for f in flag_ptrs])
+    va = (ctypes.c_int32 * n)(*[int(v) for v in values])
+    _check(lib().bs_wait_signals(n, fa, va, int(timeout_ns), err_ptr, _stream(stream)))
 
 
 def copy_ptr(dst_ptr: int, src_ptr: int, nbytes: int, stream=None) -> None:

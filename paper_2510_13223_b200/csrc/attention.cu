@@ -45,6 +45,27 @@ constexpr int kMaxSplit = 64;   // intra-GPU split-K limit
 
 constexpr int kMaxLocal = 4;  // shards fused into one launch (bs_split_decode_attention_local)
 
+// One attention problem: a set of requests whose KV is split into shards, some of which
+// may be processed by other launches (on other GPUs).  All ranges of a (request, kv-head)
+// arrive on one counter; the last arriver merges.  Every pointer may be a peer mapping.
+struct ProbDesc {
+  const __nv_bfloat16* q;
+  const int32_t* kv_split;
+  int32_t n_shards;
+  int32_t nsplit;  // CTA ranges of the problem over all its shards (all launches / GPUs)
+  int32_t merged;  // 1: write bf16 O + lse; 0: (o~, m, l)
+  int32_t sys;     // shards on several GPUs: system-scope arrival / done counters
+  float* o;
+  float* m;
+  float* l;
+  __nv_bfloat16* out;
+  float* lse;
+  float* ws_o;
+  float* ws_ml;
+  int32_t* ws_cnt;
+  int32_t* done;   // +1 per merged (request, kv-head), monotonic; or NULL
+};
+
 // One KV shard of the launch: where its pages live and how its blocks are cut into CTAs.
 struct ShardDesc {
   const uint8_t* kv;  // pool base + layer * layer_bytes
@@ -58,27 +79,18 @@ struct ShardDesc {
   int32_t layer_row0;  // tensor-map row of (layer, block 0, K, head 0, slot 0)
   int32_t pool_hkv;    // kv heads of the pool (tensor-map addressing)
   int32_t pool_head_lo;  // first kv head of this launch inside the pool
+  int32_t prob;        // problem of this shard (index into AttnParams::pb)
+  int32_t range_base;  // problem range index of this shard's first CTA range
 };
 
 struct AttnParams {
   ShardDesc sh[kMaxLocal];
+  ProbDesc pb[kMaxLocal];
   int32_t n_local;
-  const __nv_bfloat16* q;
-  const int32_t* kv_split;
-  int32_t n_shards;
   float scale_log2;
   int32_t hq, hkv;          // hq: q heads of the MODEL (row stride); hkv: kv heads in this launch
   int32_t model_head_lo;    // first kv head of the launch in the model (q / output rows)
-  int32_t nsplit;           // grid.x = CTA ranges per (request, kv-head) over all shards
-  int32_t merged;           // 1: write bf16 O + lse (local shards merged); 0: (o~, m, l)
-  float* o;
-  float* m;
-  float* l;
-  __nv_bfloat16* out;
-  float* lse;
-  float* ws_o;
-  float* ws_ml;
-  int32_t* ws_cnt;
+  int32_t grid_x;           // CTA ranges of this launch over its shards
 };
 
 struct TMaps {
@@ -154,10 +166,19 @@ __device__ __forceinline__ float reduce_scatter16(float (&v)[16]) {
 // CTA's partial; the last-arriving CTA of the (request, kv-head) then merges all partials
 // in fixed order, re-arms the arrival counter and writes the output.  Called by every
 // thread of the CTA after a __syncthreads.
+__device__ __forceinline__ void count_done(const ProbDesc& P) {
+  // the caller's barrier orders every thread's output stores before this; the release is
+  // cumulative, so a waiter that acquires the counter sees the outputs
+  if (P.sys)
+    asm volatile("red.release.sys.global.add.s32 [%0], 1;" ::"l"(P.done) : "memory");
+  else
+    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(P.done) : "memory");
+}
+
 template <int D, int G>
-__device__ __forceinline__ void cta_combine_and_store(const AttnParams& p, int b, int g, int gm,
-                                                      int sp, const float* s_acc, const float* s_ml,
-                                                      float* s_w, int* s_flag) {
+__device__ __forceinline__ void cta_combine_and_store(const ProbDesc& P, int hq, int hkv, int b, int g,
+                                                      int gm, int sp, const float* s_acc,
+                                                      const float* s_ml, float* s_w, int* s_flag) {
   for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
     const int h = idx / D, x = idx - h * D;
     float M = -INFINITY;
@@ -173,41 +194,51 @@ __device__ __forceinline__ void cta_combine_and_store(const AttnParams& p, int b
         O += s_acc[(w * G + h) * D + x] * f;
       }
     }
-    const int64_t row = (int64_t)b * p.hq + gm * G + h;
+    const int64_t row = (int64_t)b * hq + gm * G + h;
     const bool any = L > 0.f;
-    if (p.nsplit == 1) {
-      if (p.merged) {
-        p.out[row * D + x] = __float2bfloat16_rn(any ? O / L : 0.f);
-        if (x == 0 && p.lse) p.lse[row] = any ? M * kLn2 + logf(L) : -INFINITY;
+    if (P.nsplit == 1) {
+      if (P.merged) {
+        P.out[row * D + x] = __float2bfloat16_rn(any ? O / L : 0.f);
+        if (x == 0 && P.lse) P.lse[row] = any ? M * kLn2 + logf(L) : -INFINITY;
       } else {
-        p.o[row * D + x] = any ? O / L : 0.f;
+        P.o[row * D + x] = any ? O / L : 0.f;
         if (x == 0) {
-          p.m[row] = any ? M * kLn2 : -INFINITY;
-          p.l[row] = L;
+          P.m[row] = any ? M * kLn2 : -INFINITY;
+          P.l[row] = L;
         }
       }
     } else {
-      const int64_t part = row * p.nsplit + sp;
-      p.ws_o[part * D + x] = any ? O / L : 0.f;
+      const int64_t part = row * P.nsplit + sp;
+      P.ws_o[part * D + x] = any ? O / L : 0.f;
       if (x == 0) {
-        p.ws_ml[part * 2] = any ? M : -INFINITY;  // log2 units
-        p.ws_ml[part * 2 + 1] = L;
+        P.ws_ml[part * 2] = any ? M : -INFINITY;  // log2 units
+        P.ws_ml[part * 2 + 1] = L;
       }
     }
   }
-  if (p.nsplit == 1) return;
+  if (P.nsplit == 1) {
+    if (P.done) {
+      __syncthreads();
+      if (threadIdx.x == 0) count_done(P);
+    }
+    return;
+  }
 
-  // ---- split-K / local shards: the last CTA of this (request, kv-head) merges ---------
+  // ---- split-K / several shards: the last CTA of this (request, kv-head) merges --------
   // The barrier orders every thread's partial stores before thread 0's acq_rel atomic
   // (release is cumulative), and the winner's acquire + barrier order the other CTAs'
-  // partials before this CTA's loads -- one gpu-scope atomic per CTA instead of a full
-  // fence (CCTL.IVALL) in every thread.
+  // partials before this CTA's loads -- one atomic per CTA instead of a full fence
+  // (CCTL.IVALL) in every thread.  System scope when the problem's shards run on several
+  // GPUs: the other ranges' partials then arrive over NVLink from the peers' CTAs.
   __syncthreads();
   if (threadIdx.x == 0) {
-    int32_t* cnt = p.ws_cnt + (int64_t)b * p.hkv + g;
+    int32_t* cnt = P.ws_cnt + (int64_t)b * hkv + g;
     int prev;
-    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(cnt) : "memory");
-    const int last = prev == p.nsplit - 1;
+    if (P.sys)
+      asm volatile("atom.acq_rel.sys.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(cnt) : "memory");
+    else
+      asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(cnt) : "memory");
+    const int last = prev == P.nsplit - 1;
     if (last) *cnt = 0;  // every CTA has arrived: re-arm for the next call
     s_flag[0] = last;
   }
@@ -218,14 +249,14 @@ __device__ __forceinline__ void cta_combine_and_store(const AttnParams& p, int b
   {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int h = warp; h < G; h += kWarps) {
-      const int64_t row = (int64_t)b * p.hq + gm * G + h;
-      const float* ml = p.ws_ml + row * p.nsplit * 2;
+      const int64_t row = (int64_t)b * hq + gm * G + h;
+      const float* ml = P.ws_ml + row * P.nsplit * 2;
       float mj[2], lj[2];
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         const int j = lane + 32 * t;
-        mj[t] = j < p.nsplit ? __ldcg(ml + 2 * j) : -INFINITY;
-        lj[t] = j < p.nsplit ? __ldcg(ml + 2 * j + 1) : 0.f;
+        mj[t] = j < P.nsplit ? __ldcg(ml + 2 * j) : -INFINITY;
+        lj[t] = j < P.nsplit ? __ldcg(ml + 2 * j + 1) : 0.f;
       }
       float M = fmaxf(mj[0], mj[1]);
 #pragma unroll
@@ -241,14 +272,14 @@ __device__ __forceinline__ void cta_combine_and_store(const AttnParams& p, int b
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         const int j = lane + 32 * t;
-        if (j < p.nsplit) s_w[h * kMaxSplit + j] = L > 0.f ? w[t] / L : 0.f;
+        if (j < P.nsplit) s_w[h * kMaxSplit + j] = L > 0.f ? w[t] / L : 0.f;
       }
       if (lane == 0) {
-        if (p.merged) {
-          if (p.lse) p.lse[row] = L > 0.f ? M * kLn2 + logf(L) : -INFINITY;
+        if (P.merged) {
+          if (P.lse) P.lse[row] = L > 0.f ? M * kLn2 + logf(L) : -INFINITY;
         } else {
-          p.m[row] = L > 0.f ? M * kLn2 : -INFINITY;
-          p.l[row] = L;
+          P.m[row] = L > 0.f ? M * kLn2 : -INFINITY;
+          P.l[row] = L;
         }
       }
     }
@@ -256,13 +287,17 @@ __device__ __forceinline__ void cta_combine_and_store(const AttnParams& p, int b
   __syncthreads();
   for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
     const int h = idx / D, x = idx - h * D;
-    const int64_t row = (int64_t)b * p.hq + gm * G + h;
-    const float* po = p.ws_o + row * p.nsplit * D + x;
+    const int64_t row = (int64_t)b * hq + gm * G + h;
+    const float* po = P.ws_o + row * P.nsplit * D + x;
     float O = 0.f;
 #pragma unroll 8
-    for (int j = 0; j < p.nsplit; ++j) O += s_w[h * kMaxSplit + j] * __ldcg(po + (int64_t)j * D);
-    if (p.merged) p.out[row * D + x] = __float2bfloat16_rn(O);
-    else p.o[row * D + x] = O;
+    for (int j = 0; j < P.nsplit; ++j) O += s_w[h * kMaxSplit + j] * __ldcg(po + (int64_t)j * D);
+    if (P.merged) P.out[row * D + x] = __float2bfloat16_rn(O);
+    else P.o[row * D + x] = O;
+  }
+  if (P.done) {
+    __syncthreads();
+    if (threadIdx.x == 0) count_done(P);
   }
 }
 
@@ -278,8 +313,9 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
   const int js = shard_of(p, spg);
   const ShardDesc& sd = p.sh[js];
   const int sp = spg - sd.split_off;
+  const ProbDesc& P = p.pb[sd.prob];
 
-  const int32_t* ks = p.kv_split + (int64_t)b * (p.n_shards + 1) + sd.shard_id;
+  const int32_t* ks = P.kv_split + (int64_t)b * (P.n_shards + 1) + sd.shard_id;
   const int32_t len = max(__ldg(ks + 1) - __ldg(ks), 0);
   const int32_t nblk = (len + 15) >> 4;
   const int32_t blo = sp * sd.bps;
@@ -322,7 +358,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
   // duplicated into both halves of a packed pair ({q_e, q_e}) for token-pair FFMA2
   float2 qq[G][DPL];
   {
-    const __nv_bfloat16* qp = p.q + ((int64_t)b * p.hq + gm * G) * D + lane * DPL;
+    const __nv_bfloat16* qp = P.q + ((int64_t)b * p.hq + gm * G) * D + lane * DPL;
 #pragma unroll
     for (int h = 0; h < G; ++h) {
       float qf[DPL];
@@ -484,7 +520,8 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
     }
   }
   __syncthreads();
-  cta_combine_and_store<D, G>(p, b, g, gm, spg, s_acc, s_ml, s_w, s_flag);
+  cta_combine_and_store<D, G>(P, p.hq, p.hkv, b, g, gm, sd.range_base + sp, s_acc, s_ml,
+                              s_w, s_flag);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -569,8 +606,9 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
   const int js = shard_of(p, spg);
   const ShardDesc& sd = p.sh[js];
   const int sp = spg - sd.split_off;
+  const ProbDesc& P = p.pb[sd.prob];
 
-  const int32_t* ks = p.kv_split + (int64_t)b * (p.n_shards + 1) + sd.shard_id;
+  const int32_t* ks = P.kv_split + (int64_t)b * (P.n_shards + 1) + sd.shard_id;
   const int32_t len = max(__ldg(ks + 1) - __ldg(ks), 0);
   const int32_t nblk = (len + 15) >> 4;
   const int32_t blo = sp * sd.bps;
@@ -618,7 +656,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
   // q^T B-fragments (bf16 pairs) for head n = gq (zero padding for n >= G)
   uint32_t bq[KS][2];
   {
-    const uint32_t* qrow = reinterpret_cast<const uint32_t*>(p.q + ((int64_t)b * p.hq + gm * G + gq) * D);
+    const uint32_t* qrow = reinterpret_cast<const uint32_t*>(P.q + ((int64_t)b * p.hq + gm * G + gq) * D);
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk) {
       bq[kk][0] = gq < G ? __ldg(qrow + 8 * kk + tq) : 0u;
@@ -745,7 +783,8 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
     }
   }
   __syncthreads();
-  cta_combine_and_store<D, G>(p, b, g, gm, spg, s_acc, s_ml, s_w, s_flag);
+  cta_combine_and_store<D, G>(P, p.hq, p.hkv, b, g, gm, sd.range_base + sp, s_acc, s_ml,
+                              s_w, s_flag);
 }
 
 // Pipeline depth / residency per (head_dim, group): STAGES blocks (K+V pages) per warp in
@@ -780,11 +819,13 @@ Variant variant_for(int d, int G) {
   return G <= 4 ? Variant{4, 3, false} : Variant{6, 2, false};
 }
 
+constexpr int kMaxProbShards = 16;  // shards of one problem (over all GPUs)
+
 struct Plan {
-  int bps;                   // blocks per CTA range (common to the launch's shards)
-  int nsplit;                // total CTA ranges per (request, kv-head)
-  int split_off[kMaxLocal];  // first range of each shard
-  int nsplit_s[kMaxLocal];   // ranges of each shard
+  int bps;                        // blocks per CTA range (common to the problem's shards)
+  int nsplit;                     // total CTA ranges per (request, kv-head)
+  int split_off[kMaxProbShards];  // first range of each shard
+  int nsplit_s[kMaxProbShards];   // ranges of each shard
   size_t ws_bytes, off_ml, off_cnt;
 };
 
@@ -794,6 +835,8 @@ struct Plan {
 // hkv: kv heads handled by the launch (grid.y); hq: q heads of the model (partial rows).
 bs_status make_plan(int batch, int G, int hq, int hkv, int d, int n_local, const int* max_blocks,
                     bool merged, Plan* out) {
+  if (n_local < 1 || n_local > kMaxProbShards)
+    return set_error(BS_ERR_INVALID_ARG, "attention plan: %d shards (1..%d)", n_local, kMaxProbShards);
   const int sms = sm_count(current_device());
   const int64_t slots = (int64_t)sms * variant_for(d, G).minb;
   const int64_t base = (int64_t)batch * hkv;
@@ -862,7 +905,7 @@ bs_status launch_attn_v(const AttnParams& p, int batch, cudaStream_t stream) {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
     configured_dev = dev;
   }
-  dim3 grid(p.nsplit, p.hkv, batch);
+  dim3 grid(p.grid_x, p.hkv, batch);
   split_decode_attn<D, G, STAGES, MINB><<<grid, kWarps * 32, S::kTotal, stream>>>(p);
   return check_launch("split_decode_attn");
 }
@@ -877,7 +920,7 @@ bs_status launch_attn_mma(const AttnParams& p, const TMaps& tm, int batch, cudaS
                          cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
     configured_dev = dev;
   }
-  dim3 grid(p.nsplit, p.hkv, batch);
+  dim3 grid(p.grid_x, p.hkv, batch);
   split_decode_attn_mma<D, G, STAGES, MINB><<<grid, kWarps * 32, S::kTotal, stream>>>(p, tm);
   return check_launch("split_decode_attn_mma");
 }
@@ -1038,6 +1081,8 @@ bs_status run_attention(const LaunchArgs& a) {
     sd.shard_id = a.shard_ids[j];
     sd.bps = pl.bps;
     sd.split_off = pl.split_off[j];
+    sd.prob = 0;
+    sd.range_base = pl.split_off[j];
     sd.pool_hkv = pool->desc.num_kv_heads;
     sd.pool_head_lo = a.pool_head_lo;
     sd.layer_row0 =
@@ -1048,25 +1093,27 @@ bs_status run_attention(const LaunchArgs& a) {
       else have_maps = false;
     }
   }
-  p.q = static_cast<const __nv_bfloat16*>(a.q);
-  p.kv_split = a.kv_split;
-  p.n_shards = a.n_shards;
   p.scale_log2 = a.scale * bs::kLog2e;
   p.hq = a.num_q_heads;
   p.hkv = a.n_kv_heads;
   p.model_head_lo = a.model_head_lo;
-  p.nsplit = pl.nsplit;
-  p.merged = a.merged ? 1 : 0;
-  p.o = a.o;
-  p.m = a.m;
-  p.l = a.l;
-  p.out = static_cast<__nv_bfloat16*>(a.out);
-  p.lse = a.lse;
+  p.grid_x = pl.nsplit;
+  bs::ProbDesc& P = p.pb[0];
+  P.q = static_cast<const __nv_bfloat16*>(a.q);
+  P.kv_split = a.kv_split;
+  P.n_shards = a.n_shards;
+  P.nsplit = pl.nsplit;
+  P.merged = a.merged ? 1 : 0;
+  P.o = a.o;
+  P.m = a.m;
+  P.l = a.l;
+  P.out = static_cast<__nv_bfloat16*>(a.out);
+  P.lse = a.lse;
   if (pl.ws_bytes) {
     uint8_t* ws = static_cast<uint8_t*>(a.workspace);
-    p.ws_o = reinterpret_cast<float*>(ws);
-    p.ws_ml = reinterpret_cast<float*>(ws + pl.off_ml);
-    p.ws_cnt = reinterpret_cast<int32_t*>(ws + pl.off_cnt);
+    P.ws_o = reinterpret_cast<float*>(ws);
+    P.ws_ml = reinterpret_cast<float*>(ws + pl.off_ml);
+    P.ws_cnt = reinterpret_cast<int32_t*>(ws + pl.off_cnt);
   }
   cudaStream_t s = static_cast<cudaStream_t>(a.stream);
   const bs::TMaps* tmp = have_maps ? &tm : nullptr;
@@ -1232,6 +1279,138 @@ bs_status bs_split_decode_attention_local(int32_t n_local, const bs_kv_pool* con
   a.workspace_bytes = workspace_bytes;
   a.stream = stream;
   return run_attention(a);
+}
+
+bs_status bs_attention_problem_workspace_size(int32_t batch, int32_t num_q_heads,
+                                              int32_t num_kv_heads, int32_t head_dim,
+                                              int32_t n_shards, const int32_t* max_blocks,
+                                              size_t* bytes) {
+  BS_REQUIRE(bytes && max_blocks, "bs_attention_problem_workspace_size: NULL argument");
+  BS_REQUIRE(batch >= 0 && num_kv_heads >= 1 && num_q_heads >= num_kv_heads &&
+                 num_q_heads % num_kv_heads == 0,
+             "bs_attention_problem_workspace_size: bad batch / heads");
+  BS_REQUIRE(n_shards >= 1 && n_shards <= bs::kMaxProbShards,
+             "bs_attention_problem_workspace_size: %d shards (1..%d)", n_shards, bs::kMaxProbShards);
+  for (int j = 0; j < n_shards; ++j)
+    BS_REQUIRE(max_blocks[j] >= 1, "bs_attention_problem_workspace_size: max_blocks < 1");
+  const int G = num_q_heads / num_kv_heads;
+  if (G != 1 && G != 2 && G != 4 && G != 8)
+    return bs::set_error(BS_ERR_UNSUPPORTED, "query group G=%d not in {1,2,4,8}", G);
+  if (head_dim != 64 && head_dim != 128)
+    return bs::set_error(BS_ERR_UNSUPPORTED, "head_dim %d not in {64,128}", head_dim);
+  bs::Plan pl;
+  bs_status st = bs::make_plan(batch, G, num_q_heads, num_kv_heads, head_dim, n_shards, max_blocks,
+                               true, &pl);
+  if (st != BS_OK) return st;
+  *bytes = pl.ws_bytes;
+  return BS_OK;
+}
+
+bs_status bs_split_decode_attention_tasks(int32_t n_problems, const bs_attn_problem* problems,
+                                          int32_t n_tasks, const bs_attn_task* tasks,
+                                          int32_t layer, int32_t batch, int32_t num_q_heads,
+                                          float scale, void* stream) {
+  BS_REQUIRE(problems && tasks, "bs_split_decode_attention_tasks: NULL array");
+  BS_REQUIRE(n_problems >= 1 && n_problems <= bs::kMaxLocal && n_tasks >= 1 && n_tasks <= bs::kMaxLocal,
+             "bs_split_decode_attention_tasks: %d problems / %d tasks (1..%d each)", n_problems,
+             n_tasks, bs::kMaxLocal);
+  BS_REQUIRE(tasks[0].pool, "bs_split_decode_attention_tasks: NULL pool");
+  const bs_kv_pool_desc& d0 = tasks[0].pool->desc;
+  const int hkv = d0.num_kv_heads, d = d0.head_dim;
+  for (int t = 0; t < n_tasks; ++t) {
+    const bs_attn_task& k = tasks[t];
+    BS_REQUIRE(k.pool && k.block_tables, "bs_split_decode_attention_tasks: task %d: NULL pool / table", t);
+    BS_REQUIRE(!k.pool->host, "bs_split_decode_attention_tasks: host-tier pools are fetched first");
+    BS_REQUIRE(k.pool->desc.num_kv_heads == hkv && k.pool->desc.head_dim == d &&
+                   k.pool->desc.num_layers == d0.num_layers,
+               "bs_split_decode_attention_tasks: pools must share geometry");
+    BS_REQUIRE(k.problem >= 0 && k.problem < n_problems, "bs_split_decode_attention_tasks: task %d: problem %d",
+               t, k.problem);
+    BS_REQUIRE(k.shard_id >= 0 && k.shard_id < problems[k.problem].n_shards,
+               "bs_split_decode_attention_tasks: task %d: shard %d", t, k.shard_id);
+  }
+  BS_REQUIRE(layer >= 0 && layer < d0.num_layers, "bs_split_decode_attention_tasks: layer %d", layer);
+  BS_REQUIRE(batch >= 0, "bs_split_decode_attention_tasks: batch < 0");
+  BS_REQUIRE(num_q_heads >= hkv && num_q_heads % hkv == 0,
+             "bs_split_decode_attention_tasks: num_q_heads %d not a multiple of Hkv %d", num_q_heads, hkv);
+  BS_REQUIRE(scale > 0.f && scale == scale, "bs_split_decode_attention_tasks: bad scale");
+  const int G = num_q_heads / hkv;
+  if (G != 1 && G != 2 && G != 4 && G != 8)
+    return bs::set_error(BS_ERR_UNSUPPORTED, "query group G=%d not in {1,2,4,8}", G);
+  bs::Plan plans[bs::kMaxLocal];
+  bs::AttnParams p{};
+  for (int i = 0; i < n_problems; ++i) {
+    const bs_attn_problem& pr = problems[i];
+    BS_REQUIRE(pr.q && pr.kv_split && pr.max_blocks && pr.out,
+               "bs_split_decode_attention_tasks: problem %d: NULL q / kv_split / max_blocks / out", i);
+    BS_REQUIRE(((uintptr_t)pr.q & 15) == 0 && ((uintptr_t)pr.out & 15) == 0,
+               "bs_split_decode_attention_tasks: q / out must be 16-B aligned");
+    BS_REQUIRE(pr.n_shards >= 1 && pr.n_shards <= bs::kMaxProbShards,
+               "bs_split_decode_attention_tasks: problem %d: %d shards", i, pr.n_shards);
+    for (int j = 0; j < pr.n_shards; ++j)
+      BS_REQUIRE(pr.max_blocks[j] >= 1, "bs_split_decode_attention_tasks: max_blocks < 1");
+    bs_status st = bs::make_plan(batch, G, num_q_heads, hkv, d, pr.n_shards, pr.max_blocks, true, &plans[i]);
+    if (st != BS_OK) return st;
+    BS_REQUIRE(plans[i].ws_bytes == 0 || (pr.workspace && pr.workspace_bytes >= plans[i].ws_bytes &&
+                                          ((uintptr_t)pr.workspace & 15) == 0),
+               "bs_split_decode_attention_tasks: problem %d: workspace needs %zu bytes (got %zu)", i,
+               plans[i].ws_bytes, pr.workspace_bytes);
+    bs::ProbDesc& P = p.pb[i];
+    P.q = static_cast<const __nv_bfloat16*>(pr.q);
+    P.kv_split = pr.kv_split;
+    P.n_shards = pr.n_shards;
+    P.nsplit = plans[i].nsplit;
+    P.merged = 1;
+    P.sys = pr.cross_device ? 1 : 0;
+    P.out = static_cast<__nv_bfloat16*>(pr.out);
+    P.lse = pr.lse;
+    P.done = pr.done;
+    if (plans[i].ws_bytes) {
+      uint8_t* ws = static_cast<uint8_t*>(pr.workspace);
+      P.ws_o = reinterpret_cast<float*>(ws);
+      P.ws_ml = reinterpret_cast<float*>(ws + plans[i].off_ml);
+      P.ws_cnt = reinterpret_cast<int32_t*>(ws + plans[i].off_cnt);
+    }
+  }
+  if (batch == 0) return BS_OK;
+  bs::TMaps tm;
+  bool have_maps = bs::variant_for(d, G).mma;
+  int off = 0;
+  for (int t = 0; t < n_tasks; ++t) {
+    const bs_attn_task& k = tasks[t];
+    const bs_kv_pool* pool = k.pool;
+    const bs::Plan& pl = plans[k.problem];
+    bs::ShardDesc& sd = p.sh[t];
+    sd.kv = pool->base + (size_t)layer * pool->layer_bytes;
+    sd.chunk_bytes = (int64_t)pool->chunk_bytes;
+    sd.v_off = (int64_t)pool->desc.num_kv_heads * pool->page_bytes;
+    sd.bt = k.block_tables;
+    sd.max_blocks = problems[k.problem].max_blocks[k.shard_id];
+    sd.shard_id = k.shard_id;
+    sd.bps = pl.bps;
+    sd.split_off = off;
+    off += pl.nsplit_s[k.shard_id];
+    sd.pool_hkv = hkv;
+    sd.pool_head_lo = 0;
+    sd.layer_row0 = (int32_t)((int64_t)layer * pool->desc.num_blocks * 2 * hkv * 16);
+    sd.prob = k.problem;
+    sd.range_base = pl.split_off[k.shard_id];
+    if (have_maps) {
+      const CUtensorMap* m = pool_tensor_map(pool);
+      if (m) tm.m[t] = *m;
+      else have_maps = false;
+    }
+  }
+  p.n_local = n_tasks;
+  p.scale_log2 = scale * bs::kLog2e;
+  p.hq = num_q_heads;
+  p.hkv = hkv;
+  p.model_head_lo = 0;
+  p.grid_x = off;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bs::TMaps* tmp = have_maps ? &tm : nullptr;
+  if (d == 128) return bs::launch_attn_d<128>(p, tmp, G, batch, s);
+  return bs::launch_attn_d<64>(p, tmp, G, batch, s);
 }
 
 }  // extern "C"

@@ -37,6 +37,35 @@ __global__ void wait_kernel(const int32_t* flag, int32_t value, uint64_t timeout
   }
 }
 
+constexpr int kMaxWaits = 8;
+struct Waits {
+  const int32_t* flag[kMaxWaits];
+  int32_t value[kMaxWaits];
+  int32_t n;
+};
+
+__global__ void wait_many_kernel(const Waits w, uint64_t timeout_ns, int32_t* err) {
+  if ((int)threadIdx.x >= w.n) return;
+  const int32_t* flag = w.flag[threadIdx.x];
+  const int32_t value = w.value[threadIdx.x];
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  unsigned ns = 32;
+  while (true) {
+    int32_t v;
+    asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (v >= value) break;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (timeout_ns && t - t0 > timeout_ns) {
+      if (err) atomicExch(err, 1);
+      break;
+    }
+    __nanosleep(ns);
+    if (ns < 4096) ns <<= 1;
+  }
+}
+
 }  // namespace
 }  // namespace bs
 
@@ -53,6 +82,21 @@ bs_status bs_wait_signal(const int32_t* flag, int32_t value, uint64_t timeout_ns
   BS_REQUIRE(flag, "bs_wait_signal: NULL flag");
   bs::wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(flag, value, timeout_ns, err);
   return bs::check_launch("wait_kernel");
+}
+
+bs_status bs_wait_signals(int32_t n, const int32_t* const* flags, const int32_t* values,
+                          uint64_t timeout_ns, int32_t* err, void* stream) {
+  BS_REQUIRE(n >= 1 && n <= bs::kMaxWaits, "bs_wait_signals: n=%d (1..%d)", n, bs::kMaxWaits);
+  BS_REQUIRE(flags && values, "bs_wait_signals: NULL array");
+  bs::Waits w{};
+  for (int i = 0; i < n; ++i) {
+    BS_REQUIRE(flags[i], "bs_wait_signals: NULL flag %d", i);
+    w.flag[i] = flags[i];
+    w.value[i] = values[i];
+  }
+  w.n = n;
+  bs::wait_many_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(w, timeout_ns, err);
+  return bs::check_launch("wait_many_kernel");
 }
 
 }  // extern "C"

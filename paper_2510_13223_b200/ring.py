@@ -120,6 +120,16 @@ class CudaOps:
                                                         batch, hq)
         return torch.zeros(max(n, 16), dtype=torch.uint8, device=device)
 
+    def attention_tasks(self, problems, tasks, layer, batch, hq):
+        """H4 + H5 + H6 fused across GPUs: partials go straight into each problem's home
+        workspace (peer-mapped), the last-arriving CTA merges (one launch)."""
+        from . import split_decode_attention_tasks
+        split_decode_attention_tasks(problems, tasks, layer, batch, hq, self.scale)
+
+    def problem_workspace_size(self, batch, hq, hkv, head_dim, max_blocks):
+        from . import attention_problem_workspace_size
+        return attention_problem_workspace_size(batch, hq, hkv, head_dim, max_blocks)
+
     def migrate_local(self, src, dst, layer, src_ids, dst_ids, host_ids=None):
         """Local hand-off copy: the copy kernel (SMs) or, with host id lists, the copy
         engines (DMA, no SM time -- the attention launch keeps every SM)."""
@@ -180,11 +190,16 @@ class P2PLinks:
       prev's shard-1 partial [l]   -> prev.part_recv[l]    then prev.flag(part, l) = epoch
       hand-off chunks (cold pool)  -> prev.home pool (the copy kernel writes the remote
                                       view directly)       then prev.flag(mig, l) = epoch
-    Acks (back-pressure before a buffer is reused next step): q_ack, part_ack."""
+    Acks (back-pressure before a buffer is reused next step): q_ack, part_ack.
+
+    With ``fused`` (the fused exchange): this rank's attention problem -- out, lse, the
+    per-layer workspaces and `done` counters -- is exported too, and the predecessor's is
+    mapped: the cold-shard CTAs write prev's partials into prev's workspace and the last
+    arriver merges into prev's out / lse (no partial push, no merge launch)."""
     KINDS = ("mig", "q", "part", "q_ack", "part_ack")
 
     def __init__(self, rank, world, num_layers, home_pool, q_like, part_numel, handoff_dst_ids,
-                 device, group, timeout_ms=20000):
+                 device, group, timeout_ms=20000, fused=None):
         from . import ipc_export, ipc_import, pool_view
         self.L = num_layers
         self.flags = torch.zeros(len(self.KINDS) * num_layers, dtype=torch.int32, device=device)
@@ -196,6 +211,10 @@ class P2PLinks:
                 "part_recv": ipc_export(self.part_recv), "home": ipc_export(home_pool.data),
                 "home_blocks": home_pool.num_blocks,
                 "handoff_dst": [int(x) for x in handoff_dst_ids.cpu().tolist()]}
+        if fused is not None:
+            for k in ("out", "lse", "ws", "done"):
+                mine[k] = ipc_export(fused[k])
+            mine["ws_stride"] = fused["ws"].shape[1]
         everyone = [None] * world
         dist.all_gather_object(everyone, mine, group=group)
         prev, nxt = (rank - 1) % world, (rank + 1) % world
@@ -217,6 +236,11 @@ class P2PLinks:
                                    device.index if device.index is not None else 0)
         self.prev_handoff_dst = torch.tensor(everyone[prev]["handoff_dst"], dtype=torch.int32,
                                              device=device)
+        self.fused = fused
+        if fused is not None:  # prev's problem buffers (raw peer addresses)
+            self.prev_out, self.prev_lse = open_(prev, "out"), open_(prev, "lse")
+            self.prev_ws, self.prev_done = open_(prev, "ws"), open_(prev, "done")
+            self.prev_ws_stride = everyone[prev]["ws_stride"]
 
     def flag(self, base: int, kind: str, layer: int) -> int:
         return base + 4 * (self.KINDS.index(kind) * self.L + layer)
@@ -243,7 +267,8 @@ class ShardedDecodeStep:
                  kv_split, num_q_heads: int, num_layers: int, head_dim: int,
                  handoff_src_ids=None, handoff_dst_ids=None, chunk_bytes: int = 0,
                  pg_attn=None, pg_mig=None, lookahead: int = 1, device=None,
-                 fuse_local: bool = True, copy_engine: bool = False, transport: str = "nccl"):
+                 fuse_local: bool = True, copy_engine: bool = False, transport: str = "nccl",
+                 fused_exchange: bool = True):
         self.ops, self.ex = ops, ex
         self.rank, self.world = rank, world
         self.prev, self.next = (rank - 1) % world, (rank + 1) % world
@@ -285,15 +310,35 @@ class ShardedDecodeStep:
         self.transport = transport if world > 1 else "local"
         self.links = None
         self.epoch = 0
+        self.fused_exchange = False
         if self.transport == "p2p":
             pn = self.part_cold[0][4].numel()
+            fused = None
+            if fused_exchange and hasattr(ops, "attention_tasks"):
+                # my problem: shard 0 on my home pool, shard 1 on next's cold pool; every
+                # rank must plan it identically -> exchange the block-table widths first
+                widths = [None] * world
+                dist.all_gather_object(widths, (int(home_bt.shape[1]), int(cold_bt.shape[1])),
+                                       group=pg_attn)
+                self.mb_mine = [widths[rank][0], widths[self.next][1]]
+                self.mb_prev = [widths[self.prev][0], widths[rank][1]]
+                nws = ops.problem_workspace_size(self.B, num_q_heads, home_pool.num_kv_heads,
+                                                 head_dim, self.mb_mine)
+                fused = {"out": torch.empty((num_layers, self.B, num_q_heads, head_dim),
+                                            dtype=torch.bfloat16, device=dev),
+                         "lse": torch.empty((num_layers, self.B, num_q_heads), dtype=torch.float32,
+                                            device=dev),
+                         "ws": torch.zeros((num_layers, (max(nws, 1) + 255) // 256 * 256),
+                                           dtype=torch.uint8, device=dev),  # 256-B aligned rows
+                         "done": torch.zeros(num_layers, dtype=torch.int32, device=dev)}
             ok, why = True, ""
             try:
                 self.links = P2PLinks(rank, world, num_layers, home_pool,
                                       torch.empty((num_layers, self.B, num_q_heads, head_dim),
                                                   dtype=torch.bfloat16, device=dev),
                                       pn, handoff_dst_ids if handoff_dst_ids is not None else
-                                      torch.zeros(0, dtype=torch.int32), dev, pg_attn)
+                                      torch.zeros(0, dtype=torch.int32), dev, pg_attn,
+                                      fused=fused)
             except Exception as e:  # e.g. no peer access between these GPUs
                 ok, why = False, repr(e)
             # every rank must take the same transport: fall back to NCCL unless all mapped
@@ -309,6 +354,9 @@ class ShardedDecodeStep:
             self.q_prev = self.links.q_prev
             self.push = torch.cuda.Stream(device=dev)
             self.merge_s = torch.cuda.Stream(device=dev)
+            self.fused_exchange = self.links.fused is not None
+            if self.fused_exchange:
+                self.hkv = home_pool.num_kv_heads
         self.ev = {k: [ex.event() for _ in range(num_layers)]
                    for k in ("mig_done", "layer_start", "q_ready", "part_ready")}
         self.out_ready = [ex.event() for _ in range(num_layers)]
@@ -324,6 +372,10 @@ class ShardedDecodeStep:
         + 8 signal / wait kernels of the P2P protocol."""
         mig = 0 if self.n_handoff == 0 or self.ce_ids is not None else (
             1 if self.world == 1 or self.transport == "p2p" else 2)
+        if self.transport == "p2p" and self.fused_exchange:
+            # 1 fused attention launch; q push + signal, hand-off signal, 1 combined wait,
+            # q-ack signal, done wait (per layer)
+            return self.L * (1 + mig + 6)
         if self.transport == "p2p":  # + the tiny signal / wait kernels of the protocol
             return self.L * (3 + mig + 8)
         attn = 1 if self.fuse_local else 3
@@ -336,6 +388,8 @@ class ShardedDecodeStep:
         events recorded on the launching streams (CUDA only).  ``inputs_ready[l]``: an
         event the step waits for before reading q[l] (e.g. its H2D copy); after the call,
         ``self.out_ready[l]`` is recorded once out[l] / lse[l] are final (per-layer D2H)."""
+        if self.transport == "p2p" and self.fused_exchange:
+            return self._enqueue_p2p_fused(q, out, lse, timers, inputs_ready)
         if self.transport == "p2p":
             return self._enqueue_p2p(q, out, lse, timers, inputs_ready)
         ex, ops, E = self.ex, self.ops, self.ev
@@ -410,6 +464,94 @@ class ShardedDecodeStep:
                     ops.merge([self.part_own[layer], self.part_recv[layer]], out[layer],
                               None if lse is None else lse[layer])
                     ex.record(self.out_ready[layer], ex.comm)
+        ex.end()
+
+    def outputs(self):
+        """(out, lse) buffers the step merges into when the exchange is fused (peers write
+        them); passing these to enqueue avoids a per-layer copy.  None otherwise."""
+        if self.fused_exchange:
+            return self.links.fused["out"], self.links.fused["lse"]
+        return None
+
+    def _enqueue_p2p_fused(self, q, out, lse, timers, inputs_ready):
+        """N>1, fused exchange (SURVEY.md §8(e) "fused B200 variant"): per layer ONE launch
+        runs shard 0 of my requests (home pool) and shard 1 of prev's (cold pool); each CTA
+        writes its partial into the owning problem's workspace -- prev's through the IPC
+        mapping -- and the last arriver of a (request, kv-head), on either GPU, merges into
+        that problem's out / lse and bumps its `done` counter.  Remaining flags: hand-off
+        arrival (mig), q arrival (q) and q-buffer reuse (q_ack); the done counters also
+        guard workspace reuse across steps (target (epoch - 1) * B * Hkv)."""
+        from . import copy_ptr, kv_migrate_layer, signal, wait_signal, wait_signals
+        ex, ops, E, lk = self.ex, self.ops, self.ev, self.links
+        F = lk.fused
+        self.epoch += 1
+        e = self.epoch
+        per_call = self.B * self.hkv
+        to, err = lk.timeout_ns, lk.err.data_ptr()
+        qb = q[0].numel() * q.element_size()
+        own_out = out is not None and out.data_ptr() == F["out"].data_ptr()
+        own_lse = lse is None or lse.data_ptr() == F["lse"].data_ptr()
+        ob, lb = F["out"][0].numel() * 2, F["lse"][0].numel() * 4
+        ex.begin()
+        for s_ in (self.push, self.merge_s):
+            s_.wait_stream(torch.cuda.current_stream())
+        with ex.use(ex.comm):  # q of my requests -> next (their cold instance)
+            for layer in range(self.L):
+                if inputs_ready is not None:
+                    ex.wait(ex.comm, inputs_ready[layer])
+                wait_signal(lk.my_flag("q_ack", layer), e - 1, to, err)
+                copy_ptr(lk.next_q_prev + layer * qb, q[layer].data_ptr(), qb)
+                signal(lk.flag(lk.next_flags, "q", layer), e)
+        for layer in range(self.L):
+            with ex.use(ex.copy):  # hand-off: my cold pool -> prev's home pool, pushed
+                if self.lookahead >= 0 and layer - self.lookahead >= 0:
+                    ex.wait(ex.copy, E["layer_start"][layer - self.lookahead])
+                if timers is not None:
+                    timers[layer][2].record(ex.copy)
+                if self.n_handoff:
+                    kv_migrate_layer(self.cold, lk.prev_home, layer, self.src_ids,
+                                     lk.prev_handoff_dst)
+                signal(lk.flag(lk.prev_flags, "mig", layer), e)
+                if timers is not None:
+                    timers[layer][3].record(ex.copy)
+            with ex.use(ex.compute):
+                ex.record(E["layer_start"][layer], ex.compute)
+                if inputs_ready is not None:
+                    ex.wait(ex.compute, inputs_ready[layer])
+                my_done = F["done"][layer:layer + 1].data_ptr()
+                prev_done = lk.prev_done + 4 * layer
+                wait_signals([lk.my_flag("mig", layer), lk.my_flag("q", layer), my_done, prev_done],
+                             [e, e, (e - 1) * per_call, (e - 1) * per_call], to, err)
+                if timers is not None:
+                    timers[layer][0].record(ex.compute)
+                mine = {"q": q[layer], "kv_split": self.kv_split, "max_blocks": self.mb_mine,
+                        "out": F["out"][layer], "lse": F["lse"][layer], "workspace": F["ws"][layer],
+                        "done": F["done"][layer:layer + 1], "cross_device": True}
+                theirs = {"q": self.q_prev[layer], "kv_split": self.kv_split,
+                          "max_blocks": self.mb_prev, "out": lk.prev_out + layer * ob,
+                          "lse": lk.prev_lse + layer * lb,
+                          "workspace": lk.prev_ws + layer * lk.prev_ws_stride,
+                          "workspace_bytes": lk.prev_ws_stride, "done": prev_done,
+                          "cross_device": True}
+                ops.attention_tasks([mine, theirs], [(self.home, self.home_bt, 0, 0),
+                                                     (self.cold, self.cold_bt, 1, 1)],
+                                    layer, self.B, self.hq)
+                if timers is not None:
+                    timers[layer][1].record(ex.compute)
+                ex.record(E["part_ready"][layer], ex.compute)
+            with torch.cuda.stream(self.push):  # prev's q[l] consumed -> ack
+                self.push.wait_event(E["part_ready"][layer])
+                signal(lk.flag(lk.prev_flags, "q_ack", layer), e)
+            with torch.cuda.stream(self.merge_s):  # my out[l] final once every merge landed
+                wait_signal(F["done"][layer:layer + 1].data_ptr(), e * per_call, to, err)
+                if not own_out:
+                    out[layer].copy_(F["out"][layer])
+                if not own_lse:
+                    lse[layer].copy_(F["lse"][layer])
+                self.out_ready[layer].record(self.merge_s)
+        cur = torch.cuda.current_stream()
+        for s_ in (self.push, self.merge_s):
+            cur.wait_stream(s_)
         ex.end()
 
     def _enqueue_p2p(self, q, out, lse, timers, inputs_ready):

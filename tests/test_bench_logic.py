@@ -58,3 +58,10 @@ def test_cli_help():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--help"],
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "--transport" in r.stdout and "--impl" in r.stdout
+
+
+def test_step_stats():
+    s = bench.step_stats([1.0, 2.0, 3.0, 4.0])
+    assert s["median"] == 2.5 and s["min"] == 1.0 and s["max"] == 4.0 and s["mean"] == 2.5
+    assert abs(s["ci95"] - 1.96 * (5 / 3) ** 0.5 / 2) < 1e-4 and s["n"] == 4
+    assert bench.step_stats([]) is None

@@ -33,7 +33,7 @@ def _dev(a):
     return torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).view(torch.bfloat16).cuda()
 
 
-def run_rank(rank, world, port, errq):
+def run_rank(rank, world, port, errq, fused):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -61,7 +61,8 @@ def run_rank(rank, world, port, errq):
                                  cp, i32(cold.block_tables), i32(ks), SHAPE.hq, SHAPE.n_layers, SHAPE.d,
                                  handoff_src_ids=i32(free_cold), handoff_dst_ids=i32(free_home),
                                  chunk_bytes=hp.chunk_bytes, pg_attn=dist.group.WORLD,
-                                 device=dev, transport="p2p")
+                                 device=dev, transport="p2p", fused_exchange=fused)
+        assert step.transport == "p2p" and step.fused_exchange == fused
         q = _dev(own.q)
         for _ in range(2):   # two epochs
             out = torch.full(q.shape, float("nan"), dtype=torch.bfloat16, device=dev)
@@ -97,12 +98,13 @@ def _free_port():
     return p
 
 
+@pytest.mark.parametrize("fused", [True, False], ids=["fused-exchange", "push-partials"])
 @pytest.mark.parametrize("world", [2, 3])
-def test_ring_p2p_on_one_gpu(world):
+def test_ring_p2p_on_one_gpu(world, fused):
     ctx = mp.get_context("spawn")
     errq = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=run_rank, args=(r, world, port, errq)) for r in range(world)]
+    procs = [ctx.Process(target=run_rank, args=(r, world, port, errq, fused)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:

@@ -166,7 +166,7 @@ __device__ __forceinline__ float reduce_scatter16(float (&v)[16]) {
 // CTA's partial; the last-arriving CTA of the (request, kv-head) then merges all partials
 // in fixed order, re-arms the arrival counter and writes the output.  Called by every
 // thread of the CTA after a __syncthreads.
-__device__ __forceinline__ void count_done(const ProbDesc& P) {
+__device__ __forceinline__ void count_done(const ProbDesc& P) {  // P: a local copy
   // the caller's barrier orders every thread's output stores before this; the release is
   // cumulative, so a waiter that acquires the counter sees the outputs
   if (P.sys)
@@ -176,7 +176,7 @@ __device__ __forceinline__ void count_done(const ProbDesc& P) {
 }
 
 template <int D, int G>
-__device__ __forceinline__ void cta_combine_and_store(const ProbDesc& P, int hq, int hkv, int b, int g,
+__device__ __forceinline__ void cta_combine_and_store(const ProbDesc P, int hq, int hkv, int b, int g,
                                                       int gm, int sp, const float* s_acc,
                                                       const float* s_ml, float* s_w, int* s_flag) {
   for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {

@@ -171,7 +171,7 @@ bs_status bs_split_decode_attention(const bs_kv_pool* pool, int32_t layer, const
  * shards and intra-shard split-K ranges -- in fixed order (shard-major) into bf16 O
  * and fp32 lse (natural log).  Equivalent to bs_split_decode_attention per shard +
  * bs_merge_partials, without the partial round trip and the extra launches.
- * pools / block_tables / max_blocks / shard_ids: HOST arrays of n_local (1..4) entries;
+ * pools / block_tables / max_blocks / shard_ids: HOST arrays of n_local (1..8) entries;
  * the pools must share num_layers / num_kv_heads / head_dim.  out bf16 [B][Hq][D] and
  * lse fp32 [B][Hq] (or NULL) are DEVICE buffers.  Workspace rules as for H4. */
 bs_status bs_split_decode_attention_local_workspace_size(int32_t n_local,
@@ -216,7 +216,7 @@ bs_status bs_split_decode_attention_local(int32_t n_local, const bs_kv_pool* con
  *   cross_device 1 when the problem's shards run on more than one GPU
  * bs_attn_task: one shard of one problem processed by THIS launch: pool (device-resident,
  *   this GPU), block_tables DEVICE [batch][max_blocks[shard_id]], shard_id, problem index.
- * 1 <= n_tasks <= 4, 1 <= n_problems <= 4; all tasks' pools share num_kv_heads / head_dim /
+ * 1 <= n_tasks <= 8, 1 <= n_problems <= 8; all tasks' pools share num_kv_heads / head_dim /
  * num_layers; all problems have `batch` requests of num_q_heads heads.  The caller
  * guarantees that every task of a problem is launched exactly once per call epoch.
  * PAPER.md gives no fused variant; this is the B200 form of "E^(1) / O^(1) is sent back
@@ -360,7 +360,10 @@ size_t bs_ipc_handle_bytes(void);
 bs_status bs_signal(int32_t* flag, int32_t value, void* stream);
 bs_status bs_wait_signal(const int32_t* flag, int32_t value, uint64_t timeout_ns, int32_t* err,
                          void* stream);
-/* Several waits in one launch: until *flags[i] >= values[i] for every i < n (1..8);
+/* bs_signal for n (1..16) flags in one launch, all set to `value`; HOST array of device
+ * (or peer-mapped) pointers. */
+bs_status bs_signals(int32_t n, int32_t* const* flags, int32_t value, void* stream);
+/* Several waits in one launch: until *flags[i] >= values[i] for every i < n (1..16);
  * flags / values are HOST arrays (of device pointers / values). */
 bs_status bs_wait_signals(int32_t n, const int32_t* const* flags, const int32_t* values,
                           uint64_t timeout_ns, int32_t* err, void* stream);

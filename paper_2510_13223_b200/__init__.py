@@ -38,6 +38,7 @@ EXPORTED_SYMBOLS = (
     "bs_copy_bytes", "bs_split_decode_attention_local_workspace_size",
     "bs_split_decode_attention_local", "bs_signal", "bs_wait_signal",
     "bs_attention_problem_workspace_size", "bs_split_decode_attention_tasks", "bs_wait_signals",
+    "bs_signals",
 )
 
 
@@ -116,6 +117,7 @@ def lib():
         "bs_signal": ([_p, _i32, _p], _i32),
         "bs_wait_signal": ([_p, _i32, ctypes.c_uint64, _p, _p], _i32),
         "bs_wait_signals": ([_i32, _p, _p, ctypes.c_uint64, _p, _p], _i32),
+        "bs_signals": ([_i32, _p, _i32, _p], _i32),
         "bs_split_decode_attention_local_workspace_size": ([_i32, _p, _p, _i32, _i32,
                                                             ctypes.POINTER(_sz)], _i32),
         "bs_split_decode_attention_local": ([_i32, _p, _i32, _p, _i32, _i32, _p, _p, _p, _p, _i32,
@@ -549,9 +551,16 @@ def wait_signal(flag_ptr: int, value: int, timeout_ns: int = 0, err_ptr: int | N
     _check(lib().bs_wait_signal(flag_ptr, int(value), int(timeout_ns), err_ptr, _stream(stream)))
 
 
+def signals(flag_ptrs, value: int, stream=None) -> None:
+    """One launch: after all prior work on the stream, *flag_ptrs[i] = value (<= 16)."""
+    n = len(flag_ptrs)
+    fa = (ctypes.c_void_p * n)(*[int(f) for f in flag_ptrs])
+    _check(lib().bs_signals(n, fa, int(value), _stream(stream)))
+
+
 def wait_signals(flag_ptrs, values, timeout_ns: int = 0, err_ptr: int | None = None,
                  stream=None) -> None:
-    """One launch: the stream waits until *flag_ptrs[i] >= values[i] for every i (<= 8)."""
+    """One launch: the stream waits until *flag_ptrs[i] >= values[i] for every i (<= 16)."""
     n = len(flag_ptrs)
     fa = (ctypes.c_void_p * n)(*[int(f) for f in flag_ptrs])
     va = (ctypes.c_int32 * n)(*[int(v) for v in values])

@@ -43,7 +43,7 @@ constexpr int kWarps = 4;
 constexpr int kBtMax = 512;     // blocks per CTA range (bt cached in smem)
 constexpr int kMaxSplit = 64;   // intra-GPU split-K limit
 
-constexpr int kMaxLocal = 4;  // shards fused into one launch (bs_split_decode_attention_local)
+constexpr int kMaxLocal = 8;  // shards (tasks) / problems of one launch
 
 // One attention problem: a set of requests whose KV is split into shards, some of which
 // may be processed by other launches (on other GPUs).  All ranges of a (request, kv-head)

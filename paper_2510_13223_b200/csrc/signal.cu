@@ -37,7 +37,19 @@ __global__ void wait_kernel(const int32_t* flag, int32_t value, uint64_t timeout
   }
 }
 
-constexpr int kMaxWaits = 8;
+constexpr int kMaxWaits = 16;
+
+struct Flags {
+  int32_t* flag[kMaxWaits];
+  int32_t n;
+};
+
+__global__ void signal_many_kernel(const Flags f, int32_t value) {
+  if ((int)threadIdx.x >= f.n) return;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(f.flag[threadIdx.x]), "r"(value) : "memory");
+}
+
 struct Waits {
   const int32_t* flag[kMaxWaits];
   int32_t value[kMaxWaits];
@@ -82,6 +94,19 @@ bs_status bs_wait_signal(const int32_t* flag, int32_t value, uint64_t timeout_ns
   BS_REQUIRE(flag, "bs_wait_signal: NULL flag");
   bs::wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(flag, value, timeout_ns, err);
   return bs::check_launch("wait_kernel");
+}
+
+bs_status bs_signals(int32_t n, int32_t* const* flags, int32_t value, void* stream) {
+  BS_REQUIRE(n >= 1 && n <= bs::kMaxWaits, "bs_signals: n=%d (1..%d)", n, bs::kMaxWaits);
+  BS_REQUIRE(flags, "bs_signals: NULL array");
+  bs::Flags f{};
+  for (int i = 0; i < n; ++i) {
+    BS_REQUIRE(flags[i], "bs_signals: NULL flag %d", i);
+    f.flag[i] = flags[i];
+  }
+  f.n = n;
+  bs::signal_many_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(f, value);
+  return bs::check_launch("signal_many_kernel");
 }
 
 bs_status bs_wait_signals(int32_t n, const int32_t* const* flags, const int32_t* values,

@@ -128,6 +128,68 @@ def mig_extra_cases(args, iters=20, warm=5):
     return out
 
 
+def tasks_cases(iters=20, warm=5):
+    """Cost of the fused cross-GPU exchange epilogue on one GPU: two C2 problems (B=64 x
+    2048, 2 shards each, 4 GiB of KV) as (i) two single-GPU fused launches, (ii) two
+    task launches each mixing a shard of both problems (the N=2 ring's launch shape) with
+    gpu-scope counters, (iii) the same with system-scope counters + done counters."""
+    dev = torch.device("cuda")
+    shape = synth.LLAMA2_7B
+    lens = np.full(64, 2048)
+    ks = synth.block_aligned_split(lens, 2)
+    probs = []
+    for seed in (1, 2):
+        case = synth.device_shards(shape, lens, ks, seed=seed, device=dev, layers=1)
+        pools = [bs.KVPool(1, pt.shape[1], shape.hkv, shape.d, base=pt.reshape(-1)) for pt in case.pools]
+        bts = [torch.from_numpy(bt).to(dev) for bt in case.block_tables]
+        mb = [t.shape[1] for t in bts]
+        n = bs.attention_problem_workspace_size(64, shape.hq, shape.hkv, shape.d, mb)
+        probs.append({"pools": pools, "bts": bts, "q": case.q[0], "ks": torch.from_numpy(ks).to(dev),
+                      "mb": mb, "ws": torch.zeros(max(n, 256), dtype=torch.uint8, device=dev),
+                      "out": torch.empty(64, shape.hq, shape.d, dtype=torch.bfloat16, device=dev),
+                      "lse": torch.empty(64, shape.hq, device=dev),
+                      "done": torch.zeros(1, dtype=torch.int32, device=dev)})
+    sc = synth.default_scale(shape.d)
+    kv = int(lens.sum()) * 2 * shape.hkv * shape.d * 2 * 2
+
+    def desc(P, cross):
+        return {"q": P["q"], "kv_split": P["ks"], "max_blocks": P["mb"], "out": P["out"],
+                "lse": P["lse"], "workspace": P["ws"], "done": P["done"] if cross else None,
+                "cross_device": cross}
+
+    def local():
+        for P in probs:
+            bs.split_decode_attention_local(P["pools"], 0, P["q"], P["bts"], [0, 1], P["ks"], sc,
+                                            P["out"], P["lse"], P["ws"])
+
+    def tasks(cross):
+        A, B = probs
+        d = [desc(A, cross), desc(B, cross)]
+        bs.split_decode_attention_tasks(d, [(A["pools"][0], A["bts"][0], 0, 0),
+                                            (B["pools"][1], B["bts"][1], 1, 1)], 0, 64, shape.hq, sc)
+        bs.split_decode_attention_tasks(d, [(A["pools"][1], A["bts"][1], 1, 0),
+                                            (B["pools"][0], B["bts"][0], 0, 1)], 0, 64, shape.hq, sc)
+    out = []
+    for name, fn in (("two_local_fused_launches", local), ("two_task_launches_gpu_scope",
+                                                             lambda: tasks(False)),
+                     ("two_task_launches_sys_scope_done", lambda: tasks(True))):
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(iters):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / iters
+        r = {"case": "tasks_C2x2_" + name, "us": round(ms * 1e3, 2),
+             "kv_GBps": round(kv / (ms * 1e-3) / 1e9, 1)}
+        print(json.dumps(r), flush=True)
+        out.append(r)
+    return out
+
+
 ATTN = {
     "C2_mha_B64_2048": (synth.LLAMA2_7B, [2048] * 64),
     "C2_shard_B64_1024": (synth.LLAMA2_7B, [1024] * 64),
@@ -141,7 +203,7 @@ ATTN = {
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", choices=["attn", "mig"])
+    ap.add_argument("--only", choices=["attn", "mig", "tasks"])
     ap.add_argument("--case")
     ap.add_argument("--json")
     ap.add_argument("--iters", type=int, default=20)
@@ -167,6 +229,8 @@ def main():
                 res.append(r)
     if args.only in (None, "mig"):
         res += mig_extra_cases(args)
+    if args.only in (None, "tasks"):
+        res += tasks_cases(iters=args.iters)
     if args.json:
         with open(args.json, "w") as f:
             json.dump(res, f, indent=1)

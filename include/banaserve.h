@@ -186,6 +186,32 @@ bs_status bs_split_decode_attention_local(int32_t n_local, const bs_kv_pool* con
                                           void* out, float* lse, void* workspace,
                                           size_t workspace_bytes, void* stream);
 
+/* Ragged plan for mixed lengths (FlashInfer-style plan / run; C4's Alpaca + LongBench
+ * mix): from the HOST copy of kv_split, cut every (request, local shard) into ranges of
+ * at most `max_blocks_per_range` blocks (0 = automatic: the uniform planner's range length,
+ * >= 16 blocks) -- empty shards get no CTA, short requests one range per shard,
+ * long ones several -- instead of the uniform grid's max_blocks-wide cut.  One plan
+ * serves every layer of a decode step.
+ * work: HOST int32 [capacity][4] (NULL with capacity 0 = query the count in *n_work);
+ * the caller copies the first *n_work items to a 16-B aligned DEVICE buffer.
+ * *max_parts: most ranges of one request (<= 64); *workspace_bytes: scratch for
+ * bs_split_decode_attention_local_ragged (0 if no request has > 1 range).
+ * Results are identical in value to the uniform path (same formulas); the summation
+ * order of the merge follows the plan's ranges (shard-major, then range). */
+bs_status bs_attention_ragged_plan(int32_t batch, int32_t n_shards, const int32_t* kv_split_host,
+                                   int32_t n_local, const int32_t* shard_ids, int32_t num_q_heads,
+                                   int32_t num_kv_heads, int32_t head_dim,
+                                   int32_t max_blocks_per_range, int32_t* work, int32_t capacity,
+                                   int32_t* n_work, int32_t* max_parts, size_t* workspace_bytes);
+/* bs_split_decode_attention_local over a ragged plan (work: DEVICE copy of the plan's
+ * items, n_work of them; max_parts from the plan).  Same outputs and workspace rules. */
+bs_status bs_split_decode_attention_local_ragged(
+    int32_t n_local, const bs_kv_pool* const* pools, int32_t layer, const void* q, int32_t batch,
+    int32_t num_q_heads, const int32_t* const* block_tables, const int32_t* max_blocks,
+    const int32_t* shard_ids, const int32_t* kv_split, int32_t n_shards, float scale,
+    const int32_t* work, int32_t n_work, int32_t max_parts, void* out, float* lse, void* workspace,
+    size_t workspace_bytes, void* stream);
+
 /* H4 + H5 + H6 fused across GPUs ("fused B200 variant"; PAPER.md:220,
  * :233-237): an attention PROBLEM is a batch of requests whose KV shards may live on
  * several GPUs.  Every launch that holds a shard of it writes that shard's per-range

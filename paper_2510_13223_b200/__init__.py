@@ -38,7 +38,7 @@ EXPORTED_SYMBOLS = (
     "bs_copy_bytes", "bs_split_decode_attention_local_workspace_size",
     "bs_split_decode_attention_local", "bs_signal", "bs_wait_signal",
     "bs_attention_problem_workspace_size", "bs_split_decode_attention_tasks", "bs_wait_signals",
-    "bs_signals",
+    "bs_signals", "bs_attention_ragged_plan", "bs_split_decode_attention_local_ragged",
 )
 
 
@@ -118,6 +118,12 @@ def lib():
         "bs_wait_signal": ([_p, _i32, ctypes.c_uint64, _p, _p], _i32),
         "bs_wait_signals": ([_i32, _p, _p, ctypes.c_uint64, _p, _p], _i32),
         "bs_signals": ([_i32, _p, _i32, _p], _i32),
+        "bs_attention_ragged_plan": ([_i32, _i32, _p, _i32, _p, _i32, _i32, _i32, _i32, _p, _i32,
+                                      ctypes.POINTER(_i32), ctypes.POINTER(_i32),
+                                      ctypes.POINTER(_sz)], _i32),
+        "bs_split_decode_attention_local_ragged": ([_i32, _p, _i32, _p, _i32, _i32, _p, _p, _p, _p,
+                                                    _i32, _f32, _p, _i32, _i32, _p, _p, _p, _sz,
+                                                    _p], _i32),
         "bs_split_decode_attention_local_workspace_size": ([_i32, _p, _p, _i32, _i32,
                                                             ctypes.POINTER(_sz)], _i32),
         "bs_split_decode_attention_local": ([_i32, _p, _i32, _p, _i32, _i32, _p, _p, _p, _p, _i32,
@@ -374,6 +380,58 @@ def split_decode_attention_tasks(problems, tasks, layer: int, batch: int, num_q_
         ta[t] = _Task(pool.handle.value, _dptr(bt, torch.int32), int(shard), int(prob))
     _check(lib().bs_split_decode_attention_tasks(len(problems), pa, len(tasks), ta, layer, batch,
                                                  num_q_heads, float(scale), _stream(stream)))
+
+
+class RaggedPlan:
+    """Host result of bs_attention_ragged_plan: ``work`` int32 [n][4] (copy to the device
+    with :meth:`to`), ``max_parts`` and ``workspace_bytes``."""
+
+    def __init__(self, work, max_parts, workspace_bytes):
+        self.work, self.max_parts, self.workspace_bytes = work, max_parts, workspace_bytes
+        self.n_work = int(work.shape[0])
+        self.device_work = None
+
+    def to(self, device):
+        self.device_work = torch.from_numpy(self.work).to(device)
+        return self
+
+
+def attention_ragged_plan(kv_split_host, shard_ids, num_q_heads: int, num_kv_heads: int,
+                          head_dim: int, max_blocks_per_range: int = 0) -> RaggedPlan:
+    import numpy as np
+    ks = np.ascontiguousarray(np.asarray(kv_split_host, dtype=np.int32))
+    B, n1 = ks.shape
+    n = len(shard_ids)
+    sa = (ctypes.c_int32 * n)(*[int(x) for x in shard_ids])
+    nw, mp, wsb = _i32(), _i32(), _sz()
+    args = (B, n1 - 1, ks.ctypes.data, n, sa, num_q_heads, num_kv_heads, head_dim,
+            max_blocks_per_range)
+    _check(lib().bs_attention_ragged_plan(*args, None, 0, ctypes.byref(nw), ctypes.byref(mp),
+                                          ctypes.byref(wsb)))
+    work = np.zeros((nw.value, 4), dtype=np.int32)
+    _check(lib().bs_attention_ragged_plan(*args, work.ctypes.data, nw.value, ctypes.byref(nw),
+                                          ctypes.byref(mp), ctypes.byref(wsb)))
+    return RaggedPlan(work, mp.value, wsb.value)
+
+
+def split_decode_attention_local_ragged(pools, layer: int, q: torch.Tensor, block_tables,
+                                        shard_ids, kv_split: torch.Tensor, scale: float,
+                                        plan: RaggedPlan, out: torch.Tensor, lse: torch.Tensor,
+                                        workspace: torch.Tensor | None = None, stream=None) -> None:
+    """H4+H6 fused over local shards, CTAs from a ragged plan (``plan.to(device)`` first)."""
+    n = len(pools)
+    B, hq, d = q.shape
+    pa = (ctypes.c_void_p * n)(*[p.handle.value for p in pools])
+    ba = (ctypes.c_void_p * n)(*[_dptr(t, torch.int32) for t in block_tables])
+    mb = (ctypes.c_int32 * n)(*[int(t.shape[1]) for t in block_tables])
+    sa = (ctypes.c_int32 * n)(*[int(x) for x in shard_ids])
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check(lib().bs_split_decode_attention_local_ragged(
+        n, pa, layer, _dptr(q, torch.bfloat16), B, hq, ba, mb, sa, _dptr(kv_split, torch.int32),
+        kv_split.shape[1] - 1, float(scale), _dptr(plan.device_work, torch.int32), plan.n_work,
+        plan.max_parts, _dptr(out, torch.bfloat16),
+        _dptr(lse, torch.float32) if lse is not None else None, _dptr(workspace), ws_bytes,
+        _stream(stream)))
 
 
 def merge_partials(o_parts, m_parts, l_parts, out: torch.Tensor, lse: torch.Tensor | None = None,

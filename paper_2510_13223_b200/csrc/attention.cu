@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
+#include <vector>
 
 #include "internal.h"
 #include "ptx.cuh"
@@ -91,6 +92,9 @@ struct AttnParams {
   int32_t hq, hkv;          // hq: q heads of the MODEL (row stride); hkv: kv heads in this launch
   int32_t model_head_lo;    // first kv head of the launch in the model (q / output rows)
   int32_t grid_x;           // CTA ranges of this launch over its shards
+  const int4* work;         // ragged plan (bs_attention_ragged_plan) or NULL: one item per
+                            // item = (request, shard << 16 | slot, first block,
+                            // blocks << 8 | ranges of the request); grid.x = items * hkv
 };
 
 struct TMaps {
@@ -104,6 +108,39 @@ __device__ __forceinline__ int shard_of(const AttnParams& p, int spg) {
   for (int i = 1; i < kMaxLocal; ++i)
     if (i < p.n_local && spg >= p.sh[i].split_off) j = i;
   return j;
+}
+
+// What one CTA computes: request b, shard js of the launch, blocks [blo, blo + nb) of the
+// shard, partial slot, and the request's range count (-1: the problem's uniform nsplit).
+struct CtaWork {
+  int b, g, js, blo, nb, slot, nparts;
+};
+
+__device__ __forceinline__ CtaWork cta_work(const AttnParams& p) {
+  CtaWork w;
+  if (p.work) {  // ragged plan: grid.x = item * Hkv + kv head (heads of an item adjacent:
+                 // they read neighbouring pages of the same blocks)
+    const int item = blockIdx.x / p.hkv;
+    w.g = blockIdx.x - item * p.hkv;
+    const int4 it = __ldg(p.work + item);
+    w.b = it.x;
+    w.js = it.y >> 16;
+    w.slot = it.y & 0xffff;
+    w.blo = it.z;
+    w.nb = it.w >> 8;
+    w.nparts = it.w & 0xff;
+  } else {       // uniform plan: grid = (ranges over the launch's shards, kv heads, requests)
+    const int spg = blockIdx.x;
+    w.b = blockIdx.z;
+    w.g = blockIdx.y;
+    w.js = shard_of(p, spg);
+    const int sp = spg - p.sh[w.js].split_off;
+    w.blo = sp * p.sh[w.js].bps;
+    w.nb = p.sh[w.js].bps;
+    w.slot = p.sh[w.js].range_base + sp;
+    w.nparts = -1;
+  }
+  return w;
 }
 
 template <int D, int G, int STAGES>
@@ -176,8 +213,10 @@ __device__ __forceinline__ void count_done(const ProbDesc& P) {  // P: a local c
 }
 
 template <int D, int G>
+// sp: this CTA's partial slot; nparts: ranges of the request to merge (P.nsplit, or the
+// request's own count under a ragged plan); P.nsplit is the workspace slot stride.
 __device__ __forceinline__ void cta_combine_and_store(const ProbDesc P, int hq, int hkv, int b, int g,
-                                                      int gm, int sp, const float* s_acc,
+                                                      int gm, int sp, int nparts, const float* s_acc,
                                                       const float* s_ml, float* s_w, int* s_flag) {
   for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
     const int h = idx / D, x = idx - h * D;
@@ -196,7 +235,7 @@ __device__ __forceinline__ void cta_combine_and_store(const ProbDesc P, int hq, 
     }
     const int64_t row = (int64_t)b * hq + gm * G + h;
     const bool any = L > 0.f;
-    if (P.nsplit == 1) {
+    if (nparts == 1) {
       if (P.merged) {
         P.out[row * D + x] = __float2bfloat16_rn(any ? O / L : 0.f);
         if (x == 0 && P.lse) P.lse[row] = any ? M * kLn2 + logf(L) : -INFINITY;
@@ -216,7 +255,7 @@ __device__ __forceinline__ void cta_combine_and_store(const ProbDesc P, int hq, 
       }
     }
   }
-  if (P.nsplit == 1) {
+  if (nparts == 1) {
     if (P.done) {
       __syncthreads();
       if (threadIdx.x == 0) count_done(P);
@@ -238,7 +277,7 @@ __device__ __forceinline__ void cta_combine_and_store(const ProbDesc P, int hq, 
       asm volatile("atom.acq_rel.sys.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(cnt) : "memory");
     else
       asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(cnt) : "memory");
-    const int last = prev == P.nsplit - 1;
+    const int last = prev == nparts - 1;
     if (last) *cnt = 0;  // every CTA has arrived: re-arm for the next call
     s_flag[0] = last;
   }
@@ -255,8 +294,8 @@ __device__ __forceinline__ void cta_combine_and_store(const ProbDesc P, int hq, 
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         const int j = lane + 32 * t;
-        mj[t] = j < P.nsplit ? __ldcg(ml + 2 * j) : -INFINITY;
-        lj[t] = j < P.nsplit ? __ldcg(ml + 2 * j + 1) : 0.f;
+        mj[t] = j < nparts ? __ldcg(ml + 2 * j) : -INFINITY;
+        lj[t] = j < nparts ? __ldcg(ml + 2 * j + 1) : 0.f;
       }
       float M = fmaxf(mj[0], mj[1]);
 #pragma unroll
@@ -272,7 +311,7 @@ __device__ __forceinline__ void cta_combine_and_store(const ProbDesc P, int hq, 
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         const int j = lane + 32 * t;
-        if (j < P.nsplit) s_w[h * kMaxSplit + j] = L > 0.f ? w[t] / L : 0.f;
+        if (j < nparts) s_w[h * kMaxSplit + j] = L > 0.f ? w[t] / L : 0.f;
       }
       if (lane == 0) {
         if (P.merged) {
@@ -291,7 +330,7 @@ __device__ __forceinline__ void cta_combine_and_store(const ProbDesc P, int hq, 
     const float* po = P.ws_o + row * P.nsplit * D + x;
     float O = 0.f;
 #pragma unroll 8
-    for (int j = 0; j < P.nsplit; ++j) O += s_w[h * kMaxSplit + j] * __ldcg(po + (int64_t)j * D);
+    for (int j = 0; j < nparts; ++j) O += s_w[h * kMaxSplit + j] * __ldcg(po + (int64_t)j * D);
     if (P.merged) P.out[row * D + x] = __float2bfloat16_rn(O);
     else P.o[row * D + x] = O;
   }
@@ -309,40 +348,45 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int spg = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
-  const int js = shard_of(p, spg);
+  const CtaWork cw = cta_work(p);
+  const int g = cw.g, b = cw.b, js = cw.js;
   const ShardDesc& sd = p.sh[js];
-  const int sp = spg - sd.split_off;
   const ProbDesc& P = p.pb[sd.prob];
 
+  // One memory round trip before the first TMA: the CTA's block-table row (independent
+  // of the length), each warp's first STAGES block ids and the shard length are loaded
+  // together; lane 0 of every warp then issues its first copies before the CTA barrier.
+  const int32_t blo = cw.blo;
+  const int64_t row0 = (int64_t)b * sd.max_blocks + blo;
+  const int nb_tab = max(min(cw.nb, sd.max_blocks - blo), 0);
+  constexpr int kIdPerThread = kBtMax / (kWarps * 32);
+  int32_t idv[kIdPerThread];
+#pragma unroll
+  for (int r = 0; r < kIdPerThread; ++r) {
+    const int i = threadIdx.x + r * kWarps * 32;
+    idv[r] = i < nb_tab ? __ldg(sd.bt + row0 + i) : 0;
+  }
+  int32_t first[STAGES];
+#pragma unroll
+  for (int k = 0; k < STAGES; ++k)
+    first[k] = (lane == 0 && warp + k * kWarps < nb_tab) ? __ldg(sd.bt + row0 + warp + k * kWarps) : 0;
   const int32_t* ks = P.kv_split + (int64_t)b * (P.n_shards + 1) + sd.shard_id;
   const int32_t len = max(__ldg(ks + 1) - __ldg(ks), 0);
   const int32_t nblk = (len + 15) >> 4;
-  const int32_t blo = sp * sd.bps;
-  const int32_t nb_cta = max(min(nblk, blo + sd.bps) - blo, 0);
+  const int32_t nb_cta = max(min(nblk, blo + cw.nb) - blo, 0);
+  const int nparts = cw.nparts < 0 ? P.nsplit : cw.nparts;
 
   int32_t* s_bt = reinterpret_cast<int32_t*>(smem + S::kBtOff);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBarOff) + warp * STAGES;
   float* s_p = reinterpret_cast<float*>(smem + S::kPOff) + warp * G * 16;
   uint8_t* ring = smem + warp * STAGES * S::kStage;
 
-  for (int i = threadIdx.x; i < nb_cta; i += blockDim.x)
-    s_bt[i] = __ldg(sd.bt + (int64_t)b * sd.max_blocks + blo + i);
-  if (lane == 0) {
-#pragma unroll
-    for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&bars[s], 1);
-    ptx::fence_mbar_init();
-  }
-  __syncthreads();
-
   const int nmine = nb_cta > warp ? (nb_cta - warp + kWarps - 1) / kWarps : 0;
   const uint8_t* kv_head = sd.kv + (int64_t)(sd.pool_head_lo + g) * S::kPage;
   const int gm = p.model_head_lo + g;  // kv head index in the model
   uint64_t policy = 0;
-  if (lane == 0) policy = ptx::policy_evict_first();
-  auto issue = [&](int k) {
+  auto issue = [&](int k, int64_t phys) {  // lane 0 only
     const int s = k % STAGES;
-    const int64_t phys = s_bt[warp + k * kWarps];
     const uint8_t* kp = kv_head + phys * sd.chunk_bytes;
     uint8_t* dst = ring + s * S::kStage;
     ptx::mbar_expect_tx(&bars[s], 2 * S::kPage);
@@ -350,9 +394,20 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
     ptx::bulk_g2s_evict_first(dst + S::kPage, kp + sd.v_off, S::kPage, &bars[s], policy);
   };
   if (lane == 0) {
-    for (int k = 0; k < min(STAGES, nmine); ++k) issue(k);
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&bars[s], 1);
+    ptx::fence_mbar_init();
+    policy = ptx::policy_evict_first();
+#pragma unroll
+    for (int k = 0; k < STAGES; ++k)
+      if (k < nmine) issue(k, first[k]);
   }
-  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < kIdPerThread; ++r) {
+    const int i = threadIdx.x + r * kWarps * 32;
+    if (i < nb_cta) s_bt[i] = idv[r];
+  }
+  __syncthreads();  // block table + barrier inits visible to the CTA
 
   // q for the G heads of this group, this lane's dims, pre-scaled into log2 units and
   // duplicated into both halves of a packed pair ({q_e, q_e}) for token-pair FFMA2
@@ -487,7 +542,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
     __syncwarp();
     if (lane == 0 && k + STAGES < nmine) {
       ptx::fence_proxy_async_smem();
-      issue(k + STAGES);
+      issue(k + STAGES, s_bt[warp + (k + STAGES) * kWarps]);
     }
     __syncwarp();
   }
@@ -520,8 +575,8 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
     }
   }
   __syncthreads();
-  cta_combine_and_store<D, G>(P, p.hq, p.hkv, b, g, gm, sd.range_base + sp, s_acc, s_ml,
-                              s_w, s_flag);
+  cta_combine_and_store<D, G>(P, p.hq, p.hkv, b, g, gm, cw.slot, nparts, s_acc, s_ml, s_w,
+                              s_flag);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -602,43 +657,47 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int gq = lane >> 2, tq = lane & 3;  // mma groupID / thread-in-group
-  const int spg = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
-  const int js = shard_of(p, spg);
+  const CtaWork cw = cta_work(p);
+  const int g = cw.g, b = cw.b, js = cw.js;
   const ShardDesc& sd = p.sh[js];
-  const int sp = spg - sd.split_off;
   const ProbDesc& P = p.pb[sd.prob];
 
+  // One memory round trip before the first TMA: the CTA's block-table row (independent
+  // of the length), each warp's first STAGES block ids and the shard length are loaded
+  // together; lane 0 of every warp then issues its first copies before the CTA barrier.
+  const int32_t blo = cw.blo;
+  const int64_t row0 = (int64_t)b * sd.max_blocks + blo;
+  const int nb_tab = max(min(cw.nb, sd.max_blocks - blo), 0);
+  constexpr int kIdPerThread = kBtMax / (kWarps * 32);
+  int32_t idv[kIdPerThread];
+#pragma unroll
+  for (int r = 0; r < kIdPerThread; ++r) {
+    const int i = threadIdx.x + r * kWarps * 32;
+    idv[r] = i < nb_tab ? __ldg(sd.bt + row0 + i) : 0;
+  }
+  int32_t first[STAGES];
+#pragma unroll
+  for (int k = 0; k < STAGES; ++k)
+    first[k] = (lane == 0 && warp + k * kWarps < nb_tab) ? __ldg(sd.bt + row0 + warp + k * kWarps) : 0;
   const int32_t* ks = P.kv_split + (int64_t)b * (P.n_shards + 1) + sd.shard_id;
   const int32_t len = max(__ldg(ks + 1) - __ldg(ks), 0);
   const int32_t nblk = (len + 15) >> 4;
-  const int32_t blo = sp * sd.bps;
-  const int32_t nb_cta = max(min(nblk, blo + sd.bps) - blo, 0);
+  const int32_t nb_cta = max(min(nblk, blo + cw.nb) - blo, 0);
+  const int nparts = cw.nparts < 0 ? P.nsplit : cw.nparts;
 
   int32_t* s_bt = reinterpret_cast<int32_t*>(smem + S::kBtOff);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBarOff) + warp * STAGES;
   uint8_t* s_pt = smem + S::kPOff + warp * 8 * 16 * 2;
   uint8_t* ring = smem + warp * STAGES * S::kStage;
 
-  for (int i = threadIdx.x; i < nb_cta; i += blockDim.x)
-    s_bt[i] = __ldg(sd.bt + (int64_t)b * sd.max_blocks + blo + i);
-  if (lane == 0) {
-#pragma unroll
-    for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&bars[s], 1);
-    ptx::fence_mbar_init();
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm.m[shard_of(p, blockIdx.x)])) : "memory");
-  }
-  __syncthreads();
-
   const int nmine = nb_cta > warp ? (nb_cta - warp + kWarps - 1) / kWarps : 0;
   const int gm = p.model_head_lo + g;
   const int head = sd.pool_head_lo + g;
   const CUtensorMap* tmap = &tm.m[js];
   uint64_t policy = 0;
-  if (lane == 0) policy = ptx::policy_evict_first();
   const uint32_t ring_u32 = ptx::smem_u32(ring);
-  auto issue = [&](int k) {  // lane 0 only
+  auto issue = [&](int k, int32_t phys) {  // lane 0 only
     const int s = k % STAGES;
-    const int32_t phys = s_bt[warp + k * kWarps];
     const int32_t row_k = sd.layer_row0 + ((phys * 2 + 0) * sd.pool_hkv + head) * 16;
     const int32_t row_v = row_k + sd.pool_hkv * 16;
     const uint32_t st = ring_u32 + s * S::kStage;
@@ -649,9 +708,22 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
       tma_load_2d(st + (NB + bx) * S::kBox, tmap, 64 * bx, row_v, &bars[s], policy);
     }
   };
-  if (lane == 0)
-    for (int k = 0; k < min(STAGES, nmine); ++k) issue(k);
-  __syncwarp();
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&bars[s], 1);
+    ptx::fence_mbar_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
+    policy = ptx::policy_evict_first();
+#pragma unroll
+    for (int k = 0; k < STAGES; ++k)
+      if (k < nmine) issue(k, first[k]);
+  }
+#pragma unroll
+  for (int r = 0; r < kIdPerThread; ++r) {
+    const int i = threadIdx.x + r * kWarps * 32;
+    if (i < nb_cta) s_bt[i] = idv[r];
+  }
+  __syncthreads();  // block table + barrier inits visible to the CTA
 
   // q^T B-fragments (bf16 pairs) for head n = gq (zero padding for n >= G)
   uint32_t bq[KS][2];
@@ -748,7 +820,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
     __syncwarp();
     if (lane == 0 && k + STAGES < nmine) {
       ptx::fence_proxy_async_smem();
-      issue(k + STAGES);
+      issue(k + STAGES, s_bt[warp + (k + STAGES) * kWarps]);
     }
     __syncwarp();
   }
@@ -783,8 +855,8 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
     }
   }
   __syncthreads();
-  cta_combine_and_store<D, G>(P, p.hq, p.hkv, b, g, gm, sd.range_base + sp, s_acc, s_ml,
-                              s_w, s_flag);
+  cta_combine_and_store<D, G>(P, p.hq, p.hkv, b, g, gm, cw.slot, nparts, s_acc, s_ml, s_w,
+                              s_flag);
 }
 
 // Pipeline depth / residency per (head_dim, group): STAGES blocks (K+V pages) per warp in
@@ -905,7 +977,7 @@ bs_status launch_attn_v(const AttnParams& p, int batch, cudaStream_t stream) {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
     configured_dev = dev;
   }
-  dim3 grid(p.grid_x, p.hkv, batch);
+  const dim3 grid = p.work ? dim3(p.grid_x * p.hkv, 1, 1) : dim3(p.grid_x, p.hkv, batch);
   split_decode_attn<D, G, STAGES, MINB><<<grid, kWarps * 32, S::kTotal, stream>>>(p);
   return check_launch("split_decode_attn");
 }
@@ -920,7 +992,7 @@ bs_status launch_attn_mma(const AttnParams& p, const TMaps& tm, int batch, cudaS
                          cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
     configured_dev = dev;
   }
-  dim3 grid(p.grid_x, p.hkv, batch);
+  const dim3 grid = p.work ? dim3(p.grid_x * p.hkv, 1, 1) : dim3(p.grid_x, p.hkv, batch);
   split_decode_attn_mma<D, G, STAGES, MINB><<<grid, kWarps * 32, S::kTotal, stream>>>(p, tm);
   return check_launch("split_decode_attn_mma");
 }
@@ -1011,6 +1083,8 @@ struct LaunchArgs {
   void* workspace;
   size_t workspace_bytes;
   void* stream;
+  const int32_t* work;  // ragged plan (device int4 items) or NULL
+  int32_t n_work, max_parts;
 };
 
 bs_status validate_common(const LaunchArgs& a, int* G_out) {
@@ -1061,8 +1135,24 @@ bs_status run_attention(const LaunchArgs& a) {
              "attention: q / output must be 16-B aligned");
   const int d = a.pools[0]->desc.head_dim;
   bs::Plan pl;
-  st = bs::make_plan(a.batch, G, a.num_q_heads, a.n_kv_heads, d, a.n_local, a.max_blocks, a.merged, &pl);
-  if (st != BS_OK) return st;
+  if (a.work) {  // ragged plan: ranges come from the work list, slots up to max_parts
+    BS_REQUIRE(a.n_work >= 1 && a.max_parts >= 1 && a.max_parts <= bs::kMaxSplit,
+               "attention: ragged plan with %d items / %d parts", a.n_work, a.max_parts);
+    BS_REQUIRE(((uintptr_t)a.work & 15) == 0, "attention: work list must be 16-B aligned");
+    pl = bs::Plan{};
+    pl.bps = bs::kBtMax;
+    pl.nsplit = a.max_parts;
+    for (int j = 0; j < a.n_local; ++j) pl.split_off[j] = 0;
+    if (a.max_parts > 1) {
+      const size_t parts = (size_t)a.batch * a.num_q_heads * a.max_parts;
+      pl.off_ml = parts * d * 4;
+      pl.off_cnt = pl.off_ml + parts * 2 * 4;
+      pl.ws_bytes = pl.off_cnt + (size_t)a.batch * a.n_kv_heads * 4;
+    }
+  } else {
+    st = bs::make_plan(a.batch, G, a.num_q_heads, a.n_kv_heads, d, a.n_local, a.max_blocks, a.merged, &pl);
+    if (st != BS_OK) return st;
+  }
   BS_REQUIRE(pl.ws_bytes == 0 || (a.workspace && a.workspace_bytes >= pl.ws_bytes &&
                                   ((uintptr_t)a.workspace & 15) == 0),
              "attention: workspace needs %zu bytes (got %zu)", pl.ws_bytes, a.workspace_bytes);
@@ -1097,7 +1187,8 @@ bs_status run_attention(const LaunchArgs& a) {
   p.hq = a.num_q_heads;
   p.hkv = a.n_kv_heads;
   p.model_head_lo = a.model_head_lo;
-  p.grid_x = pl.nsplit;
+  p.grid_x = a.work ? a.n_work : pl.nsplit;
+  p.work = reinterpret_cast<const int4*>(a.work);
   bs::ProbDesc& P = p.pb[0];
   P.q = static_cast<const __nv_bfloat16*>(a.q);
   P.kv_split = a.kv_split;
@@ -1411,6 +1502,145 @@ bs_status bs_split_decode_attention_tasks(int32_t n_problems, const bs_attn_prob
   const bs::TMaps* tmp = have_maps ? &tm : nullptr;
   if (d == 128) return bs::launch_attn_d<128>(p, tmp, G, batch, s);
   return bs::launch_attn_d<64>(p, tmp, G, batch, s);
+}
+
+bs_status bs_attention_ragged_plan(int32_t batch, int32_t n_shards, const int32_t* kv_split_host,
+                                   int32_t n_local, const int32_t* shard_ids, int32_t num_q_heads,
+                                   int32_t num_kv_heads, int32_t head_dim,
+                                   int32_t max_blocks_per_range, int32_t* work, int32_t capacity,
+                                   int32_t* n_work, int32_t* max_parts, size_t* workspace_bytes) {
+  BS_REQUIRE(kv_split_host && shard_ids && n_work && max_parts && workspace_bytes,
+             "bs_attention_ragged_plan: NULL argument");
+  BS_REQUIRE(batch >= 1 && n_shards >= 1 && n_local >= 1 && n_local <= bs::kMaxLocal,
+             "bs_attention_ragged_plan: batch %d / %d shards / %d local", batch, n_shards, n_local);
+  BS_REQUIRE(num_kv_heads >= 1 && num_q_heads >= num_kv_heads && num_q_heads % num_kv_heads == 0,
+             "bs_attention_ragged_plan: bad heads");
+  BS_REQUIRE(head_dim == 64 || head_dim == 128, "bs_attention_ragged_plan: head_dim %d", head_dim);
+  BS_REQUIRE(max_blocks_per_range >= 0 && max_blocks_per_range <= bs::kBtMax,
+             "bs_attention_ragged_plan: max_blocks_per_range %d (0..%d)", max_blocks_per_range,
+             bs::kBtMax);
+  for (int t = 0; t < n_local; ++t)
+    BS_REQUIRE(shard_ids[t] >= 0 && shard_ids[t] < n_shards, "bs_attention_ragged_plan: shard %d",
+               shard_ids[t]);
+  const int G = num_q_heads / num_kv_heads;
+  if (G != 1 && G != 2 && G != 4 && G != 8)
+    return bs::set_error(BS_ERR_UNSUPPORTED, "query group G=%d not in {1,2,4,8}", G);
+  std::vector<int32_t> nblk((size_t)batch * n_local);
+  for (int b = 0; b < batch; ++b)
+    for (int t = 0; t < n_local; ++t) {
+      const int32_t* ks = kv_split_host + (int64_t)b * (n_shards + 1) + shard_ids[t];
+      const int32_t len = std::max(ks[1] - ks[0], 0);
+      nblk[(size_t)b * n_local + t] = (len + 15) / 16;
+    }
+  // range length (automatic): the uniform planner's choice for the same shard widths
+  // (its wave model), so balanced batches get the uniform grid's cut; the ragged list then
+  // drops the empty (request, shard) CTAs and gives short requests a single range
+  int bps = max_blocks_per_range;
+  if (bps == 0) {
+    int mb[bs::kMaxProbShards];
+    for (int t = 0; t < n_local; ++t) {
+      mb[t] = 1;
+      for (int b = 0; b < batch; ++b) mb[t] = std::max(mb[t], nblk[(size_t)b * n_local + t]);
+    }
+    bs::Plan pl;
+    bs_status st = bs::make_plan(batch, G, num_q_heads, num_kv_heads, head_dim, n_local, mb, true, &pl);
+    if (st != BS_OK) return st;
+    bps = std::min(bs::kBtMax, std::max(16, pl.bps));
+  }
+  int32_t count = 0, most = 1;
+  auto emit = [&](int b, int t, int slot, int blo, int nb, int parts) {
+    if (work && count < capacity) {
+      int32_t* w = work + 4 * (size_t)count;
+      w[0] = b;
+      w[1] = (t << 16) | slot;
+      w[2] = blo;
+      w[3] = (nb << 8) | parts;
+    }
+    ++count;
+  };
+  for (int b = 0; b < batch; ++b) {
+    int pb = bps, parts = 0;
+    for (;;) {  // a request's ranges must fit kMaxSplit slots: widen its ranges if not
+      parts = 0;
+      for (int t = 0; t < n_local; ++t) parts += (nblk[(size_t)b * n_local + t] + pb - 1) / pb;
+      if (parts <= bs::kMaxSplit) break;
+      pb = std::min(bs::kBtMax, pb * 2);
+      if (pb == bs::kBtMax) {
+        parts = 0;
+        for (int t = 0; t < n_local; ++t) parts += (nblk[(size_t)b * n_local + t] + pb - 1) / pb;
+        if (parts > bs::kMaxSplit)
+          return bs::set_error(BS_ERR_UNSUPPORTED, "request %d: %d ranges > %d", b, parts, bs::kMaxSplit);
+        break;
+      }
+    }
+    if (parts == 0) {  // empty everywhere: one item writes the empty result
+      emit(b, 0, 0, 0, 0, 1);
+      continue;
+    }
+    most = std::max(most, parts);
+    int slot = 0;
+    for (int t = 0; t < n_local; ++t) {  // shard-major, then range: the fixed merge order
+      const int nb = nblk[(size_t)b * n_local + t];
+      if (nb == 0) continue;
+      const int nr = (nb + pb - 1) / pb, base = nb / nr, rem = nb % nr;
+      int blo = 0;
+      for (int r = 0; r < nr; ++r) {
+        const int len = base + (r < rem ? 1 : 0);
+        emit(b, t, slot++, blo, len, parts);
+        blo += len;
+      }
+    }
+  }
+  *n_work = count;
+  *max_parts = most;
+  *workspace_bytes = most > 1 ? (size_t)batch * num_q_heads * most * (head_dim + 2) * 4 +
+                                    (size_t)batch * num_kv_heads * 4
+                              : 0;
+  if (work && count > capacity)
+    return bs::set_error(BS_ERR_INVALID_ARG, "bs_attention_ragged_plan: %d items > capacity %d", count,
+                         capacity);
+  return BS_OK;
+}
+
+bs_status bs_split_decode_attention_local_ragged(
+    int32_t n_local, const bs_kv_pool* const* pools, int32_t layer, const void* q, int32_t batch,
+    int32_t num_q_heads, const int32_t* const* block_tables, const int32_t* max_blocks,
+    const int32_t* shard_ids, const int32_t* kv_split, int32_t n_shards, float scale,
+    const int32_t* work, int32_t n_work, int32_t max_parts, void* out, float* lse, void* workspace,
+    size_t workspace_bytes, void* stream) {
+  BS_REQUIRE(pools && block_tables && max_blocks && shard_ids && work,
+             "bs_split_decode_attention_local_ragged: NULL array");
+  BS_REQUIRE(n_local >= 1 && n_local <= bs::kMaxLocal, "bs_split_decode_attention_local_ragged: %d shards",
+             n_local);
+  BS_REQUIRE(pools[0], "bs_split_decode_attention_local_ragged: NULL pool");
+  LaunchArgs a{};
+  a.n_local = n_local;
+  for (int j = 0; j < n_local; ++j) {
+    a.pools[j] = pools[j];
+    a.bts[j] = block_tables[j];
+    a.max_blocks[j] = max_blocks[j];
+    a.shard_ids[j] = shard_ids[j];
+    BS_REQUIRE(pools[j] && pools[j]->desc.num_kv_heads == pools[0]->desc.num_kv_heads,
+               "bs_split_decode_attention_local_ragged: shards must share num_kv_heads");
+  }
+  a.n_kv_heads = a.num_kv_heads_total = pools[0]->desc.num_kv_heads;
+  a.layer = layer;
+  a.batch = batch;
+  a.num_q_heads = num_q_heads;
+  a.n_shards = n_shards;
+  a.q = q;
+  a.kv_split = kv_split;
+  a.scale = scale;
+  a.merged = true;
+  a.out = out;
+  a.lse = lse;
+  a.workspace = workspace;
+  a.workspace_bytes = workspace_bytes;
+  a.stream = stream;
+  a.work = work;
+  a.n_work = n_work;
+  a.max_parts = max_parts;
+  return run_attention(a);
 }
 
 }  // extern "C"

@@ -190,6 +190,63 @@ def tasks_cases(iters=20, warm=5):
     return out
 
 
+def ragged_cases(iters=20, warm=5):
+    """Mixed-length shards through the single-GPU fused launch: uniform grid (max_blocks-
+    wide ranges) vs the ragged plan (bs_attention_ragged_plan).  GB/s = algorithmic bytes
+    (KV + q + bf16 O + lse + block table) / time."""
+    dev = torch.device("cuda")
+    out = []
+    cases = {
+        "C4_gqa8_mixed_B256": (synth.LLAMA2_70B, synth.mixed_lengths(256, seed=0) // 8),
+        "C4_gqa8_mixed_B256_seed3": (synth.LLAMA2_70B, synth.mixed_lengths(256, seed=3) // 8),
+        "C2_mha_B64_2048": (synth.LLAMA2_7B, np.full(64, 2048)),
+        "C3_gqa4_B8_8192": (synth.LLAMA3_8B, np.full(8, 8192)),
+    }
+    for name, (shape, lens) in cases.items():
+        lens = np.asarray(lens, dtype=np.int64)
+        ks = np.stack([np.zeros_like(lens), lens], 1).astype(np.int32)
+        case = synth.device_shards(shape, lens, ks, seed=1, device=dev, layers=1)
+        pool = bs.KVPool(1, case.pools[0].shape[1], shape.hkv, shape.d, base=case.pools[0].reshape(-1))
+        bts = [torch.from_numpy(case.block_tables[0]).to(dev)]
+        ksd = torch.from_numpy(ks).to(dev)
+        B = len(lens)
+        sc = synth.default_scale(shape.d)
+        o = torch.empty(B, shape.hq, shape.d, dtype=torch.bfloat16, device=dev)
+        lse = torch.empty(B, shape.hq, device=dev)
+        wsu = torch.zeros(max(16, bs.split_decode_attention_local_workspace_size(
+            [pool], [bts[0].shape[1]], B, shape.hq)), dtype=torch.uint8, device=dev)
+        plan = bs.attention_ragged_plan(ks, [0], shape.hq, shape.hkv, shape.d).to(dev)
+        wsr = torch.zeros(max(16, plan.workspace_bytes), dtype=torch.uint8, device=dev)
+        alg = int(lens.sum()) * 2 * shape.hkv * shape.d * 2 + B * shape.hq * shape.d * 2 + \
+            B * shape.hq * (shape.d * 2 + 4) + 4 * int(sum(synth.ceil_div(int(x), 16) for x in lens))
+        fns = {"uniform": lambda: bs.split_decode_attention_local([pool], 0, case.q[0], bts, [0], ksd,
+                                                                  sc, o, lse, wsu),
+               "ragged": lambda: bs.split_decode_attention_local_ragged([pool], 0, case.q[0], bts,
+                                                                        [0], ksd, sc, plan, o, lse, wsr)}
+        for kind, fn in fns.items():
+            for _ in range(warm):
+                fn()
+            torch.cuda.synchronize()
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(iters)]
+            for a, b in evs:
+                a.record()
+                fn()
+                b.record()
+            torch.cuda.synchronize()
+            t = sorted(a.elapsed_time(b) for a, b in evs)
+            med = t[len(t) // 2]
+            r = {"case": f"{name}_{kind}", "B": B, "G": shape.group, "tokens": int(lens.sum()),
+                 "us": round(med * 1e3, 2), "GBps": round(alg / (med * 1e-3) / 1e9, 1), "bytes": alg,
+                 "items": plan.n_work if kind == "ragged" else None,
+                 "max_parts": plan.max_parts if kind == "ragged" else None}
+            print(json.dumps(r), flush=True)
+            out.append(r)
+        del case, pool
+        torch.cuda.empty_cache()
+    return out
+
+
 ATTN = {
     "C2_mha_B64_2048": (synth.LLAMA2_7B, [2048] * 64),
     "C2_shard_B64_1024": (synth.LLAMA2_7B, [1024] * 64),
@@ -199,18 +256,28 @@ ATTN = {
     "C3_gqa4_B8_32768_1gpu": (synth.LLAMA3_8B, [32768] * 8),
     "C4_gqa8_mixed_B256": (synth.LLAMA2_70B, list(synth.mixed_lengths(256, seed=0) // 8)),
 }
+# diagnostics: same KV bytes, different group size / kv-head count (--diag)
+DIAG = {
+    "D_hkv8_G1_B256_2048": (synth.Shape(1, 8, 8, 128), [2048] * 256),
+    "D_hkv8_G4_B256_2048": (synth.Shape(1, 32, 8, 128), [2048] * 256),
+    "D_hkv8_G8_B256_2048": (synth.Shape(1, 64, 8, 128), [2048] * 256),
+    "D_hkv32_G1_B64_2048": (synth.Shape(1, 32, 32, 128), [2048] * 64),
+    "D_hkv32_G2_B64_2048": (synth.Shape(1, 64, 32, 128), [2048] * 64),
+    "D_hkv8_G8_B256_684": (synth.Shape(1, 64, 8, 128), [684] * 256),
+}
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", choices=["attn", "mig", "tasks"])
+    ap.add_argument("--only", choices=["attn", "mig", "tasks", "ragged"])
     ap.add_argument("--case")
     ap.add_argument("--json")
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--diag", action="store_true", help="group-size / kv-head diagnostics")
     args = ap.parse_args()
     res = []
     if args.only in (None, "attn"):
-        for name, (shape, lens) in ATTN.items():
+        for name, (shape, lens) in (DIAG if args.diag else ATTN).items():
             if args.case and args.case != name:
                 continue
             r = attn_case(name, shape, lens, iters=args.iters)
@@ -231,6 +298,8 @@ def main():
         res += mig_extra_cases(args)
     if args.only in (None, "tasks"):
         res += tasks_cases(iters=args.iters)
+    if args.only in (None, "ragged"):
+        res += ragged_cases(iters=args.iters)
     if args.json:
         with open(args.json, "w") as f:
             json.dump(res, f, indent=1)

@@ -405,13 +405,16 @@ class ShardedDecodeStep:
                         ex.wait(ex.comm, inputs_ready[layer])
                     _sendrecv(self.pg_attn, q[layer], self.next, self.q_prev[layer], self.prev)
                     ex.record(E["q_ready"][layer], ex.comm)
+        # lookahead -2 at N=1: the hand-off copy runs on the compute stream right before its
+        # layer's attention (serial) -- both are HBM-bound on one GPU
+        mig_s = ex.compute if (self.lookahead == -2 and self.world == 1) else ex.copy
         for layer in range(self.L):
             # ---- H2/H3: migration channel ---------------------------------------------
-            with ex.use(ex.copy):
+            with ex.use(mig_s):
                 if self.lookahead >= 0 and layer - self.lookahead >= 0:
                     ex.wait(ex.copy, E["layer_start"][layer - self.lookahead])
                 if timers is not None:
-                    timers[layer][2].record(ex.copy)
+                    timers[layer][2].record(mig_s)
                 if self.n_handoff:
                     if self.world == 1:
                         ops.migrate_local(self.cold, self.home, layer, self.src_ids, self.dst_ids,
@@ -421,8 +424,8 @@ class ShardedDecodeStep:
                         _sendrecv(self.pg_mig, self.stage_send, self.prev, self.stage_recv, self.next)
                         ops.scatter(self.home, layer, self.dst_ids, self.stage_recv)
                 if timers is not None:
-                    timers[layer][3].record(ex.copy)
-                ex.record(E["mig_done"][layer], ex.copy)
+                    timers[layer][3].record(mig_s)
+                ex.record(E["mig_done"][layer], mig_s)
             # ---- H4: attention over both pools -------------------------------------------
             with ex.use(ex.compute):
                 ex.record(E["layer_start"][layer], ex.compute)

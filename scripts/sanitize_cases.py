@@ -51,6 +51,21 @@ def main():
         ws = torch.zeros(max(16, bs.split_decode_attention_local_workspace_size(
             pools, [t.shape[1] for t in bts], B, hq)), dtype=torch.uint8, device="cuda")
         bs.split_decode_attention_local(pools, 0, q, bts, [0, 1], ksd, synth.default_scale(d), out, lse, ws)
+        # ragged plan over the same local shards
+        plan = bs.attention_ragged_plan(ks, [0, 1], hq, 2, d, max_blocks_per_range=16).to("cuda")
+        wsr = torch.zeros(max(16, plan.workspace_bytes), dtype=torch.uint8, device="cuda")
+        bs.split_decode_attention_local_ragged(pools, 0, q, bts, [0, 1], ksd, synth.default_scale(d),
+                                               plan, out, lse, wsr)
+        # tasks: the same problem cut over two launches (stand-ins for two GPUs), sys scope
+        mb = [t.shape[1] for t in bts]
+        wst = torch.zeros(max(256, bs.attention_problem_workspace_size(B, hq, 2, d, mb)),
+                          dtype=torch.uint8, device="cuda")
+        done = torch.zeros(1, dtype=torch.int32, device="cuda")
+        prob = {"q": q, "kv_split": ksd, "max_blocks": mb, "out": out, "lse": lse, "workspace": wst,
+                "done": done, "cross_device": True}
+        for j in range(2):
+            bs.split_decode_attention_tasks([prob], [(pools[j], bts[j], j, 0)], 0, B, hq,
+                                            synth.default_scale(d))
         # migration kernels
         dst = bs.KVPool(1, 64, 2, d)
         ids = torch.tensor([x for x in shards[1].block_tables.ravel() if x >= 0], dtype=torch.int32).cuda()

@@ -15,7 +15,12 @@
  *    the device memory it describes.
  *  - Host-visible arguments are validated (NULLs, ranges, alignment, supported shapes).
  *    Device arrays (block tables, ids, splits) are NOT validated: out-of-range ids are
- *    undefined behaviour, as for any CUDA kernel argument.
+ *    undefined behaviour, as for any CUDA kernel argument -- except in the debug build
+ *    (libbanaserve_debug.so, compiled with -DBS_DEBUG=1, loaded by the Python binding
+ *    when BS_DEBUG=1): there a validation kernel checks them on the device first, the
+ *    call synchronises its stream and, on a violation, returns BS_ERR_INVALID_ARG
+ *    without launching and ORs a code into bs_debug_error_code (1 block-table id out of
+ *    range, 2 kv_split inconsistent with the table width, 4 migration id out of range).
  *  - Supported shapes: bf16 KV, block_size 16, head_dim 64 or 128, query group
  *    G = num_q_heads / num_kv_heads in {1, 2, 4, 8}.  Others -> BS_ERR_UNSUPPORTED.
  */
@@ -49,6 +54,11 @@ enum { BS_DTYPE_BF16 = 0 };
 const char* bs_last_error(void);
 /* BS_ABI_VERSION of the loaded library. */
 int32_t bs_abi_version(void);
+/* 1 in the debug build (device-side validation of index arrays), 0 otherwise. */
+int32_t bs_debug_build(void);
+/* Codes of the debug checks that failed so far (OR of 1/2/4, see above); reset != 0
+ * clears them.  Always 0 in a release build. */
+int32_t bs_debug_error_code(int32_t reset);
 
 /* ------------------------------------------------------------------------------ */
 /* H0: paged KV pool + block allocator.                                             */

@@ -39,6 +39,7 @@ EXPORTED_SYMBOLS = (
     "bs_split_decode_attention_local", "bs_signal", "bs_wait_signal",
     "bs_attention_problem_workspace_size", "bs_split_decode_attention_tasks", "bs_wait_signals",
     "bs_signals", "bs_attention_ragged_plan", "bs_split_decode_attention_local_ragged",
+    "bs_debug_build", "bs_debug_error_code",
 )
 
 
@@ -59,7 +60,8 @@ _lib = None
 
 
 def lib_path() -> str:
-    return _build.LIB
+    """The library lib() loads: the debug build when BS_DEBUG=1."""
+    return _build.LIB_DEBUG if os.environ.get("BS_DEBUG") == "1" else _build.LIB
 
 
 def lib():
@@ -67,9 +69,10 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.LIB
+    debug = os.environ.get("BS_DEBUG") == "1"   # device-side index checks (debug build)
+    path = _build.LIB_DEBUG if debug else _build.LIB
     try:
-        path = _build.build()
+        path = _build.build(debug=debug)
     except Exception as e:  # no nvcc on this machine: use the shipped .so if present
         if not os.path.exists(path):
             raise ImportError(f"libbanaserve.so missing and cannot be built: {e}") from e
@@ -77,6 +80,8 @@ def lib():
     sig = {
         "bs_last_error": ([], ctypes.c_char_p),
         "bs_abi_version": ([], _i32),
+        "bs_debug_build": ([], _i32),
+        "bs_debug_error_code": ([_i32], _i32),
         "bs_kv_pool_bytes": ([ctypes.POINTER(_Desc)], _sz),
         "bs_kv_chunk_bytes": ([ctypes.POINTER(_Desc)], _sz),
         "bs_kv_pool_create": ([ctypes.POINTER(_Desc), _p, ctypes.POINTER(_p)], _i32),

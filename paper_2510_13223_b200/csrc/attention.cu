@@ -1207,6 +1207,10 @@ bs_status run_attention(const LaunchArgs& a) {
     P.ws_cnt = reinterpret_cast<int32_t*>(ws + pl.off_cnt);
   }
   cudaStream_t s = static_cast<cudaStream_t>(a.stream);
+  for (int j = 0; j < a.n_local; ++j)
+    BS_DEBUG_CHECK(bs::debug_check_table(a.kv_split, a.n_shards, a.shard_ids[j], a.batch, a.bts[j],
+                                         a.max_blocks[j], a.pools[j]->desc.num_blocks, s,
+                                         "attention block table / kv_split"));
   const bs::TMaps* tmp = have_maps ? &tm : nullptr;
   if (d == 128) return bs::launch_attn_d<128>(p, tmp, G, a.batch, s);
   return bs::launch_attn_d<64>(p, tmp, G, a.batch, s);
@@ -1499,6 +1503,13 @@ bs_status bs_split_decode_attention_tasks(int32_t n_problems, const bs_attn_prob
   p.model_head_lo = 0;
   p.grid_x = off;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int t = 0; t < n_tasks; ++t) {
+    const bs_attn_problem& pr = problems[tasks[t].problem];
+    BS_DEBUG_CHECK(bs::debug_check_table(pr.kv_split, pr.n_shards, tasks[t].shard_id, batch,
+                                         tasks[t].block_tables, pr.max_blocks[tasks[t].shard_id],
+                                         tasks[t].pool->desc.num_blocks, s,
+                                         "attention task block table / kv_split"));
+  }
   const bs::TMaps* tmp = have_maps ? &tm : nullptr;
   if (d == 128) return bs::launch_attn_d<128>(p, tmp, G, batch, s);
   return bs::launch_attn_d<64>(p, tmp, G, batch, s);

@@ -42,6 +42,24 @@ bs_status launch_copy_chunks(const uint8_t* src_base, const int32_t* src_ids, ui
                              int max_ctas = 0, int32_t n_layers = 1, int64_t src_layer_stride = 0,
                              int64_t dst_layer_stride = 0);
 
+#ifdef BS_DEBUG
+// debug build: validate device index arrays before a launch (debug.cu)
+bs_status debug_check_ids(const int32_t* ids, int32_t n, int32_t limit, cudaStream_t s,
+                          const char* what);
+bs_status debug_check_table(const int32_t* kv_split, int32_t n_shards, int32_t shard, int32_t batch,
+                            const int32_t* bt, int32_t max_blocks, int32_t num_blocks, cudaStream_t s,
+                            const char* what);
+#define BS_DEBUG_CHECK(expr)              \
+  do {                                    \
+    const bs_status _st = (expr);         \
+    if (_st != BS_OK) return _st;         \
+  } while (0)
+#else
+#define BS_DEBUG_CHECK(expr) \
+  do {                       \
+  } while (0)
+#endif
+
 }  // namespace bs
 
 #define BS_REQUIRE(cond, ...)                                          \

@@ -304,6 +304,10 @@ bs_status bs_kv_migrate_layer_ex(const bs_kv_pool* src, bs_kv_pool* dst, int32_t
   // a host-tier pool is behind PCIe / C2C: a few CTAs keep it saturated, the rest of the
   // SMs stay with the layer's compute (three-stage pipeline, Fig. 6)
   const int max_ctas = (src->host || dst->host) ? kHostCopyCtas : dev_copy_ctas();
+  BS_DEBUG_CHECK(bs::debug_check_ids(src_ids, n, src->desc.num_blocks, static_cast<cudaStream_t>(stream),
+                                     "bs_kv_migrate_layer src_ids"));
+  BS_DEBUG_CHECK(bs::debug_check_ids(dst_ids, n, dst->desc.num_blocks, static_cast<cudaStream_t>(stream),
+                                     "bs_kv_migrate_layer dst_ids"));
   return bs::launch_copy_chunks(src->base + (size_t)layer * src->layer_bytes, src_ids,
                                 dst->base + (size_t)layer * dst->layer_bytes, dst_ids, n,
                                 src->chunk_bytes, src->page_bytes, method,
@@ -320,6 +324,10 @@ bs_status bs_kv_migrate_layers(const bs_kv_pool* src, bs_kv_pool* dst, int32_t l
   BS_REQUIRE(n >= 0, "bs_kv_migrate_layers: n < 0");
   BS_REQUIRE(n == 0 || (src_ids && dst_ids), "bs_kv_migrate_layers: NULL ids");
   const int max_ctas = (src->host || dst->host) ? kHostCopyCtas : 0;
+  BS_DEBUG_CHECK(bs::debug_check_ids(src_ids, n, src->desc.num_blocks, static_cast<cudaStream_t>(stream),
+                                     "bs_kv_migrate_layers src_ids"));
+  BS_DEBUG_CHECK(bs::debug_check_ids(dst_ids, n, dst->desc.num_blocks, static_cast<cudaStream_t>(stream),
+                                     "bs_kv_migrate_layers dst_ids"));
   return bs::launch_copy_chunks(src->base + (size_t)layer_lo * src->layer_bytes, src_ids,
                                 dst->base + (size_t)layer_lo * dst->layer_bytes, dst_ids, n,
                                 src->chunk_bytes, src->page_bytes, BS_MIGRATE_VEC16,
@@ -403,6 +411,10 @@ bs_status bs_kv_migrate_heads_layer(const bs_kv_pool* src, bs_kv_pool* dst, int3
   BS_REQUIRE(n >= 0, "bs_kv_migrate_heads_layer: n < 0");
   if (n == 0) return BS_OK;
   BS_REQUIRE(src_ids && dst_ids, "bs_kv_migrate_heads_layer: NULL ids");
+  BS_DEBUG_CHECK(bs::debug_check_ids(src_ids, n, src->desc.num_blocks, static_cast<cudaStream_t>(stream),
+                                     "bs_kv_migrate_heads_layer src_ids"));
+  BS_DEBUG_CHECK(bs::debug_check_ids(dst_ids, n, dst->desc.num_blocks, static_cast<cudaStream_t>(stream),
+                                     "bs_kv_migrate_heads_layer dst_ids"));
   const int sms = bs::sm_count(bs::current_device());
   const int64_t total = (int64_t)n * 2 * n_heads;
   const int wpc = 8;
@@ -429,6 +441,8 @@ bs_status bs_kv_gather_layer(const bs_kv_pool* src, int32_t layer, const int32_t
   BS_REQUIRE(n >= 0, "bs_kv_gather_layer: n < 0");
   BS_REQUIRE(n == 0 || (ids && staging), "bs_kv_gather_layer: NULL ids/staging");
   BS_REQUIRE(((uintptr_t)staging & 15) == 0, "bs_kv_gather_layer: staging not 16-B aligned");
+  BS_DEBUG_CHECK(bs::debug_check_ids(ids, n, src->desc.num_blocks, static_cast<cudaStream_t>(stream),
+                                     "bs_kv_gather_layer ids"));
   return bs::launch_copy_chunks(src->base + (size_t)layer * src->layer_bytes, ids,
                                 static_cast<uint8_t*>(staging), nullptr, n, src->chunk_bytes,
                                 src->page_bytes, BS_MIGRATE_AUTO, static_cast<cudaStream_t>(stream),
@@ -442,6 +456,8 @@ bs_status bs_kv_scatter_layer(bs_kv_pool* dst, int32_t layer, const int32_t* ids
   BS_REQUIRE(n >= 0, "bs_kv_scatter_layer: n < 0");
   BS_REQUIRE(n == 0 || (ids && staging), "bs_kv_scatter_layer: NULL ids/staging");
   BS_REQUIRE(((uintptr_t)staging & 15) == 0, "bs_kv_scatter_layer: staging not 16-B aligned");
+  BS_DEBUG_CHECK(bs::debug_check_ids(ids, n, dst->desc.num_blocks, static_cast<cudaStream_t>(stream),
+                                     "bs_kv_scatter_layer ids"));
   return bs::launch_copy_chunks(static_cast<const uint8_t*>(staging), nullptr,
                                 dst->base + (size_t)layer * dst->layer_bytes, ids, n,
                                 dst->chunk_bytes, dst->page_bytes, BS_MIGRATE_AUTO,

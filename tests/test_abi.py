@@ -167,3 +167,17 @@ def test_split_k_workspace_plan():
     assert L.bs_split_decode_attention_workspace_size(h, 1, 32, 2048, ctypes.byref(sz)) == 0
     assert sz.value > 0 and (sz.value - 1 * 8 * 4) % (32 * (128 + 2) * 4) == 0
     L.bs_kv_pool_destroy(h)
+
+
+def test_debug_build_exports_the_same_abi():
+    """libbanaserve_debug.so (-DBS_DEBUG=1) exports every declared symbol and reports
+    itself as the debug build; the release library does not."""
+    from paper_2510_13223_b200 import build as b
+    path = b.build(debug=True)
+    dbg = ctypes.CDLL(path)
+    for name in header_functions():
+        assert hasattr(dbg, name), name
+    dbg.bs_debug_build.restype = ctypes.c_int32
+    assert dbg.bs_debug_build() == 1
+    assert bs.lib().bs_debug_build() == 0
+    assert bs.lib().bs_debug_error_code(0) == 0

@@ -57,6 +57,17 @@ def omp_threads() -> int:
     return len(os.sched_getaffinity(0))
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -490,8 +501,21 @@ def cpu_baseline(case, budget_s=12.0, reqs_per_sample=32, n_samples=4):
     t_attn = ta_tot / units * (BATCH / reqs_per_sample)
     t_mig = tm_tot / units * N_HANDOFF
     t_step = SHAPE.n_layers * (t_attn + t_mig)
+    # the same units on one thread (timings at 1 thread and all cores)
+    threads = oracle.get_threads()
+    oracle.set_threads(1)
+    t1a = t1m = 0.0
+    n1 = 2
+    for i in range(n1):
+        a, m = time_oracle_sample(samples[i % n_samples], scale)
+        t1a += a
+        t1m += m
+    oracle.set_threads(threads)
+    t_step1 = SHAPE.n_layers * (t1a / n1 * (BATCH / reqs_per_sample) + t1m / n1 * N_HANDOFF)
     return {"value": round(BATCH / t_step, 4), "unit": "tokens/s", "kind": "oracle",
             "cores": omp_threads(),
+            "value_1_thread": round(BATCH / t_step1, 4),
+            "nproc": os.cpu_count(), "cpu_model": cpu_model(),
             "sample": (f"{units} timed (layer, {reqs_per_sample}-request) units from {n_samples} "
                        f"extracted samples (both shards + LSE merge) + 1 hand-off request's "
                        f"chunks each, fp64 C oracle; extrapolated linearly to B={BATCH}, "

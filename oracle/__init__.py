@@ -46,6 +46,10 @@ def lib():
     global _lib
     if _lib is None:
         L = ctypes.CDLL(build())
+        L.or_set_threads.argtypes = [_i32]
+        L.or_set_threads.restype = None
+        L.or_get_threads.argtypes = []
+        L.or_get_threads.restype = _i32
         L.or_bf16_to_f64.argtypes = [ctypes.c_uint16]
         L.or_bf16_to_f64.restype = _f64
         L.or_kv_bytes_per_token_layer.argtypes = [_i32, _i32, _i32]
@@ -259,3 +263,12 @@ def attention_full(pools, block_tables, layer, q, kv_split, scale):
     parts = [attention_shard(p, layer, q, bt, kv_split, j, scale)
              for j, (p, bt) in enumerate(zip(pools, block_tables))]
     return merge_partials([x[0] for x in parts], [x[1] for x in parts], [x[2] for x in parts])
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads of the oracle's loops (for timing reports: 1 thread vs all cores)."""
+    lib().or_set_threads(int(n))
+
+
+def get_threads() -> int:
+    return int(lib().or_get_threads())

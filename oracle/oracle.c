@@ -35,9 +35,14 @@
  * Build: gcc -O2 -fopenmp -shared -fPIC oracle/oracle.c -o oracle/liboracle.so -lm
  */
 #include <math.h>
+#include <omp.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+
+/* Thread count of the OpenMP loops (timing reports only: 1 thread vs all cores). */
+void or_set_threads(int32_t n) { omp_set_num_threads(n > 0 ? n : 1); }
+int32_t or_get_threads(void) { return omp_get_max_threads(); }
 
 /* ------------------------------------------------------------------------- */
 /* Scalars                                                                    */

@@ -24,11 +24,11 @@ import paper_2510_13223_b200 as bs  # noqa: E402
 import synth  # noqa: E402
 
 
-def attn_case(name, shape, lens, iters=20, warm=5):
+def attn_case(name, shape, lens, iters=20, warm=5, seed=1):
     dev = torch.device("cuda")
     lens = np.asarray(lens, dtype=np.int64)
     ks = np.stack([np.zeros_like(lens), lens], 1).astype(np.int32)
-    case = synth.device_shards(shape, lens, ks, seed=1, device=dev, layers=1)
+    case = synth.device_shards(shape, lens, ks, seed=seed, device=dev, layers=1)
     pt, bt = case.pools[0], case.block_tables[0]
     pool = bs.KVPool(1, pt.shape[1], shape.hkv, shape.d, base=pt.reshape(-1))
     B = len(lens)
@@ -274,13 +274,26 @@ def main():
     ap.add_argument("--json")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--diag", action="store_true", help="group-size / kv-head diagnostics")
+    ap.add_argument("--seeds", type=int, default=1,
+                    help="repeat every attention case over seeds 0..n-1 (block placement and "
+                         "values; C4 also its lengths) and report mean / spread")
     args = ap.parse_args()
     res = []
     if args.only in (None, "attn"):
         for name, (shape, lens) in (DIAG if args.diag else ATTN).items():
             if args.case and args.case != name:
                 continue
-            r = attn_case(name, shape, lens, iters=args.iters)
+            if args.seeds <= 1:
+                r = attn_case(name, shape, lens, iters=args.iters)
+            else:
+                runs = []
+                for sd in range(args.seeds):
+                    ln = (synth.mixed_lengths(256, seed=sd) // 8) if name.startswith("C4") else lens
+                    runs.append(attn_case(name, shape, ln, iters=args.iters, seed=sd))
+                g = [x["GBps"] for x in runs]
+                r = {"case": name, "seeds": args.seeds, "GBps_mean": round(float(np.mean(g)), 1),
+                     "GBps_min": min(g), "GBps_max": max(g),
+                     "us_mean": round(float(np.mean([x["us"] for x in runs])), 2)}
             print(json.dumps(r), flush=True)
             res.append(r)
     if args.only in (None, "mig"):

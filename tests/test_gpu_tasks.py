@@ -130,3 +130,34 @@ def test_tasks_argument_errors(bs):
     bad = dict(d0, workspace=None, workspace_bytes=0)
     with pytest.raises(bs.BSError):   # a 2-shard problem needs its workspace
         bs.split_decode_attention_tasks([bad], [(A.pools[0], A.bts[0], 0, 0)], 0, 2, 4, 0.125)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_tasks_fuzz(bs, seed):
+    """Random shapes, lengths (incl. empty), unaligned splits, 1-4 shards per problem and a
+    random assignment of the shards of two problems to 1-3 concurrent launches."""
+    rng = np.random.default_rng(100 + seed)
+    G = int(rng.choice([1, 2, 4, 8]))
+    d = int(rng.choice([64, 128]))
+    n_shards = int(rng.integers(1, 5))
+    B = int(rng.integers(1, 9))
+    shape = synth.Shape(1, 2 * G, 2, d)
+    lens_a = tuple(int(x) for x in rng.integers(0, 1500, B))
+    lens_b = tuple(int(x) for x in rng.integers(0, 1500, B))
+    A = Problem(bs, shape, lens_a, n_shards, seed=seed, cross_device=bool(seed % 2))
+    Bp = Problem(bs, shape, lens_b, n_shards, seed=seed + 50, cross_device=bool(seed % 2))
+    n_launch = int(rng.integers(1, 4))
+    owner = [(int(rng.integers(0, n_launch)), int(rng.integers(0, n_launch))) for _ in range(n_shards)]
+    sc = synth.default_scale(d)
+    streams = [torch.cuda.Stream() for _ in range(n_launch)]
+    torch.cuda.synchronize()
+    for li, st in enumerate(streams):
+        tasks = [(A.pools[j], A.bts[j], j, 0) for j in range(n_shards) if owner[j][0] == li]
+        tasks += [(Bp.pools[j], Bp.bts[j], j, 1) for j in range(n_shards) if owner[j][1] == li]
+        if tasks:
+            bs.split_decode_attention_tasks([A.desc(0), Bp.desc(0)], tasks, 0, B, shape.hq, sc,
+                                            stream=st)
+    torch.cuda.synchronize()
+    for P in (A, Bp):
+        assert P.done[0].item() == B * shape.hkv
+        P.check(0)

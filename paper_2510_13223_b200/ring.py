@@ -275,6 +275,18 @@ class ShardedDecodeStep:
         self.home, self.home_bt = home_pool, home_bt
         self.cold, self.cold_bt = cold_pool, cold_bt
         self.kv_split = kv_split
+        # the cold pool holds shard 1 of prev's requests: index them with prev's split
+        self.kv_split_cold = kv_split
+        if world > 1:
+            host = kv_split.cpu().numpy() if isinstance(kv_split, torch.Tensor) else kv_split
+            everyone = [None] * world
+            dist.all_gather_object(everyone, host.tolist(), group=pg_attn)
+            if isinstance(kv_split, torch.Tensor):
+                self.kv_split_cold = torch.tensor(everyone[(rank - 1) % world], dtype=kv_split.dtype,
+                                                  device=kv_split.device)
+            else:
+                import numpy as np
+                self.kv_split_cold = np.asarray(everyone[(rank - 1) % world], dtype=host.dtype)
         self.L, self.hq, self.d = num_layers, num_q_heads, head_dim
         self.B = kv_split.shape[0]
         self.src_ids, self.dst_ids = handoff_src_ids, handoff_dst_ids
@@ -448,7 +460,7 @@ class ShardedDecodeStep:
                 if self.world > 1:
                     ex.wait(ex.compute, E["q_ready"][layer])
                 qc = q[layer] if self.world == 1 else self.q_prev[layer]
-                ops.attention(self.cold, layer, qc, self.cold_bt, self.kv_split, 1,
+                ops.attention(self.cold, layer, qc, self.cold_bt, self.kv_split_cold, 1,
                               self.part_cold[layer])
                 if timers is not None:
                     timers[layer][1].record(ex.compute)
@@ -530,7 +542,7 @@ class ShardedDecodeStep:
                 mine = {"q": q[layer], "kv_split": self.kv_split, "max_blocks": self.mb_mine,
                         "out": F["out"][layer], "lse": F["lse"][layer], "workspace": F["ws"][layer],
                         "done": F["done"][layer:layer + 1], "cross_device": True}
-                theirs = {"q": self.q_prev[layer], "kv_split": self.kv_split,
+                theirs = {"q": self.q_prev[layer], "kv_split": self.kv_split_cold,
                           "max_blocks": self.mb_prev, "out": lk.prev_out + layer * ob,
                           "lse": lk.prev_lse + layer * lb,
                           "workspace": lk.prev_ws + layer * lk.prev_ws_stride,
@@ -598,7 +610,7 @@ class ShardedDecodeStep:
                 ops.attention(self.home, layer, q[layer], self.home_bt, self.kv_split, 0,
                               self.part_own[layer])
                 wait_signal(lk.my_flag("q", layer), e, to, err)    # prev's q arrived
-                ops.attention(self.cold, layer, self.q_prev[layer], self.cold_bt, self.kv_split,
+                ops.attention(self.cold, layer, self.q_prev[layer], self.cold_bt, self.kv_split_cold,
                               1, self.part_cold[layer])
                 signal(lk.flag(lk.prev_flags, "q_ack", layer), e)
                 if timers is not None:

@@ -22,6 +22,12 @@ LENS = (37, 64, 100)
 N_HANDOFF_BLOCKS = 5
 
 
+def lens_of(rank):
+    """Every rank has the same batch size but its own lengths (so its own split points:
+    the cold instance must index its predecessor's requests with the predecessor's split)."""
+    return tuple(n + 17 * rank for n in LENS)
+
+
 class NpPool:
     def __init__(self, arr):
         self.data = arr  # uint16 [L][NB][2][Hkv][16][d]
@@ -77,11 +83,12 @@ def handoff_bytes(owner_seed):
 
 def rank_setup(rank, world):
     prev, nxt = (rank - 1) % world, (rank + 1) % world
-    ks = synth.block_aligned_split(LENS, 2)
-    own = synth.gen_dense(SHAPE, LENS, seed=rank)
-    prv = synth.gen_dense(SHAPE, LENS, seed=prev)
+    ks = synth.block_aligned_split(lens_of(rank), 2)
+    ks_prev = synth.block_aligned_split(lens_of(prev), 2)
+    own = synth.gen_dense(SHAPE, lens_of(rank), seed=rank)
+    prv = synth.gen_dense(SHAPE, lens_of(prev), seed=prev)
     home = synth.place_shards(own, ks, seed=rank, spare_blocks=N_HANDOFF_BLOCKS + 2)[0]
-    cold = synth.place_shards(prv, ks, seed=prev, spare_blocks=N_HANDOFF_BLOCKS + 2)[1]
+    cold = synth.place_shards(prv, ks_prev, seed=prev, spare_blocks=N_HANDOFF_BLOCKS + 2)[1]
     free_home = [i for i in range(home.pool.shape[1]) if not home.used[i]][:N_HANDOFF_BLOCKS]
     free_cold = [i for i in range(cold.pool.shape[1]) if not cold.used[i]][:N_HANDOFF_BLOCKS]
     cold.pool[:, free_cold] = handoff_bytes(rank)       # what I hand off to prev

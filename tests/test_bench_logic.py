@@ -65,3 +65,19 @@ def test_step_stats():
     assert s["median"] == 2.5 and s["min"] == 1.0 and s["max"] == 4.0 and s["mean"] == 2.5
     assert abs(s["ci95"] - 1.96 * (5 / 3) ** 0.5 / 2) < 1e-4 and s["n"] == 4
     assert bench.step_stats([]) is None
+
+
+def test_clock_summary_keeps_samples_under_load(tmp_path):
+    c = bench.ClockSampler(0)
+
+    class _P:
+        pass
+    c.proc = _P()
+    f = open(tmp_path / "c.csv", "w+")
+    f.write("345, 1965, Not Active, Not Active, Not Active, Not Active, 0\n"       # idle
+            "1965, 1965, Not Active, Not Active, Not Active, Active, 100\n"
+            "1950, 1965, Not Active, Not Active, Not Active, Not Active, 98\n")
+    f.flush()
+    c.f = f
+    s = c.summary()
+    assert s["sm_mhz"] == 1957.5 and s["samples"] == 2 and s["reasons"] == ["sw_power_cap"]

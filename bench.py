@@ -91,7 +91,8 @@ def ncu_traffic():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 20 ms during the timed region
+    (samples with < 50 % utilisation -- before the region starts -- are dropped)."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap,utilization.gpu")
@@ -105,11 +106,11 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.f,
+                 "--format=csv,noheader,nounits", "-lms", "20"], stdout=self.f,
                 stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.proc = None
-        time.sleep(0.3)
+        time.sleep(1.0)   # nvidia-smi is sampling before the timed region starts
         return self
 
     def __exit__(self, *exc):

@@ -207,7 +207,9 @@ bs_status bs_split_decode_attention_local(int32_t n_local, const bs_kv_pool* con
  * *max_parts: most ranges of one request (<= 64); *workspace_bytes: scratch for
  * bs_split_decode_attention_local_ragged (0 if no request has > 1 range).
  * Results are identical in value to the uniform path (same formulas); the summation
- * order of the merge follows the plan's ranges (shard-major, then range). */
+ * order of the merge follows the plan's slots (shard-major, then range).  Items are
+ * listed longest range first (stable; the CTA dispatch order), so a request's items need
+ * not be adjacent; environment BS_RAGGED_ORDER=0 keeps request order. */
 bs_status bs_attention_ragged_plan(int32_t batch, int32_t n_shards, const int32_t* kv_split_host,
                                    int32_t n_local, const int32_t* shard_ids, int32_t num_q_heads,
                                    int32_t num_kv_heads, int32_t head_dim,

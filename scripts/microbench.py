@@ -60,6 +60,61 @@ def attn_case(name, shape, lens, iters=20, warm=5, seed=1):
             "ws": ws.numel() > 16}
 
 
+L2_BYTES = 126 * 2**20
+
+
+def attn_case_graph(name, shape, lens, iters=40, seed=1):
+    """Device time of back-to-back launches without host overhead: ``iters`` launches are
+    captured into one CUDA graph (per-launch time = replay time / iters), cycling over
+    enough layers that the KV they read (>= 3x L2) cannot be served from L2.  Small
+    problems (C3 B=1: 33 MB) are host-launch-bound under per-call event timing; this is
+    the kernel's own latency as a graph-captured decode step would see it."""
+    dev = torch.device("cuda")
+    lens = np.asarray(lens, dtype=np.int64)
+    ks = np.stack([np.zeros_like(lens), lens], 1).astype(np.int32)
+    kv = int(lens.sum()) * 2 * shape.hkv * shape.d * 2
+    nl = int(min(32, max(1, -(-3 * L2_BYTES // max(kv, 1)))))
+    case = synth.device_shards(shape, lens, ks, seed=seed, device=dev, layers=nl)
+    pt, bt = case.pools[0], case.block_tables[0]
+    pool = bs.KVPool(nl, pt.shape[1], shape.hkv, shape.d, base=pt.reshape(-1))
+    B = len(lens)
+    btd = torch.from_numpy(bt).to(dev)
+    ksd = torch.from_numpy(ks).to(dev)
+    o = torch.empty(B, shape.hq, shape.d, device=dev)
+    m = torch.empty(B, shape.hq, device=dev)
+    l = torch.empty(B, shape.hq, device=dev)
+    ws = torch.zeros(max(16, bs.split_decode_attention_workspace_size(pool, B, shape.hq, bt.shape[1])),
+                     dtype=torch.uint8, device=dev)
+    sc = synth.default_scale(shape.d)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for x in range(nl):  # warm (also configures the kernel attributes outside capture)
+            bs.split_decode_attention(pool, x, case.q[x], btd, ksd, 0, sc, o, m, l, ws, stream=s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for i in range(iters):
+            x = i % nl
+            bs.split_decode_attention(pool, x, case.q[x], btd, ksd, 0, sc, o, m, l, ws, stream=s)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(10):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) / iters)
+    med = sorted(ts)[len(ts) // 2]
+    alg = kv + B * shape.hq * shape.d * 2 + B * shape.hq * (shape.d + 2) * 4 + 4 * int(
+        sum(synth.ceil_div(int(x), 16) for x in lens))
+    return {"case": name, "timing": "graph", "B": B, "G": shape.group, "tokens": int(lens.sum()),
+            "layers_cycled": nl, "us": round(med * 1e3, 2),
+            "GBps": round(alg / (med * 1e-3) / 1e9, 1), "bytes": alg}
+
+
 def mig_case(name, shape, n_pairs, method, iters=20, warm=5):
     dev = torch.device("cuda")
     nb = n_pairs + 64
@@ -215,15 +270,22 @@ def ragged_cases(iters=20, warm=5):
         lse = torch.empty(B, shape.hq, device=dev)
         wsu = torch.zeros(max(16, bs.split_decode_attention_local_workspace_size(
             [pool], [bts[0].shape[1]], B, shape.hq)), dtype=torch.uint8, device=dev)
-        plan = bs.attention_ragged_plan(ks, [0], shape.hq, shape.hkv, shape.d).to(dev)
-        wsr = torch.zeros(max(16, plan.workspace_bytes), dtype=torch.uint8, device=dev)
+        plans = {}
+        for kind, bps, order in (("ragged", 0, "1"), ("ragged_reqorder", 0, "0"),
+                                 ("ragged_bps64", 64, "1"), ("ragged_bps32", 32, "1")):
+            os.environ["BS_RAGGED_ORDER"] = order
+            pl = bs.attention_ragged_plan(ks, [0], shape.hq, shape.hkv, shape.d,
+                                          max_blocks_per_range=bps).to(dev)
+            plans[kind] = (pl, torch.zeros(max(16, pl.workspace_bytes), dtype=torch.uint8, device=dev))
+        os.environ.pop("BS_RAGGED_ORDER")
         alg = int(lens.sum()) * 2 * shape.hkv * shape.d * 2 + B * shape.hq * shape.d * 2 + \
             B * shape.hq * (shape.d * 2 + 4) + 4 * int(sum(synth.ceil_div(int(x), 16) for x in lens))
-        fns = {"uniform": lambda: bs.split_decode_attention_local([pool], 0, case.q[0], bts, [0], ksd,
-                                                                  sc, o, lse, wsu),
-               "ragged": lambda: bs.split_decode_attention_local_ragged([pool], 0, case.q[0], bts,
-                                                                        [0], ksd, sc, plan, o, lse, wsr)}
-        for kind, fn in fns.items():
+        fns = {"uniform": (None, lambda: bs.split_decode_attention_local([pool], 0, case.q[0], bts, [0],
+                                                                         ksd, sc, o, lse, wsu))}
+        for kind, (pl, wsr) in plans.items():
+            fns[kind] = (pl, lambda pl=pl, wsr=wsr: bs.split_decode_attention_local_ragged(
+                [pool], 0, case.q[0], bts, [0], ksd, sc, pl, o, lse, wsr))
+        for kind, (plan, fn) in fns.items():
             for _ in range(warm):
                 fn()
             torch.cuda.synchronize()
@@ -238,8 +300,8 @@ def ragged_cases(iters=20, warm=5):
             med = t[len(t) // 2]
             r = {"case": f"{name}_{kind}", "B": B, "G": shape.group, "tokens": int(lens.sum()),
                  "us": round(med * 1e3, 2), "GBps": round(alg / (med * 1e-3) / 1e9, 1), "bytes": alg,
-                 "items": plan.n_work if kind == "ragged" else None,
-                 "max_parts": plan.max_parts if kind == "ragged" else None}
+                 "items": plan.n_work if plan is not None else None,
+                 "max_parts": plan.max_parts if plan is not None else None}
             print(json.dumps(r), flush=True)
             out.append(r)
         del case, pool
@@ -274,6 +336,8 @@ def main():
     ap.add_argument("--json")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--diag", action="store_true", help="group-size / kv-head diagnostics")
+    ap.add_argument("--graph", action="store_true",
+                    help="attention: time graph-captured back-to-back launches over >= 3x L2 of KV")
     ap.add_argument("--seeds", type=int, default=1,
                     help="repeat every attention case over seeds 0..n-1 (block placement and "
                          "values; C4 also its lengths) and report mean / spread")
@@ -283,7 +347,9 @@ def main():
         for name, (shape, lens) in (DIAG if args.diag else ATTN).items():
             if args.case and args.case != name:
                 continue
-            if args.seeds <= 1:
+            if args.graph:
+                r = attn_case_graph(name, shape, lens)
+            elif args.seeds <= 1:
                 r = attn_case(name, shape, lens, iters=args.iters)
             else:
                 runs = []

@@ -24,8 +24,12 @@ def check_plan(plan, ks, shard_ids, bps, hq, hkv, d):
         nb, parts = nbp >> 8, nbp & 0xFF
         seen.setdefault(int(b), []).append((int(t), int(slot), int(blo), int(nb), int(parts)))
     assert sorted(seen) == list(range(B))
+    # dispatch order: longest range first
+    nbs = [int(x) >> 8 for x in w[:, 3]]
+    assert nbs == sorted(nbs, reverse=True)
     most = 1
     for b, items in seen.items():
+        items.sort(key=lambda x: x[1])  # by slot
         nblk = [-(-max(int(ks[b, j + 1] - ks[b, j]), 0) // 16) for j in shard_ids]
         parts = {p for *_, p in items}
         assert len(parts) == 1

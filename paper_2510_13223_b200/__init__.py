@@ -61,7 +61,9 @@ _lib = None
 
 def lib_path() -> str:
     """The library lib() loads: the debug build when BS_DEBUG=1."""
-    return _build.LIB_DEBUG if os.environ.get("BS_DEBUG") == "1" else _build.LIB
+    if os.environ.get("BS_DEBUG") == "1":
+        return _build.LIB_DEBUG
+    return _build.LIB_TIMELINE if os.environ.get("BS_TIMELINE") == "1" else _build.LIB
 
 
 def lib():
@@ -70,9 +72,10 @@ def lib():
     if _lib is not None:
         return _lib
     debug = os.environ.get("BS_DEBUG") == "1"   # device-side index checks (debug build)
-    path = _build.LIB_DEBUG if debug else _build.LIB
+    timeline = not debug and os.environ.get("BS_TIMELINE") == "1"  # kernel timeline stamps
+    path = _build.LIB_DEBUG if debug else (_build.LIB_TIMELINE if timeline else _build.LIB)
     try:
-        path = _build.build(debug=debug)
+        path = _build.build(debug=debug, timeline=timeline)
     except Exception as e:  # no nvcc on this machine: use the shipped .so if present
         if not os.path.exists(path):
             raise ImportError(f"libbanaserve.so missing and cannot be built: {e}") from e

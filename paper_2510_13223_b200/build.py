@@ -22,6 +22,9 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build", "banaserve")
 LIB = os.path.join(PKG, "libbanaserve.so")
 LIB_DEBUG = os.path.join(PKG, "libbanaserve_debug.so")   # -DBS_DEBUG=1 (device-side checks)
+# -DBS_TIMELINE=1: per-CTA %globaltimer stamps in the attention kernel (diagnostics only,
+# scripts/attn_timeline.py; never built by __graft_entry__.build())
+LIB_TIMELINE = os.path.join(PKG, "libbanaserve_timeline.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
@@ -58,9 +61,10 @@ def _deps_mtime() -> float:
     return max(os.path.getmtime(f) for f in files)
 
 
-def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
-    lib_path = LIB_DEBUG if debug else LIB
-    build_dir = BUILD + ("_debug" if debug else "")
+def build(force: bool = False, verbose: bool = False, debug: bool = False,
+          timeline: bool = False) -> str:
+    lib_path = LIB_DEBUG if debug else (LIB_TIMELINE if timeline else LIB)
+    build_dir = BUILD + ("_debug" if debug else ("_timeline" if timeline else ""))
     if not force and os.path.exists(lib_path) and os.path.getmtime(lib_path) >= _deps_mtime():
         return lib_path
     os.makedirs(build_dir, exist_ok=True)
@@ -68,6 +72,8 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False) -> st
     extra = ["-Xptxas", "-v"] if verbose else []
     if debug:
         extra += ["-DBS_DEBUG=1"]
+    if timeline:
+        extra += ["-DBS_TIMELINE=1"]
 
     def compile_one(src):
         obj = os.path.join(build_dir, os.path.basename(src) + ".o")

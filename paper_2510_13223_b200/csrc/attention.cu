@@ -46,6 +46,28 @@ constexpr int kMaxSplit = 64;   // intra-GPU split-K limit
 
 constexpr int kMaxLocal = 8;  // shards (tasks) / problems of one launch
 
+#ifdef BS_TIMELINE
+// Diagnostics build only: per-CTA %globaltimer stamps (ns) of the tensor-core kernel --
+// [0] entry, [1] first K/V stage landed (warp 0), [2] all warps' loops done, [3] arrival
+// counter resolved, [4] exit, [5] smid | last-arriver << 16.  Read by bs_timeline_read.
+constexpr int kTlCtas = 16384;
+__device__ unsigned long long g_timeline[kTlCtas][6];
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define BS_TL(k)                                                                              \
+  do {                                                                                        \
+    const unsigned _lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);     \
+    if (threadIdx.x == 0 && _lin < kTlCtas) g_timeline[_lin][k] = tl_now();                  \
+  } while (0)
+#else
+#define BS_TL(k) \
+  do {           \
+  } while (0)
+#endif
+
 // One attention problem: a set of requests whose KV is split into shards, some of which
 // may be processed by other launches (on other GPUs).  All ranges of a (request, kv-head)
 // arrive on one counter; the last arriver merges.  Every pointer may be a peer mapping.
@@ -282,6 +304,7 @@ __device__ __forceinline__ void cta_combine_and_store(const ProbDesc P, int hq, 
     s_flag[0] = last;
   }
   __syncthreads();
+  BS_TL(3);
   if (!s_flag[0]) return;
   // per-head weights w_j = l_j 2^(m_j - M) / L: one warp per head, lanes over the ranges
   // (<= kMaxSplit = 64 -> 2 per lane); butterfly reductions keep the result deterministic
@@ -697,6 +720,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
   static_assert(G <= 8, "one n8 tile of heads");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  BS_TL(0);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int gq = lane >> 2, tq = lane & 3;  // mma groupID / thread-in-group
@@ -794,6 +818,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
     const int s = k % STAGES;
     ptx::mbar_wait(&bars[s], (uint32_t)((k / STAGES) & 1));
     __syncwarp();
+    if (k == 0 && warp == 0) BS_TL(1);
     const int blk = blo + warp + k * kWarps;
     const int nvalid = min(16, len - blk * 16);
     const uint32_t st = ring_u32 + s * S::kStage;
@@ -878,6 +903,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
     l_run[j] = x;
   }
   __syncthreads();  // rings idle: reuse them for the combine
+  BS_TL(2);
   float* s_acc = reinterpret_cast<float*>(smem);  // [kWarps][G][D]
   float* s_ml = reinterpret_cast<float*>(smem + S::kMlOff);
   float* s_w = reinterpret_cast<float*>(smem + S::kWOff);
@@ -900,6 +926,16 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
   __syncthreads();
   cta_combine_and_store<D, G>(P, p.hq, p.hkv, b, g, gm, cw.slot, nparts, s_acc, s_ml, s_w,
                               s_flag);
+#ifdef BS_TIMELINE
+  BS_TL(4);
+  {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const unsigned lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    if (threadIdx.x == 0 && lin < kTlCtas)
+      g_timeline[lin][5] = smid | ((unsigned long long)(nparts == 1 || s_flag[0]) << 16);
+  }
+#endif
 }
 
 // Pipeline depth / residency per (head_dim, group): STAGES blocks (K+V pages) per warp in
@@ -1280,6 +1316,20 @@ bs_status workspace_impl(int n_local, const bs_kv_pool* const* pools, const int3
 }  // namespace
 
 extern "C" {
+
+#ifdef BS_TIMELINE
+// Diagnostics build only (not declared in include/banaserve.h): copy / clear the stamps.
+bs_status bs_timeline_read(void* host, size_t bytes) {
+  const size_t n = std::min(bytes, sizeof(bs::g_timeline));
+  const cudaError_t e = cudaMemcpyFromSymbol(host, bs::g_timeline, n);
+  return e == cudaSuccess ? BS_OK : bs::set_error(BS_ERR_CUDA, "timeline: %s", cudaGetErrorString(e));
+}
+bs_status bs_timeline_reset(void) {
+  static unsigned long long zeros[bs::kTlCtas][6];
+  const cudaError_t e = cudaMemcpyToSymbol(bs::g_timeline, zeros, sizeof(zeros));
+  return e == cudaSuccess ? BS_OK : bs::set_error(BS_ERR_CUDA, "timeline: %s", cudaGetErrorString(e));
+}
+#endif
 
 bs_status bs_split_decode_attention_workspace_size(const bs_kv_pool* pool, int32_t batch,
                                                    int32_t num_q_heads, int32_t max_blocks,

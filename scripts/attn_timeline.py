@@ -1,0 +1,114 @@
+#!/usr/bin/env python
+"""Per-CTA timeline of one attention launch (diagnostics; needs the BS_TIMELINE build).
+
+    BS_TIMELINE=1 python scripts/attn_timeline.py [--case C3_gqa4_B1_8192] [--json out.json]
+
+The timeline build (`build(timeline=True)`, libbanaserve_timeline.so) stamps %globaltimer
+in every CTA of the tensor-core kernel: entry, first K/V stage landed (warp 0), all loops
+done, arrival counter resolved, exit.  L2 is flushed (256 MiB write) before the timed
+launch, so every K/V byte comes from HBM.  Output: quantiles (us, relative to the first
+CTA's entry) of each stamp and of the phases between them, split by last-arriver.
+"""
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+os.environ["BS_TIMELINE"] = "1"
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "scripts"))
+
+import paper_2510_13223_b200 as bs  # noqa: E402
+import synth  # noqa: E402
+from microbench import ATTN  # noqa: E402
+
+KT = 16384
+
+
+def q(x, ps=(0, 10, 50, 90, 100)):
+    x = np.asarray(x, dtype=np.float64)
+    return {f"p{p}": round(float(np.percentile(x, p)), 2) for p in ps} if len(x) else {}
+
+
+def run(name, reps=5):
+    shape, lens = ATTN[name]
+    dev = torch.device("cuda")
+    lens = np.asarray(lens, dtype=np.int64)
+    ks = np.stack([np.zeros_like(lens), lens], 1).astype(np.int32)
+    case = synth.device_shards(shape, lens, ks, seed=1, device=dev, layers=1)
+    pt, bt = case.pools[0], case.block_tables[0]
+    pool = bs.KVPool(1, pt.shape[1], shape.hkv, shape.d, base=pt.reshape(-1))
+    B = len(lens)
+    btd = torch.from_numpy(bt).to(dev)
+    ksd = torch.from_numpy(ks).to(dev)
+    o = torch.empty(B, shape.hq, shape.d, device=dev)
+    m = torch.empty(B, shape.hq, device=dev)
+    l = torch.empty(B, shape.hq, device=dev)
+    ws = torch.zeros(max(16, bs.split_decode_attention_workspace_size(pool, B, shape.hq, bt.shape[1])),
+                     dtype=torch.uint8, device=dev)
+    sc = synth.default_scale(shape.d)
+    flush = torch.empty(256 * 2**20, dtype=torch.uint8, device=dev)
+    L = bs.lib()
+    L.bs_timeline_read.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+    L.bs_timeline_read.restype = ctypes.c_int32
+    out = []
+    for _ in range(reps):
+        bs.split_decode_attention(pool, 0, case.q[0], btd, ksd, 0, sc, o, m, l, ws)
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        assert L.bs_timeline_reset() == 0
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        bs.split_decode_attention(pool, 0, case.q[0], btd, ksd, 0, sc, o, m, l, ws)
+        b.record()
+        torch.cuda.synchronize()
+        buf = np.zeros((KT, 6), dtype=np.uint64)
+        assert L.bs_timeline_read(buf.ctypes.data, buf.nbytes) == 0
+        out.append((a.elapsed_time(b) * 1e3, buf))
+    ev_us, buf = sorted(out, key=lambda x: x[0])[len(out) // 2]
+    nz = buf[:, 4] > 0
+    t = buf[nz].astype(np.int64)
+    t0 = t[:, 0].min()
+    rel = (t[:, :5] - t0) / 1e3
+    last = ((t[:, 5] >> 16) & 1).astype(bool)
+    has3 = t[:, 3] > 0     # CTAs that took part in a split-K arrival
+    has1 = t[:, 1] > 0
+    res = {
+        "case": name, "ctas": int(nz.sum()), "event_us": round(ev_us, 2),
+        "span_us": round(float(rel[:, 4].max()), 2),
+        "entry": q(rel[:, 0]),
+        "first_data_after_entry": q((rel[:, 1] - rel[:, 0])[has1]),
+        "loop_done_after_entry": q(rel[:, 2] - rel[:, 0]),
+        "loop_done": q(rel[:, 2]),
+        "arrival_after_loop": q((rel[:, 3] - rel[:, 2])[has3]),
+        "merge_last_arriver": q((rel[:, 4] - rel[:, 3])[last & has3]),
+        "epilogue_single_range": q((rel[:, 4] - rel[:, 2])[~has3]),
+        "exit_last_arriver": q(rel[last, 4]),
+        "exit_others": q(rel[~last, 4]),
+        "sms_used": int(len(np.unique(t[:, 5] & 0xFFFF))),
+    }
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--case", action="append")
+    ap.add_argument("--json")
+    args = ap.parse_args()
+    res = []
+    for c in args.case or ["C3_gqa4_B1_8192", "C3_gqa4_B8_8192", "C2_mha_B64_2048"]:
+        r = run(c)
+        print(json.dumps(r), flush=True)
+        res.append(r)
+    if args.json:
+        with open(args.json, "w") as f:
+            json.dump(res, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

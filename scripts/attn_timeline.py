@@ -92,6 +92,12 @@ def run(name, reps=5):
         "exit_others": q(rel[~last, 4]),
         "sms_used": int(len(np.unique(t[:, 5] & 0xFFFF))),
     }
+    # per-SM load: loop duration grouped by how many CTAs of the launch ran on the same SM
+    sm = (t[:, 5] & 0xFFFF).astype(np.int64)
+    per_sm = np.bincount(sm, minlength=int(sm.max()) + 1)[sm]
+    loop = rel[:, 2] - rel[:, 0]
+    res["loop_by_ctas_on_sm"] = {int(c): dict(n=int((per_sm == c).sum()), **q(loop[per_sm == c]))
+                                 for c in np.unique(per_sm)}
     return res
 
 

@@ -66,6 +66,21 @@ def main():
         for j in range(2):
             bs.split_decode_attention_tasks([prob], [(pools[j], bts[j], j, 0)], 0, B, hq,
                                             synth.default_scale(d))
+        # one long request: intra-GPU split-K over up to 64 ranges (the merge's unrolled
+        # 16-deep loads plus remainder, and its cross-thread-group reduction for G*D < 512)
+        lg = synth.gen_dense(shape, (8192,), seed=4)
+        kl = np.array([[0, 8192]], dtype=np.int32)
+        sl = synth.place_shards(lg, kl, seed=5)[0]
+        pl_ = bs.KVPool(1, sl.pool.shape[1], 2, d)
+        pl_.data.copy_(dev_bf16(sl.pool))
+        btl = torch.from_numpy(sl.block_tables).cuda()
+        o = torch.empty(1, hq, d, device="cuda")
+        m = torch.empty(1, hq, device="cuda")
+        l = torch.empty(1, hq, device="cuda")
+        wsl = torch.zeros(max(16, bs.split_decode_attention_workspace_size(pl_, 1, hq, btl.shape[1])),
+                          dtype=torch.uint8, device="cuda")
+        bs.split_decode_attention(pl_, 0, dev_bf16(lg.q[0]), btl, torch.from_numpy(kl).cuda(), 0,
+                                  synth.default_scale(d), o, m, l, wsl)
         # migration kernels
         dst = bs.KVPool(1, 64, 2, d)
         ids = torch.tensor([x for x in shards[1].block_tables.ravel() if x >= 0], dtype=torch.int32).cuda()

@@ -49,7 +49,8 @@ constexpr int kMaxLocal = 8;  // shards (tasks) / problems of one launch
 #ifdef BS_TIMELINE
 // Diagnostics build only: per-CTA %globaltimer stamps (ns) of the tensor-core kernel --
 // [0] entry, [1] first K/V stage landed (warp 0), [2] all warps' loops done, [3] arrival
-// counter resolved, [4] exit, [5] smid | last-arriver << 16.  Read by bs_timeline_read.
+// counter resolved, [4] exit, [5] smid | last-arriver << 16 | blocks << 20.  Read by
+// bs_timeline_read.
 constexpr int kTlCtas = 16384;
 __device__ unsigned long long g_timeline[kTlCtas][6];
 __device__ __forceinline__ unsigned long long tl_now() {
@@ -933,7 +934,8 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     const unsigned lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     if (threadIdx.x == 0 && lin < kTlCtas)
-      g_timeline[lin][5] = smid | ((unsigned long long)(nparts == 1 || s_flag[0]) << 16);
+      g_timeline[lin][5] = smid | ((unsigned long long)(nparts == 1 || s_flag[0]) << 16) |
+                           ((unsigned long long)nb_cta << 20);
   }
 #endif
 }

@@ -35,7 +35,7 @@ def q(x, ps=(0, 10, 50, 90, 100)):
     return {f"p{p}": round(float(np.percentile(x, p)), 2) for p in ps} if len(x) else {}
 
 
-def run(name, reps=5):
+def run(name, reps=5, ragged_bps=None):
     shape, lens = ATTN[name]
     dev = torch.device("cuda")
     lens = np.asarray(lens, dtype=np.int64)
@@ -52,19 +52,27 @@ def run(name, reps=5):
     ws = torch.zeros(max(16, bs.split_decode_attention_workspace_size(pool, B, shape.hq, bt.shape[1])),
                      dtype=torch.uint8, device=dev)
     sc = synth.default_scale(shape.d)
+    call = lambda: bs.split_decode_attention(pool, 0, case.q[0], btd, ksd, 0, sc, o, m, l, ws)  # noqa: E731
+    if ragged_bps is not None:  # fused local path over a ragged plan (longest range first)
+        plan = bs.attention_ragged_plan(ks, [0], shape.hq, shape.hkv, shape.d,
+                                        max_blocks_per_range=ragged_bps).to(dev)
+        wsr = torch.zeros(max(16, plan.workspace_bytes), dtype=torch.uint8, device=dev)
+        ob = torch.empty(B, shape.hq, shape.d, dtype=torch.bfloat16, device=dev)
+        call = lambda: bs.split_decode_attention_local_ragged([pool], 0, case.q[0], [btd], [0], ksd, sc,  # noqa: E731
+                                                              plan, ob, l, wsr)
     flush = torch.empty(256 * 2**20, dtype=torch.uint8, device=dev)
     L = bs.lib()
     L.bs_timeline_read.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
     L.bs_timeline_read.restype = ctypes.c_int32
     out = []
     for _ in range(reps):
-        bs.split_decode_attention(pool, 0, case.q[0], btd, ksd, 0, sc, o, m, l, ws)
+        call()
         flush.fill_(1)
         torch.cuda.synchronize()
         assert L.bs_timeline_reset() == 0
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        bs.split_decode_attention(pool, 0, case.q[0], btd, ksd, 0, sc, o, m, l, ws)
+        call()
         b.record()
         torch.cuda.synchronize()
         buf = np.zeros((KT, 6), dtype=np.uint64)
@@ -79,7 +87,8 @@ def run(name, reps=5):
     has3 = t[:, 3] > 0     # CTAs that took part in a split-K arrival
     has1 = t[:, 1] > 0
     res = {
-        "case": name, "ctas": int(nz.sum()), "event_us": round(ev_us, 2),
+        "case": name + ("" if ragged_bps is None else f"_ragged_bps{ragged_bps}"),
+        "ctas": int(nz.sum()), "event_us": round(ev_us, 2),
         "span_us": round(float(rel[:, 4].max()), 2),
         "entry": q(rel[:, 0]),
         "first_data_after_entry": q((rel[:, 1] - rel[:, 0])[has1]),
@@ -96,6 +105,14 @@ def run(name, reps=5):
     sm = (t[:, 5] & 0xFFFF).astype(np.int64)
     per_sm = np.bincount(sm, minlength=int(sm.max()) + 1)[sm]
     loop = rel[:, 2] - rel[:, 0]
+    nbk = (t[:, 5] >> 20).astype(np.int64)
+    res["max_blocks_per_cta"] = int(nbk.max())
+    res["loop_us_per_block_by_size"] = {}
+    for lo, hi in ((1, 16), (16, 64), (64, 128), (128, 256), (256, 513)):
+        sel = (nbk >= lo) & (nbk < hi)
+        if sel.any():
+            res["loop_us_per_block_by_size"][f"{lo}-{hi - 1}"] = dict(
+                n=int(sel.sum()), loop_us=q(loop[sel]), start_us=q(rel[sel, 0]))
     res["loop_by_ctas_on_sm"] = {int(c): dict(n=int((per_sm == c).sum()), **q(loop[per_sm == c]))
                                  for c in np.unique(per_sm)}
     return res
@@ -105,12 +122,15 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--case", action="append")
     ap.add_argument("--json")
+    ap.add_argument("--ragged-bps", type=int, action="append",
+                    help="also run the fused local path over a ragged plan (0 = automatic range)")
     args = ap.parse_args()
     res = []
     for c in args.case or ["C3_gqa4_B1_8192", "C3_gqa4_B8_8192", "C2_mha_B64_2048"]:
-        r = run(c)
-        print(json.dumps(r), flush=True)
-        res.append(r)
+        for rb in [None] + (args.ragged_bps or []):
+            r = run(c, ragged_bps=rb)
+            print(json.dumps(r), flush=True)
+            res.append(r)
     if args.json:
         with open(args.json, "w") as f:
             json.dump(res, f, indent=1)

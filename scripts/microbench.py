@@ -245,6 +245,9 @@ def tasks_cases(iters=20, warm=5):
     return out
 
 
+RAGGED_EXTRA_BPS = []
+
+
 def ragged_cases(iters=20, warm=5):
     """Mixed-length shards through the single-GPU fused launch: uniform grid (max_blocks-
     wide ranges) vs the ragged plan (bs_attention_ragged_plan).  GB/s = algorithmic bytes
@@ -271,8 +274,10 @@ def ragged_cases(iters=20, warm=5):
         wsu = torch.zeros(max(16, bs.split_decode_attention_local_workspace_size(
             [pool], [bts[0].shape[1]], B, shape.hq)), dtype=torch.uint8, device=dev)
         plans = {}
-        for kind, bps, order in (("ragged", 0, "1"), ("ragged_reqorder", 0, "0"),
-                                 ("ragged_bps64", 64, "1"), ("ragged_bps32", 32, "1")):
+        variants = [("ragged", 0, "1"), ("ragged_reqorder", 0, "0"), ("ragged_bps64", 64, "1"),
+                    ("ragged_bps32", 32, "1")]
+        variants += [(f"ragged_bps{x}", x, "1") for x in RAGGED_EXTRA_BPS]
+        for kind, bps, order in variants:
             os.environ["BS_RAGGED_ORDER"] = order
             pl = bs.attention_ragged_plan(ks, [0], shape.hq, shape.hkv, shape.d,
                                           max_blocks_per_range=bps).to(dev)
@@ -336,6 +341,8 @@ def main():
     ap.add_argument("--json")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--diag", action="store_true", help="group-size / kv-head diagnostics")
+    ap.add_argument("--ragged-bps", type=int, action="append", default=[],
+                    help="extra ragged-plan range lengths to time")
     ap.add_argument("--graph", action="store_true",
                     help="attention: time graph-captured back-to-back launches over >= 3x L2 of KV")
     ap.add_argument("--seeds", type=int, default=1,
@@ -378,6 +385,7 @@ def main():
     if args.only in (None, "tasks"):
         res += tasks_cases(iters=args.iters)
     if args.only in (None, "ragged"):
+        RAGGED_EXTRA_BPS.extend(args.ragged_bps)
         res += ragged_cases(iters=args.iters)
     if args.json:
         with open(args.json, "w") as f:

@@ -547,7 +547,7 @@ def run_reference(args, rank, world, device):
     case = synth.device_shards(SHAPE, lens, ks, seed=0, device=gen_dev,
                                spare_blocks=N_HANDOFF * handoff_chunks, layers=nl)
     scale = synth.default_scale(SHAPE.d)
-    reqs = 8
+    reqs = 32   # ~70 ms of oracle work per step on 16 cores: a stable sample, minutes at most
     samples = [oracle_sample(case, [(reqs * i + r) % BATCH for r in range(reqs)], i % nl,
                              handoff_chunks) for i in range(2)]
     for i in range(args.warmup):

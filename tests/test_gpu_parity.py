@@ -137,6 +137,28 @@ def test_shapes_ragged_unaligned_empty_shards(bs, d, G):
                              parts, out, lse)
 
 
+@pytest.mark.parametrize("G,scale", [(1, 1.0), (4, 1.5), (8, 2.0)])
+def test_scores_beyond_fp32_exp_range(bs, G, scale):
+    """A large scale (R-A2: an explicit argument; 11-23x 1/sqrt(d)) puts the planted
+    needles' scores past fp32 exp's range (88.7): the max-shifted exponentials (R-A3) keep
+    every partial and the merge finite, and the results still match the fp64 oracle."""
+    shape = synth.Shape(1, 2 * G, 2, 128)
+    lens = (1, 100, 700, 2000)
+    dense = synth.gen_dense(shape, lens, seed=90 + G)
+    ks = synth.random_split(lens, 2, seed=G)
+    shards = synth.place_shards(dense, ks, seed=G + 1)
+    pools = gpu_pools(bs, shape, [s.pool for s in shards])
+    bts = [s.block_tables for s in shards]
+    parts, out, lse = run_split_attention(bs, shape, pools, bts, ks, dense.q[0], 0, scale)
+    assert bool(torch.isfinite(out.float()).all()) and bool(torch.isfinite(lse).all())
+    ref_lse = oracle.merge_partials(*zip(*[oracle.attention_shard(p.pool, 0, dense.q[0], p.block_tables,
+                                                                    ks, j, scale)
+                                           for j, p in enumerate(shards)]))[1]
+    assert ref_lse.max() > 88.7        # the regime this test is for
+    check_against_oracle(shape, [s.pool for s in shards], bts, ks, dense.q[0], 0, scale, parts, out,
+                         lse)
+
+
 @pytest.mark.parametrize("n_shards", [1, 8])
 def test_many_shards_and_split_k(bs, n_shards):
     """B=1 long context forces the intra-GPU split-K (workspace + last-CTA merge)."""

@@ -117,6 +117,9 @@ int32_t bs_kv_pool_num_free(const bs_kv_pool* pool);
 /* ids must be distinct (caller contract).  src and dst must have equal             */
 /* num_kv_heads / head_dim / block_size / num_layers.  Same device, or dst a remote */
 /* view (peer-mapped), or src a remote view (P2P pull).  n == 0 is a no-op.          */
+/* A view whose desc.device is another GPU's ordinal is a remote view: the copy is  */
+/* NVLink-bound and runs on one CTA per SM (env BS_REMOTE_COPY_CTAS overrides), so  */
+/* it leaves the other SM slots to the compute beside it.                           */
 /* method: BS_MIGRATE_AUTO picks the fastest; VEC16 = 16-byte vector LDG/STG copy;  */
 /* BULK = TMA bulk copies (cp.async.bulk) global->smem->global.                      */
 /* ------------------------------------------------------------------------------ */

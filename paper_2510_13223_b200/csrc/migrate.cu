@@ -14,6 +14,7 @@
 //     cp.async.bulk shared->global in bulk groups); no registers touch the payload.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <vector>
 
@@ -282,6 +283,21 @@ static int dev_copy_ctas() {
   return v;
 }
 
+// A push into a pool owned by another GPU (a peer-mapped view, desc.device = the owner's
+// ordinal) is NVLink-bound, not HBM-bound: one 8-warp CTA per SM keeps >= 9 MB of loads
+// and stores in flight -- far more than 900 GB/s x the link's round trip needs -- while a
+// full grid (8 CTAs x 256 threads per SM) would hold every SM's thread slots for the
+// whole, slower, transfer and starve the attention launch beside it
+// (BS_REMOTE_COPY_CTAS overrides; 0 = no cap).
+static int remote_copy_ctas() {
+  const char* e = getenv("BS_REMOTE_COPY_CTAS");
+  return e ? std::max(0, atoi(e)) : bs::sm_count(bs::current_device());
+}
+
+static bool is_remote(const bs_kv_pool* p) {
+  return !p->host && p->desc.device >= 0 && p->desc.device != bs::current_device();
+}
+
 static bool same_geometry(const bs_kv_pool* a, const bs_kv_pool* b) {
   return a->desc.num_layers == b->desc.num_layers && a->desc.num_kv_heads == b->desc.num_kv_heads &&
          a->desc.head_dim == b->desc.head_dim && a->desc.block_size == b->desc.block_size &&
@@ -303,7 +319,8 @@ bs_status bs_kv_migrate_layer_ex(const bs_kv_pool* src, bs_kv_pool* dst, int32_t
              "bs_kv_migrate_layer: bad method %d", method);
   // a host-tier pool is behind PCIe / C2C: a few CTAs keep it saturated, the rest of the
   // SMs stay with the layer's compute (three-stage pipeline, Fig. 6)
-  const int max_ctas = (src->host || dst->host) ? kHostCopyCtas : dev_copy_ctas();
+  int max_ctas = (src->host || dst->host) ? kHostCopyCtas : dev_copy_ctas();
+  if (max_ctas == 0 && (is_remote(src) || is_remote(dst))) max_ctas = remote_copy_ctas();
   BS_DEBUG_CHECK(bs::debug_check_ids(src_ids, n, src->desc.num_blocks, static_cast<cudaStream_t>(stream),
                                      "bs_kv_migrate_layer src_ids"));
   BS_DEBUG_CHECK(bs::debug_check_ids(dst_ids, n, dst->desc.num_blocks, static_cast<cudaStream_t>(stream),

@@ -209,7 +209,7 @@ class P2PLinks:
         self.timeout_ns = int(timeout_ms) * 1_000_000
         mine = {"flags": ipc_export(self.flags), "q_prev": ipc_export(self.q_prev),
                 "part_recv": ipc_export(self.part_recv), "home": ipc_export(home_pool.data),
-                "home_blocks": home_pool.num_blocks,
+                "home_blocks": home_pool.num_blocks, "device": torch.cuda.current_device(),
                 "handoff_dst": [int(x) for x in handoff_dst_ids.cpu().tolist()]}
         if fused is not None:
             for k in ("out", "lse", "ws", "done"):
@@ -231,9 +231,11 @@ class P2PLinks:
         self.prev_part_recv = open_(prev, "part_recv")
         self.prev_flags = open_(prev, "flags")
         prev_home = open_(prev, "home")
+        # the view's device is the OWNER's ordinal: a push into another GPU's pool is sized
+        # for NVLink (bs_kv_migrate_layer caps its CTAs), a same-GPU view is a local copy
         self.prev_home = pool_view(home_pool.num_layers, everyone[prev]["home_blocks"],
                                    home_pool.num_kv_heads, home_pool.head_dim, prev_home,
-                                   device.index if device.index is not None else 0)
+                                   everyone[prev]["device"])
         self.prev_handoff_dst = torch.tensor(everyone[prev]["handoff_dst"], dtype=torch.int32,
                                              device=device)
         self.fused = fused

@@ -121,6 +121,7 @@ class SeqShardedStep:
                                              ("pool", self.pool.data))}
         mine["ws_stride"] = stride
         mine["pool_blocks"] = self.pool.num_blocks
+        mine["device"] = dev.index if dev.index is not None else torch.cuda.current_device()
         mine["handoff_dst"] = ([] if self.dst_ids is None else
                                [int(x) for x in self.dst_ids.cpu().tolist()])
         everyone = [None] * W
@@ -147,8 +148,7 @@ class SeqShardedStep:
             nxt = self.next
             base = self.pool.data.data_ptr() if nxt == self.rank else open_(nxt, "pool")
             self.next_pool = pool_view(self.L, everyone[nxt]["pool_blocks"], self.pool.num_kv_heads,
-                                       self.pool.head_dim, base,
-                                       dev.index if dev.index is not None else 0)
+                                       self.pool.head_dim, base, everyone[nxt]["device"])
             self.next_dst = torch.tensor(everyone[nxt]["handoff_dst"], dtype=torch.int32, device=dev)
         self.ack_s = torch.cuda.Stream(device=dev)
         self.out_s = torch.cuda.Stream(device=dev)

@@ -138,21 +138,32 @@ def test_measured_costs_drive_layer_moves(bs):
     assert pl.plan(costs, delta=0.3, rho=1.0)[0] == []
 
 
-def test_rho_between_measured_costs_picks_kv_heads(bs):
-    """Heavy layer weights make MigrateLayer's measured cost exceed MigrateKVHeads'; with
-    rho between the two Benefit/Cost ratios, Alg. 1 falls through to head moves."""
-    from paper_2510_13223_b200.control import HEADS
+def test_rho_between_measured_costs_picks_the_cheaper_module(bs):
+    """Heavy layer weights make MigrateLayer's measured cost exceed MigrateKVHeads' (on an
+    idle B200; the test follows whichever is cheaper as measured): with rho between the
+    two Benefit/Cost ratios, Alg. 1 takes only the cheaper module (line 12 or line 14)."""
+    from paper_2510_13223_b200.control import HEADS, LAYER
     shape, dense, ks, src, pl, bts = _setup(bs, weight_mib=512)
     costs = _costs(bs, pl, dense, ks, bts, shape)
     nblk = pl.ids[0].numel()
     page = pl.pools[0].chunk_bytes // (2 * HKV)
     c_layer = costs.layer_cost(nblk * pl.pools[0].chunk_bytes, 512 * 2**20)
     c_head = costs.head_cost(L * nblk * 2 * page)
-    assert c_layer > c_head
     benefit = 2.0 - abs(1.5 - 0.5)                        # either module moves 0.5 of load
     rho = benefit / (c_layer * c_head) ** 0.5
-    moves, load, n_layers, n_heads = pl.plan(costs, delta=0.3, rho=rho)
-    assert moves == [(HEADS, 0, 1), (HEADS, 0, 1)]
+    cheaper = HEADS if c_head < c_layer else LAYER
+    assert pl.plan(costs, delta=0.3, rho=rho)[0] == [(cheaper, 0, 1)] * 2
+    assert pl.plan(costs, delta=0.3, rho=benefit / min(c_layer, c_head) * 1.01)[0] == []
+
+
+def test_kv_head_moves_executed(bs):
+    """Layer migration unsupported on the overloaded device (Alg. 1 line 12 fails): the
+    cycle moves KV heads (line 14) and MigrateKVHeads executes them."""
+    from paper_2510_13223_b200.control import HEADS
+    shape, dense, ks, src, pl, bts = _setup(bs, weight_mib=1)
+    costs = _costs(bs, pl, dense, ks, bts, shape)
+    moves, load, n_layers, n_heads = pl.plan(costs, delta=0.3, rho=1.0, supports_layer=[0, 1])
+    assert moves == [(HEADS, 0, 1), (HEADS, 0, 1)] and load == [1.0, 1.0] and n_heads == [2, 2]
     pl.execute(moves)
     torch.cuda.synchronize()
     assert pl.executed == [("heads", 3, 0, 1), ("heads", 2, 0, 1)]

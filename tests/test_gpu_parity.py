@@ -281,6 +281,30 @@ def test_migration_random_pairs_bit_exact(bs, method, d, hkv):
     assert np.array_equal(host_u16(dst_g.data), ref)
 
 
+@pytest.mark.parametrize("ctas", [None, "3"])
+def test_migration_into_remote_view_bit_exact(bs, ctas, monkeypatch):
+    """A destination view whose desc.device names another GPU is a remote view (NVLink
+    push): the copy runs on one CTA per SM (or BS_REMOTE_COPY_CTAS) instead of the full
+    grid.  Emulated here over local memory with a foreign ordinal: still bit-exact."""
+    if ctas is not None:
+        monkeypatch.setenv("BS_REMOTE_COPY_CTAS", ctas)
+    shape = synth.Shape(2, 8, 8, 128)
+    nb = 400
+    src_np = random_pool(shape, nb, 2, seed=11)
+    dst_np = np.full((2, nb, 2, 8, 16, 128), synth.DST_SENTINEL, dtype=np.uint16)
+    src_g, dst_g = gpu_pools(bs, shape, [src_np, dst_np])
+    view = bs.pool_view(2, nb, 8, 128, dst_g.data.data_ptr(), torch.cuda.current_device() + 1)
+    rng = np.random.default_rng(4)
+    ref = dst_np.copy()
+    for layer, n in ((0, 390), (1, 7)):
+        s = rng.permutation(nb)[:n].astype(np.int32)
+        t = rng.permutation(nb)[:n].astype(np.int32)
+        bs.kv_migrate_layer(src_g, view, layer, dev_i32(s), dev_i32(t))
+        oracle.migrate_layer(src_np, ref, layer, s, t)
+    torch.cuda.synchronize()
+    assert np.array_equal(host_u16(dst_g.data), ref)
+
+
 def test_gather_scatter_roundtrip_equals_migrate(bs):
     """The two-sided transport halves (pack -> [send/recv] -> unpack) are the same copy."""
     shape = synth.Shape(2, 8, 8, 128)

@@ -77,6 +77,8 @@ def lib():
         L.or_migrate_heads_layer.argtypes = [_p, _i32, _i32, _p, _i32, _i32, _i32, _i32, _i32, _p,
                                              _p, _i32, _i32, _i32, _i32]
         L.or_migrate_heads_layer.restype = None
+        L.or_append_token.argtypes = [_p, _i32, _i32, _i32, _i32, _i32, _p, _p, _i32, _p, _i32, _p]
+        L.or_append_token.restype = None
         L.or_attention_shard.argtypes = [_p, _i32, _i32, _i32, _i32, _i32, _p, _i32, _i32, _p,
                                          _i32, _p, _i32, _i32, _f32, _p, _p, _p]
         L.or_attention_shard.restype = None
@@ -183,6 +185,25 @@ def migrate_layer(src_pool: np.ndarray, dst_pool: np.ndarray, layer: int, src_id
         return
     lib().or_migrate_layer(_ptr(src_pool), nbs, _ptr(dst_pool), dst_pool.shape[1], hkv, bs, d,
                            layer, _ptr(s), _ptr(t), int(s.size))
+
+
+def append_token(pool: np.ndarray, layer: int, k_new, v_new, block_tables, pos) -> None:
+    """(H7) In place on ``pool`` (uint16 [L][NB][2][Hkv][bs][d]): the decoded token's K/V
+    (uint16 bf16 bits [B][Hkv][d]) into local token ``pos[b]`` of each request's shard
+    (block ``block_tables[b][pos // bs]``, slot ``pos % bs``); ``pos[b] < 0`` skips.
+    The paper is silent (reading R-A9: the current token's K/V is in the cache)."""
+    assert pool.dtype == np.uint16 and pool.flags.c_contiguous
+    L, nb, two, hkv, bs, d = pool.shape
+    k = _c(k_new, np.uint16)
+    v = _c(v_new, np.uint16)
+    bt = _c(block_tables, np.int32)
+    p = _c(pos, np.int32)
+    B = p.shape[0]
+    assert k.shape == (B, hkv, d) and v.shape == (B, hkv, d) and bt.shape[0] == B
+    if B == 0:
+        return
+    lib().or_append_token(_ptr(pool), nb, hkv, bs, d, layer, _ptr(k), _ptr(v), B, _ptr(bt),
+                          bt.shape[1], _ptr(p))
 
 
 def migrate_heads_layer(src_pool: np.ndarray, dst_pool: np.ndarray, layer: int, src_ids, dst_ids,

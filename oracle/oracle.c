@@ -171,6 +171,31 @@ void or_migrate_layer(const uint16_t* src_pool, int32_t src_blocks, uint16_t* ds
 }
 
 /* ------------------------------------------------------------------------- */
+/* H7 (adjacent to the path): append the decoded token's K/V.    */
+/* The paper is silent; reading R-A9: seq_len includes the token being decoded, */
+/* whose K/V is already in the cache when attention runs -- this writes it.     */
+/* For every request b with pos[b] >= 0: for every kv head g and dim x,         */
+/*   pool[layer][bt[b][pos/bs]][K][g][pos%bs][x] = k_new[b][g][x]               */
+/*   pool[layer][bt[b][pos/bs]][V][g][pos%bs][x] = v_new[b][g][x]               */
+/* (bit copy, uint16).  pos[b] < 0: request skipped.                            */
+/* ------------------------------------------------------------------------- */
+void or_append_token(uint16_t* pool, int32_t n_blocks, int32_t h_kv, int32_t bs, int32_t d,
+                     int32_t layer, const uint16_t* k_new, const uint16_t* v_new, int32_t batch,
+                     const int32_t* block_tables, int32_t max_blocks, const int32_t* pos) {
+  for (int32_t b = 0; b < batch; ++b) {
+    if (pos[b] < 0) continue;
+    const int32_t block = block_tables[(int64_t)b * max_blocks + pos[b] / bs];
+    const int32_t slot = pos[b] % bs;
+    for (int32_t g = 0; g < h_kv; ++g)
+      for (int32_t x = 0; x < d; ++x) {
+        const int64_t src = ((int64_t)b * h_kv + g) * d + x;
+        pool[elem_index(n_blocks, h_kv, bs, d, layer, block, 0, g, slot, x)] = k_new[src];
+        pool[elem_index(n_blocks, h_kv, bs, d, layer, block, 1, g, slot, x)] = v_new[src];
+      }
+  }
+}
+
+/* ------------------------------------------------------------------------- */
 /* NEXT F2: head-granular attention-level migration -- the paper's literal text: */
 /* "partition the KV Cache along the attention head dimension and selectively  */
 /* migrate only the KV states of certain heads" (Alg. 1 */

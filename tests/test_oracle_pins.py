@@ -344,3 +344,54 @@ def test_migrate_heads_pages_and_head_split_attention():
     ref, _ = sdpa_reference(dense, 0, sc)
     cat = np.concatenate([o_full[:, :c0 * G], o_c], axis=1)   # merge = concat for a head split
     assert np.abs(cat - ref).max() < 1e-12
+
+
+# ---------------------------------------------------------------------------- H7 append
+
+def append_case(seed=0, lens=(37, 64, 129, 200, 17), layer=1):
+    """A 2-layer toy-shaped cache laid out from the FULL dense KV, and the same cache with
+    each request's last token (the one being decoded, reading R-A9) not yet written in
+    ``layer`` (its slot poisoned with bf16 NaN).  Positions cover a mid-block slot (36),
+    the last slot of a block (63), the first slot of a new block (128, 16) and 199."""
+    shape = synth.Shape(n_layers=2, hq=4, hkv=2, d=64)
+    dense = synth.gen_dense(shape, lens, seed)
+    ks = np.stack([np.zeros(len(lens)), np.asarray(lens)], axis=1).astype(np.int32)
+    full = synth.place_shards(dense, ks, seed=seed)[0]
+    pos = np.asarray(lens, dtype=np.int32) - 1
+    partial = full.pool.copy()
+    for b, p in enumerate(pos):
+        partial[layer, full.block_tables[b, p // 16], :, :, p % 16, :] = synth.BF16_NAN
+    k_new = np.stack([dense.k[b][layer, p] for b, p in enumerate(pos)])   # [B][Hkv][d]
+    v_new = np.stack([dense.v[b][layer, p] for b, p in enumerate(pos)])
+    return dense, ks, full, partial, pos, k_new, v_new
+
+
+def test_append_token_completes_the_paged_cache():
+    """(H7) Appending each request's decoded token reproduces, byte for byte, the cache
+    laid out from the full dense KV (pins block = bt[pos // 16], slot = pos % 16, K before
+    V, head order, the layer); every other byte is untouched; attention over the completed
+    cache equals torch's fp64 SDPA over the dense KV including that token."""
+    layer = 1
+    dense, ks, full, partial, pos, k_new, v_new = append_case(layer=layer)
+    before = partial.copy()
+    oracle.append_token(partial, layer, k_new, v_new, full.block_tables, pos)
+    assert np.array_equal(partial, full.pool)
+    assert np.array_equal(partial[0], before[0])          # other layer untouched
+    sc = synth.default_scale(64)
+    o, m, l = oracle.attention_shard(partial, layer, dense.q[layer], full.block_tables, ks, 0, sc)
+    ref_o, ref_lse = sdpa_reference(dense, layer, sc)
+    assert np.abs(o - ref_o).max() < 1e-12
+    assert np.abs(m + np.log(l) - ref_lse).max() < 1e-12
+
+
+def test_append_token_negative_position_skips():
+    layer = 1
+    dense, ks, full, partial, pos, k_new, v_new = append_case(layer=layer)
+    skip = pos.copy()
+    skip[2] = -1
+    oracle.append_token(partial, layer, k_new, v_new, full.block_tables, skip)
+    b, p = 2, int(pos[2])
+    blk = full.block_tables[b, p // 16]
+    assert np.all(partial[layer, blk, :, :, p % 16, :] == synth.BF16_NAN)
+    partial[layer, blk, :, :, p % 16, :] = full.pool[layer, blk, :, :, p % 16, :]
+    assert np.array_equal(partial, full.pool)

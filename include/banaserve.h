@@ -132,6 +132,24 @@ bs_status bs_kv_migrate_layer_ex(const bs_kv_pool* src, bs_kv_pool* dst, int32_t
                                  const int32_t* src_ids, const int32_t* dst_ids, int32_t n,
                                  int32_t method, void* stream);
 
+/* ------------------------------------------------------------------------------ */
+/* H7 (adjacent to the path): append the decoded token's K/V.       */
+/* The paper is silent; reading R-A9: seq_len includes the token being decoded, so  */
+/* its K/V is written to the cache before attention (H4) runs.  For every request b */
+/* with pos[b] >= 0, kv head g:                                                      */
+/*   K page (layer, block_tables[b][pos[b]/16], g), slot pos[b]%16 <- k_new[b][g][:] */
+/*   V page (same block, g),                        slot pos[b]%16 <- v_new[b][g][:] */
+/* a bit copy; pos[b] < 0 skips request b.  pos is the shard-LOCAL token index (the  */
+/* shard that holds the sequence's end).                                             */
+/* k_new, v_new DEVICE bf16 [batch][num_kv_heads][head_dim], 16-B aligned.           */
+/* block_tables DEVICE int32 [batch][max_blocks]; pos DEVICE int32 [batch].          */
+/* Device arrays are not validated (block ids must be < num_blocks, pos[b]/16 <      */
+/* max_blocks).  Enqueued on `stream`; never synchronises.                           */
+/* ------------------------------------------------------------------------------ */
+bs_status bs_kv_append_token(bs_kv_pool* pool, int32_t layer, const void* k_new, const void* v_new,
+                             int32_t batch, const int32_t* block_tables, int32_t max_blocks,
+                             const int32_t* pos, void* stream);
+
 /* Copy-engine variant (DMA, no SM time -- for the host tier's fetch / store legs, which
  * should not compete with attention for SMs): HOST int32 id arrays (validated), runs of
  * consecutive ids coalesced, one cudaMemcpyBatchAsync per call on a non-NULL stream

@@ -39,7 +39,7 @@ EXPORTED_SYMBOLS = (
     "bs_split_decode_attention_local", "bs_signal", "bs_wait_signal",
     "bs_attention_problem_workspace_size", "bs_split_decode_attention_tasks", "bs_wait_signals",
     "bs_signals", "bs_attention_ragged_plan", "bs_split_decode_attention_local_ragged",
-    "bs_debug_build", "bs_debug_error_code",
+    "bs_debug_build", "bs_debug_error_code", "bs_kv_append_token",
 )
 
 
@@ -95,6 +95,7 @@ def lib():
         "bs_kv_migrate_layer": ([_p, _p, _i32, _p, _p, _i32, _p], _i32),
         "bs_kv_migrate_layer_ex": ([_p, _p, _i32, _p, _p, _i32, _i32, _p], _i32),
         "bs_kv_migrate_layer_ce": ([_p, _p, _i32, _p, _p, _i32, _p], _i32),
+        "bs_kv_append_token": ([_p, _i32, _p, _p, _i32, _p, _i32, _p, _p], _i32),
         "bs_kv_gather_layer": ([_p, _i32, _p, _i32, _p, _p], _i32),
         "bs_kv_scatter_layer": ([_p, _i32, _p, _i32, _p, _p], _i32),
         "bs_split_decode_attention_workspace_size": ([_p, _i32, _i32, _i32, ctypes.POINTER(_sz)], _i32),
@@ -268,6 +269,20 @@ def kv_migrate_layer_ce(src: KVPool, dst: KVPool, layer: int, src_ids, dst_ids, 
     sa = (ctypes.c_int32 * max(n, 1))(*s)
     da = (ctypes.c_int32 * max(n, 1))(*d)
     _check(lib().bs_kv_migrate_layer_ce(src.handle, dst.handle, layer, sa, da, n, _stream(stream)))
+
+
+def kv_append_token(pool: KVPool, layer: int, k_new: torch.Tensor, v_new: torch.Tensor,
+                    block_tables: torch.Tensor, pos: torch.Tensor, stream=None) -> None:
+    """H7: the decoded token's K/V (bf16 [B, Hkv, d]) into local token ``pos[b]`` of each
+    request's shard (device int32 ``pos``; < 0 skips)."""
+    B = pos.numel()
+    for t in (k_new, v_new):
+        if t.dtype != torch.bfloat16 or not t.is_contiguous() or t.numel() != B * pool.num_kv_heads * pool.head_dim:
+            raise ValueError("k_new / v_new must be contiguous bf16 [B, Hkv, d]")
+    _check(lib().bs_kv_append_token(pool.handle, layer, _dptr(k_new, torch.bfloat16),
+                                    _dptr(v_new, torch.bfloat16), B,
+                                    _dptr(block_tables, torch.int32), int(block_tables.shape[1]),
+                                    _dptr(pos, torch.int32), _stream(stream)))
 
 
 def kv_gather_layer(src: KVPool, layer: int, ids: torch.Tensor, staging: torch.Tensor,

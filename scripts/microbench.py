@@ -245,6 +245,45 @@ def tasks_cases(iters=20, warm=5):
     return out
 
 
+def append_cases(iters=200, warm=20):
+    """H7 append (bs_kv_append_token): one launch per layer writing each request's new
+    K/V rows; per-call time graph-timed (40 captured launches) and per-call event-timed."""
+    dev = torch.device("cuda")
+    out = []
+    for name, shape, B in (("C2_B64", synth.LLAMA2_7B, 64), ("C3_B8", synth.LLAMA3_8B, 8),
+                           ("C4_B256", synth.LLAMA2_70B, 256)):
+        nb = B * 4
+        pool = bs.KVPool(1, nb, shape.hkv, shape.d)
+        bt = torch.arange(nb, dtype=torch.int32, device=dev).view(B, 4)
+        pos = torch.randint(0, 64, (B,), dtype=torch.int32, device=dev)
+        k = torch.randn(B, shape.hkv, shape.d, device=dev).to(torch.bfloat16)
+        v = torch.randn(B, shape.hkv, shape.d, device=dev).to(torch.bfloat16)
+        fn = lambda: bs.kv_append_token(pool, 0, k, v, bt, pos)  # noqa: E731
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(40):
+                    fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(iters // 40):
+            g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        us = a.elapsed_time(b) * 1e3 / (iters // 40 * 40)
+        by = 2 * B * 2 * shape.hkv * shape.d * 2   # rows read + written
+        r = {"case": f"append_{name}", "B": B, "hkv": shape.hkv, "us_graph": round(us, 2),
+             "bytes": by, "GBps": round(by / (us * 1e-6) / 1e9, 1)}
+        print(json.dumps(r), flush=True)
+        out.append(r)
+    return out
+
+
 RAGGED_EXTRA_BPS = []
 
 
@@ -336,7 +375,7 @@ DIAG = {
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", choices=["attn", "mig", "tasks", "ragged"])
+    ap.add_argument("--only", choices=["attn", "mig", "tasks", "ragged", "append"])
     ap.add_argument("--case")
     ap.add_argument("--json")
     ap.add_argument("--iters", type=int, default=20)
@@ -384,6 +423,8 @@ def main():
         res += mig_extra_cases(args)
     if args.only in (None, "tasks"):
         res += tasks_cases(iters=args.iters)
+    if args.only in (None, "append"):
+        res += append_cases()
     if args.only in (None, "ragged"):
         RAGGED_EXTRA_BPS.extend(args.ragged_bps)
         res += ragged_cases(iters=args.iters)

@@ -146,6 +146,14 @@ def test_launch_validation_without_device():
     assert f(a, 0, p, 4, 24, p, 8, p, 2, 0, float("nan"), p, p, p, None, 0, None) == bs.BS_ERR_INVALID_ARG
     assert f(a, 0, p, 4, 24, p, 8, p, 2, 0, 0.1, p, p, p, None, 0, None) == bs.BS_ERR_UNSUPPORTED
     assert b"G=3" in L.bs_last_error()
+    # H7 append: NULL pool, layer out of range, NULL arrays, misaligned rows, batch 0 no-op
+    ap = L.bs_kv_append_token
+    assert ap(None, 0, p, p, 4, p, 8, p, None) == bs.BS_ERR_INVALID_ARG
+    assert ap(a, 2, p, p, 4, p, 8, p, None) == bs.BS_ERR_INVALID_ARG
+    assert ap(a, 0, p, None, 4, p, 8, p, None) == bs.BS_ERR_INVALID_ARG
+    assert ap(a, 0, ctypes.c_void_p(0x1008), p, 4, p, 8, p, None) == bs.BS_ERR_INVALID_ARG
+    assert ap(a, 0, p, p, 4, p, 0, p, None) == bs.BS_ERR_INVALID_ARG
+    assert ap(a, 0, None, None, 0, None, 0, None, None) == bs.BS_OK
     # merge: too many parts / bad head_dim
     arr = (ctypes.c_void_p * 17)(*([0x1000] * 17))
     assert L.bs_merge_partials(17, arr, arr, arr, 1, 1, 128, p, None, None) == bs.BS_ERR_INVALID_ARG

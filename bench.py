@@ -72,6 +72,9 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+NVLINK_GBS_PER_DIR = 900.0
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -438,6 +441,20 @@ def run_ours(args, rank, world, device):
             "traffic": traffic, "traffic_source": traffic_src,
             "algorithmic_bytes_per_layer": a_bytes,
         },
+        # the hand-off copy kernel (H2): local HBM read + write at N=1 (sharing HBM with the
+        # attention beside it), NVLink payload per direction at N>1 (spec peak, unmeasured here)
+        "roofline_migrate": ({
+            "bound": "hbm", "kernel": "copy_pages_vec16 (hand-off, copy stream)",
+            "achieved": round(2 * mig_bytes / (mig_avg_ms * 1e-3) / 1e9, 1), "peak": peak,
+            "peak_source": peak_src, "unit": "GB/s",
+            "frac": round(2 * mig_bytes / (mig_avg_ms * 1e-3) / 1e9 / peak, 4),
+            "note": "read + write bytes; in-step, concurrent with the HBM-bound attention"}
+            if world == 1 else {
+            "bound": "nvlink", "kernel": ("copy_pages_vec16 push into the peer's pool"
+                                          if step.transport == "p2p" else "gather/NCCL/scatter"),
+            "achieved": round(mig_gbs, 1), "peak": NVLINK_GBS_PER_DIR,
+            "peak_source": "spec (NVLink 5: 900 GB/s per direction per GPU)", "unit": "GB/s",
+            "frac": round(mig_gbs / NVLINK_GBS_PER_DIR, 4)}) if mig_bytes else None,
         "overlap": {"step_ms": round(ms_max, 4), "compute_only_ms": round(ms_compute, 4),
                     "exposure": round((ms_max - ms_compute) / ms_compute, 4),
                     "migrate_only_ms": None if ms_mig_only is None else round(ms_mig_only, 4),

@@ -94,17 +94,62 @@ def ncu_traffic():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 20 ms during the timed region
-    (samples with < 50 % utilisation -- before the region starts -- are dropped)."""
+    """SM clock + throttle reasons sampled DURING the timed region.
+
+    Primary: NVML (nvidia-ml-py) polled every 5 ms from a host thread between __enter__
+    (right before the first timed launch) and __exit__ (after the closing synchronize), so
+    every sample lies inside the region.  Fallback (no NVML): nvidia-smi every 20 ms,
+    started 1 s early, samples with < 50 % utilisation (before the region) dropped."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap,utilization.gpu")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.nvml = None
+        self.rows = []
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        p = torch.cuda.get_device_properties(self.index)
+        bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        try:
+            h = pynvml.nvmlDeviceGetHandleByPciBusId_v2(bus)
+        except Exception:
+            h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        return pynvml, h
+
+    def _poll(self):
+        nv, h = self.nvml
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+        cmax = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        while not self.stop.is_set():
+            try:
+                clk = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((clk, cmax, 100.0,
+                                  ["Active" if r & bits[n] else "Not Active" for n in self.NAMES]))
+            except Exception:
+                pass
+            self.stop.wait(0.005)
 
     def __enter__(self):
+        import threading
+        try:
+            self.nvml = self._nvml_handle()
+        except Exception:
+            self.nvml = None
+        if self.nvml is not None:
+            self.stop = threading.Event()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return self
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.proc = subprocess.Popen(
@@ -117,42 +162,47 @@ class ClockSampler:
         return self
 
     def __exit__(self, *exc):
+        if self.nvml is not None:
+            self.stop.set()
+            self.thread.join()
         if self.proc is not None:
             self.proc.terminate()
             self.proc.wait()
 
     def summary(self):
-        if self.proc is None:
-            return None
-        self.f.seek(0)
-        rows = []
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.f.read().strip().splitlines():
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                clk, cmax = float(parts[0]), float(parts[1])
-            except ValueError:
-                continue
-            try:
-                util = float(parts[6]) if len(parts) > 6 else 100.0
-            except ValueError:
-                util = 100.0
-            rows.append((clk, cmax, util, parts[2:6]))
+        rows = self.rows
+        source = "nvml (5 ms, timed region only)"
+        if self.nvml is None:
+            if self.proc is None:
+                return None
+            source = "nvidia-smi (20 ms, utilisation >= 50 %)"
+            self.f.seek(0)
+            for line in self.f.read().strip().splitlines():
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 6:
+                    continue
+                try:
+                    clk, cmax = float(parts[0]), float(parts[1])
+                except ValueError:
+                    continue
+                try:
+                    util = float(parts[6]) if len(parts) > 6 else 100.0
+                except ValueError:
+                    util = 100.0
+                rows.append((clk, cmax, util, parts[2:6]))
+            os.unlink(self.f.name)
         busy = [r for r in rows if r[2] >= 50.0] or rows   # samples under load (else all)
         sm = [r[0] for r in busy]
         mx = [r[1] for r in busy]
         reasons = set()
         for r in busy:
-            for n, v in zip(names, r[3]):
+            for n, v in zip(self.NAMES, r[3]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
-        os.unlink(self.f.name)
         if not sm:
             return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "sm_mhz_min": min(sm), "source": source}
 
 
 # --------------------------------------------------------------------------------------

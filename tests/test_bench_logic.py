@@ -81,3 +81,15 @@ def test_clock_summary_keeps_samples_under_load(tmp_path):
     c.f = f
     s = c.summary()
     assert s["sm_mhz"] == 1957.5 and s["samples"] == 2 and s["reasons"] == ["sw_power_cap"]
+
+
+def test_clock_summary_nvml_rows():
+    """NVML samples (polled inside the timed region only) are all kept."""
+    c = bench.ClockSampler(0)
+    c.nvml = object()
+    c.rows = [(1965.0, 1965.0, 100.0, ["Not Active"] * 4),
+              (1800.0, 1965.0, 100.0, ["Not Active", "Not Active", "Not Active", "Active"]),
+              (1900.0, 1965.0, 100.0, ["Not Active"] * 4)]
+    s = c.summary()
+    assert s["sm_mhz"] == 1900.0 and s["sm_mhz_min"] == 1800.0 and s["samples"] == 3
+    assert s["reasons"] == ["sw_power_cap"] and s["source"].startswith("nvml")

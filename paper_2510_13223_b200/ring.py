@@ -395,6 +395,25 @@ class ShardedDecodeStep:
         attn = 1 if self.fuse_local else 3
         return self.L * (attn + mig)
 
+    def _migrate(self, layer, mig_s, timers) -> None:
+        """H2 of one layer on stream ``mig_s``: the hand-off (N=1: local copy kernel; N>1
+        NCCL transport: gather -> send/recv -> scatter), then its ``mig_done`` event."""
+        ex, ops, E = self.ex, self.ops, self.ev
+        with ex.use(mig_s):
+            if timers is not None:
+                timers[layer][2].record(mig_s)
+            if self.n_handoff:
+                if self.world == 1:
+                    ops.migrate_local(self.cold, self.home, layer, self.src_ids, self.dst_ids,
+                                      self.ce_ids)
+                else:
+                    ops.gather(self.cold, layer, self.src_ids, self.stage_send)
+                    _sendrecv(self.pg_mig, self.stage_send, self.prev, self.stage_recv, self.next)
+                    ops.scatter(self.home, layer, self.dst_ids, self.stage_recv)
+            if timers is not None:
+                timers[layer][3].record(mig_s)
+            ex.record(E["mig_done"][layer], mig_s)
+
     def enqueue(self, q: torch.Tensor, out: torch.Tensor, lse: torch.Tensor | None = None,
                 timers=None, inputs_ready=None) -> None:
         """q [L][B][Hq][d] bf16 of this rank's requests -> out [L][B][Hq][d] bf16 and
@@ -422,28 +441,24 @@ class ShardedDecodeStep:
         # lookahead -2 at N=1: the hand-off copy runs on the compute stream right before its
         # layer's attention (serial) -- both are HBM-bound on one GPU
         mig_s = ex.compute if (self.lookahead == -2 and self.world == 1) else ex.copy
+        # lookahead -3 at N=1: every layer's hand-off copy first (back to back on the copy
+        # stream, per-layer events as usual), the attention of layer 0 after the last one --
+        # one read/write phase, then pure-read attention
+        copies_first = self.lookahead == -3 and self.world == 1 and self.n_handoff > 0
+        if copies_first:
+            for layer in range(self.L):
+                self._migrate(layer, ex.copy, timers)
         for layer in range(self.L):
             # ---- H2/H3: migration channel ---------------------------------------------
-            with ex.use(mig_s):
+            if not copies_first:
                 if self.lookahead >= 0 and layer - self.lookahead >= 0:
-                    ex.wait(ex.copy, E["layer_start"][layer - self.lookahead])
-                if timers is not None:
-                    timers[layer][2].record(mig_s)
-                if self.n_handoff:
-                    if self.world == 1:
-                        ops.migrate_local(self.cold, self.home, layer, self.src_ids, self.dst_ids,
-                                          self.ce_ids)
-                    else:
-                        ops.gather(self.cold, layer, self.src_ids, self.stage_send)
-                        _sendrecv(self.pg_mig, self.stage_send, self.prev, self.stage_recv, self.next)
-                        ops.scatter(self.home, layer, self.dst_ids, self.stage_recv)
-                if timers is not None:
-                    timers[layer][3].record(mig_s)
-                ex.record(E["mig_done"][layer], mig_s)
+                    with ex.use(ex.copy):
+                        ex.wait(ex.copy, E["layer_start"][layer - self.lookahead])
+                self._migrate(layer, mig_s, timers)
             # ---- H4: attention over both pools -------------------------------------------
             with ex.use(ex.compute):
                 ex.record(E["layer_start"][layer], ex.compute)
-                ex.wait(ex.compute, E["mig_done"][layer])
+                ex.wait(ex.compute, E["mig_done"][self.L - 1 if copies_first and layer == 0 else layer])
                 if inputs_ready is not None:
                     ex.wait(ex.compute, inputs_ready[layer])
                 if timers is not None:

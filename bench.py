@@ -84,8 +84,8 @@ def peaks():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    p = os.path.join(ROOT, "profiles", "ncu_attention.json")
+def ncu_traffic(name: str = "ncu_attention.json"):
+    p = os.path.join(ROOT, "profiles", name)
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
@@ -498,7 +498,8 @@ def run_ours(args, rank, world, device):
             "achieved": round(2 * mig_bytes / (mig_avg_ms * 1e-3) / 1e9, 1), "peak": peak,
             "peak_source": peak_src, "unit": "GB/s",
             "frac": round(2 * mig_bytes / (mig_avg_ms * 1e-3) / 1e9 / peak, 4),
-            "note": "read + write bytes; in-step, concurrent with the HBM-bound attention"}
+            "note": "read + write bytes; in-step, concurrent with the HBM-bound attention",
+            "traffic": ncu_traffic("ncu_copy.json")[0], "traffic_source": ncu_traffic("ncu_copy.json")[1]}
             if world == 1 else {
             "bound": "nvlink", "kernel": ("copy_pages_vec16 push into the peer's pool"
                                           if step.transport == "p2p" else "gather/NCCL/scatter"),

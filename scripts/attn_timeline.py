@@ -115,6 +115,32 @@ def run(name, reps=5, ragged_bps=None):
                 n=int(sel.sum()), loop_us=q(loop[sel]), start_us=q(rel[sel, 0]))
     res["loop_by_ctas_on_sm"] = {int(c): dict(n=int((per_sm == c).sum()), **q(loop[per_sm == c]))
                                  for c in np.unique(per_sm)}
+    # where the spread comes from: loop time by SM-id quarter (the two dies are expected
+    # to split the id range), by grid position, and whether the same SMs are slow in every
+    # repetition (correlation of per-SM mean loop time between repetitions)
+    nsm = int(sm.max()) + 1
+    res["loop_by_sm_quarter"] = {f"{k * nsm // 4}-{(k + 1) * nsm // 4 - 1}": q(
+        loop[(sm >= k * nsm // 4) & (sm < (k + 1) * nsm // 4)]) for k in range(4)}
+    lin = np.nonzero(nz)[0]
+    res["loop_by_grid_quarter"] = {f"q{k}": q(loop[(lin >= k * len(lin) // 4) & (lin < (k + 1) * len(lin) // 4)])
+                                   for k in range(4)}
+
+    def per_sm_mean(b):
+        m = b[:, 4] > 0
+        tt = b[m].astype(np.int64)
+        s_ = (tt[:, 5] & 0xFFFF).astype(np.int64)
+        lp = (tt[:, 2] - tt[:, 0]) / 1e3
+        cnt = np.bincount(s_, minlength=nsm)
+        tot = np.bincount(s_, weights=lp, minlength=nsm)
+        return np.where(cnt > 0, tot / np.maximum(cnt, 1), np.nan)
+    means = [per_sm_mean(b) for _, b in out]
+    cors = []
+    for i in range(len(means)):
+        for j in range(i + 1, len(means)):
+            ok = ~np.isnan(means[i]) & ~np.isnan(means[j])
+            if ok.sum() > 2:
+                cors.append(float(np.corrcoef(means[i][ok], means[j][ok])[0, 1]))
+    res["per_sm_loop_correlation_across_reps"] = q(cors) if cors else {}
     return res
 
 

@@ -143,8 +143,9 @@ bs_status bs_kv_migrate_layer_ex(const bs_kv_pool* src, bs_kv_pool* dst, int32_t
 /* shard that holds the sequence's end).                                             */
 /* k_new, v_new DEVICE bf16 [batch][num_kv_heads][head_dim], 16-B aligned.           */
 /* block_tables DEVICE int32 [batch][max_blocks]; pos DEVICE int32 [batch].          */
-/* Device arrays are not validated (block ids must be < num_blocks, pos[b]/16 <      */
-/* max_blocks).  Enqueued on `stream`; never synchronises.                           */
+/* Device arrays are not validated in release builds (block ids must be <         */
+/* num_blocks, pos[b]/16 < max_blocks); the debug build checks them (code 8: a     */
+/* position past the table).  Enqueued on `stream`; never synchronises.              */
 /* ------------------------------------------------------------------------------ */
 bs_status bs_kv_append_token(bs_kv_pool* pool, int32_t layer, const void* k_new, const void* v_new,
                              int32_t batch, const int32_t* block_tables, int32_t max_blocks,

@@ -55,6 +55,8 @@ bs_status bs_kv_append_token(bs_kv_pool* pool, int32_t layer, const void* k_new,
   BS_REQUIRE(((uintptr_t)k_new & 15) == 0 && ((uintptr_t)v_new & 15) == 0,
              "bs_kv_append_token: k_new / v_new must be 16-B aligned");
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  BS_DEBUG_CHECK(bs::debug_check_append(pos, batch, block_tables, max_blocks, pool->desc.num_blocks, s,
+                                        "bs_kv_append_token positions / block table"));
   bs::append_token_kernel<<<batch, 256, 0, s>>>(
       pool->base + (size_t)layer * pool->layer_bytes, (int64_t)pool->chunk_bytes,
       pool->desc.num_kv_heads, pool->desc.head_dim, static_cast<const uint4*>(k_new),

@@ -1,6 +1,6 @@
 // Debug build only (BS_DEBUG=1, libbanaserve_debug.so; SURVEY.md §8(b) "a debug build adds
 // device-side bounds checks that set an error flag the harness reads"): before a kernel
-// consumes DEVICE index arrays (block ids, block tables, kv_split), a small validation
+// consumes DEVICE index arrays (block ids, block tables, kv_split, append positions), a small validation
 // kernel checks them on the device; the call then synchronises its stream, and on a
 // violation records the code (bs_debug_error_code) and returns BS_ERR_INVALID_ARG without
 // launching the real kernel.  Release builds compile none of this (bs_debug_build() == 0).
@@ -44,6 +44,21 @@ __global__ void check_table_kernel(const int32_t* kv_split, int32_t n_shards, in
   }
 }
 
+// H7 append: pos[b] < 0 (skip) or pos[b] / 16 < max_blocks, and its block id in range
+__global__ void check_append_kernel(const int32_t* pos, int32_t batch, const int32_t* bt,
+                                    int32_t max_blocks, int32_t num_blocks, int32_t* bad) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < batch; b += gridDim.x * blockDim.x) {
+    const int32_t p = pos[b];
+    if (p < 0) continue;
+    if (p / 16 >= max_blocks) {
+      atomicOr(bad, 8);
+      continue;
+    }
+    const int32_t x = bt[(int64_t)b * max_blocks + p / 16];
+    if (x < 0 || x >= num_blocks) atomicOr(bad, 1);
+  }
+}
+
 int32_t* flag_buffer() {
   static int32_t* buf[64] = {nullptr};
   const int d = current_device();
@@ -81,6 +96,15 @@ bs_status debug_check_table(const int32_t* kv_split, int32_t n_shards, int32_t s
   int32_t* flag = flag_buffer();
   cudaMemsetAsync(flag, 0, sizeof(int32_t), s);
   check_table_kernel<<<batch, 128, 0, s>>>(kv_split, n_shards, shard, bt, max_blocks, num_blocks, flag);
+  return finish(flag, s, what);
+}
+
+bs_status debug_check_append(const int32_t* pos, int32_t batch, const int32_t* bt, int32_t max_blocks,
+                             int32_t num_blocks, cudaStream_t s, const char* what) {
+  if (batch <= 0) return BS_OK;
+  int32_t* flag = flag_buffer();
+  cudaMemsetAsync(flag, 0, sizeof(int32_t), s);
+  check_append_kernel<<<(batch + 255) / 256, 256, 0, s>>>(pos, batch, bt, max_blocks, num_blocks, flag);
   return finish(flag, s, what);
 }
 

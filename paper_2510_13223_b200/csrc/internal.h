@@ -49,6 +49,8 @@ bs_status debug_check_ids(const int32_t* ids, int32_t n, int32_t limit, cudaStre
 bs_status debug_check_table(const int32_t* kv_split, int32_t n_shards, int32_t shard, int32_t batch,
                             const int32_t* bt, int32_t max_blocks, int32_t num_blocks, cudaStream_t s,
                             const char* what);
+bs_status debug_check_append(const int32_t* pos, int32_t batch, const int32_t* bt, int32_t max_blocks,
+                             int32_t num_blocks, cudaStream_t s, const char* what);
 #define BS_DEBUG_CHECK(expr)              \
   do {                                    \
     const bs_status _st = (expr);         \

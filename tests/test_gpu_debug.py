@@ -1,7 +1,7 @@
 """Debug build (BS_DEBUG=1 -> libbanaserve_debug.so): device index arrays
 are validated on the device before the launch; a violation returns BS_ERR_INVALID_ARG
 without launching and sets bs_debug_error_code (1 table id, 2 kv_split vs table width,
-4 migration id).  Runs in a subprocess so the release library of the other tests is not
+4 migration id, 8 append position past the table).  Runs in a subprocess so the release library of the other tests is not
 loaded next to the debug one."""
 import os
 import subprocess
@@ -57,6 +57,18 @@ try:
 except bs.BSError as e:
     assert e.status == bs.BS_ERR_INVALID_ARG
 assert bs.lib().bs_debug_error_code(1) & 2
+# H7 append: valid, position past the table (code 8), block id out of range (code 1)
+kn = torch.zeros(2, 2, 64, dtype=torch.bfloat16, device=dev)
+bs.kv_append_token(pool, 0, kn, kn, bt, i32([3, -1]))
+torch.cuda.synchronize()
+assert bs.lib().bs_debug_error_code(0) == 0
+for p, tab, code in (([16 * bt.shape[1], 0], bt, 8), ([0, 0], bad, 1)):
+    try:
+        bs.kv_append_token(pool, 0, kn, kn, tab, i32(p))
+        raise SystemExit("invalid append accepted")
+    except bs.BSError as e:
+        assert e.status == bs.BS_ERR_INVALID_ARG
+    assert bs.lib().bs_debug_error_code(1) == code, code
 print("debug checks ok")
 '''
 

@@ -20,7 +20,8 @@
  *    when BS_DEBUG=1): there a validation kernel checks them on the device first, the
  *    call synchronises its stream and, on a violation, returns BS_ERR_INVALID_ARG
  *    without launching and ORs a code into bs_debug_error_code (1 block-table id out of
- *    range, 2 kv_split inconsistent with the table width, 4 migration id out of range).
+ *    range, 2 kv_split inconsistent with the table width, 4 migration id out of range,
+ *    8 append position past the table).
  *  - Supported shapes: bf16 KV, block_size 16, head_dim 64 or 128, query group
  *    G = num_q_heads / num_kv_heads in {1, 2, 4, 8}.  Others -> BS_ERR_UNSUPPORTED.
  */

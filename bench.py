@@ -165,6 +165,10 @@ class ClockSampler:
         if self.nvml is not None:
             self.stop.set()
             self.thread.join()
+            try:
+                self.nvml[0].nvmlShutdown()
+            except Exception:
+                pass
         if self.proc is not None:
             self.proc.terminate()
             self.proc.wait()

@@ -252,8 +252,21 @@ def build_workload(bs, device, rank=0, world=1, layers=None, transport="p2p"):
         pg_attn=dist.group.WORLD if world > 1 else None,
         pg_mig=dist.new_group(list(range(world))) if world > 1 else None,
         lookahead=int(os.environ.get("BS_LOOKAHEAD", "-1")), device=device, copy_engine=os.environ.get("BS_HANDOFF_CE", "0") == "1",
-        transport=transport)
+        transport=transport, append=append_inputs(cold, cold_bt, ks, device, L) if (
+            world == 1 and os.environ.get("BS_BENCH_APPEND", "0") == "1") else None)
     return case, pools, step, ks
+
+
+def append_inputs(cold, cold_bt, ks, device, L):
+    """H7 inputs for the N=1 step (BS_BENCH_APPEND=1): each request's last token sits in the
+    cold shard; its K/V rows as they are already stored, so the append rewrites the same
+    bytes every step (the attention results do not change)."""
+    pos = (np.asarray(ks)[:, 2] - np.asarray(ks)[:, 1] - 1).astype(np.int64)
+    blk = torch.as_tensor(np.asarray(cold_bt)[np.arange(len(pos)), pos // 16], device=device)
+    slot = torch.as_tensor(pos % 16, device=device)
+    k_new = torch.stack([cold.data[l, blk, 0, :, slot, :] for l in range(L)]).contiguous()
+    v_new = torch.stack([cold.data[l, blk, 1, :, slot, :] for l in range(L)]).contiguous()
+    return k_new, v_new, torch.as_tensor(pos, dtype=torch.int32, device=device)
 
 
 def handoff_src_ids(case, n):

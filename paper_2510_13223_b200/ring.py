@@ -139,6 +139,11 @@ class CudaOps:
         else:
             self._mig(src, dst, layer, src_ids, dst_ids)
 
+    def append(self, pool, layer, k_new, v_new, block_tables, pos):
+        """H7: the decoded token's K/V into its shard's block (one launch)."""
+        from . import kv_append_token
+        kv_append_token(pool, layer, k_new, v_new, block_tables, pos)
+
     def gather(self, pool, layer, ids, staging):
         self._gather(pool, layer, ids, staging)
 
@@ -270,7 +275,7 @@ class ShardedDecodeStep:
                  handoff_src_ids=None, handoff_dst_ids=None, chunk_bytes: int = 0,
                  pg_attn=None, pg_mig=None, lookahead: int = 1, device=None,
                  fuse_local: bool = True, copy_engine: bool = False, transport: str = "nccl",
-                 fused_exchange: bool = True):
+                 fused_exchange: bool = True, append=None):
         self.ops, self.ex = ops, ex
         self.rank, self.world = rank, world
         self.prev, self.next = (rank - 1) % world, (rank + 1) % world
@@ -299,6 +304,10 @@ class ShardedDecodeStep:
             self.ce_ids = (handoff_src_ids.cpu().tolist(), handoff_dst_ids.cpu().tolist())
         self.pg_attn, self.pg_mig = pg_attn, pg_mig
         self.lookahead = lookahead
+        # H7 at N=1: (k_new [L][B][Hkv][d], v_new, pos [B]) -- each request's decoded token
+        # is written into the cold pool (the shard holding the sequence's end) on the
+        # migration stream, before that layer's mig_done event gates its attention
+        self.append = append if (append is not None and world == 1) else None
         dev = device
         # N=1: both shards are local -> one fused attention + merge launch per layer
         self.fuse_local = fuse_local and world == 1 and hasattr(ops, "attention_local")
@@ -393,7 +402,7 @@ class ShardedDecodeStep:
         if self.transport == "p2p":  # + the tiny signal / wait kernels of the protocol
             return self.L * (3 + mig + 8)
         attn = 1 if self.fuse_local else 3
-        return self.L * (attn + mig)
+        return self.L * (attn + mig + (1 if self.append is not None else 0))
 
     def _migrate(self, layer, mig_s, timers) -> None:
         """H2 of one layer on stream ``mig_s``: the hand-off (N=1: local copy kernel; N>1
@@ -410,6 +419,9 @@ class ShardedDecodeStep:
                     ops.gather(self.cold, layer, self.src_ids, self.stage_send)
                     _sendrecv(self.pg_mig, self.stage_send, self.prev, self.stage_recv, self.next)
                     ops.scatter(self.home, layer, self.dst_ids, self.stage_recv)
+            if self.append is not None:  # H7 rides the migration stream: attention of this
+                k_new, v_new, pos = self.append  # layer waits for mig_done either way
+                ops.append(self.cold, layer, k_new[layer], v_new[layer], self.cold_bt, pos)
             if timers is not None:
                 timers[layer][3].record(mig_s)
             ex.record(E["mig_done"][layer], mig_s)

@@ -514,3 +514,44 @@ def test_fuzz_random_configs(bs, seed):
     assert torch.equal(torch.isfinite(lse2), fin)
     if fin.any():
         assert (lse2[fin] - lse[fin]).abs().max().item() <= 2 * LSE_TOL
+
+
+def test_full_size_c4_gpu_shard_all_requests_layers_0_and_last(bs):
+    """C4 parity on layers {0, L-1} over ALL requests.  One GPU's share of
+    the 8-way split -- shard 3 of all 256 mixed-length requests (empty for the short ones),
+    all 80 layers of the Llama-2-70B shape resident (~60 GB) -- through the ragged plan the
+    C4 microbenchmark times; every request of layers 0 and 79 against the oracle."""
+    shape = synth.LLAMA2_70B
+    lens = synth.mixed_lengths(256, seed=0)
+    ks8 = synth.block_aligned_split(lens, 8)
+    shard_lens = (ks8[:, 4] - ks8[:, 3]).astype(np.int64)
+    ks = np.stack([np.zeros_like(shard_lens), shard_lens], 1).astype(np.int32)
+    case = synth.device_shards(shape, shard_lens, ks, seed=53, device="cuda")
+    pt, bt = case.pools[0], case.block_tables[0]
+    pool = bs.KVPool(shape.n_layers, pt.shape[1], shape.hkv, shape.d, base=pt.reshape(-1))
+    B = len(lens)
+    sc = synth.default_scale(shape.d)
+    plan = bs.attention_ragged_plan(ks, [0], shape.hq, shape.hkv, shape.d).to("cuda")
+    ws = torch.zeros(max(16, plan.workspace_bytes), dtype=torch.uint8, device="cuda")
+    btd, ksd = dev_i32(bt), dev_i32(ks)
+    assert (shard_lens == 0).any() and (shard_lens > 2048).any()
+    for layer in (0, shape.n_layers - 1):
+        out = torch.full((B, shape.hq, shape.d), float("nan"), dtype=torch.bfloat16, device="cuda")
+        lse = torch.full((B, shape.hq), float("nan"), device="cuda")
+        bs.split_decode_attention_local_ragged([pool], layer, case.q[layer], [btd], [0], ksd, sc,
+                                               plan, out, lse, ws)
+        torch.cuda.synchronize()
+        host = pt[layer:layer + 1].cpu().view(torch.int16).numpy().view(np.uint16)
+        q = case.q[layer].cpu().view(torch.int16).numpy().view(np.uint16)
+        o, m, l = oracle.attention_shard(host, 0, q, bt, ks, 0, sc)
+        fin = l > 0
+        ref_lse = np.where(fin, m + np.log(np.where(fin, l, 1.0)), -np.inf)
+        got = out.float().cpu().double().numpy()
+        gl = lse.cpu().double().numpy()
+        assert np.array_equal(np.isneginf(gl), ~fin) and np.all(got[~fin] == 0)
+        err = np.abs(got - o)
+        assert err.max() <= ABS_TOL
+        assert (err.max(-1)[fin] / np.abs(o).max(-1)[fin]).max() <= ROW_REL_TOL
+        assert np.abs(gl[fin] - ref_lse[fin]).max() <= LSE_TOL
+    del case, pool
+    torch.cuda.empty_cache()

@@ -555,3 +555,64 @@ def test_full_size_c4_gpu_shard_all_requests_layers_0_and_last(bs):
         assert np.abs(gl[fin] - ref_lse[fin]).max() <= LSE_TOL
     del case, pool
     torch.cuda.empty_cache()
+
+
+def test_full_size_c5_gpu_share_prefix_migrated_layerwise_layers_0_and_last(bs):
+    """SURVEY.md §8(d) C5 at one GPU's full share (n = 8: requests i mod 8 == 0 of the
+    512-request burst, prompts log-uniform[128, 16k], Llama-3-8B shape, 32 layers): the
+    first half of every request's blocks (prefix hit, r = 0.5) lives in a global-store
+    pool; layer by layer it is migrated (H2, copy stream) into the blocks the request's
+    table points at, and each layer's attention (compute stream) waits for its own
+    migration event (H3).  Layers 0 and 31: migrated blocks bit-exact, every request's
+    attention == oracle."""
+    shape = synth.LLAMA3_8B
+    g = torch.Generator().manual_seed(0)
+    lo, hi = np.log(128.0), np.log(16384.0)
+    lens_all = np.exp(lo + (hi - lo) * torch.rand(512, generator=g).numpy()).astype(np.int64)
+    lens = lens_all[0::8]
+    B = len(lens)
+    ks = np.stack([np.zeros_like(lens), lens], 1).astype(np.int32)
+    case = synth.device_shards(shape, lens, ks, seed=61, device="cuda")
+    pt, bt = case.pools[0], case.block_tables[0]
+    L = shape.n_layers
+    prefix = [int(x) for b in range(B) for x in bt[b, : synth.ceil_div(int(lens[b]), 16) // 2]]
+    pidx = torch.tensor(prefix, dtype=torch.long, device="cuda")
+    store_t = pt.index_select(1, pidx).contiguous()            # the store holds the prefixes
+    pt.index_fill_(1, pidx, float("nan"))                      # not resident on this GPU yet
+    home = bs.KVPool(L, pt.shape[1], shape.hkv, shape.d, base=pt.reshape(-1))
+    store = bs.KVPool(L, store_t.shape[1], shape.hkv, shape.d, base=store_t.reshape(-1))
+    src_ids = dev_i32(np.arange(len(prefix)))
+    dst_ids = dev_i32(prefix)
+    sc = synth.default_scale(shape.d)
+    btd, ksd = dev_i32(bt), dev_i32(ks)
+    o = torch.empty(L, B, shape.hq, shape.d, device="cuda")
+    m = torch.empty(L, B, shape.hq, device="cuda")
+    l = torch.empty(L, B, shape.hq, device="cuda")
+    ws = torch.zeros(max(16, bs.split_decode_attention_workspace_size(home, B, shape.hq, bt.shape[1])),
+                     dtype=torch.uint8, device="cuda")
+    copy_s, comp_s = torch.cuda.Stream(), torch.cuda.Stream()
+    done = [torch.cuda.Event() for _ in range(L)]
+    copy_s.wait_stream(torch.cuda.current_stream())
+    comp_s.wait_stream(torch.cuda.current_stream())
+    for layer in range(L):
+        with torch.cuda.stream(copy_s):
+            bs.kv_migrate_layer(store, home, layer, src_ids, dst_ids, stream=copy_s)
+            done[layer].record(copy_s)
+        with torch.cuda.stream(comp_s):
+            comp_s.wait_event(done[layer])
+            bs.split_decode_attention(home, layer, case.q[layer], btd, ksd, 0, sc, o[layer], m[layer],
+                                      l[layer], ws, stream=comp_s)
+    torch.cuda.synchronize()
+    for layer in (0, L - 1):
+        got_blocks = pt[layer].index_select(0, pidx)
+        assert torch.equal(got_blocks.view(torch.int16), store_t[layer].view(torch.int16))
+        host = pt[layer:layer + 1].cpu().view(torch.int16).numpy().view(np.uint16)
+        q = case.q[layer].cpu().view(torch.int16).numpy().view(np.uint16)
+        ro, rm, rl = oracle.attention_shard(host, 0, q, bt, ks, 0, sc)
+        go = o[layer].cpu().double().numpy()
+        err = np.abs(go - ro)
+        assert err.max() <= PART_TOL
+        glse = (m[layer] + torch.log(l[layer])).cpu().double().numpy()
+        assert np.abs(glse - (rm + np.log(rl))).max() <= LSE_TOL
+    del case, home, store, store_t
+    torch.cuda.empty_cache()

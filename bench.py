@@ -46,7 +46,7 @@ SHAPE = synth.LLAMA2_7B
 BATCH, SEQ, N_SHARDS, N_HANDOFF = 64, 2048, 2, 3
 WORKLOAD = ("C2: Llama-2-7B shape (L=32, Hq=Hkv=32, d=128, bf16 KV), decode B=64 x 2048 "
             "tokens, KV split 2-way decode/prefill pool, 3 x 2048-token requests handed off "
-            "prefill->decode layer-wise per step")
+            "prefill->decode layer-wise per step, each request's decoded-token K/V appended")
 FALLBACK_HBM_GBS = 6650.0
 
 
@@ -252,21 +252,21 @@ def build_workload(bs, device, rank=0, world=1, layers=None, transport="p2p"):
         pg_attn=dist.group.WORLD if world > 1 else None,
         pg_mig=dist.new_group(list(range(world))) if world > 1 else None,
         lookahead=int(os.environ.get("BS_LOOKAHEAD", "-1")), device=device, copy_engine=os.environ.get("BS_HANDOFF_CE", "0") == "1",
-        transport=transport, append=append_inputs(cold, cold_bt, ks, device, L) if (
-            world == 1 and os.environ.get("BS_BENCH_APPEND", "0") == "1") else None)
+        transport=transport, append=append_inputs(rank, device, L) if (
+            os.environ.get("BS_BENCH_APPEND", "1") == "1" and (world == 1 or transport == "p2p"))
+        else None)
     return case, pools, step, ks
 
 
-def append_inputs(cold, cold_bt, ks, device, L):
-    """H7 inputs for the N=1 step (BS_BENCH_APPEND=1): each request's last token sits in the
-    cold shard; its K/V rows as they are already stored, so the append rewrites the same
-    bytes every step (the attention results do not change)."""
-    pos = (np.asarray(ks)[:, 2] - np.asarray(ks)[:, 1] - 1).astype(np.int64)
-    blk = torch.as_tensor(np.asarray(cold_bt)[np.arange(len(pos)), pos // 16], device=device)
-    slot = torch.as_tensor(pos % 16, device=device)
-    k_new = torch.stack([cold.data[l, blk, 0, :, slot, :] for l in range(L)]).contiguous()
-    v_new = torch.stack([cold.data[l, blk, 1, :, slot, :] for l in range(L)]).contiguous()
-    return k_new, v_new, torch.as_tensor(pos, dtype=torch.int32, device=device)
+def append_inputs(rank, device, L):
+    """H7 inputs of the step (on by default; BS_BENCH_APPEND=0 drops H7): the decoded
+    token's K/V of this rank's 64 requests for every layer, kv_new [L][2][B][Hkv][d] bf16,
+    seeded; the step writes them at the end of each request's shard 1 (the cold pool of
+    this rank at N=1, of the next rank at N>1) before that layer's attention."""
+    g = torch.Generator(device=device)
+    g.manual_seed(7777 + rank)
+    return torch.randn((L, 2, BATCH, SHAPE.hkv, SHAPE.d), generator=g, device=device,
+                       dtype=torch.bfloat16)
 
 
 def handoff_src_ids(case, n):
@@ -419,11 +419,18 @@ def run_ours(args, rank, world, device):
 
     qb = q_dev[0].numel() * q_dev.element_size()
     ob, lb = out[0].numel() * out.element_size(), lse[0].numel() * lse.element_size()
+    # H7: the decoded token's K/V are step inputs like q (host -> the step's append buffer)
+    kv_dev = step.append
+    kv_host = kv_dev.cpu().pin_memory() if kv_dev is not None else None
+    kvb = 0 if kv_dev is None else kv_dev[0].numel() * kv_dev.element_size()
 
     def e2e_step():  # every copy through the library's own bs_copy_bytes (C-ABI)
         h2d.wait_stream(cur)
         for layer in range(L):
             bs.copy_ptr(q_dev.data_ptr() + layer * qb, q_host.data_ptr() + layer * qb, qb, stream=h2d)
+            if kv_dev is not None:
+                bs.copy_ptr(kv_dev.data_ptr() + layer * kvb, kv_host.data_ptr() + layer * kvb, kvb,
+                            stream=h2d)
             q_ev[layer].record(h2d)
         step.enqueue(q_dev, out, lse, inputs_ready=q_ev)
         for layer in range(L):
@@ -477,7 +484,8 @@ def run_ours(args, rank, world, device):
             "workload": WORKLOAD,
             "layers": L, "batch": BATCH, "seq_len": SEQ, "num_q_heads": SHAPE.hq,
             "num_kv_heads": SHAPE.hkv, "head_dim": SHAPE.d, "kv_shards": N_SHARDS,
-            "handoff_requests_per_step": N_HANDOFF, "parallelism": (f"ring of {world} instances (home + cold per GPU), {step.transport} transport"
+            "handoff_requests_per_step": N_HANDOFF,
+            "h7_append": step.append is not None, "parallelism": (f"ring of {world} instances (home + cold per GPU), {step.transport} transport"
                             + (", fused exchange (partials stored into the home GPU's workspace, "
                                "last-arriving CTA merges)" if step.fused_exchange else "")
                             + (f" (p2p unavailable: {step.fallback_reason})"
@@ -535,7 +543,8 @@ def run_ours(args, rank, world, device):
         "gpu_launches": step.launches_per_step * K,
         "e2e": {"value": round(BATCH * world / (e2e_ms * 1e-3), 2), "unit": "tokens/s",
                 "ms_per_step": round(e2e_ms, 4),
-                "h2d_bytes_per_step": q.numel() * q.element_size(),
+                "h2d_bytes_per_step": q.numel() * q.element_size() + (
+                    0 if step.append is None else step.append.numel() * step.append.element_size()),
                 "d2h_bytes_per_step": out.numel() * out.element_size() + lse.numel() * lse.element_size()},
         "clocks": clk.summary(),
     }
@@ -562,7 +571,14 @@ def time_oracle_sample(sample, scale):
     sp, sbt, sks, sq, src = sample
     n_chunks = src.shape[1]
     dst = np.empty_like(src)
+    # H7 inputs: each sampled request's decoded token at the end of shard 1 (its stored
+    # rows serve as the new K/V: data preparation, outside the timed region)
+    pos = (sks[:, 2] - sks[:, 1] - 1).astype(np.int32)
+    blk = sbt[1][np.arange(len(pos)), pos // 16]
+    k_new = np.ascontiguousarray(sp[1][0, blk, 0, :, pos % 16, :])
+    v_new = np.ascontiguousarray(sp[1][0, blk, 1, :, pos % 16, :])
     t = time.perf_counter()
+    oracle.append_token(sp[1], 0, k_new, v_new, sbt[1], pos)
     parts = [oracle.attention_shard(p, 0, sq, bt, sks, j, scale) for j, (p, bt) in enumerate(zip(sp, sbt))]
     oracle.merge_partials([x[0] for x in parts], [x[1] for x in parts], [x[2] for x in parts])
     ta = time.perf_counter() - t
@@ -612,7 +628,7 @@ def cpu_baseline(case, budget_s=12.0, reqs_per_sample=32, n_samples=4):
             "value_1_thread": round(BATCH / t_step1, 4),
             "nproc": os.cpu_count(), "cpu_model": cpu_model(),
             "sample": (f"{units} timed (layer, {reqs_per_sample}-request) units from {n_samples} "
-                       f"extracted samples (both shards + LSE merge) + 1 hand-off request's "
+                       f"extracted samples (H7 append + both shards + LSE merge) + 1 hand-off request's "
                        f"chunks each, fp64 C oracle; extrapolated linearly to B={BATCH}, "
                        f"{N_HANDOFF} hand-offs, {SHAPE.n_layers} layers"),
             "measured_seconds": round(ta_tot + tm_tot, 3)}
@@ -647,7 +663,7 @@ def run_reference(args, rank, world, device):
     t_step = SHAPE.n_layers * (ta / args.steps * BATCH / reqs + tm / args.steps * N_HANDOFF)
     v = BATCH / t_step
     cores = omp_threads()
-    sample = (f"per step: 1 layer x {reqs} requests (both shards + merge) + 1 hand-off request's "
+    sample = (f"per step: 1 layer x {reqs} requests (H7 append + both shards + merge) + 1 hand-off request's "
               f"chunks, fp64 C oracle; extrapolated to B={BATCH}, {N_HANDOFF} hand-offs, "
               f"{SHAPE.n_layers} layers")
     return {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "tokens/s",

@@ -204,7 +204,7 @@ class P2PLinks:
     KINDS = ("mig", "q", "part", "q_ack", "part_ack")
 
     def __init__(self, rank, world, num_layers, home_pool, q_like, part_numel, handoff_dst_ids,
-                 device, group, timeout_ms=20000, fused=None):
+                 device, group, timeout_ms=20000, fused=None, kv_like=None):
         from . import ipc_export, ipc_import, pool_view
         self.L = num_layers
         self.flags = torch.zeros(len(self.KINDS) * num_layers, dtype=torch.int32, device=device)
@@ -212,10 +212,14 @@ class P2PLinks:
         self.q_prev = torch.empty_like(q_like)
         self.part_recv = torch.empty((num_layers, part_numel), dtype=torch.float32, device=device)
         self.timeout_ns = int(timeout_ms) * 1_000_000
+        # H7: prev's decoded-token K/V rows [L][2][B][Hkv][d], pushed with its q
+        self.kv_prev = None if kv_like is None else torch.empty_like(kv_like)
         mine = {"flags": ipc_export(self.flags), "q_prev": ipc_export(self.q_prev),
                 "part_recv": ipc_export(self.part_recv), "home": ipc_export(home_pool.data),
                 "home_blocks": home_pool.num_blocks, "device": torch.cuda.current_device(),
                 "handoff_dst": [int(x) for x in handoff_dst_ids.cpu().tolist()]}
+        if self.kv_prev is not None:
+            mine["kv_prev"] = ipc_export(self.kv_prev)
         if fused is not None:
             for k in ("out", "lse", "ws", "done"):
                 mine[k] = ipc_export(fused[k])
@@ -232,6 +236,7 @@ class P2PLinks:
                 self._opened[key] = (ipc_import(h, off), off)
             return self._opened[key][0]
         self.next_q_prev = open_(nxt, "q_prev")
+        self.next_kv_prev = open_(nxt, "kv_prev") if self.kv_prev is not None else None
         self.next_flags = open_(nxt, "flags")
         self.prev_part_recv = open_(prev, "part_recv")
         self.prev_flags = open_(prev, "flags")
@@ -304,10 +309,26 @@ class ShardedDecodeStep:
             self.ce_ids = (handoff_src_ids.cpu().tolist(), handoff_dst_ids.cpu().tolist())
         self.pg_attn, self.pg_mig = pg_attn, pg_mig
         self.lookahead = lookahead
-        # H7 at N=1: (k_new [L][B][Hkv][d], v_new, pos [B]) -- each request's decoded token
-        # is written into the cold pool (the shard holding the sequence's end) on the
-        # migration stream, before that layer's mig_done event gates its attention
-        self.append = append if (append is not None and world == 1) else None
+        # H7: ``append`` = kv_new [L][2][B][Hkv][d] bf16, the decoded token's K/V of this
+        # rank's requests.  The token sits at the end of shard 1 -- this rank's cold pool at
+        # N=1, the next rank's cold pool at N>1 (pushed there with q) -- or, for a request
+        # whose shard 1 is empty, at the end of shard 0 in this rank's home pool.
+        self.append = append
+        if append is not None:
+            import numpy as np
+            ksh = (kv_split.cpu().numpy() if isinstance(kv_split, torch.Tensor) else
+                   np.asarray(kv_split)).astype(np.int64)
+            l0, l1 = ksh[:, 1] - ksh[:, 0], ksh[:, 2] - ksh[:, 1]
+            i32 = lambda x: torch.as_tensor(x.astype(np.int32), device=device)  # noqa: E731
+            self.pos_tail = i32(np.where(l1 > 0, l1 - 1, -1))         # my requests, shard 1
+            self.pos_home = i32(np.where(l1 > 0, -1, l0 - 1)) if (l1 == 0).any() else None
+            if world > 1:
+                kc = self.kv_split_cold
+                kc = (kc.cpu().numpy() if isinstance(kc, torch.Tensor) else np.asarray(kc)).astype(np.int64)
+                c1 = kc[:, 2] - kc[:, 1]
+                self.pos_prev = i32(np.where(c1 > 0, c1 - 1, -1))     # prev's requests, my cold
+            if world > 1 and not (transport == "p2p" and fused_exchange):
+                raise NotImplementedError("H7 append at N>1 needs the fused P2P exchange")
         dev = device
         # N=1: both shards are local -> one fused attention + merge launch per layer
         self.fuse_local = fuse_local and world == 1 and hasattr(ops, "attention_local")
@@ -361,7 +382,7 @@ class ShardedDecodeStep:
                                                   dtype=torch.bfloat16, device=dev),
                                       pn, handoff_dst_ids if handoff_dst_ids is not None else
                                       torch.zeros(0, dtype=torch.int32), dev, pg_attn,
-                                      fused=fused)
+                                      fused=fused, kv_like=append)
             except Exception as e:  # e.g. no peer access between these GPUs
                 ok, why = False, repr(e)
             # every rank must take the same transport: fall back to NCCL unless all mapped
@@ -377,11 +398,12 @@ class ShardedDecodeStep:
             self.q_prev = self.links.q_prev
             self.push = torch.cuda.Stream(device=dev)
             self.merge_s = torch.cuda.Stream(device=dev)
+            self.app_s = torch.cuda.Stream(device=dev)  # H7 appends (wait for prev's push)
             self.fused_exchange = self.links.fused is not None
             if self.fused_exchange:
                 self.hkv = home_pool.num_kv_heads
         self.ev = {k: [ex.event() for _ in range(num_layers)]
-                   for k in ("mig_done", "layer_start", "q_ready", "part_ready")}
+                   for k in ("mig_done", "layer_start", "q_ready", "part_ready", "app_done")}
         self.out_ready = [ex.event() for _ in range(num_layers)]
 
     def _recv_buffer(self, like: torch.Tensor):
@@ -395,16 +417,17 @@ class ShardedDecodeStep:
         + 8 signal / wait kernels of the P2P protocol."""
         mig = 0 if self.n_handoff == 0 or self.ce_ids is not None else (
             1 if self.world == 1 or self.transport == "p2p" else 2)
+        app = 0 if self.append is None else 1 + (self.pos_home is not None)
         if self.transport == "p2p" and self.fused_exchange:
             # 1 fused attention launch; q push + signal, hand-off signal, 1 combined wait,
-            # q-ack signal, done wait (per layer)
-            return self.L * (1 + mig + 6)
+            # q-ack signal, done wait (per layer); H7: q-flag wait + append(s)
+            return self.L * (1 + mig + 6 + (app + 1 if app else 0))
         if self.transport == "p2p":  # + the tiny signal / wait kernels of the protocol
             return self.L * (3 + mig + 8)
         attn = 1 if self.fuse_local else 3
-        return self.L * (attn + mig + (1 if self.append is not None else 0))
+        return self.L * (attn + mig + app)
 
-    def _migrate(self, layer, mig_s, timers) -> None:
+    def _migrate(self, layer, mig_s, timers, inputs_ready=None) -> None:
         """H2 of one layer on stream ``mig_s``: the hand-off (N=1: local copy kernel; N>1
         NCCL transport: gather -> send/recv -> scatter), then its ``mig_done`` event."""
         ex, ops, E = self.ex, self.ops, self.ev
@@ -419,9 +442,13 @@ class ShardedDecodeStep:
                     ops.gather(self.cold, layer, self.src_ids, self.stage_send)
                     _sendrecv(self.pg_mig, self.stage_send, self.prev, self.stage_recv, self.next)
                     ops.scatter(self.home, layer, self.dst_ids, self.stage_recv)
-            if self.append is not None:  # H7 rides the migration stream: attention of this
-                k_new, v_new, pos = self.append  # layer waits for mig_done either way
-                ops.append(self.cold, layer, k_new[layer], v_new[layer], self.cold_bt, pos)
+            if self.append is not None and self.world == 1:  # H7 rides the migration stream:
+                kv = self.append[layer]                      # attention waits for mig_done
+                if inputs_ready is not None:
+                    ex.wait(mig_s, inputs_ready[layer])
+                ops.append(self.cold, layer, kv[0], kv[1], self.cold_bt, self.pos_tail)
+                if self.pos_home is not None:
+                    ops.append(self.home, layer, kv[0], kv[1], self.home_bt, self.pos_home)
             if timers is not None:
                 timers[layer][3].record(mig_s)
             ex.record(E["mig_done"][layer], mig_s)
@@ -459,14 +486,14 @@ class ShardedDecodeStep:
         copies_first = self.lookahead == -3 and self.world == 1 and self.n_handoff > 0
         if copies_first:
             for layer in range(self.L):
-                self._migrate(layer, ex.copy, timers)
+                self._migrate(layer, ex.copy, timers, inputs_ready)
         for layer in range(self.L):
             # ---- H2/H3: migration channel ---------------------------------------------
             if not copies_first:
                 if self.lookahead >= 0 and layer - self.lookahead >= 0:
                     with ex.use(ex.copy):
                         ex.wait(ex.copy, E["layer_start"][layer - self.lookahead])
-                self._migrate(layer, mig_s, timers)
+                self._migrate(layer, mig_s, timers, inputs_ready)
             # ---- H4: attention over both pools -------------------------------------------
             with ex.use(ex.compute):
                 ex.record(E["layer_start"][layer], ex.compute)
@@ -536,16 +563,32 @@ class ShardedDecodeStep:
         own_out = out is not None and out.data_ptr() == F["out"].data_ptr()
         own_lse = lse is None or lse.data_ptr() == F["lse"].data_ptr()
         ob, lb = F["out"][0].numel() * 2, F["lse"][0].numel() * 4
+        app = self.append
+        kvb = 0 if app is None else app[0].numel() * app.element_size()
         ex.begin()
-        for s_ in (self.push, self.merge_s):
+        for s_ in (self.push, self.merge_s, self.app_s):
             s_.wait_stream(torch.cuda.current_stream())
-        with ex.use(ex.comm):  # q of my requests -> next (their cold instance)
+        with ex.use(ex.comm):  # q (+ H7: the token's K/V) of my requests -> next (their cold instance)
             for layer in range(self.L):
                 if inputs_ready is not None:
                     ex.wait(ex.comm, inputs_ready[layer])
                 wait_signal(lk.my_flag("q_ack", layer), e - 1, to, err)
                 copy_ptr(lk.next_q_prev + layer * qb, q[layer].data_ptr(), qb)
+                if app is not None:
+                    copy_ptr(lk.next_kv_prev + layer * kvb, app[layer].data_ptr(), kvb)
                 signal(lk.flag(lk.next_flags, "q", layer), e)
+        if app is not None:  # H7: prev's tokens into my cold pool, mine (empty shard 1) at home
+            with torch.cuda.stream(self.app_s):
+                for layer in range(self.L):
+                    if self.pos_home is not None:
+                        if inputs_ready is not None:
+                            self.app_s.wait_event(inputs_ready[layer])
+                        ops.append(self.home, layer, app[layer][0], app[layer][1], self.home_bt,
+                                   self.pos_home)
+                    wait_signal(lk.my_flag("q", layer), e, to, err)
+                    kv = lk.kv_prev[layer]
+                    ops.append(self.cold, layer, kv[0], kv[1], self.cold_bt, self.pos_prev)
+                    E["app_done"][layer].record(self.app_s)
         for layer in range(self.L):
             with ex.use(ex.copy):  # hand-off: my cold pool -> prev's home pool, pushed
                 if self.lookahead >= 0 and layer - self.lookahead >= 0:
@@ -566,6 +609,8 @@ class ShardedDecodeStep:
                 prev_done = lk.prev_done + 4 * layer
                 wait_signals([lk.my_flag("mig", layer), lk.my_flag("q", layer), my_done, prev_done],
                              [e, e, (e - 1) * per_call, (e - 1) * per_call], to, err)
+                if app is not None:
+                    ex.wait(ex.compute, E["app_done"][layer])
                 if timers is not None:
                     timers[layer][0].record(ex.compute)
                 mine = {"q": q[layer], "kv_split": self.kv_split, "max_blocks": self.mb_mine,
@@ -594,7 +639,7 @@ class ShardedDecodeStep:
                     lse[layer].copy_(F["lse"][layer])
                 self.out_ready[layer].record(self.merge_s)
         cur = torch.cuda.current_stream()
-        for s_ in (self.push, self.merge_s):
+        for s_ in (self.push, self.merge_s, self.app_s):
             cur.wait_stream(s_)
         ex.end()
 

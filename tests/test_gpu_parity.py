@@ -442,6 +442,14 @@ def test_bench_step_c2_sampled():
     step.enqueue(case.q, out, lse)
     torch.cuda.synchronize()
     assert torch.equal(home.data[:, step.dst_ids.long()].view(torch.int16), src_before.view(torch.int16))
+    # H7 in the step: every request's decoded-token K/V sits at the end of its shard 1
+    assert step.append is not None
+    pos = (ks[:, 2] - ks[:, 1] - 1).astype(np.int64)
+    blk = torch.as_tensor(case.block_tables[1][np.arange(len(pos)), pos // 16], device=dev)
+    slot = torch.as_tensor(pos % 16, device=dev)
+    for kv in (0, 1):
+        got_rows = torch.stack([cold.data[l, blk, kv, :, slot, :] for l in range(2)])
+        assert torch.equal(got_rows.view(torch.int16), step.append[:, kv].view(torch.int16))
     sc = synth.default_scale(128)
     sample = [0, 31, 63]
     for layer in range(2):

@@ -392,6 +392,7 @@ class ShardedDecodeStep:
                 self.links = None
                 self.transport = "nccl"
                 self.fallback_reason = why or "a peer could not map the IPC buffers"
+                self.append = None  # H7 at N>1 rides the P2P q push only
         if self.transport == "p2p":
             self.part_recv = [split_partial(self.links.part_recv[layer], self.B, self.hq, self.d)
                               + (None, self.links.part_recv[layer]) for layer in range(num_layers)]

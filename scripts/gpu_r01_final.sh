@@ -12,7 +12,7 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/b
 echo "reference rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:split_decode -s 2 -c 1 -o gpurun_out/bench_attn -f python scripts/profile_bench_attention.py > gpurun_out/ncu_bench_attn.log 2>&1
 echo "ncu full rc=$?"
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'split_decode|copy_pages|merge_partials' --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'split_decode|copy_pages|merge_partials|append_token' --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1
 echo "ncu launches rc=$?"
 BS_RING_SAME_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_n2_same_gpu.json 2> gpurun_out/bench_n2_same_gpu.err
 echo "n2 rc=$?"

@@ -408,29 +408,33 @@ def run_ours(args, rank, world, device):
     # l's attention waits only for its own q), O / lse copied D2H layer by layer as each
     # layer finishes, then the host waits for the step's result (the next decode step needs
     # it).  The copies ride the copy engines under the previous/next layers' compute.
-    q_host = q.cpu().pin_memory()
+    # The step's inputs of layer l -- q_l and (H7) the decoded token's K/V kv_l -- sit
+    # packed in one row [q_l | kv_l] of a pinned host buffer and of a device buffer, so each
+    # layer is ONE copy; the step reads q and its append K/V as strided views of that buffer.
+    kv0 = step.append
+    qb = q[0].numel() * q.element_size()
+    kvb = 0 if kv0 is None else kv0[0].numel() * kv0.element_size()
+    rowb = qb + kvb
+    in_host = torch.empty((L, rowb), dtype=torch.uint8).pin_memory()
+    in_dev = torch.empty((L, rowb), dtype=torch.uint8, device=device)
+    in_host[:, :qb].copy_(q.cpu().view(torch.uint8).reshape(L, qb))
+    q_dev = in_dev[:, :qb].view(q.dtype).view(q.shape)
+    if kv0 is not None:
+        in_host[:, qb:].copy_(kv0.cpu().view(torch.uint8).reshape(L, kvb))
+        step.append = in_dev[:, qb:].view(kv0.dtype).view(kv0.shape)
     out_host = torch.empty(out.shape, dtype=out.dtype).pin_memory()
     lse_host = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
-    q_dev = torch.empty_like(q)
     h2d = torch.cuda.Stream(device=device)
     d2h = torch.cuda.Stream(device=device)
     q_ev = [torch.cuda.Event() for _ in range(L)]
     cur = torch.cuda.current_stream()
-
-    qb = q_dev[0].numel() * q_dev.element_size()
     ob, lb = out[0].numel() * out.element_size(), lse[0].numel() * lse.element_size()
-    # H7: the decoded token's K/V are step inputs like q (host -> the step's append buffer)
-    kv_dev = step.append
-    kv_host = kv_dev.cpu().pin_memory() if kv_dev is not None else None
-    kvb = 0 if kv_dev is None else kv_dev[0].numel() * kv_dev.element_size()
 
     def e2e_step():  # every copy through the library's own bs_copy_bytes (C-ABI)
         h2d.wait_stream(cur)
         for layer in range(L):
-            bs.copy_ptr(q_dev.data_ptr() + layer * qb, q_host.data_ptr() + layer * qb, qb, stream=h2d)
-            if kv_dev is not None:
-                bs.copy_ptr(kv_dev.data_ptr() + layer * kvb, kv_host.data_ptr() + layer * kvb, kvb,
-                            stream=h2d)
+            bs.copy_ptr(in_dev.data_ptr() + layer * rowb, in_host.data_ptr() + layer * rowb, rowb,
+                        stream=h2d)
             q_ev[layer].record(h2d)
         step.enqueue(q_dev, out, lse, inputs_ready=q_ev)
         for layer in range(L):

@@ -284,6 +284,46 @@ def append_cases(iters=200, warm=20):
     return out
 
 
+def push_view_cases(iters=20, warm=5):
+    """The P2P push kernel's own rate: bs_kv_migrate_layer into a remote view (a pool
+    handle whose desc.device is another ordinal) runs on one CTA per SM; emulated over
+    local memory, so this is the issue rate of the capped grid (HBM-bound here), to be
+    compared with NVLink's 900 GB/s per direction the real push is bounded by."""
+    dev = torch.device("cuda")
+    out = []
+    for name, shape, n in (("C2_handoff_384x256KiB", synth.LLAMA2_7B, 384),
+                           ("C4_handoff_512x64KiB", synth.LLAMA3_8B, 512),
+                           ("C2_bulk_8192x256KiB", synth.LLAMA2_7B, 8192)):
+        nb = n + 64
+        src = bs.KVPool(1, nb, shape.hkv, shape.d)
+        dst = bs.KVPool(1, nb, shape.hkv, shape.d)
+        view = bs.pool_view(1, nb, shape.hkv, shape.d, dst.data.data_ptr(),
+                            torch.cuda.current_device() + 1)
+        g = torch.Generator().manual_seed(0)
+        s_ = torch.randperm(nb, generator=g)[:n].to(torch.int32).to(dev)
+        d_ = torch.randperm(nb, generator=g)[:n].to(torch.int32).to(dev)
+        for kind, target in (("remote_view_1cta_per_sm", view), ("local_full_grid", dst)):
+            fn = lambda: bs.kv_migrate_layer(src, target, 0, s_, d_)  # noqa: E731
+            for _ in range(warm):
+                fn()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(iters):
+                fn()
+            b.record()
+            torch.cuda.synchronize()
+            us = a.elapsed_time(b) * 1e3 / iters
+            by = n * src.chunk_bytes
+            r = {"case": f"{name}_{kind}", "us": round(us, 2), "payload_GBps": round(by / (us * 1e-6) / 1e9, 1),
+                 "vs_nvlink_900": round(by / (us * 1e-6) / 1e9 / 900.0, 2)}
+            print(json.dumps(r), flush=True)
+            out.append(r)
+        del src, dst
+        torch.cuda.empty_cache()
+    return out
+
+
 RAGGED_EXTRA_BPS = []
 
 
@@ -375,7 +415,7 @@ DIAG = {
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", choices=["attn", "mig", "tasks", "ragged", "append"])
+    ap.add_argument("--only", choices=["attn", "mig", "tasks", "ragged", "append", "push"])
     ap.add_argument("--case")
     ap.add_argument("--json")
     ap.add_argument("--iters", type=int, default=20)
@@ -425,6 +465,8 @@ def main():
         res += tasks_cases(iters=args.iters)
     if args.only in (None, "append"):
         res += append_cases()
+    if args.only in (None, "push"):
+        res += push_view_cases()
     if args.only in (None, "ragged"):
         RAGGED_EXTRA_BPS.extend(args.ragged_bps)
         res += ragged_cases(iters=args.iters)

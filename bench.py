@@ -253,8 +253,7 @@ def build_workload(bs, device, rank=0, world=1, layers=None, transport="p2p"):
         pg_mig=dist.new_group(list(range(world))) if world > 1 else None,
         lookahead=int(os.environ.get("BS_LOOKAHEAD", "-1")), device=device, copy_engine=os.environ.get("BS_HANDOFF_CE", "0") == "1",
         transport=transport, append=append_inputs(rank, device, L) if (
-            os.environ.get("BS_BENCH_APPEND", "1") == "1" and (world == 1 or transport == "p2p"))
-        else None)
+            os.environ.get("BS_BENCH_APPEND", "1") == "1") else None)
     return case, pools, step, ks
 
 

@@ -327,8 +327,10 @@ class ShardedDecodeStep:
                 kc = (kc.cpu().numpy() if isinstance(kc, torch.Tensor) else np.asarray(kc)).astype(np.int64)
                 c1 = kc[:, 2] - kc[:, 1]
                 self.pos_prev = i32(np.where(c1 > 0, c1 - 1, -1))     # prev's requests, my cold
-            if world > 1 and not (transport == "p2p" and fused_exchange):
-                raise NotImplementedError("H7 append at N>1 needs the fused P2P exchange")
+            if world > 1 and transport == "p2p" and not fused_exchange:
+                raise NotImplementedError("H7 append with the pushed-partials P2P protocol")
+            # NCCL transport: prev's token K/V arrive with its q (torch.distributed P2P)
+            self.kv_prev_buf = torch.empty_like(append) if world > 1 else None
         dev = device
         # N=1: both shards are local -> one fused attention + merge launch per layer
         self.fuse_local = fuse_local and world == 1 and hasattr(ops, "attention_local")
@@ -392,7 +394,6 @@ class ShardedDecodeStep:
                 self.links = None
                 self.transport = "nccl"
                 self.fallback_reason = why or "a peer could not map the IPC buffers"
-                self.append = None  # H7 at N>1 rides the P2P q push only
         if self.transport == "p2p":
             self.part_recv = [split_partial(self.links.part_recv[layer], self.B, self.hq, self.d)
                               + (None, self.links.part_recv[layer]) for layer in range(num_layers)]
@@ -426,7 +427,7 @@ class ShardedDecodeStep:
         if self.transport == "p2p":  # + the tiny signal / wait kernels of the protocol
             return self.L * (3 + mig + 8)
         attn = 1 if self.fuse_local else 3
-        return self.L * (attn + mig + app)
+        return self.L * (attn + mig + app)  # N>1 NCCL: the appends run on the compute stream
 
     def _migrate(self, layer, mig_s, timers, inputs_ready=None) -> None:
         """H2 of one layer on stream ``mig_s``: the hand-off (N=1: local copy kernel; N>1
@@ -477,6 +478,9 @@ class ShardedDecodeStep:
                     if inputs_ready is not None:
                         ex.wait(ex.comm, inputs_ready[layer])
                     _sendrecv(self.pg_attn, q[layer], self.next, self.q_prev[layer], self.prev)
+                    if self.append is not None:  # H7: the token's K/V travel with q
+                        _sendrecv(self.pg_attn, self.append[layer], self.next,
+                                  self.kv_prev_buf[layer], self.prev)
                     ex.record(E["q_ready"][layer], ex.comm)
         # lookahead -2 at N=1: the hand-off copy runs on the compute stream right before its
         # layer's attention (serial) -- both are HBM-bound on one GPU
@@ -512,10 +516,16 @@ class ShardedDecodeStep:
                         timers[layer][1].record(ex.compute)
                     ex.record(self.out_ready[layer], ex.compute)
                     continue
+                if self.append is not None and self.world > 1 and self.pos_home is not None:
+                    ops.append(self.home, layer, self.append[layer][0], self.append[layer][1],
+                               self.home_bt, self.pos_home)
                 ops.attention(self.home, layer, q[layer], self.home_bt, self.kv_split, 0,
                               self.part_own[layer])
                 if self.world > 1:
                     ex.wait(ex.compute, E["q_ready"][layer])
+                    if self.append is not None:  # H7: prev's tokens end its shard 1 here
+                        kv = self.kv_prev_buf[layer]
+                        ops.append(self.cold, layer, kv[0], kv[1], self.cold_bt, self.pos_prev)
                 qc = q[layer] if self.world == 1 else self.q_prev[layer]
                 ops.attention(self.cold, layer, qc, self.cold_bt, self.kv_split_cold, 1,
                               self.part_cold[layer])

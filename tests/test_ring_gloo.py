@@ -3,7 +3,9 @@
 kernels (test infrastructure) and gloo as the transport.  Checks, on every rank:
   * merged O / lse of the rank's own requests == oracle attention over the whole KV,
     although shard 1 lived on the next rank and its partial came back over the wire;
-  * hand-off chunks received from the next rank landed bit-exact in the home pool."""
+  * hand-off chunks received from the next rank landed bit-exact in the home pool;
+  * H7: each request's decoded-token K/V (sent with q to the rank holding the end of its
+    shard 1 and appended there) is part of the KV the attention saw."""
 import os
 import socket
 
@@ -56,6 +58,9 @@ class OracleOps:
         out.copy_(torch.from_numpy(o).to(torch.bfloat16))
         lse.copy_(torch.from_numpy(x))
 
+    def append(self, pool, layer, k_new, v_new, bt, pos):
+        oracle.append_token(pool.data, layer, self._u16(k_new), self._u16(v_new), bt, pos.numpy())
+
     def migrate_local(self, src, dst, layer, s, d, host_ids=None):
         oracle.migrate_layer(src.data, dst.data, layer, s.numpy(), d.numpy())
 
@@ -104,6 +109,11 @@ def run_rank(rank, world, port, errq):
         own, ks, home, cold, free_home, free_cold, nxt = rank_setup(rank, world)
         sc = synth.default_scale(SHAPE.d)
         hp, cp = NpPool(home.pool), NpPool(cold.pool)
+        # H7: the decoded token's K/V of my requests (random), appended at the end of their
+        # shard 1 -- on the next rank, which receives them with q
+        gk = torch.Generator().manual_seed(99 + rank)
+        kv_new = torch.randn((SHAPE.n_layers, 2, len(LENS), SHAPE.hkv, SHAPE.d),
+                             generator=gk).to(torch.bfloat16)
         step = ShardedDecodeStep(
             OracleOps(sc), CpuExec(), rank, world, hp, home.block_tables, cp, cold.block_tables,
             ks, SHAPE.hq, SHAPE.n_layers, SHAPE.d,
@@ -111,12 +121,17 @@ def run_rank(rank, world, port, errq):
             handoff_dst_ids=torch.tensor(free_home, dtype=torch.int64),
             chunk_bytes=oracle.chunk_elems(SHAPE.hkv, 16, SHAPE.d) * 2,
             pg_attn=dist.group.WORLD if world > 1 else None,
-            pg_mig=dist.new_group(list(range(world))) if world > 1 else None)
+            pg_mig=dist.new_group(list(range(world))) if world > 1 else None, append=kv_new)
         q = torch.from_numpy(own.q.view(np.int16)).view(torch.bfloat16)
         out = torch.zeros(q.shape, dtype=torch.bfloat16)
         lse = torch.zeros(q.shape[:-1], dtype=torch.float32)
         step.enqueue(q, out, lse)
-        # reference: the rank's own requests over their whole KV (both shards)
+        # reference: the rank's own requests over their whole KV (both shards), ending with
+        # the appended token
+        bits = kv_new.view(torch.int16).numpy().view(np.uint16)
+        for b, n in enumerate(lens_of(rank)):
+            own.k[b][:, n - 1] = bits[:, 0, b]
+            own.v[b][:, n - 1] = bits[:, 1, b]
         for layer in range(SHAPE.n_layers):
             shards = synth.place_shards(own, ks, seed=rank)
             ref_o, ref_lse = oracle.attention_full([s.pool for s in shards],

@@ -327,8 +327,6 @@ class ShardedDecodeStep:
                 kc = (kc.cpu().numpy() if isinstance(kc, torch.Tensor) else np.asarray(kc)).astype(np.int64)
                 c1 = kc[:, 2] - kc[:, 1]
                 self.pos_prev = i32(np.where(c1 > 0, c1 - 1, -1))     # prev's requests, my cold
-            if world > 1 and transport == "p2p" and not fused_exchange:
-                raise NotImplementedError("H7 append with the pushed-partials P2P protocol")
             # NCCL transport: prev's token K/V arrive with its q (torch.distributed P2P)
             self.kv_prev_buf = torch.empty_like(append) if world > 1 else None
         dev = device
@@ -425,7 +423,7 @@ class ShardedDecodeStep:
             # q-ack signal, done wait (per layer); H7: q-flag wait + append(s)
             return self.L * (1 + mig + 6 + (app + 1 if app else 0))
         if self.transport == "p2p":  # + the tiny signal / wait kernels of the protocol
-            return self.L * (3 + mig + 8)
+            return self.L * (3 + mig + 8 + app)
         attn = 1 if self.fuse_local else 3
         return self.L * (attn + mig + app)  # N>1 NCCL: the appends run on the compute stream
 
@@ -663,15 +661,19 @@ class ShardedDecodeStep:
         e = self.epoch
         to, err = lk.timeout_ns, lk.err.data_ptr()
         qb = q[0].numel() * q.element_size()
+        app = self.append
+        kvb = 0 if app is None else app[0].numel() * app.element_size()
         ex.begin()
         for s_ in (self.push, self.merge_s):
             s_.wait_stream(torch.cuda.current_stream())
-        with ex.use(ex.comm):  # q of my requests -> next (their cold instance)
+        with ex.use(ex.comm):  # q (+ H7: the token's K/V) of my requests -> next
             for layer in range(self.L):
                 if inputs_ready is not None:
                     ex.wait(ex.comm, inputs_ready[layer])
                 wait_signal(lk.my_flag("q_ack", layer), e - 1, to, err)
                 copy_ptr(lk.next_q_prev + layer * qb, q[layer].data_ptr(), qb)
+                if app is not None:
+                    copy_ptr(lk.next_kv_prev + layer * kvb, app[layer].data_ptr(), kvb)
                 signal(lk.flag(lk.next_flags, "q", layer), e)
         for layer in range(self.L):
             with ex.use(ex.copy):  # hand-off: my cold pool -> prev's home pool, pushed
@@ -692,9 +694,15 @@ class ShardedDecodeStep:
                     ex.wait(ex.compute, inputs_ready[layer])
                 if timers is not None:
                     timers[layer][0].record(ex.compute)
+                if app is not None and self.pos_home is not None:
+                    ops.append(self.home, layer, app[layer][0], app[layer][1], self.home_bt,
+                               self.pos_home)
                 ops.attention(self.home, layer, q[layer], self.home_bt, self.kv_split, 0,
                               self.part_own[layer])
                 wait_signal(lk.my_flag("q", layer), e, to, err)    # prev's q arrived
+                if app is not None:  # H7: prev's tokens end its shard 1 in my cold pool
+                    kv = lk.kv_prev[layer]
+                    ops.append(self.cold, layer, kv[0], kv[1], self.cold_bt, self.pos_prev)
                 ops.attention(self.cold, layer, self.q_prev[layer], self.cold_bt, self.kv_split_cold,
                               1, self.part_cold[layer])
                 signal(lk.flag(lk.prev_flags, "q_ack", layer), e)

@@ -64,14 +64,12 @@ def run_rank(rank, world, port, errq, fused):
         i32 = lambda x: torch.as_tensor(np.asarray(x), dtype=torch.int32).cuda()
         dev = torch.device("cuda", 0)
         sc = synth.default_scale(SHAPE.d)
-        # H7 (fused exchange): each request's decoded token K/V, pushed with q to the next
-        # rank, which appends it at the end of shard 1 in its cold pool before attention
-        kv_new = None
-        if fused:
-            gk = torch.Generator(device="cuda")
-            gk.manual_seed(99 + rank)
-            kv_new = torch.randn((SHAPE.n_layers, 2, len(LENS), SHAPE.hkv, SHAPE.d), generator=gk,
-                                 device="cuda", dtype=torch.bfloat16)
+        # H7: each request's decoded token K/V, pushed with q to the next rank, which
+        # appends it at the end of shard 1 in its cold pool before attention
+        gk = torch.Generator(device="cuda")
+        gk.manual_seed(99 + rank)
+        kv_new = torch.randn((SHAPE.n_layers, 2, len(LENS), SHAPE.hkv, SHAPE.d), generator=gk,
+                             device="cuda", dtype=torch.bfloat16)
         step = ShardedDecodeStep(CudaOps(sc), CudaExec(dev), rank, world, hp, i32(home.block_tables),
                                  cp, i32(cold.block_tables), i32(ks), SHAPE.hq, SHAPE.n_layers, SHAPE.d,
                                  handoff_src_ids=i32(free_cold), handoff_dst_ids=i32(free_home),
@@ -86,11 +84,10 @@ def run_rank(rank, world, port, errq, fused):
             torch.cuda.synchronize()
             step.links.check()
             dist.barrier()
-            if kv_new is not None:  # the reference KV ends with the appended token
-                bits = kv_new.cpu().view(torch.int16).numpy().view(np.uint16)
-                for b, n in enumerate(lens_of(rank)):
-                    own.k[b][:, n - 1] = bits[:, 0, b]
-                    own.v[b][:, n - 1] = bits[:, 1, b]
+            bits = kv_new.cpu().view(torch.int16).numpy().view(np.uint16)  # the reference KV
+            for b, n in enumerate(lens_of(rank)):                          # ends with the
+                own.k[b][:, n - 1] = bits[:, 0, b]                         # appended token
+                own.v[b][:, n - 1] = bits[:, 1, b]
             shards = synth.place_shards(own, ks, seed=rank)
             for layer in range(SHAPE.n_layers):
                 ref_o, ref_lse = oracle.attention_full([s.pool for s in shards],

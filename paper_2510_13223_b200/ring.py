@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import contextlib
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -297,7 +298,6 @@ class ShardedDecodeStep:
                 self.kv_split_cold = torch.tensor(everyone[(rank - 1) % world], dtype=kv_split.dtype,
                                                   device=kv_split.device)
             else:
-                import numpy as np
                 self.kv_split_cold = np.asarray(everyone[(rank - 1) % world], dtype=host.dtype)
         self.L, self.hq, self.d = num_layers, num_q_heads, head_dim
         self.B = kv_split.shape[0]
@@ -315,7 +315,6 @@ class ShardedDecodeStep:
         # whose shard 1 is empty, at the end of shard 0 in this rank's home pool.
         self.append = append
         if append is not None:
-            import numpy as np
             ksh = (kv_split.cpu().numpy() if isinstance(kv_split, torch.Tensor) else
                    np.asarray(kv_split)).astype(np.int64)
             l0, l1 = ksh[:, 1] - ksh[:, 0], ksh[:, 2] - ksh[:, 1]

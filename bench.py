@@ -1,26 +1,37 @@
 #!/usr/bin/env python
 """bench.py -- BanaServe (arXiv 2510.13223) hot path on B200: layer-wise KV migration
-overlapped with 2-way split decode attention + exact LSE merge.
+overlapped with split decode attention + exact LSE merge.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config auto|c2|c3|c4]
+                    [--impl ours|reference] [--transport p2p|nccl]
 
-Workload (BASELINE.json configs[1], "C2"): Llama-2-7B shape (32 layers, 32 q/kv heads,
-head_dim 128, bf16 KV), decode batch 64 at 2048 tokens.  Two serving instances --
-decode D (home) and prefill P -- each own a paged pool.  Every request's KV is split
-2-way (tokens [0,1024) in D, [1024,2048) offloaded to P: attention-level migration,
+`--gpus N` > 1 without torchrun re-launches itself under `torch.distributed.run` (N ranks,
+rank r on cuda:r); under torchrun WORLD_SIZE must equal N.  Fewer visible GPUs than N is
+an error (BS_RING_SAME_GPU=1: every rank on cuda:0, a labelled functional check).
+
+Headline workload (BASELINE.json configs[1], "C2"): Llama-2-7B shape (32 layers, 32 q/kv
+heads, head_dim 128, bf16 KV), decode batch 64 at 2048 tokens per GPU.  Two serving
+instances -- decode D (home) and prefill P -- each own a paged pool; every request's KV is
+split 2-way (tokens [0,1024) in D, [1024,2048) offloaded to P: attention-level migration,
 PAPER.md:207-237 Fig. 4).  During each decode step 3 more 2048-token requests are handed
 off P -> D layer by layer on a side stream (Fig. 6; every layer's attention
-waits for its own layer's migration event; the copy stream streams ahead unthrottled --
-BS_LOOKAHEAD=-1, measured 5 % faster than lookahead 1 on one GPU).  At N=1 both instances share GPU 0 (virtual instances).  One step = all 32
-layers of: migrate(l) || [split attention on D, on P -> LSE merge -> bf16 O].
+waits for its own layer's migration event).  At N=1 both instances share GPU 0; at N>1 a
+ring of instances, one per GPU -- rank r is home for its 64 requests and cold instance of
+rank r-1; q, partials and hand-off chunks cross NVLink every layer, pushed into the
+neighbour's IPC-mapped memory (p2p) or through the library's NCCL communicator (nccl).
+Weak scaling: per-GPU work is fixed.
 
-value = decode tokens/s of the step (B / step time), inputs resident in HBM; pools are
-70 GiB >> 126 MB L2, so no L2 flush is needed.  e2e = the same through host buffers
-(q H2D from pinned memory and O/lse D2H every step).  The CPU oracle is timed beside
-it on a bounded sample (cpu_baseline).  N>1 (torchrun): a ring of instances, one per GPU
--- rank r is home for its 64 requests and cold instance of rank r-1 (holds their shard 1
-and their hand-off KV); q, partials and hand-off chunks cross NVLink every layer, pushed
-straight into the neighbour's IPC-mapped memory (--transport p2p, default) or by NCCL P2P (weak scaling: per-GPU work is fixed).  See DESIGN.md §8.
+`--config auto` (default) prints the C2 line and adds, under "extra_configs", the
+sequence-sharded configs of SURVEY.md §8(e) at the same N: C3 (Llama-3-8B GQA, 8 x 32k
+requests split N ways, merge on each request's home GPU; N=1 is the 1-GPU split-K
+baseline) and, at N >= 4, C4 (Llama-2-70B shape, 256 mixed-length requests split N ways,
+8192 tokens of KV handed to the next GPU per layer).  `--config c3|c4` makes one of them
+the headline line instead.
+
+value = decode tokens/s of the step (requests / step time), inputs resident in HBM; every
+step reads >= 4 GiB of distinct KV >> 126 MB L2, so no L2 flush is needed.  e2e = the same
+through host buffers (q H2D from pinned memory, O/lse D2H every step).  The CPU oracle is
+timed beside it on a bounded sample (cpu_baseline, rank 0).  See DESIGN.md §7-8.
 """
 from __future__ import annotations
 
@@ -42,7 +53,7 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 
 METRIC = "split decode-attn HBM GB/s & tokens/s; layer-wise KV migrate NVLink GB/s"
-SHAPE = synth.LLAMA2_7B
+SHAPE = synth.LLAMA2_7B  # C2
 BATCH, SEQ, N_SHARDS, N_HANDOFF = 64, 2048, 2, 3
 WORKLOAD = ("C2: Llama-2-7B shape (L=32, Hq=Hkv=32, d=128, bf16 KV), decode B=64 x 2048 "
             "tokens, KV split 2-way decode/prefill pool, 3 x 2048-token requests handed off "
@@ -209,8 +220,130 @@ class ClockSampler:
                 "samples": len(sm), "sm_mhz_min": min(sm), "source": source}
 
 
+class NvlinkCounters:
+    """NVLink data bytes TX / RX of this GPU (NVML field values 138 / 139, KiB, all links)
+    read right before and after the timed region: an independent count of what crossed
+    NVLink, to corroborate the kernel-event GB/s.  None where NVML lacks the fields."""
+    FIELDS = (138, 139)  # NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX
+
+    def __init__(self, index: int):
+        self.h = self.nv = None
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            p = torch.cuda.get_device_properties(index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            self.h = nv.nvmlDeviceGetHandleByPciBusId_v2(bus)
+            self.nv = nv
+        except Exception:
+            self.h = None
+
+    def read(self):
+        if self.h is None:
+            return None
+        try:
+            vals = self.nv.nvmlDeviceGetFieldValues(self.h, list(self.FIELDS))
+            if any(v.nvmlReturn != 0 for v in vals):
+                return None
+            return [int(v.value.ullVal) * 1024 for v in vals]
+        except Exception:
+            return None
+
+    @staticmethod
+    def delta(a, b, steps):
+        if a is None or b is None:
+            return None
+        return {"tx_bytes_per_step": (b[0] - a[0]) / steps, "rx_bytes_per_step": (b[1] - a[1]) / steps,
+                "source": "NVML field values 138/139 (NVLink data TX/RX, all links), read around "
+                          "the timed region"}
+
+
+def _barrier(world):
+    if world > 1:
+        torch.distributed.barrier()
+
+
+def _release(world):
+    """Free the previous workload's device memory (after every rank unmapped it)."""
+    import gc
+    _barrier(world)
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    _barrier(world)
+
+
+def _allreduce_max(t):
+    """Max over ranks (gloo needs CPU tensors, NCCL device tensors)."""
+    if torch.distributed.get_backend() == "gloo":
+        c = t.cpu()
+        torch.distributed.all_reduce(c, op=torch.distributed.ReduceOp.MAX)
+        return c
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return t
+
+
+def _max_over_ranks(x: float, world: int, device) -> float:
+    t = torch.tensor([float(x)], device=device)
+    if world > 1:
+        t = _allreduce_max(t)
+    return float(t.item())
+
+
+def _all_true(flag: bool, world: int, device) -> bool:
+    if world == 1:
+        return flag
+    return _max_over_ranks(0.0 if flag else 1.0, world, device) == 0.0
+
+
+def step_stats(per_step):
+    """Median, spread and a 95 % CI of the mean over this rank's timed steps (rank 0's
+    steps; the headline ms_per_step is the max over ranks of the mean)."""
+    n = len(per_step)
+    if n == 0:
+        return None
+    mean = statistics.fmean(per_step)
+    sd = statistics.stdev(per_step) if n > 1 else 0.0
+    return {"median": round(statistics.median(per_step), 4), "min": round(per_step[0], 4),
+            "max": round(per_step[-1], 4), "mean": round(mean, 4),
+            "ci95": round(1.96 * sd / n ** 0.5, 4), "n": n,
+            "note": "per-step boundaries are events on the main stream; steps overlap a little "
+                    "(the copy stream runs ahead), the mean over K is the exact figure"}
+
+
+def _same_gpu() -> bool:
+    return os.environ.get("BS_RING_SAME_GPU", "0") == "1"
+
+
+def _time_graph(step, q, out, lse, K, world, device):
+    """Capture one step in a CUDA graph on every rank (flags computed on the device) and
+    time K replays; None on every rank if any rank could not capture."""
+    g, why = None, ""
+    try:
+        g = step.capture(q, out, lse)
+    except Exception as e:
+        why = repr(e)[:200]
+    if not _all_true(g is not None, world, device):
+        return {"error": why or "a peer could not capture"}
+    for _ in range(2):
+        g.replay()
+    torch.cuda.synchronize()
+    _barrier(world)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(K):
+        g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    ms = _max_over_ranks(a.elapsed_time(b) / K, world, device)
+    del g
+    return {"ms_per_step": round(ms, 4), "note": "the whole step (every stream, every layer) "
+            "replayed from one CUDA graph per rank; max over ranks"}
+
+
 # --------------------------------------------------------------------------------------
-# the workload on the device
+# C2: the home/cold ring (headline)
 # --------------------------------------------------------------------------------------
 
 def build_workload(bs, device, rank=0, world=1, layers=None, transport="p2p"):
@@ -244,14 +377,15 @@ def build_workload(bs, device, rank=0, world=1, layers=None, transport="p2p"):
     src_ids = cold.alloc(handoff_blocks)
     assert src_ids == handoff_src_ids(case, handoff_blocks)
     dst_ids = home.alloc(handoff_blocks)
-    i32 = lambda x: torch.as_tensor(np.asarray(x), dtype=torch.int32).to(device)
+    i32 = lambda x: torch.as_tensor(np.asarray(x), dtype=torch.int32).to(device)  # noqa: E731
     step = ShardedDecodeStep(
         CudaOps(synth.default_scale(SHAPE.d)), CudaExec(device), rank, world, home, i32(home_bt),
         cold, i32(cold_bt), i32(ks), SHAPE.hq, L, SHAPE.d, handoff_src_ids=i32(src_ids),
         handoff_dst_ids=i32(dst_ids), chunk_bytes=home.chunk_bytes,
         pg_attn=dist.group.WORLD if world > 1 else None,
         pg_mig=dist.new_group(list(range(world))) if world > 1 else None,
-        lookahead=int(os.environ.get("BS_LOOKAHEAD", "-1")), device=device, copy_engine=os.environ.get("BS_HANDOFF_CE", "0") == "1",
+        lookahead=int(os.environ.get("BS_LOOKAHEAD", "-1")), device=device,
+        copy_engine=os.environ.get("BS_HANDOFF_CE", "0") == "1",
         transport=transport, append=append_inputs(rank, device, L) if (
             os.environ.get("BS_BENCH_APPEND", "1") == "1") else None)
     return case, pools, step, ks
@@ -293,35 +427,27 @@ def attn_bytes_per_layer(ks, fused: bool = True, q_sets: int = 1):
     return tot
 
 
-def step_stats(per_step):
-    """Median, spread and a 95 % CI of the mean over this rank's timed steps (rank 0's
-    steps; the headline ms_per_step is the max over ranks of the mean)."""
-    n = len(per_step)
-    if n == 0:
-        return None
-    mean = statistics.fmean(per_step)
-    sd = statistics.stdev(per_step) if n > 1 else 0.0
-    return {"median": round(statistics.median(per_step), 4), "min": round(per_step[0], 4),
-            "max": round(per_step[-1], 4), "mean": round(mean, 4),
-            "ci95": round(1.96 * sd / n ** 0.5, 4), "n": n,
-            "note": "per-step boundaries are events on the main stream; steps overlap a little "
-                    "(the copy stream runs ahead), the mean over K is the exact figure"}
+def _e2e_buffers(q, extra, L, device):
+    """Pinned host rows + device rows [q_l | extra_l] per layer (one H2D copy per layer)."""
+    qb = q[0].numel() * q.element_size()
+    kvb = 0 if extra is None else extra[0].numel() * extra.element_size()
+    rowb = qb + kvb
+    in_host = torch.empty((L, rowb), dtype=torch.uint8).pin_memory()
+    in_dev = torch.empty((L, rowb), dtype=torch.uint8, device=device)
+    in_host[:, :qb].copy_(q.cpu().view(torch.uint8).reshape(L, qb))
+    q_dev = in_dev[:, :qb].view(q.dtype).view(q.shape)
+    extra_dev = None
+    if extra is not None:
+        in_host[:, qb:].copy_(extra.cpu().view(torch.uint8).reshape(L, kvb))
+        extra_dev = in_dev[:, qb:].view(extra.dtype).view(extra.shape)
+    return in_host, in_dev, rowb, q_dev, extra_dev
 
 
-def _allreduce_max(t):
-    """Max over ranks (gloo needs CPU tensors, NCCL device tensors)."""
-    if torch.distributed.get_backend() == "gloo":
-        c = t.cpu()
-        torch.distributed.all_reduce(c, op=torch.distributed.ReduceOp.MAX)
-        return c
-    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    return t
-
-
-def run_ours(args, rank, world, device):
+def run_c2(args, rank, world, device):
     import paper_2510_13223_b200 as bs
 
     torch.cuda.set_device(device)
+    same_gpu = world > 1 and _same_gpu()
     case, pools, step, ks = build_workload(bs, device, rank, world, transport=args.transport)
     L = SHAPE.n_layers
     q = case.q
@@ -333,14 +459,10 @@ def run_ours(args, rank, world, device):
         lse = torch.empty((L, BATCH, SHAPE.hq), dtype=torch.float32, device=device)
     torch.cuda.synchronize()
 
-    def barrier():
-        if world > 1:
-            torch.distributed.barrier()
-
     for _ in range(args.warmup):
         step.enqueue(q, out, lse)
     torch.cuda.synchronize()
-    barrier()
+    _barrier(world)
     torch.cuda.synchronize()
 
     # ---- timed region: K steps, kernel events live on their launching streams --------
@@ -349,15 +471,20 @@ def run_ours(args, rank, world, device):
               for _ in range(K)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(K - 1)]
+    nvl = NvlinkCounters(device.index) if world > 1 else None
+    nv0 = nvl.read() if nvl else None
     with ClockSampler(torch.cuda.current_device()) as clk:
         t0.record()
+        h0 = time.perf_counter()
         for k in range(K):
             step.enqueue(q, out, lse, timers=timers[k])
             if k < K - 1:
                 step_ev[k].record()
+        host_ms = (time.perf_counter() - h0) * 1e3 / K
         t1.record()
         torch.cuda.synchronize()
-    barrier()
+    nv1 = nvl.read() if nvl else None
+    _barrier(world)
     if step.links is not None:
         step.links.check()
     ms = t0.elapsed_time(t1) / K
@@ -369,8 +496,8 @@ def run_ours(args, rank, world, device):
     n_handoff, step.n_handoff = step.n_handoff, 0
     for _ in range(2):
         step.enqueue(q, out, lse)
-    barrier()
     torch.cuda.synchronize()
+    _barrier(world)
     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     c0.record()
     for _ in range(K):
@@ -394,13 +521,15 @@ def run_ours(args, rank, world, device):
         m1.record()
         torch.cuda.synchronize()
         ms_mig_only = m0.elapsed_time(m1) / K
-    ms_compute = torch.tensor([c0.elapsed_time(c1) / K], device=device)
-    ms_t = torch.tensor([ms], device=device)
-    if world > 1:
-        ms_t = _allreduce_max(ms_t)
-        ms_compute = _allreduce_max(ms_compute)
-    ms_compute = float(ms_compute.item())
-    ms_max = float(ms_t.item())
+    ms_compute = _max_over_ranks(c0.elapsed_time(c1) / K, world, device)
+    ms_max = _max_over_ranks(ms, world, device)
+    host_ms = _max_over_ranks(host_ms, world, device)
+    # ---- the same step replayed from a CUDA graph (N=1 and the P2P transport) ----------
+    graph = None
+    if world == 1 or step.transport == "p2p":
+        graph = _time_graph(step, q, out, lse, K, world, device)
+    if step.links is not None:
+        step.links.check()
 
     # ---- e2e: same step through host buffers ----------------------------------------
     # every step: q copied H2D from pinned memory layer by layer on its own stream (layer
@@ -411,16 +540,9 @@ def run_ours(args, rank, world, device):
     # packed in one row [q_l | kv_l] of a pinned host buffer and of a device buffer, so each
     # layer is ONE copy; the step reads q and its append K/V as strided views of that buffer.
     kv0 = step.append
-    qb = q[0].numel() * q.element_size()
-    kvb = 0 if kv0 is None else kv0[0].numel() * kv0.element_size()
-    rowb = qb + kvb
-    in_host = torch.empty((L, rowb), dtype=torch.uint8).pin_memory()
-    in_dev = torch.empty((L, rowb), dtype=torch.uint8, device=device)
-    in_host[:, :qb].copy_(q.cpu().view(torch.uint8).reshape(L, qb))
-    q_dev = in_dev[:, :qb].view(q.dtype).view(q.shape)
+    in_host, in_dev, rowb, q_dev, kv_dev = _e2e_buffers(q, kv0, L, device)
     if kv0 is not None:
-        in_host[:, qb:].copy_(kv0.cpu().view(torch.uint8).reshape(L, kvb))
-        step.append = in_dev[:, qb:].view(kv0.dtype).view(kv0.shape)
+        step.append = kv_dev
     out_host = torch.empty(out.shape, dtype=out.dtype).pin_memory()
     lse_host = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
     h2d = torch.cuda.Stream(device=device)
@@ -445,17 +567,16 @@ def run_ours(args, rank, world, device):
 
     for _ in range(2):
         e2e_step()
-    barrier()
+    _barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(K):
         e2e_step()
     e1.record()
     torch.cuda.synchronize()
-    e2e_ms = torch.tensor([e0.elapsed_time(e1) / K], device=device)
-    if world > 1:
-        e2e_ms = _allreduce_max(e2e_ms)
-    e2e_ms = float(e2e_ms.item())
+    if step.links is not None:
+        step.links.check()   # every wait of the e2e steps completed in time
+    e2e_ms = _max_over_ranks(e0.elapsed_time(e1) / K, world, device)
     assert torch.equal(out_host.view(torch.int16), out.cpu().view(torch.int16))
 
     # ---- derived numbers ----------------------------------------------------------------
@@ -469,6 +590,26 @@ def run_ours(args, rank, world, device):
     peak, peak_src = peaks()
     traffic, traffic_src = ncu_traffic()
     tokens_s = BATCH * world / (ms_max * 1e-3)
+    if world == 1:
+        rmig = {
+            "bound": "hbm", "kernel": "copy_pages_vec16 (hand-off, copy stream)",
+            "achieved": round(2 * mig_bytes / (mig_avg_ms * 1e-3) / 1e9, 1), "peak": peak,
+            "peak_source": peak_src, "unit": "GB/s",
+            "frac": round(2 * mig_bytes / (mig_avg_ms * 1e-3) / 1e9 / peak, 4),
+            "note": "read + write bytes; in-step, concurrent with the HBM-bound attention",
+            "traffic": ncu_traffic("ncu_copy.json")[0], "traffic_source": ncu_traffic("ncu_copy.json")[1]}
+    elif same_gpu:
+        rmig = None   # no byte crossed NVLink: the ranks share one GPU
+    else:
+        rmig = {
+            "bound": "nvlink", "kernel": ("copy_pages_vec16 push into the peer's pool"
+                                          if step.transport == "p2p" else "gather/NCCL/scatter"),
+            "achieved": round(mig_gbs, 1), "peak": NVLINK_GBS_PER_DIR,
+            "peak_source": "spec (NVLink 5: 900 GB/s per direction per GPU)", "unit": "GB/s",
+            "frac": round(mig_gbs / NVLINK_GBS_PER_DIR, 4),
+            "note": "payload per direction per GPU (every rank sends to prev and receives from next)"}
+    if not mig_bytes:
+        rmig = None
     res = {
         "metric": METRIC,
         "value": round(tokens_s, 2),
@@ -484,17 +625,17 @@ def run_ours(args, rank, world, device):
         "dtype": "bf16",
         "data": "synthetic (seeded N(0,1) bf16 KV/q, Llama-2-7B shape, random-init; no weights)",
         "config": {
-            "workload": WORKLOAD,
+            "workload": WORKLOAD, "name": "c2",
             "layers": L, "batch": BATCH, "seq_len": SEQ, "num_q_heads": SHAPE.hq,
             "num_kv_heads": SHAPE.hkv, "head_dim": SHAPE.d, "kv_shards": N_SHARDS,
             "handoff_requests_per_step": N_HANDOFF,
-            "h7_append": step.append is not None, "parallelism": (f"ring of {world} instances (home + cold per GPU), {step.transport} transport"
+            "h7_append": step.append is not None,
+            "parallelism": (f"ring of {world} instances (home + cold per GPU), {step.transport} transport"
                             + (", fused exchange (partials stored into the home GPU's workspace, "
                                "last-arriving CTA merges)" if step.fused_exchange else "")
                             + (f" (p2p unavailable: {step.fallback_reason})"
                                if getattr(step, "fallback_reason", None) else "")
-                            + (" [ALL RANKS ON ONE GPU: functional check only]"
-                               if os.environ.get("BS_RING_SAME_GPU") == "1" else "")
+                            + (" [ALL RANKS ON ONE GPU: functional check only]" if same_gpu else "")
                             if world > 1 else "1 GPU, 2 virtual instances"),
             "l2": "no flush: resident pools 70 GiB >> 126 MB L2",
         },
@@ -506,7 +647,8 @@ def run_ours(args, rank, world, device):
         "migrate_transport": ("fused copy kernel, local HBM (N=1: both instances on GPU 0)" if world == 1
                               else ("copy kernel pushing into the peer's IPC-mapped pool (P2P, NVLink)"
                                     if step.transport == "p2p" else
-                                    "gather -> NCCL send/recv over NVLink -> scatter")),
+                                    "gather -> NCCL send/recv (library bs_comm) -> scatter")
+                              + (" [same GPU: no NVLink]" if same_gpu else "")),
         "roofline": {
             "bound": "hbm",
             "kernel": ("split_decode_attn_mma, fused local shards + LSE merge (1 launch per layer)"
@@ -520,20 +662,9 @@ def run_ours(args, rank, world, device):
             "algorithmic_bytes_per_layer": a_bytes,
         },
         # the hand-off copy kernel (H2): local HBM read + write at N=1 (sharing HBM with the
-        # attention beside it), NVLink payload per direction at N>1 (spec peak, unmeasured here)
-        "roofline_migrate": ({
-            "bound": "hbm", "kernel": "copy_pages_vec16 (hand-off, copy stream)",
-            "achieved": round(2 * mig_bytes / (mig_avg_ms * 1e-3) / 1e9, 1), "peak": peak,
-            "peak_source": peak_src, "unit": "GB/s",
-            "frac": round(2 * mig_bytes / (mig_avg_ms * 1e-3) / 1e9 / peak, 4),
-            "note": "read + write bytes; in-step, concurrent with the HBM-bound attention",
-            "traffic": ncu_traffic("ncu_copy.json")[0], "traffic_source": ncu_traffic("ncu_copy.json")[1]}
-            if world == 1 else {
-            "bound": "nvlink", "kernel": ("copy_pages_vec16 push into the peer's pool"
-                                          if step.transport == "p2p" else "gather/NCCL/scatter"),
-            "achieved": round(mig_gbs, 1), "peak": NVLINK_GBS_PER_DIR,
-            "peak_source": "spec (NVLink 5: 900 GB/s per direction per GPU)", "unit": "GB/s",
-            "frac": round(mig_gbs / NVLINK_GBS_PER_DIR, 4)}) if mig_bytes else None,
+        # attention beside it), NVLink payload per direction at N>1 on distinct GPUs
+        "roofline_migrate": rmig,
+        "nvlink_counters": NvlinkCounters.delta(nv0, nv1, K) if world > 1 else None,
         "overlap": {"step_ms": round(ms_max, 4), "compute_only_ms": round(ms_compute, 4),
                     "exposure": round((ms_max - ms_compute) / ms_compute, 4),
                     "migrate_only_ms": None if ms_mig_only is None else round(ms_mig_only, 4),
@@ -543,6 +674,8 @@ def run_ours(args, rank, world, device):
                     "note": ("N=1: the hand-off and the attention share one GPU's HBM, so the "
                              "hand-off's bytes cannot be hidden; over NVLink (N>1) its write side "
                              "leaves the GPU") if world == 1 else "N>1"},
+        "host_submit_ms_per_step": round(host_ms, 4),
+        "graph": graph,
         "gpu_launches": step.launches_per_step * K,
         "e2e": {"value": round(BATCH * world / (e2e_ms * 1e-3), 2), "unit": "tokens/s",
                 "ms_per_step": round(e2e_ms, 4),
@@ -551,8 +684,229 @@ def run_ours(args, rank, world, device):
                 "d2h_bytes_per_step": out.numel() * out.element_size() + lse.numel() * lse.element_size()},
         "clocks": clk.summary(),
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline(case, budget_s=args.cpu_seconds)
+    step.close()
+    _barrier(world)
+    return res
+
+
+# --------------------------------------------------------------------------------------
+# C3 / C4: W-way sequence sharding, W = number of GPUs
+# --------------------------------------------------------------------------------------
+
+SEQ_CONFIGS = {
+    "c3": dict(shape=synth.LLAMA3_8B, handoff_tokens=0, scaling="strong",
+               workload="C3: Llama-3-8B GQA (L=32, Hq=32, Hkv=8, d=128, bf16 KV), decode B=8 x "
+                        "32768 tokens, every request's KV split W ways (W = GPUs; block-aligned), "
+                        "request i's home = GPU i mod W merges its W partials (eq. 10)"),
+    "c4": dict(shape=synth.LLAMA2_70B, handoff_tokens=8192, scaling="strong",
+               workload="C4: Llama-2-70B shape (L=80, Hq=64, Hkv=8, d=128, bf16 KV), decode B=256 "
+                        "mixed lengths (50% U{5..40}, 50% log-uniform[2000, 32768], + U{0..511} "
+                        "generated; seed 0), every request split W ways, home = i mod W; per layer "
+                        "8192 tokens (512 chunks) of KV handed to the next GPU"),
+}
+
+
+def seq_lengths(name):
+    if name == "c3":
+        return np.full(8, 32768, dtype=np.int64)
+    return synth.mixed_lengths(256, seed=0)
+
+
+def seq_attn_bytes(shape, ks, rank, W):
+    """Algorithmic bytes of rank r's launch per layer: range r of every request (KV + block
+    table), every home's q (each rank reads all of them) and the merged bf16 O + fp32 lse of
+    the requests whose merge it performs (on average B/W of them)."""
+    B = ks.shape[0]
+    n = (ks[:, rank + 1] - ks[:, rank]).astype(np.int64)
+    kv = int(n.sum()) * 2 * shape.hkv * shape.d * 2
+    bt = int(sum(4 * synth.ceil_div(int(x), shape.bs) for x in n))
+    return kv + bt + B * shape.hq * shape.d * 2 + (B // W) * shape.hq * (shape.d * 2 + 4)
+
+
+def run_seq(args, rank, world, device, name, headline=False):
+    """One W-way sequence-sharded config (W = world) on this rank's GPU."""
+    import paper_2510_13223_b200 as bs
+    from paper_2510_13223_b200.ring import CudaOps
+    from paper_2510_13223_b200.seqshard import SeqShardedStep
+    cfg = SEQ_CONFIGS[name]
+    shape, W = cfg["shape"], world
+    lens = seq_lengths(name)
+    B, L = len(lens), shape.n_layers
+    if B % W:
+        return {"skipped": f"{B} requests do not split over {W} homes"}
+    ks = synth.block_aligned_split(lens, W)
+    n_hand = cfg["handoff_tokens"] // shape.bs
+    my_lens = (ks[:, rank + 1] - ks[:, rank]).astype(np.int64)
+    need = (sum(synth.ceil_div(int(x), shape.bs) for x in my_lens) + 2 * n_hand + 1) * L * \
+        2 * shape.hkv * shape.bs * shape.d * 2
+    free_b = torch.cuda.mem_get_info(device)[0]
+    fits = need + (4 << 30) < free_b
+    if not _all_true(fits, world, device):
+        return {"skipped": f"{name} at W={W}: {need / 1e9:.1f} GB of KV per GPU does not fit "
+                           f"({free_b / 1e9:.1f} GB free)"}
+    pool_t, bt = synth.device_pool(shape, my_lens, synth.shard_seed(7, rank), device,
+                                   spare_blocks=2 * n_hand + 1)
+    pool = bs.KVPool(L, pool_t.shape[1], shape.hkv, shape.d, base=pool_t.reshape(-1))
+    used = set(int(x) for x in bt.ravel() if x >= 0)
+    free = [i for i in range(pool_t.shape[1]) if i not in used]
+    i32 = lambda x: torch.as_tensor(np.asarray(x), dtype=torch.int32, device=device)  # noqa: E731
+    src = i32(free[:n_hand]) if n_hand else None
+    dst = i32(free[n_hand:2 * n_hand]) if n_hand else None
+    transport = "p2p" if args.transport == "p2p" else "collective"
+    step = SeqShardedStep(CudaOps(synth.default_scale(shape.d)), rank, W, pool, i32(bt), i32(ks),
+                          shape.hq, L, shape.d, shape.hkv, device=device,
+                          group=torch.distributed.group.WORLD if W > 1 else None,
+                          transport=transport, handoff_src_ids=src, handoff_dst_ids=dst)
+    same_gpu = W > 1 and _same_gpu()
+    q = synth.device_q(shape, B, 5, device)[:, rank::W].contiguous()
+    own = step.outputs()
+    if own is not None:
+        out, lse = own
+    else:
+        out = torch.empty((L, B // W, shape.hq, shape.d), dtype=torch.bfloat16, device=device)
+        lse = torch.empty((L, B // W, shape.hq), dtype=torch.float32, device=device)
+    p2p = step.transport == "p2p"
+    for _ in range(args.warmup):
+        step.enqueue(q, out, lse)
+    torch.cuda.synchronize()
+    _barrier(world)
+    torch.cuda.synchronize()
+    K = args.steps
+    timers = ([[tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in range(L)]
+               for _ in range(K)] if p2p else None)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nvl = NvlinkCounters(device.index) if W > 1 else None
+    nv0 = nvl.read() if nvl else None
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        t0.record()
+        h0 = time.perf_counter()
+        for k in range(K):
+            if p2p:
+                step.enqueue(q, out, lse, timers=timers[k])
+            else:
+                step.enqueue(q, out, lse)
+        host_ms = (time.perf_counter() - h0) * 1e3 / K
+        t1.record()
+        torch.cuda.synchronize()
+    nv1 = nvl.read() if nvl else None
+    _barrier(world)
+    step.check()
+    ms_max = _max_over_ranks(t0.elapsed_time(t1) / K, world, device)
+    host_ms = _max_over_ranks(host_ms, world, device)
+    # compute-only steps (no hand-off) -> exposure of the hand-off
+    ms_compute = None
+    if n_hand:
+        step.n_handoff = 0
+        for _ in range(2):
+            step.enqueue(q, out, lse)
+        torch.cuda.synchronize()
+        _barrier(world)
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record()
+        for _ in range(K):
+            step.enqueue(q, out, lse)
+        c1.record()
+        torch.cuda.synchronize()
+        step.n_handoff = n_hand
+        ms_compute = _max_over_ranks(c0.elapsed_time(c1) / K, world, device)
+    graph = _time_graph(step, q, out, lse, K, world, device) if p2p else None
+    step.check()
+    # e2e through host buffers (P2P transport): q H2D per layer, O / lse D2H per layer
+    e2e = None
+    if p2p:
+        in_host, in_dev, rowb, q_dev, _ = _e2e_buffers(q, None, L, device)
+        out_host = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+        lse_host = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
+        h2d, d2h = torch.cuda.Stream(device=device), torch.cuda.Stream(device=device)
+        q_ev = [torch.cuda.Event() for _ in range(L)]
+        cur = torch.cuda.current_stream()
+        ob, lb = out[0].numel() * out.element_size(), lse[0].numel() * lse.element_size()
+
+        def e2e_step():
+            h2d.wait_stream(cur)
+            for layer in range(L):
+                bs.copy_ptr(in_dev.data_ptr() + layer * rowb, in_host.data_ptr() + layer * rowb,
+                            rowb, stream=h2d)
+                q_ev[layer].record(h2d)
+            step.enqueue(q_dev, out, lse, inputs_ready=q_ev)
+            for layer in range(L):
+                d2h.wait_event(step.out_ready[layer])
+                bs.copy_ptr(out_host.data_ptr() + layer * ob, out.data_ptr() + layer * ob, ob,
+                            stream=d2h)
+                bs.copy_ptr(lse_host.data_ptr() + layer * lb, lse.data_ptr() + layer * lb, lb,
+                            stream=d2h)
+            cur.wait_stream(d2h)
+            cur.synchronize()
+        for _ in range(2):
+            e2e_step()
+        _barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(K):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        step.check()
+        e2e_ms = _max_over_ranks(e0.elapsed_time(e1) / K, world, device)
+        e2e = {"value": round(B / (e2e_ms * 1e-3), 2), "unit": "tokens/s",
+               "ms_per_step": round(e2e_ms, 4),
+               "h2d_bytes_per_step": q.numel() * q.element_size(),
+               "d2h_bytes_per_step": out.numel() * out.element_size() + lse.numel() * lse.element_size(),
+               "note": "per rank: its home requests' q in, their O / lse out; max over ranks"}
+    a_bytes = seq_attn_bytes(shape, ks, rank, W)
+    peak, peak_src = peaks()
+    res = {"metric": METRIC, "value": round(B / (ms_max * 1e-3), 2), "unit": "tokens/s",
+           "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": round(ms_max, 4),
+           "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "bf16",
+           "data": "synthetic (seeded N(0,1) bf16 KV/q, random-init; no weights)",
+           "config": {"workload": cfg["workload"], "name": name, "layers": L, "batch": B,
+                      "context_tokens": int(lens.sum()), "kv_shards": W,
+                      "num_q_heads": shape.hq, "num_kv_heads": shape.hkv, "head_dim": shape.d,
+                      "handoff_tokens_per_layer": cfg["handoff_tokens"],
+                      "parallelism": (f"{W}-way sequence sharding, {step.transport} transport"
+                                      + (", fused exchange (partials into each home's workspace, "
+                                         "last-arriving CTA merges)" if p2p else "")
+                                      + (" [ALL RANKS ON ONE GPU: functional check only]"
+                                         if same_gpu else "")),
+                      "l2": "no flush: every step reads >= 4 GiB of distinct KV per GPU >> 126 MB L2"},
+           "host_submit_ms_per_step": round(host_ms, 4), "graph": graph,
+           "gpu_launches": step.launches_per_step * K, "e2e": e2e, "clocks": clk.summary(),
+           "nvlink_counters": NvlinkCounters.delta(nv0, nv1, K) if W > 1 else None}
+    if p2p:
+        attn_ms = [a.elapsed_time(b) for tk in timers for (a, b, _, _) in tk]
+        attn_avg = statistics.fmean(attn_ms)
+        gbs = a_bytes / (attn_avg * 1e-3) / 1e9
+        res["attn_hbm_gbs_per_gpu"] = round(gbs, 1)
+        res["attn_ms_per_layer"] = round(attn_avg, 5)
+        res["roofline"] = {"bound": "hbm", "kernel": "split_decode_attn_mma via "
+                           "bs_split_decode_attention_tasks (range r of every home's requests)",
+                           "achieved": round(gbs, 1), "peak": peak, "peak_source": peak_src,
+                           "unit": "GB/s", "frac": round(gbs / peak, 4), "traffic": None,
+                           "algorithmic_bytes_per_layer": a_bytes, "rank": rank}
+        # exchange + merge tail: what the step spends per layer beyond the attention
+        # launch itself (q push, flag waits, remote partial stores and merges)
+        res["exchange_ms_per_layer"] = round(max(ms_max / L - attn_avg, 0.0), 5)
+        if n_hand:
+            mig = [c.elapsed_time(d) for tk in timers for (_, _, c, d) in tk]
+            mig_avg = statistics.fmean(mig)
+            mb = n_hand * pool.chunk_bytes
+            res["migrate_bytes_per_layer"] = mb
+            res["migrate_gbs"] = round(mb / (mig_avg * 1e-3) / 1e9, 1)
+            res["roofline_migrate"] = None if (W == 1 or same_gpu) else {
+                "bound": "nvlink", "kernel": "copy_pages_vec16 push into the next GPU's pool",
+                "achieved": res["migrate_gbs"], "peak": NVLINK_GBS_PER_DIR,
+                "peak_source": "spec (NVLink 5: 900 GB/s per direction per GPU)", "unit": "GB/s",
+                "frac": round(res["migrate_gbs"] / NVLINK_GBS_PER_DIR, 4)}
+    if ms_compute is not None:
+        res["overlap"] = {"step_ms": round(ms_max, 4), "compute_only_ms": round(ms_compute, 4),
+                          "exposure": round((ms_max - ms_compute) / ms_compute, 4),
+                          "migrate_bytes_per_step": n_hand * pool.chunk_bytes * L}
+    if headline and rank == 0 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline_seq(name, budget_s=args.cpu_seconds)
+    step.close()
+    _barrier(world)
     return res
 
 
@@ -633,52 +987,176 @@ def cpu_baseline(case, budget_s=12.0, reqs_per_sample=32, n_samples=4):
             "sample": (f"{units} timed (layer, {reqs_per_sample}-request) units from {n_samples} "
                        f"extracted samples (H7 append + both shards + LSE merge) + 1 hand-off request's "
                        f"chunks each, fp64 C oracle; extrapolated linearly to B={BATCH}, "
-                       f"{N_HANDOFF} hand-offs, {SHAPE.n_layers} layers"),
+                       f"{N_HANDOFF} hand-offs, {SHAPE.n_layers} layers (one GPU's share)"),
+            "measured_seconds": round(ta_tot + tm_tot, 3)}
+
+
+class SeqOracleSample:
+    """A bounded host sample of a sequence-sharded config for the oracle: a few seeded
+    requests of one layer with their KV in W shard pools (the config's split), plus the
+    hand-off chunks of one layer; extrapolated to the full step by context tokens."""
+
+    def __init__(self, name, W, n_req=2):
+        cfg = SEQ_CONFIGS[name]
+        self.shape, self.name, self.W = cfg["shape"], name, W
+        self.lens_all = seq_lengths(name)
+        # the requests at the 50th and 90th length percentiles (mixed-length batches: the
+        # long ones carry most of the work the extrapolation scales to)
+        order = np.argsort(self.lens_all, kind="stable")
+        qs = np.linspace(0.5, 0.9, n_req) if n_req > 1 else np.array([0.5])
+        pick = np.sort(order[(qs * (len(order) - 1)).round().astype(int)])
+        lens = self.lens_all[pick]
+        ks = synth.block_aligned_split(lens, W)
+        one = synth.Shape(1, self.shape.hq, self.shape.hkv, self.shape.d)
+        case = synth.device_shards(one, lens, ks, seed=31, device="cpu", layers=1)
+        self.sample = synth.extract_requests(case, list(range(n_req)), 0)
+        self.tokens = int(lens.sum())
+        self.n_hand = cfg["handoff_tokens"] // self.shape.bs
+        cb = 2 * self.shape.hkv * self.shape.bs * self.shape.d
+        self.src = np.zeros((1, max(self.n_hand, 1), cb), dtype=np.uint16) if self.n_hand else None
+        self.scale = synth.default_scale(self.shape.d)
+
+    def time_once(self):
+        import oracle
+        sp, sbt, sks, sq = self.sample
+        t = time.perf_counter()
+        parts = [oracle.attention_shard(p, 0, sq, bt, sks, j, self.scale)
+                 for j, (p, bt) in enumerate(zip(sp, sbt))]
+        oracle.merge_partials([x[0] for x in parts], [x[1] for x in parts], [x[2] for x in parts])
+        ta = time.perf_counter() - t
+        tm = 0.0
+        if self.src is not None:
+            src = self.src.reshape(1, self.n_hand, 2, self.shape.hkv, self.shape.bs, self.shape.d)
+            dst = np.empty_like(src)
+            t = time.perf_counter()
+            oracle.migrate_layer(src, dst, 0, np.arange(self.n_hand), np.arange(self.n_hand))
+            tm = time.perf_counter() - t
+        return ta, tm
+
+    def step_seconds(self, ta, tm):
+        """Full step: L layers x (all requests' attention scaled by context tokens + each
+        rank's hand-off chunks)."""
+        scale_tokens = float(self.lens_all.sum()) / self.tokens
+        return self.shape.n_layers * (ta * scale_tokens + tm * self.W)
+
+    def describe(self, units):
+        return (f"{units} timed units of 1 layer x {len(self.sample[3])} requests ({self.tokens} "
+                f"context tokens, all {self.W} shards + LSE merge"
+                + (f", + {self.n_hand} hand-off chunks" if self.n_hand else "")
+                + f"), fp64 C oracle; extrapolated by context tokens to all {len(self.lens_all)} "
+                f"requests and {self.shape.n_layers} layers")
+
+
+def cpu_baseline_seq(name, budget_s=12.0):
+    import oracle
+    oracle.lib()
+    W = max(1, int(os.environ.get("WORLD_SIZE", "1")))
+    smp = SeqOracleSample(name, W)
+    ta_tot = tm_tot = 0.0
+    units = 0
+    while units < 200 and ta_tot + tm_tot < budget_s:
+        ta, tm = smp.time_once()
+        ta_tot += ta
+        tm_tot += tm
+        units += 1
+    t_step = smp.step_seconds(ta_tot / units, tm_tot / units)
+    B = len(smp.lens_all)
+    return {"value": round(B / t_step, 4), "unit": "tokens/s", "kind": "oracle", "cores": omp_threads(),
+            "nproc": os.cpu_count(), "cpu_model": cpu_model(), "sample": smp.describe(units),
             "measured_seconds": round(ta_tot + tm_tot, 3)}
 
 
 def run_reference(args, rank, world, device):
-    """--impl reference: the CPU oracle as the reference arm, per step a bounded sample."""
+    """--impl reference: the CPU oracle as the reference arm, per step a bounded sample of
+    the same workload.  `ms_per_step` is the MEASURED time of one timed step (one sample);
+    `value` extrapolates that sample to the full step (stated in `extrapolation`)."""
     import oracle
 
     oracle.lib()
-    # the same seeded workload, laid out by synth (torch RNG) only -- no product code
-    gen_dev = device if torch.cuda.is_available() else torch.device("cpu")
-    nl = 2 if torch.cuda.is_available() else 1
-    lens = np.full(BATCH, SEQ, dtype=np.int64)
-    ks = synth.block_aligned_split(lens, N_SHARDS)
-    handoff_chunks = synth.ceil_div(SEQ, SHAPE.bs)
-    case = synth.device_shards(SHAPE, lens, ks, seed=0, device=gen_dev,
-                               spare_blocks=N_HANDOFF * handoff_chunks, layers=nl)
-    scale = synth.default_scale(SHAPE.d)
-    reqs = 32   # ~70 ms of oracle work per step on 16 cores: a stable sample, minutes at most
-    samples = [oracle_sample(case, [(reqs * i + r) % BATCH for r in range(reqs)], i % nl,
-                             handoff_chunks) for i in range(2)]
+    cores = omp_threads()
+    name = "c2" if args.config in ("auto", "c2") else args.config
+    if name == "c2":
+        # the same seeded workload, laid out by synth (torch RNG) only -- no product code
+        gen_dev = device if torch.cuda.is_available() else torch.device("cpu")
+        nl = 2 if torch.cuda.is_available() else 1
+        lens = np.full(BATCH, SEQ, dtype=np.int64)
+        ks = synth.block_aligned_split(lens, N_SHARDS)
+        handoff_chunks = synth.ceil_div(SEQ, SHAPE.bs)
+        case = synth.device_shards(SHAPE, lens, ks, seed=0, device=gen_dev,
+                                   spare_blocks=N_HANDOFF * handoff_chunks, layers=nl)
+        scale = synth.default_scale(SHAPE.d)
+        reqs = 32   # ~70 ms of oracle work per step on 16 cores: a stable sample, minutes at most
+        samples = [oracle_sample(case, [(reqs * i + r) % BATCH for r in range(reqs)], i % nl,
+                                 handoff_chunks) for i in range(2)]
+        one = lambda i: time_oracle_sample(samples[i % 2], scale)  # noqa: E731
+        full = lambda ta, tm: SHAPE.n_layers * (ta * BATCH / reqs + tm * N_HANDOFF)  # noqa: E731
+        B, workload = BATCH * world, WORKLOAD
+        sample = (f"per step: 1 layer x {reqs} requests (H7 append + both shards + merge) + 1 "
+                  f"hand-off request's chunks, fp64 C oracle")
+        extrap = (f"x {BATCH // reqs} requests x {N_HANDOFF} hand-offs x {SHAPE.n_layers} layers "
+                  f"(x {world} GPUs' shares, serially)")
+        full_b = lambda ta, tm: full(ta, tm) * world  # noqa: E731
+    else:
+        smp = SeqOracleSample(name, world)
+        one = lambda i: smp.time_once()  # noqa: E731
+        full_b = smp.step_seconds
+        B, workload = len(smp.lens_all), SEQ_CONFIGS[name]["workload"]
+        sample = "per step: " + smp.describe(1)
+        extrap = "by context tokens to the whole batch and all layers"
     for i in range(args.warmup):
-        time_oracle_sample(samples[i % 2], scale)
+        one(i)
     ta = tm = 0.0
     t0 = time.perf_counter()
     for i in range(args.steps):
-        a, m = time_oracle_sample(samples[i % 2], scale)
+        a, m = one(i)
         ta += a
         tm += m
     wall = time.perf_counter() - t0
-    t_step = SHAPE.n_layers * (ta / args.steps * BATCH / reqs + tm / args.steps * N_HANDOFF)
-    v = BATCH / t_step
-    cores = omp_threads()
-    sample = (f"per step: 1 layer x {reqs} requests (H7 append + both shards + merge) + 1 hand-off request's "
-              f"chunks, fp64 C oracle; extrapolated to B={BATCH}, {N_HANDOFF} hand-offs, "
-              f"{SHAPE.n_layers} layers")
+    t_full = full_b(ta / args.steps, tm / args.steps)
+    v = B / t_full
     return {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "tokens/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(t_step * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": round(wall / args.steps * 1e3, 3),
+            "extrapolation": {"full_step_ms": round(t_full * 1e3, 3), "how": extrap,
+                              "note": "value = requests / full_step_ms (extrapolated from the "
+                                      "measured sample); ms_per_step is the measured sample time"},
+            "higher_is_better": True, "scaling": "weak" if name == "c2" else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "parallelism": "CPU oracle"},
+            "config": {"workload": workload, "name": name, "parallelism": "CPU oracle"},
             "cpu_baseline": {"value": round(v, 4), "unit": "tokens/s", "kind": "oracle",
                              "cores": cores, "sample": sample},
             "e2e": {"value": round(v, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
             "measured_seconds": round(wall, 3)}
+
+
+# --------------------------------------------------------------------------------------
+# launch
+# --------------------------------------------------------------------------------------
+
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def self_launch(n: int) -> int:
+    """`--gpus N` (N > 1) outside torchrun: re-run this script under torch.distributed.run,
+    one rank per GPU; rank 0 prints the JSON line.  Returns the launcher's exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    log("bench.py: launching", n, "ranks:", " ".join(cmd))
+    return subprocess.call(cmd)
+
+
+def fail(msg: str, code: int = 2):
+    print(json.dumps({"metric": METRIC, "error": msg}), flush=True)
+    log("bench.py: error:", msg)
+    sys.exit(code)
 
 
 def main():
@@ -687,35 +1165,67 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=["auto", "c2", "c3", "c4"], default="auto",
+                    help="auto: C2 headline + C3 (and C4 at N>=4) under extra_configs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--transport", choices=["p2p", "nccl"], default=os.environ.get("BS_TRANSPORT", "p2p"),
-                    help="N>1 exchange: CUDA-IPC pushes + flags (p2p) or torch.distributed NCCL P2P")
+                    help="N>1 exchange: CUDA-IPC pushes + flags (p2p) or the library's NCCL "
+                         "communicator (nccl)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: --warmup < 3 violates the timing rules; using 3")
         args.warmup = 3
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        if args.impl == "ours" and not _same_gpu() and torch.cuda.device_count() < args.gpus:
+            fail(f"--gpus {args.gpus} but only {torch.cuda.device_count()} GPU(s) visible "
+                 "(BS_RING_SAME_GPU=1 runs every rank on cuda:0 as a functional check)")
+        sys.exit(self_launch(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # functional check of the N>1 path on a 1-GPU box: every rank on cuda:0 (time-sliced,
-    # numbers meaningless), gloo for the host plumbing, P2P transport
-    same_gpu = os.environ.get("BS_RING_SAME_GPU", "0") == "1"
-    device = torch.device("cuda", 0 if same_gpu else local)
+    if world != args.gpus:
+        fail(f"WORLD_SIZE={world} but --gpus {args.gpus}: launch one rank per GPU")
+    same_gpu = _same_gpu()
     if args.impl == "reference":  # rank 0 alone runs it; other ranks exit without work
+        device = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
         if rank == 0:
             print(json.dumps(run_reference(args, rank, world, device)), flush=True)
         return
+    if world > 1 and not same_gpu and torch.cuda.device_count() < world:
+        fail(f"{world} ranks but {torch.cuda.device_count()} GPU(s) visible")
+    # functional check of the N>1 path on a 1-GPU box: every rank on cuda:0 (time-sliced,
+    # numbers meaningless), gloo for the host plumbing, P2P transport
+    device = torch.device("cuda", 0 if same_gpu else local)
+    torch.cuda.set_device(device)
     if world > 1:
-        torch.cuda.set_device(device)
         if same_gpu:
             args.transport = "p2p"
             torch.distributed.init_process_group("gloo")
         else:
             torch.distributed.init_process_group("nccl", device_id=device)
     try:
-        res = run_ours(args, rank, world, device)
+        head = "c2" if args.config == "auto" else args.config
+        if head == "c2":
+            res = run_c2(args, rank, world, device)
+        else:
+            res = run_seq(args, rank, world, device, head, headline=True)
+            if "skipped" in res:
+                fail(res["skipped"])
+        if args.config == "auto":
+            extras = {}
+            for name in ("c3", "c4"):
+                if name == "c4" and world < 4:
+                    extras[name] = {"skipped": "C4's 457-533 GB of KV needs >= 4 GPUs"}
+                    continue
+                _release(world)
+                try:
+                    extras[name] = run_seq(args, rank, world, device, name)
+                except Exception as e:  # report, keep the headline line
+                    extras[name] = {"error": repr(e)[:300]}
+                    log(f"extra config {name} failed:", repr(e))
+            res["extra_configs"] = extras
         if rank == 0:
             print(json.dumps(res), flush=True)
     finally:

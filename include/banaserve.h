@@ -263,9 +263,11 @@ bs_status bs_split_decode_attention_local_ragged(
  *   q          bf16 [batch][num_q_heads][head_dim] (readable by the launching GPU)
  *   kv_split   DEVICE int32 [batch][n_shards+1] (the launching GPU's copy)
  *   max_blocks HOST int32 [n_shards]: block-table width of EVERY shard of the problem
- *              (n_shards <= 16); together with batch / heads / head_dim / the SM count it
- *              fixes the range plan, so every GPU must pass the same values and be the
- *              same GPU model
+ *              (n_shards <= 16); together with batch / heads / head_dim it fixes the
+ *              range plan, so every GPU must pass the same values.  The plan uses only
+ *              these rank-invariant inputs (a fixed 148 x 3 CTA-slot model, no device
+ *              query, no environment switch), so GPUs of different SM counts or
+ *              environments still cut the ranges identically
  *   out, lse   home GPU bf16 [batch][num_q_heads][head_dim], fp32 [batch][num_q_heads]
  *              (lse may be NULL)
  *   workspace  home GPU scratch of bs_attention_problem_workspace_size bytes, zero-filled
@@ -394,6 +396,15 @@ bs_status bs_comm_destroy(bs_comm* comm);
  * H5 partial exchange: a partial is one contiguous fp32 buffer [o~ | m | l]. */
 bs_status bs_sendrecv(bs_comm* comm, const void* sendbuf, size_t send_bytes, int32_t send_peer,
                       void* recvbuf, size_t recv_bytes, int32_t recv_peer, void* stream);
+/* Many sends and receives of raw bytes in ONE NCCL group (HOST arrays of n_send /
+ * n_recv entries; DEVICE buffers): the W-way exchanges of the sequence-sharded step --
+ * q of a home to every peer (an all-gather), each shard's partial (o~, m, l) to its
+ * request's home ("O^(1) (or E^(2)) is sent back").  Zero-byte entries are
+ * skipped; every rank must post matching pairs.  Returns BS_ERR_NCCL on an NCCL error. */
+bs_status bs_exchange(bs_comm* comm, int32_t n_send, const void* const* send_bufs,
+                      const size_t* send_bytes, const int32_t* send_peers, int32_t n_recv,
+                      void* const* recv_bufs, const size_t* recv_bytes, const int32_t* recv_peers,
+                      void* stream);
 /* H2 over NCCL: gather chunk(layer, src_ids[i]) into staging (n * chunk bytes, DEVICE)
  * and send it to `peer`; the peer's bs_kv_recv_layer receives into its staging and
  * scatters to chunk(layer, dst_ids[i]).  Bit-exact, same pair order on both sides. */
@@ -428,6 +439,22 @@ bs_status bs_signals(int32_t n, int32_t* const* flags, int32_t value, void* stre
  * flags / values are HOST arrays (of device pointers / values). */
 bs_status bs_wait_signals(int32_t n, const int32_t* const* flags, const int32_t* values,
                           uint64_t timeout_ns, int32_t* err, void* stream);
+/* "*flag >= value" is wrap-safe: flags and counters are int32 and wrap after 2^31, so a
+ * wait is satisfied when (int32_t)(*flag - value) >= 0 (the two are always within 2^31).
+ * err may point to device memory or to page-locked host memory (the host can poll it
+ * without synchronising); a timeout stores 1 there with a system-scope store.
+ *
+ * Device-epoch variants, for steps captured in a CUDA graph: the value of
+ * flag i is computed on the device when the kernel runs, (*epoch) * mul[i] + add[i]
+ * (int32, wrapping), so a replayed graph signals / waits for the current step.  epoch:
+ * DEVICE int32 step counter owned by the caller; bs_epoch_advance enqueues *epoch += 1.
+ * flags / mul / add: HOST arrays of n (1..16) entries. */
+bs_status bs_signals_epoch(int32_t n, int32_t* const* flags, const int32_t* mul, const int32_t* add,
+                           const int32_t* epoch, void* stream);
+bs_status bs_wait_signals_epoch(int32_t n, const int32_t* const* flags, const int32_t* mul,
+                                const int32_t* add, const int32_t* epoch, uint64_t timeout_ns,
+                                int32_t* err, void* stream);
+bs_status bs_epoch_advance(int32_t* epoch, void* stream);
 bs_status bs_ipc_export(const void* dev_ptr, void* handle_out, size_t* offset_out);
 bs_status bs_ipc_import(const void* handle, size_t offset, void** dev_ptr_out);
 bs_status bs_ipc_close(void* dev_ptr, size_t offset);

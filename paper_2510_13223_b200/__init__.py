@@ -39,7 +39,8 @@ EXPORTED_SYMBOLS = (
     "bs_split_decode_attention_local", "bs_signal", "bs_wait_signal",
     "bs_attention_problem_workspace_size", "bs_split_decode_attention_tasks", "bs_wait_signals",
     "bs_signals", "bs_attention_ragged_plan", "bs_split_decode_attention_local_ragged",
-    "bs_debug_build", "bs_debug_error_code", "bs_kv_append_token",
+    "bs_debug_build", "bs_debug_error_code", "bs_kv_append_token", "bs_exchange",
+    "bs_signals_epoch", "bs_wait_signals_epoch", "bs_epoch_advance",
 )
 
 
@@ -127,6 +128,10 @@ def lib():
         "bs_wait_signal": ([_p, _i32, ctypes.c_uint64, _p, _p], _i32),
         "bs_wait_signals": ([_i32, _p, _p, ctypes.c_uint64, _p, _p], _i32),
         "bs_signals": ([_i32, _p, _i32, _p], _i32),
+        "bs_signals_epoch": ([_i32, _p, _p, _p, _p, _p], _i32),
+        "bs_wait_signals_epoch": ([_i32, _p, _p, _p, _p, ctypes.c_uint64, _p, _p], _i32),
+        "bs_epoch_advance": ([_p, _p], _i32),
+        "bs_exchange": ([_p, _i32, _p, _p, _p, _i32, _p, _p, _p, _p], _i32),
         "bs_attention_ragged_plan": ([_i32, _i32, _p, _i32, _p, _i32, _i32, _i32, _i32, _p, _i32,
                                       ctypes.POINTER(_i32), ctypes.POINTER(_i32),
                                       ctypes.POINTER(_sz)], _i32),
@@ -499,6 +504,19 @@ class Comm:
                                  _stream(stream)))
 
 
+    def exchange(self, sends, recvs, stream=None) -> None:
+        """One NCCL group of raw-byte sends [(tensor, peer)] and receives [(tensor, peer)]
+        (bs_exchange) on ``stream``."""
+        ns, nr = len(sends), len(recvs)
+        sb = (ctypes.c_void_p * max(ns, 1))(*[_dptr(t) for t, _ in sends])
+        sz = (ctypes.c_size_t * max(ns, 1))(*[t.numel() * t.element_size() for t, _ in sends])
+        sp = (ctypes.c_int32 * max(ns, 1))(*[int(p) for _, p in sends])
+        rb = (ctypes.c_void_p * max(nr, 1))(*[_dptr(t) for t, _ in recvs])
+        rz = (ctypes.c_size_t * max(nr, 1))(*[t.numel() * t.element_size() for t, _ in recvs])
+        rp = (ctypes.c_int32 * max(nr, 1))(*[int(p) for _, p in recvs])
+        _check(lib().bs_exchange(self.handle, ns, sb, sz, sp, nr, rb, rz, rp, _stream(stream)))
+
+
 def nccl_unique_id() -> bytes:
     n = lib().bs_nccl_unique_id_bytes()
     buf = ctypes.create_string_buffer(n)
@@ -621,22 +639,29 @@ def t_layer_model(s_total_bytes: float, b_net_bytes_per_s: float, t_sync_s: floa
     return s_total_bytes / b_net_bytes_per_s + t_sync_s
 
 
+def wrap_i32(x: int) -> int:
+    """x as the int32 the device holds (flags and counters wrap after 2^31; the waits
+    compare wrap-safely)."""
+    return ((int(x) + (1 << 31)) % (1 << 32)) - (1 << 31)
+
+
 def signal(flag_ptr: int, value: int, stream=None) -> None:
     """After all prior work on the stream: *flag = value (flag may be peer-mapped)."""
-    _check(lib().bs_signal(flag_ptr, int(value), _stream(stream)))
+    _check(lib().bs_signal(flag_ptr, wrap_i32(value), _stream(stream)))
 
 
 def wait_signal(flag_ptr: int, value: int, timeout_ns: int = 0, err_ptr: int | None = None,
                 stream=None) -> None:
-    """The stream waits until *flag >= value (gives up after timeout_ns, setting *err)."""
-    _check(lib().bs_wait_signal(flag_ptr, int(value), int(timeout_ns), err_ptr, _stream(stream)))
+    """The stream waits until *flag >= value, wrap-safe (gives up after timeout_ns,
+    setting *err)."""
+    _check(lib().bs_wait_signal(flag_ptr, wrap_i32(value), int(timeout_ns), err_ptr, _stream(stream)))
 
 
 def signals(flag_ptrs, value: int, stream=None) -> None:
     """One launch: after all prior work on the stream, *flag_ptrs[i] = value (<= 16)."""
     n = len(flag_ptrs)
     fa = (ctypes.c_void_p * n)(*[int(f) for f in flag_ptrs])
-    _check(lib().bs_signals(n, fa, int(value), _stream(stream)))
+    _check(lib().bs_signals(n, fa, wrap_i32(value), _stream(stream)))
 
 
 def wait_signals(flag_ptrs, values, timeout_ns: int = 0, err_ptr: int | None = None,
@@ -644,8 +669,40 @@ def wait_signals(flag_ptrs, values, timeout_ns: int = 0, err_ptr: int | None = N
     """One launch: the stream waits until *flag_ptrs[i] >= values[i] for every i (<= 16)."""
     n = len(flag_ptrs)
     fa = (ctypes.c_void_p * n)(*[int(f) for f in flag_ptrs])
-    va = (ctypes.c_int32 * n)(*[int(v) for v in values])
+    va = (ctypes.c_int32 * n)(*[wrap_i32(v) for v in values])
     _check(lib().bs_wait_signals(n, fa, va, int(timeout_ns), err_ptr, _stream(stream)))
+
+
+def _epoch_arrays(flag_ptrs, mul, add):
+    n = len(flag_ptrs)
+    mul = [mul] * n if isinstance(mul, int) else list(mul)
+    add = [add] * n if isinstance(add, int) else list(add)
+    if len(mul) != n or len(add) != n:
+        raise ValueError("flags / mul / add length mismatch")
+    return (n, (ctypes.c_void_p * n)(*[int(f) for f in flag_ptrs]),
+            (ctypes.c_int32 * n)(*[wrap_i32(v) for v in mul]),
+            (ctypes.c_int32 * n)(*[wrap_i32(v) for v in add]))
+
+
+def signals_epoch(flag_ptrs, epoch_ptr: int, mul=1, add=0, stream=None) -> None:
+    """One launch: after all prior work on the stream, *flag_ptrs[i] = (*epoch) * mul[i] +
+    add[i], computed on the device (CUDA-graph capturable steps)."""
+    n, fa, ma, aa = _epoch_arrays(flag_ptrs, mul, add)
+    _check(lib().bs_signals_epoch(n, fa, ma, aa, int(epoch_ptr), _stream(stream)))
+
+
+def wait_signals_epoch(flag_ptrs, epoch_ptr: int, mul=1, add=0, timeout_ns: int = 0,
+                       err_ptr: int | None = None, stream=None) -> None:
+    """One launch: the stream waits until *flag_ptrs[i] >= (*epoch) * mul[i] + add[i]
+    (device-computed, wrap-safe) for every i (<= 16)."""
+    n, fa, ma, aa = _epoch_arrays(flag_ptrs, mul, add)
+    _check(lib().bs_wait_signals_epoch(n, fa, ma, aa, int(epoch_ptr), int(timeout_ns), err_ptr,
+                                       _stream(stream)))
+
+
+def epoch_advance(epoch_ptr: int, stream=None) -> None:
+    """Enqueue *epoch += 1 (the device step counter of a graph-capturable step)."""
+    _check(lib().bs_epoch_advance(int(epoch_ptr), _stream(stream)))
 
 
 def copy_ptr(dst_ptr: int, src_ptr: int, nbytes: int, stream=None) -> None:

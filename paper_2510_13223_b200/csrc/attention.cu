@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <type_traits>
 #include <vector>
@@ -986,12 +987,18 @@ struct Plan {
 // local shards for bs_split_decode_attention_local): pick the CTA range length that
 // minimises waves x blocks-per-CTA (+ a fixed per-CTA cost), i.e. fills the SM slots.
 // hkv: kv heads handled by the launch (grid.y); hq: q heads of the model (partial rows).
+// Problems whose shards live on several GPUs (bs_split_decode_attention_tasks) are planned
+// by every GPU that runs one of their shards, and the last-arriver merge needs the same
+// range cut everywhere: their plan uses only rank-invariant inputs -- the problem's shape,
+// a fixed slot count (a B200's 148 SMs x 3 resident CTAs) and no environment switches.
+constexpr int kInvariantSlots = 148 * 3;
+
 bs_status make_plan(int batch, int G, int hq, int hkv, int d, int n_local, const int* max_blocks,
-                    bool merged, Plan* out) {
+                    bool merged, Plan* out, bool rank_invariant = false) {
   if (n_local < 1 || n_local > kMaxProbShards)
     return set_error(BS_ERR_INVALID_ARG, "attention plan: %d shards (1..%d)", n_local, kMaxProbShards);
-  const int sms = sm_count(current_device());
-  const int64_t slots = (int64_t)sms * variant_for(d, G).minb;
+  const int64_t slots = rank_invariant ? (int64_t)kInvariantSlots
+                                       : (int64_t)sm_count(current_device()) * variant_for(d, G).minb;
   const int64_t base = (int64_t)batch * hkv;
   int mb_max = 1;
   for (int j = 0; j < n_local; ++j) mb_max = std::max(mb_max, max_blocks[j]);
@@ -1006,7 +1013,8 @@ bs_status make_plan(int batch, int G, int hq, int hkv, int d, int n_local, const
   int best_bps = -1;
   double best = 1e300;
   for (int pass = 0; pass < 2 && best_bps < 0; ++pass) {  // pass 1: without the cap
-    const int cap = pass == 0 ? std::min(kBtMax, std::max(max_bps, min_bps)) : kBtMax;
+    const int cap =
+        pass == 0 && !rank_invariant ? std::min(kBtMax, std::max(max_bps, min_bps)) : kBtMax;
     int last_bps = -1;
     for (int ns = 1; ns <= kMaxSplit; ++ns) {
       const int bps = std::max(min_bps, (mb_max + ns - 1) / ns);
@@ -1051,12 +1059,12 @@ bs_status make_plan(int batch, int G, int hq, int hkv, int d, int n_local, const
 template <int D, int G, int STAGES, int MINB>
 bs_status launch_attn_v(const AttnParams& p, int batch, cudaStream_t stream) {
   using S = Smem<D, G, STAGES>;
-  static int configured_dev = -1;
-  const int dev = current_device();
-  if (configured_dev != dev) {
+  static std::atomic<uint64_t> configured{0};  // per-device function attribute
+  const uint64_t bit = 1ull << (current_device() & 63);
+  if (!(configured.load() & bit)) {
     cudaFuncSetAttribute(split_decode_attn<D, G, STAGES, MINB>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
-    configured_dev = dev;
+    configured.fetch_or(bit);
   }
   const dim3 grid = p.work ? dim3(p.grid_x * p.hkv, 1, 1) : dim3(p.grid_x, p.hkv, batch);
   split_decode_attn<D, G, STAGES, MINB><<<grid, kWarps * 32, S::kTotal, stream>>>(p);
@@ -1066,12 +1074,12 @@ bs_status launch_attn_v(const AttnParams& p, int batch, cudaStream_t stream) {
 template <int D, int G, int STAGES, int MINB>
 bs_status launch_attn_mma(const AttnParams& p, const TMaps& tm, int batch, cudaStream_t stream) {
   using S = MmaSmem<D, G, STAGES>;
-  static int configured_dev = -1;
-  const int dev = current_device();
-  if (configured_dev != dev) {
+  static std::atomic<uint64_t> configured{0};  // per-device function attribute
+  const uint64_t bit = 1ull << (current_device() & 63);
+  if (!(configured.load() & bit)) {
     cudaFuncSetAttribute(split_decode_attn_mma<D, G, STAGES, MINB>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
-    configured_dev = dev;
+    configured.fetch_or(bit);
   }
   const dim3 grid = p.work ? dim3(p.grid_x * p.hkv, 1, 1) : dim3(p.grid_x, p.hkv, batch);
   split_decode_attn_mma<D, G, STAGES, MINB><<<grid, kWarps * 32, S::kTotal, stream>>>(p, tm);
@@ -1490,7 +1498,7 @@ bs_status bs_attention_problem_workspace_size(int32_t batch, int32_t num_q_heads
     return bs::set_error(BS_ERR_UNSUPPORTED, "head_dim %d not in {64,128}", head_dim);
   bs::Plan pl;
   bs_status st = bs::make_plan(batch, G, num_q_heads, num_kv_heads, head_dim, n_shards, max_blocks,
-                               true, &pl);
+                               true, &pl, /*rank_invariant=*/true);
   if (st != BS_OK) return st;
   *bytes = pl.ws_bytes;
   return BS_OK;
@@ -1539,7 +1547,8 @@ bs_status bs_split_decode_attention_tasks(int32_t n_problems, const bs_attn_prob
                "bs_split_decode_attention_tasks: problem %d: %d shards", i, pr.n_shards);
     for (int j = 0; j < pr.n_shards; ++j)
       BS_REQUIRE(pr.max_blocks[j] >= 1, "bs_split_decode_attention_tasks: max_blocks < 1");
-    bs_status st = bs::make_plan(batch, G, num_q_heads, hkv, d, pr.n_shards, pr.max_blocks, true, &plans[i]);
+    bs_status st = bs::make_plan(batch, G, num_q_heads, hkv, d, pr.n_shards, pr.max_blocks, true, &plans[i],
+                                 /*rank_invariant=*/true);
     if (st != BS_OK) return st;
     BS_REQUIRE(plans[i].ws_bytes == 0 || (pr.workspace && pr.workspace_bytes >= plans[i].ws_bytes &&
                                           ((uintptr_t)pr.workspace & 15) == 0),

@@ -143,6 +143,34 @@ bs_status bs_sendrecv(bs_comm* comm, const void* sendbuf, size_t send_bytes, int
   return BS_OK;
 }
 
+bs_status bs_exchange(bs_comm* comm, int32_t n_send, const void* const* send_bufs,
+                      const size_t* send_bytes, const int32_t* send_peers, int32_t n_recv,
+                      void* const* recv_bufs, const size_t* recv_bytes, const int32_t* recv_peers,
+                      void* stream) {
+  BS_REQUIRE(comm, "bs_exchange: NULL comm");
+  BS_REQUIRE(n_send >= 0 && n_recv >= 0, "bs_exchange: negative count");
+  BS_REQUIRE(n_send == 0 || (send_bufs && send_bytes && send_peers), "bs_exchange: NULL send array");
+  BS_REQUIRE(n_recv == 0 || (recv_bufs && recv_bytes && recv_peers), "bs_exchange: NULL recv array");
+  for (int i = 0; i < n_send; ++i)
+    BS_REQUIRE(send_peers[i] >= 0 && send_peers[i] < comm->nranks && (send_bytes[i] == 0 || send_bufs[i]),
+               "bs_exchange: send %d: peer %d / buffer", i, send_peers[i]);
+  for (int i = 0; i < n_recv; ++i)
+    BS_REQUIRE(recv_peers[i] >= 0 && recv_peers[i] < comm->nranks && (recv_bytes[i] == 0 || recv_bufs[i]),
+               "bs_exchange: recv %d: peer %d / buffer", i, recv_peers[i]);
+  NcclApi* a = nccl();
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ncclResult_t r = a->GroupStart();
+  if (r != ncclSuccess) return nccl_err("ncclGroupStart", r);
+  for (int i = 0; i < n_send && r == ncclSuccess; ++i)
+    if (send_bytes[i]) r = a->Send(send_bufs[i], send_bytes[i], ncclUint8, send_peers[i], comm->comm, s);
+  for (int i = 0; i < n_recv && r == ncclSuccess; ++i)
+    if (recv_bytes[i]) r = a->Recv(recv_bufs[i], recv_bytes[i], ncclUint8, recv_peers[i], comm->comm, s);
+  const ncclResult_t r2 = a->GroupEnd();
+  if (r != ncclSuccess) return nccl_err("ncclSend / ncclRecv", r);
+  if (r2 != ncclSuccess) return nccl_err("ncclGroupEnd", r2);
+  return BS_OK;
+}
+
 bs_status bs_kv_send_layer(const bs_kv_pool* src, int32_t layer, const int32_t* src_ids, int32_t n,
                            int32_t peer, bs_comm* comm, void* staging, void* stream) {
   bs_status st = bs_kv_gather_layer(src, layer, src_ids, n, staging, stream);

@@ -14,6 +14,8 @@
 //     cp.async.bulk shared->global in bulk groups); no registers touch the payload.
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <algorithm>
 #include <cstdlib>
 #include <vector>
@@ -205,11 +207,14 @@ bs_status launch_copy_t(const uint8_t* src_base, const int32_t* src_ids, uint8_t
   const int sms = sm_count(current_device());
   if (method == BS_MIGRATE_BULK) {
     const int smem = kBulkStages * PAGE_BYTES;
-    static bool configured = false;
-    if (!configured) {
+    // the shared-memory opt-in is a per-device function attribute: track it per device
+    static std::atomic<uint64_t> configured{0};
+    const int dev = current_device();
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(configured.load() & bit)) {
       cudaFuncSetAttribute(copy_pages_bulk<PAGE_BYTES>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      configured = true;
+      configured.fetch_or(bit);
     }
     int64_t grid = std::min<int64_t>(total, (int64_t)sms * 2);
     if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);

@@ -6,7 +6,9 @@ rank prev = r-1 (mod N) (Fig. 4: KV2 "offloaded to a cold GPU"
   home pool  (rank r): shard 0 of r's requests   + free blocks receiving hand-offs
   cold pool  (rank r): shard 1 of prev's requests + KV being handed off to prev
 
-Per layer l (every exchange is point-to-point, NCCL via torch.distributed on GPUs):
+Per layer l (every exchange is point-to-point: pushes into peer memory with the P2P
+transport, or the library's own NCCL communicator -- bs_exchange through the C-ABI --
+with the NCCL transport):
   migration  : cold pool --gather--> send to prev ; recv from next --scatter--> home pool
                (H2 two-sided transport; at N=1 the fused copy kernel P -> D)
   q exchange : send q_l of my requests to next (their cold instance); recv prev's q_l
@@ -22,9 +24,10 @@ merge), ordered by events; the attention of layer l waits for layer l's migratio
 exchange, prev = next = self, and both shards being local, attention over both pools and
 the LSE merge run as ONE fused launch (bs_split_decode_attention_local).
 
-The protocol is written against two small interfaces -- ``ops`` (the kernels) and
-``ex`` (streams/events) -- so the identical code runs on GPUs with libbanaserve.so and
-on CPU under gloo in the tests (where ``ops`` is test infrastructure).
+The protocol is written against three small interfaces -- ``ops`` (the kernels), ``ex``
+(streams/events) and a wire (``exchange(sends, recvs)``: transport.NcclWire on GPUs) --
+so the identical code runs on GPUs with libbanaserve.so and on CPU under gloo in the
+tests (where ``ops`` and the wire are test infrastructure).
 """
 from __future__ import annotations
 
@@ -33,6 +36,8 @@ import contextlib
 import numpy as np
 import torch
 import torch.distributed as dist
+
+from .transport import ErrorFlag, NcclWire
 
 
 class CudaExec:
@@ -169,13 +174,9 @@ def split_partial(flat: torch.Tensor, batch: int, hq: int, d: int):
     return o, m, l
 
 
-def _sendrecv(pg, send: torch.Tensor, to: int, recv: torch.Tensor, frm: int):
+def _sendrecv(wire, send: torch.Tensor, to: int, recv: torch.Tensor, frm: int):
     """One grouped send+recv (ring neighbours; symmetric on every rank => no deadlock)."""
-    s = send.reshape(-1).view(torch.uint8)   # bytes on the wire (any dtype, any backend)
-    r = recv.reshape(-1).view(torch.uint8)
-    ops = [dist.P2POp(dist.isend, s, to, group=pg), dist.P2POp(dist.irecv, r, frm, group=pg)]
-    for w in dist.batch_isend_irecv(ops):
-        w.wait()
+    wire.exchange([(send, to)], [(recv, frm)])
 
 
 def _all_ranks_true(flag: bool, pg, device) -> bool:
@@ -209,7 +210,10 @@ class P2PLinks:
         from . import ipc_export, ipc_import, pool_view
         self.L = num_layers
         self.flags = torch.zeros(len(self.KINDS) * num_layers, dtype=torch.int32, device=device)
-        self.err = torch.zeros(1, dtype=torch.int32, device=device)
+        self.err = ErrorFlag()   # timeout flag of every wait kernel (pinned host int32)
+        # device step counter: every flag value / wait target is computed from it on the
+        # device, so a step captured in a CUDA graph replays with the right epoch
+        self.epoch = torch.zeros(1, dtype=torch.int32, device=device)
         self.q_prev = torch.empty_like(q_like)
         self.part_recv = torch.empty((num_layers, part_numel), dtype=torch.float32, device=device)
         self.timeout_ns = int(timeout_ms) * 1_000_000
@@ -262,8 +266,7 @@ class P2PLinks:
         return self.flag(self.flags.data_ptr(), kind, layer)
 
     def check(self):
-        if int(self.err.item()) != 0:
-            raise RuntimeError("P2P transport: a peer signal timed out")
+        self.err.check("P2P transport")
 
     def close(self):
         from . import ipc_close
@@ -281,7 +284,11 @@ class ShardedDecodeStep:
                  handoff_src_ids=None, handoff_dst_ids=None, chunk_bytes: int = 0,
                  pg_attn=None, pg_mig=None, lookahead: int = 1, device=None,
                  fuse_local: bool = True, copy_engine: bool = False, transport: str = "nccl",
-                 fused_exchange: bool = True, append=None):
+                 fused_exchange: bool = True, append=None, wire_attn=None, wire_mig=None):
+        """``wire_attn`` / ``wire_mig``: the byte movers of the NCCL transport (q, K/V and
+        partials on the comm stream; hand-off chunks on the copy stream) -- by default two
+        transport.NcclWire communicators of the library (C-ABI), created collectively when
+        the step resolves to the NCCL transport."""
         self.ops, self.ex = ops, ex
         self.rank, self.world = rank, world
         self.prev, self.next = (rank - 1) % world, (rank + 1) % world
@@ -367,6 +374,16 @@ class ShardedDecodeStep:
                 self.mb_prev = [widths[self.prev][0], widths[rank][1]]
                 nws = ops.problem_workspace_size(self.B, num_q_heads, home_pool.num_kv_heads,
                                                  head_dim, self.mb_mine)
+                # my problem is planned here (shard 0) and on next (shard 1): both must cut
+                # the same ranges (the library plans from rank-invariant inputs); check it
+                nws_prev = ops.problem_workspace_size(self.B, num_q_heads, home_pool.num_kv_heads,
+                                                      head_dim, self.mb_prev)
+                sizes = [None] * world
+                dist.all_gather_object(sizes, (int(nws), int(nws_prev)), group=pg_attn)
+                bad = [r for r in range(world) if sizes[(r + 1) % world][1] != sizes[r][0]]
+                if bad:  # every rank sees the same list: all raise together
+                    raise RuntimeError(f"problems {bad} planned differently by their home and "
+                                       f"cold ranks: {sizes}")
                 fused = {"out": torch.empty((num_layers, self.B, num_q_heads, head_dim),
                                             dtype=torch.bfloat16, device=dev),
                          "lse": torch.empty((num_layers, self.B, num_q_heads), dtype=torch.float32,
@@ -391,6 +408,12 @@ class ShardedDecodeStep:
                 self.links = None
                 self.transport = "nccl"
                 self.fallback_reason = why or "a peer could not map the IPC buffers"
+        self.wire_attn, self.wire_mig = wire_attn, wire_mig
+        if self.transport == "nccl":  # every rank takes this branch together (collective)
+            if self.wire_attn is None:
+                self.wire_attn = NcclWire(pg_attn)
+            if self.wire_mig is None:
+                self.wire_mig = NcclWire(pg_mig)
         if self.transport == "p2p":
             self.part_recv = [split_partial(self.links.part_recv[layer], self.B, self.hq, self.d)
                               + (None, self.links.part_recv[layer]) for layer in range(num_layers)]
@@ -420,9 +443,10 @@ class ShardedDecodeStep:
         if self.transport == "p2p" and self.fused_exchange:
             # 1 fused attention launch; q push + signal, hand-off signal, 1 combined wait,
             # q-ack signal, done wait (per layer); H7: q-flag wait + append(s)
-            return self.L * (1 + mig + 6 + (app + 1 if app else 0))
+            # (+1 per step: the device epoch advance)
+            return self.L * (1 + mig + 6 + (app + 1 if app else 0)) + 1
         if self.transport == "p2p":  # + the tiny signal / wait kernels of the protocol
-            return self.L * (3 + mig + 8 + app)
+            return self.L * (3 + mig + 8 + app) + 1
         attn = 1 if self.fuse_local else 3
         return self.L * (attn + mig + app)  # N>1 NCCL: the appends run on the compute stream
 
@@ -439,7 +463,7 @@ class ShardedDecodeStep:
                                       self.ce_ids)
                 else:
                     ops.gather(self.cold, layer, self.src_ids, self.stage_send)
-                    _sendrecv(self.pg_mig, self.stage_send, self.prev, self.stage_recv, self.next)
+                    _sendrecv(self.wire_mig, self.stage_send, self.prev, self.stage_recv, self.next)
                     ops.scatter(self.home, layer, self.dst_ids, self.stage_recv)
             if self.append is not None and self.world == 1:  # H7 rides the migration stream:
                 kv = self.append[layer]                      # attention waits for mig_done
@@ -459,9 +483,10 @@ class ShardedDecodeStep:
         events recorded on the launching streams (CUDA only).  ``inputs_ready[l]``: an
         event the step waits for before reading q[l] (e.g. its H2D copy); after the call,
         ``self.out_ready[l]`` is recorded once out[l] / lse[l] are final (per-layer D2H)."""
-        if self.transport == "p2p" and self.fused_exchange:
-            return self._enqueue_p2p_fused(q, out, lse, timers, inputs_ready)
         if self.transport == "p2p":
+            self.links.check()   # a timed-out wait of an earlier step poisons its outputs
+            if self.fused_exchange:
+                return self._enqueue_p2p_fused(q, out, lse, timers, inputs_ready)
             return self._enqueue_p2p(q, out, lse, timers, inputs_ready)
         ex, ops, E = self.ex, self.ops, self.ev
         if self.world > 1 and (self.q_prev is None or self.q_prev.shape != q.shape):
@@ -474,9 +499,9 @@ class ShardedDecodeStep:
                 for layer in range(self.L):
                     if inputs_ready is not None:
                         ex.wait(ex.comm, inputs_ready[layer])
-                    _sendrecv(self.pg_attn, q[layer], self.next, self.q_prev[layer], self.prev)
+                    _sendrecv(self.wire_attn, q[layer], self.next, self.q_prev[layer], self.prev)
                     if self.append is not None:  # H7: the token's K/V travel with q
-                        _sendrecv(self.pg_attn, self.append[layer], self.next,
+                        _sendrecv(self.wire_attn, self.append[layer], self.next,
                                   self.kv_prev_buf[layer], self.prev)
                     ex.record(E["q_ready"][layer], ex.comm)
         # lookahead -2 at N=1: the hand-off copy runs on the compute stream right before its
@@ -538,12 +563,23 @@ class ShardedDecodeStep:
             else:
                 with ex.use(ex.comm):
                     ex.wait(ex.comm, E["part_ready"][layer])
-                    _sendrecv(self.pg_attn, self.part_cold[layer][4], self.prev,
+                    _sendrecv(self.wire_attn, self.part_cold[layer][4], self.prev,
                               self.part_recv[layer][4], self.next)
                     ops.merge([self.part_own[layer], self.part_recv[layer]], out[layer],
                               None if lse is None else lse[layer])
                     ex.record(self.out_ready[layer], ex.comm)
         ex.end()
+
+    def close(self):
+        """Unmap the neighbours' buffers and free the library's NCCL communicators (call on
+        every rank, then barrier, before any rank frees memory its peers mapped)."""
+        if self.links is not None:
+            self.links.close()
+        for name in ("wire_attn", "wire_mig"):
+            w = getattr(self, name, None)
+            if w is not None and hasattr(w, "close"):
+                w.close()
+            setattr(self, name, None)
 
     def outputs(self):
         """(out, lse) buffers the step merges into when the exchange is fused (peers write
@@ -559,20 +595,23 @@ class ShardedDecodeStep:
         mapping -- and the last arriver of a (request, kv-head), on either GPU, merges into
         that problem's out / lse and bumps its `done` counter.  Remaining flags: hand-off
         arrival (mig), q arrival (q) and q-buffer reuse (q_ack); the done counters also
-        guard workspace reuse across steps (target (epoch - 1) * B * Hkv)."""
-        from . import copy_ptr, kv_migrate_layer, signal, wait_signal, wait_signals
+        guard workspace reuse across steps (target (epoch - 1) * B * Hkv).  Every flag
+        value and wait target is computed on the device from the step counter
+        ``links.epoch`` (advanced first), so the step can be captured in a CUDA graph."""
+        from . import copy_ptr, epoch_advance, kv_migrate_layer, signals_epoch, wait_signals_epoch
         ex, ops, E, lk = self.ex, self.ops, self.ev, self.links
         F = lk.fused
         self.epoch += 1
-        e = self.epoch
-        per_call = self.B * self.hkv
-        to, err = lk.timeout_ns, lk.err.data_ptr()
+        ep = lk.epoch.data_ptr()
+        pc = self.B * self.hkv
+        to, err = lk.timeout_ns, lk.err.ptr
         qb = q[0].numel() * q.element_size()
         own_out = out is not None and out.data_ptr() == F["out"].data_ptr()
         own_lse = lse is None or lse.data_ptr() == F["lse"].data_ptr()
         ob, lb = F["out"][0].numel() * 2, F["lse"][0].numel() * 4
         app = self.append
         kvb = 0 if app is None else app[0].numel() * app.element_size()
+        epoch_advance(ep)   # on the current stream, before every stream forks from it
         ex.begin()
         for s_ in (self.push, self.merge_s, self.app_s):
             s_.wait_stream(torch.cuda.current_stream())
@@ -580,11 +619,11 @@ class ShardedDecodeStep:
             for layer in range(self.L):
                 if inputs_ready is not None:
                     ex.wait(ex.comm, inputs_ready[layer])
-                wait_signal(lk.my_flag("q_ack", layer), e - 1, to, err)
+                wait_signals_epoch([lk.my_flag("q_ack", layer)], ep, 1, -1, to, err)
                 copy_ptr(lk.next_q_prev + layer * qb, q[layer].data_ptr(), qb)
                 if app is not None:
                     copy_ptr(lk.next_kv_prev + layer * kvb, app[layer].data_ptr(), kvb)
-                signal(lk.flag(lk.next_flags, "q", layer), e)
+                signals_epoch([lk.flag(lk.next_flags, "q", layer)], ep)
         if app is not None:  # H7: prev's tokens into my cold pool, mine (empty shard 1) at home
             with torch.cuda.stream(self.app_s):
                 for layer in range(self.L):
@@ -593,7 +632,7 @@ class ShardedDecodeStep:
                             self.app_s.wait_event(inputs_ready[layer])
                         ops.append(self.home, layer, app[layer][0], app[layer][1], self.home_bt,
                                    self.pos_home)
-                    wait_signal(lk.my_flag("q", layer), e, to, err)
+                    wait_signals_epoch([lk.my_flag("q", layer)], ep, 1, 0, to, err)
                     kv = lk.kv_prev[layer]
                     ops.append(self.cold, layer, kv[0], kv[1], self.cold_bt, self.pos_prev)
                     E["app_done"][layer].record(self.app_s)
@@ -606,7 +645,7 @@ class ShardedDecodeStep:
                 if self.n_handoff:
                     kv_migrate_layer(self.cold, lk.prev_home, layer, self.src_ids,
                                      lk.prev_handoff_dst)
-                signal(lk.flag(lk.prev_flags, "mig", layer), e)
+                signals_epoch([lk.flag(lk.prev_flags, "mig", layer)], ep)
                 if timers is not None:
                     timers[layer][3].record(ex.copy)
             with ex.use(ex.compute):
@@ -615,8 +654,8 @@ class ShardedDecodeStep:
                     ex.wait(ex.compute, inputs_ready[layer])
                 my_done = F["done"][layer:layer + 1].data_ptr()
                 prev_done = lk.prev_done + 4 * layer
-                wait_signals([lk.my_flag("mig", layer), lk.my_flag("q", layer), my_done, prev_done],
-                             [e, e, (e - 1) * per_call, (e - 1) * per_call], to, err)
+                wait_signals_epoch([lk.my_flag("mig", layer), lk.my_flag("q", layer), my_done,
+                                    prev_done], ep, [1, 1, pc, pc], [0, 0, -pc, -pc], to, err)
                 if app is not None:
                     ex.wait(ex.compute, E["app_done"][layer])
                 if timers is not None:
@@ -638,9 +677,9 @@ class ShardedDecodeStep:
                 ex.record(E["part_ready"][layer], ex.compute)
             with torch.cuda.stream(self.push):  # prev's q[l] consumed -> ack
                 self.push.wait_event(E["part_ready"][layer])
-                signal(lk.flag(lk.prev_flags, "q_ack", layer), e)
+                signals_epoch([lk.flag(lk.prev_flags, "q_ack", layer)], ep)
             with torch.cuda.stream(self.merge_s):  # my out[l] final once every merge landed
-                wait_signal(F["done"][layer:layer + 1].data_ptr(), e * per_call, to, err)
+                wait_signals_epoch([F["done"][layer:layer + 1].data_ptr()], ep, pc, 0, to, err)
                 if not own_out:
                     out[layer].copy_(F["out"][layer])
                 if not own_lse:
@@ -653,15 +692,17 @@ class ShardedDecodeStep:
 
     def _enqueue_p2p(self, q, out, lse, timers, inputs_ready):
         """N>1 over CUDA IPC: every exchange is a push into the neighbour's memory followed
-        by a flag; consumers' streams wait on their local flags (epoch = step counter)."""
-        from . import copy_ptr, kv_migrate_layer, signal, wait_signal
+        by a flag; consumers' streams wait on their local flags (epoch = the device step
+        counter ``links.epoch``, so the step is graph-capturable)."""
+        from . import copy_ptr, epoch_advance, kv_migrate_layer, signals_epoch, wait_signals_epoch
         ex, ops, E, lk = self.ex, self.ops, self.ev, self.links
         self.epoch += 1
-        e = self.epoch
-        to, err = lk.timeout_ns, lk.err.data_ptr()
+        ep = lk.epoch.data_ptr()
+        to, err = lk.timeout_ns, lk.err.ptr
         qb = q[0].numel() * q.element_size()
         app = self.append
         kvb = 0 if app is None else app[0].numel() * app.element_size()
+        epoch_advance(ep)
         ex.begin()
         for s_ in (self.push, self.merge_s):
             s_.wait_stream(torch.cuda.current_stream())
@@ -669,11 +710,11 @@ class ShardedDecodeStep:
             for layer in range(self.L):
                 if inputs_ready is not None:
                     ex.wait(ex.comm, inputs_ready[layer])
-                wait_signal(lk.my_flag("q_ack", layer), e - 1, to, err)
+                wait_signals_epoch([lk.my_flag("q_ack", layer)], ep, 1, -1, to, err)
                 copy_ptr(lk.next_q_prev + layer * qb, q[layer].data_ptr(), qb)
                 if app is not None:
                     copy_ptr(lk.next_kv_prev + layer * kvb, app[layer].data_ptr(), kvb)
-                signal(lk.flag(lk.next_flags, "q", layer), e)
+                signals_epoch([lk.flag(lk.next_flags, "q", layer)], ep)
         for layer in range(self.L):
             with ex.use(ex.copy):  # hand-off: my cold pool -> prev's home pool, pushed
                 if self.lookahead >= 0 and layer - self.lookahead >= 0:
@@ -683,12 +724,12 @@ class ShardedDecodeStep:
                 if self.n_handoff:
                     kv_migrate_layer(self.cold, lk.prev_home, layer, self.src_ids,
                                      lk.prev_handoff_dst)
-                signal(lk.flag(lk.prev_flags, "mig", layer), e)
+                signals_epoch([lk.flag(lk.prev_flags, "mig", layer)], ep)
                 if timers is not None:
                     timers[layer][3].record(ex.copy)
             with ex.use(ex.compute):
                 ex.record(E["layer_start"][layer], ex.compute)
-                wait_signal(lk.my_flag("mig", layer), e, to, err)  # next's hand-off arrived
+                wait_signals_epoch([lk.my_flag("mig", layer)], ep, 1, 0, to, err)  # hand-off in
                 if inputs_ready is not None:
                     ex.wait(ex.compute, inputs_ready[layer])
                 if timers is not None:
@@ -698,29 +739,29 @@ class ShardedDecodeStep:
                                self.pos_home)
                 ops.attention(self.home, layer, q[layer], self.home_bt, self.kv_split, 0,
                               self.part_own[layer])
-                wait_signal(lk.my_flag("q", layer), e, to, err)    # prev's q arrived
+                wait_signals_epoch([lk.my_flag("q", layer)], ep, 1, 0, to, err)  # prev's q in
                 if app is not None:  # H7: prev's tokens end its shard 1 in my cold pool
                     kv = lk.kv_prev[layer]
                     ops.append(self.cold, layer, kv[0], kv[1], self.cold_bt, self.pos_prev)
                 ops.attention(self.cold, layer, self.q_prev[layer], self.cold_bt, self.kv_split_cold,
                               1, self.part_cold[layer])
-                signal(lk.flag(lk.prev_flags, "q_ack", layer), e)
+                signals_epoch([lk.flag(lk.prev_flags, "q_ack", layer)], ep)
                 if timers is not None:
                     timers[layer][1].record(ex.compute)
                 ex.record(E["part_ready"][layer], ex.compute)
             with torch.cuda.stream(self.push):  # prev's shard-1 partial -> prev
                 self.push.wait_event(E["part_ready"][layer])
-                wait_signal(lk.my_flag("part_ack", layer), e - 1, to, err)
+                wait_signals_epoch([lk.my_flag("part_ack", layer)], ep, 1, -1, to, err)
                 flat = self.part_cold[layer][4]
                 copy_ptr(lk.prev_part_recv + layer * flat.numel() * 4, flat.data_ptr(),
                          flat.numel() * 4)
-                signal(lk.flag(lk.prev_flags, "part", layer), e)
+                signals_epoch([lk.flag(lk.prev_flags, "part", layer)], ep)
             with torch.cuda.stream(self.merge_s):  # my shard-1 partial from next -> merge
-                wait_signal(lk.my_flag("part", layer), e, to, err)
+                wait_signals_epoch([lk.my_flag("part", layer)], ep, 1, 0, to, err)
                 self.merge_s.wait_event(E["part_ready"][layer])
                 ops.merge([self.part_own[layer], self.part_recv[layer]], out[layer],
                           None if lse is None else lse[layer])
-                signal(lk.flag(lk.next_flags, "part_ack", layer), e)
+                signals_epoch([lk.flag(lk.next_flags, "part_ack", layer)], ep)
                 self.out_ready[layer].record(self.merge_s)
         cur = torch.cuda.current_stream()
         for s_ in (self.push, self.merge_s):
@@ -729,10 +770,12 @@ class ShardedDecodeStep:
 
     def capture(self, q: torch.Tensor, out: torch.Tensor, lse: torch.Tensor | None = None):
         """Capture one full step (all layers, every stream) into a CUDA graph; replaying it
-        re-runs the step with whatever q / pools hold at replay time (N=1 / local only:
-        the P2P and NCCL transports talk to other processes)."""
-        if self.world != 1:
-            raise RuntimeError("graph capture is for the single-GPU step")
+        re-runs the step with whatever q / pools hold at replay time.  N=1, and N>1 with the
+        P2P transport: its flags are computed on the device from the step counter, so
+        every rank captures its own graph (after the same number of eager steps) and the
+        ranks replay them together, one replay per step.  The NCCL transport is eager only."""
+        if self.world != 1 and self.transport != "p2p":
+            raise RuntimeError("graph capture needs the single-GPU step or the P2P transport")
         self.enqueue(q, out, lse)          # warm-up: lazy attributes, workspaces, maps
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()

@@ -20,10 +20,12 @@ Transports:
                CUDA-IPC mapping and the last-arriving CTA (on any rank) merges into
                home h's out / lse and bumps h's `done` counter.  q is pushed into the
                peers' q buffers by the copy engines, with epoch flags and acks.
-  "collective" (any backend, incl. gloo on CPU) -- all_gather of q, W attention calls
-               writing (o~, m, l) partials, point-to-point sends of each partial to its
-               home, then the home's merge call.  The tests run it with the oracle as
-               the kernels.
+  "collective" (the two-sided fallback) -- q of every home to every peer, W attention
+               calls writing (o~, m, l) partials, each partial sent to its home, then the
+               home's merge call; the bytes move through a wire (``exchange(sends,
+               recvs)``): on GPUs the library's own NCCL communicator (bs_exchange via
+               transport.NcclWire), in the CPU tests a gloo wire with the oracle as the
+               kernels.
 
 Optional hand-off (C4: "each destination GPU receives 8192 tokens of migrated KV per
 step"): n chunks of rank r's pool are pushed, layer by layer, into rank r+1's pool
@@ -36,6 +38,7 @@ import torch
 import torch.distributed as dist
 
 from .ring import _all_ranks_true, split_partial
+from .transport import ErrorFlag, NcclWire
 
 
 def _rows(x, h: int, W: int):
@@ -46,26 +49,21 @@ def _rows(x, h: int, W: int):
     return np.ascontiguousarray(x[h::W])
 
 
-def _sendrecv_many(pg, sends, recvs):
-    """Grouped point-to-point exchange: sends = [(tensor, peer)], recvs = [(tensor, peer)]."""
-    ops = [dist.P2POp(dist.isend, t.reshape(-1).view(torch.uint8), p, group=pg) for t, p in sends]
-    ops += [dist.P2POp(dist.irecv, t.reshape(-1).view(torch.uint8), p, group=pg) for t, p in recvs]
-    if ops:
-        for w in dist.batch_isend_irecv(ops):
-            w.wait()
-
-
 class SeqShardedStep:
     KINDS = ("q", "q_ack", "mig")
 
     def __init__(self, ops, rank: int, world: int, pool, block_tables: torch.Tensor,
                  kv_split: torch.Tensor, num_q_heads: int, num_layers: int, head_dim: int,
                  num_kv_heads: int, device=None, group=None, transport: str = "p2p",
-                 handoff_src_ids=None, handoff_dst_ids=None, timeout_ms: int = 20000):
+                 handoff_src_ids=None, handoff_dst_ids=None, timeout_ms: int = 20000,
+                 wire=None):
         """pool: this rank's KV pool (range `rank` of every request); block_tables
         [B_total, mb] its block ids per request; kv_split [B_total, W+1] (same on every
-        rank).  B_total must be a multiple of W: home h serves requests h, h+W, ..."""
+        rank).  B_total must be a multiple of W: home h serves requests h, h+W, ...
+        ``wire``: byte mover of the collective transport (default: a transport.NcclWire
+        over ``group``, created collectively if the step resolves to it)."""
         self.ops, self.rank, self.world = ops, rank, world
+        self.timeout_ns = int(timeout_ms) * 1_000_000
         self.pool, self.L, self.hq, self.d, self.hkv = pool, num_layers, num_q_heads, head_dim, num_kv_heads
         self.group, self.device = group, device
         Bt = int(kv_split.shape[0])
@@ -82,7 +80,9 @@ class SeqShardedStep:
         self.n_handoff = 0 if handoff_src_ids is None else int(handoff_src_ids.numel())
         self.prev, self.next = (rank - 1) % W, (rank + 1) % W
         self.epoch = 0
-        self.transport = transport if W > 1 else "collective"
+        # W = 1 keeps the P2P transport's fused launch (one task, no peers): the 1-GPU
+        # split-K baseline of the same shapes runs the same kernel as W > 1
+        self.transport = transport
         self.fallback_reason = None
         widths = [None] * W
         if W > 1:
@@ -96,9 +96,14 @@ class SeqShardedStep:
                 self._setup_p2p()
             except Exception as e:  # e.g. no peer access
                 ok, why = False, repr(e)
-            if not _all_ranks_true(ok, group, device):
+            if not (_all_ranks_true(ok, group, device) if W > 1 else ok):
+                if W == 1:
+                    raise RuntimeError(f"sequence-sharded step setup failed: {why}")
                 self.transport, self.fallback_reason = "collective", why or "a peer could not map"
+        self.wire = wire
         if self.transport == "collective":
+            if self.wire is None and W > 1:
+                self.wire = NcclWire(group)
             self._setup_collective()
 
     # ------------------------------------------------------------------ P2P (fused)
@@ -108,24 +113,34 @@ class SeqShardedStep:
         nws = self.ops.problem_workspace_size(Bh, hq, self.hkv, d, self.max_blocks)
         stride = (max(nws, 1) + 255) // 256 * 256
         self.flags = torch.zeros(len(self.KINDS) * W * L, dtype=torch.int32, device=dev)
-        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.err = ErrorFlag()
+        self.epoch_dev = torch.zeros(1, dtype=torch.int32, device=dev)  # device step counter
         self.q_in = torch.empty((W, L, Bh, hq, d), dtype=torch.bfloat16, device=dev)
         self.out_buf = torch.empty((L, Bh, hq, d), dtype=torch.bfloat16, device=dev)
         self.lse_buf = torch.empty((L, Bh, hq), dtype=torch.float32, device=dev)
         self.ws = torch.zeros((L, stride), dtype=torch.uint8, device=dev)
         self.done = torch.zeros(L, dtype=torch.int32, device=dev)
-        self.timeout_ns = 20_000 * 1_000_000
-        mine = {k: ipc_export(t) for k, t in (("flags", self.flags), ("q_in", self.q_in),
-                                             ("out", self.out_buf), ("lse", self.lse_buf),
-                                             ("ws", self.ws), ("done", self.done),
-                                             ("pool", self.pool.data))}
+        mine = {} if W == 1 else {
+            k: ipc_export(t) for k, t in (("flags", self.flags), ("q_in", self.q_in),
+                                         ("out", self.out_buf), ("lse", self.lse_buf),
+                                         ("ws", self.ws), ("done", self.done),
+                                         ("pool", self.pool.data))}
         mine["ws_stride"] = stride
+        mine["ws_bytes"] = nws   # the range plan's size: must agree on every rank
         mine["pool_blocks"] = self.pool.num_blocks
         mine["device"] = dev.index if dev.index is not None else torch.cuda.current_device()
         mine["handoff_dst"] = ([] if self.dst_ids is None else
                                [int(x) for x in self.dst_ids.cpu().tolist()])
         everyone = [None] * W
-        dist.all_gather_object(everyone, mine, group=self.group)
+        if W > 1:
+            dist.all_gather_object(everyone, mine, group=self.group)
+        else:
+            everyone = [mine]
+        # every rank plans every home's problem from the same rank-invariant inputs (the
+        # library's fixed slot model): a mismatch would corrupt the last-arriver merge
+        if len({e["ws_bytes"] for e in everyone}) != 1:
+            raise RuntimeError(f"ranks planned the attention problems differently: "
+                               f"{[e['ws_bytes'] for e in everyone]}")
         self._opened = []
 
         def open_(who, name):
@@ -163,10 +178,12 @@ class SeqShardedStep:
         return self.peer[who]["flags"] + 4 * i
 
     def check(self):
-        if self.transport == "p2p" and int(self.err.item()) != 0:
-            raise RuntimeError("sequence-sharded step: a peer signal timed out")
+        if self.transport == "p2p":
+            self.err.check("sequence-sharded step")
 
     def close(self):
+        """Unmap the peers' buffers and free the NCCL communicator (call on every rank,
+        then barrier, before any rank frees the memory its peers mapped)."""
         from . import ipc_close
         for ptr, off in getattr(self, "_opened", []):
             try:
@@ -174,6 +191,9 @@ class SeqShardedStep:
             except Exception:
                 pass
         self._opened = []
+        if getattr(self, "wire", None) is not None and hasattr(self.wire, "close"):
+            self.wire.close()
+            self.wire = None
 
     def outputs(self):
         return (self.out_buf, self.lse_buf) if self.transport == "p2p" else None
@@ -183,43 +203,61 @@ class SeqShardedStep:
         if self.transport != "p2p":
             return self.L * (self.world + 1 + (2 if self.n_handoff else 0))
         # attention, combined wait, q-push wait + signals, ack signals, done wait (+ hand-off
-        # copy and its signal)
-        return self.L * (1 + 1 + 2 + 1 + 1 + (2 if self.n_handoff else 0))
+        # copy and its signal); + the device epoch advance once per step
+        return self.L * (1 + 1 + 2 + 1 + 1 + (2 if self.n_handoff else 0)) + 1
 
-    def _enqueue_p2p(self, q, out, lse):
-        from . import copy_ptr, kv_migrate_layer, signal, signals, wait_signal, wait_signals
+    def _enqueue_p2p(self, q, out, lse, timers=None, inputs_ready=None):
+        """``timers[l]`` = (attn_start, attn_end, mig_start, mig_end) events recorded on the
+        launching streams; ``inputs_ready[l]``: event the step waits for before reading
+        q[l] (its H2D copy); ``out_ready[l]`` is recorded once out[l] / lse[l] are final."""
+        from . import copy_ptr, epoch_advance, kv_migrate_layer, signals_epoch, wait_signals_epoch
         W, r, L = self.world, self.rank, self.L
         self.epoch += 1
-        e = self.epoch
-        to, err = self.timeout_ns, self.err.data_ptr()
-        per_call = self.Bh * self.hkv
+        ep = self.epoch_dev.data_ptr()
+        to, err = self.timeout_ns, self.err.ptr
+        pc = self.Bh * self.hkv
         qb = q[0].numel() * q.element_size()
         ob, lb = self.out_buf[0].numel() * 2, self.lse_buf[0].numel() * 4
         peers = [p for p in range(W) if p != r]
         cur = torch.cuda.current_stream()
+        epoch_advance(ep)   # flag values / wait targets are computed from it on the device
         for s in (self.comm, self.copy, self.ack_s, self.out_s):
             s.wait_stream(cur)
         with torch.cuda.stream(self.comm):  # my q_l -> every peer's q_in[r][l]
             for layer in range(L):
-                wait_signals([self.flag(r, "q_ack", p, layer) for p in peers], [e - 1] * len(peers),
-                             to, err)
+                if inputs_ready is not None:
+                    self.comm.wait_event(inputs_ready[layer])
+                if peers:
+                    wait_signals_epoch([self.flag(r, "q_ack", p, layer) for p in peers], ep, 1, -1,
+                                       to, err)
                 for p in peers:
                     copy_ptr(self.peer[p]["q_in"] + (r * L + layer) * qb, q[layer].data_ptr(), qb)
-                signals([self.flag(p, "q", r, layer) for p in peers], e)
+                if peers:
+                    signals_epoch([self.flag(p, "q", r, layer) for p in peers], ep)
         compute = cur
         for layer in range(L):
             if self.n_handoff:
                 with torch.cuda.stream(self.copy):
+                    if timers is not None:
+                        timers[layer][2].record(self.copy)
                     kv_migrate_layer(self.pool, self.next_pool, layer, self.src_ids, self.next_dst)
-                    signal(self.flag(self.next, "mig", r, layer), e)
+                    if timers is not None:
+                        timers[layer][3].record(self.copy)
+                    signals_epoch([self.flag(self.next, "mig", r, layer)], ep)
             waits = [self.flag(r, "q", p, layer) for p in peers]
-            vals = [e] * len(peers)
+            mul, add = [1] * len(peers), [0] * len(peers)
             waits += [self.peer[h]["done"] + 4 * layer for h in range(W)]
-            vals += [(e - 1) * per_call] * W
+            mul += [pc] * W
+            add += [-pc] * W
             if self.n_handoff:
                 waits.append(self.flag(r, "mig", self.prev, layer))
-                vals.append(e)
-            wait_signals(waits, vals, to, err, stream=compute)
+                mul.append(1)
+                add.append(0)
+            wait_signals_epoch(waits, ep, mul, add, to, err, stream=compute)
+            if inputs_ready is not None:
+                compute.wait_event(inputs_ready[layer])
+            if timers is not None:
+                timers[layer][0].record(compute)
             problems = []
             for h in range(W):
                 P = self.peer[h]
@@ -232,13 +270,15 @@ class SeqShardedStep:
             with torch.cuda.stream(compute):
                 self.ops.attention_tasks(problems, [(self.pool, self.bt_h[h], r, h) for h in range(W)],
                                          layer, self.Bh, self.hq)
+            if timers is not None:
+                timers[layer][1].record(compute)
             self.part_ready[layer].record(compute)
             with torch.cuda.stream(self.ack_s):  # every home's q_l consumed -> acks
                 self.ack_s.wait_event(self.part_ready[layer])
                 if peers:
-                    signals([self.flag(p, "q_ack", r, layer) for p in peers], e)
+                    signals_epoch([self.flag(p, "q_ack", r, layer) for p in peers], ep)
             with torch.cuda.stream(self.out_s):  # my out_l final once all merges landed
-                wait_signal(self.done[layer:layer + 1].data_ptr(), e * per_call, to, err)
+                wait_signals_epoch([self.done[layer:layer + 1].data_ptr()], ep, pc, 0, to, err)
                 if out.data_ptr() != self.out_buf.data_ptr():
                     out[layer].copy_(self.out_buf[layer])
                 if lse is not None and lse.data_ptr() != self.lse_buf.data_ptr():
@@ -254,6 +294,7 @@ class SeqShardedStep:
                                               self.device)
         self.parts = [mk() for _ in range(W)]      # my shard's partial of home h's requests
         self.recv = [mk() for _ in range(W)]       # home: partial of my requests from rank s
+        self.q_all = None                          # [W][B_h][Hq][d]: every home's q_l
         if self.n_handoff:
             cb = getattr(self.pool, "chunk_bytes", None) or self.pool.data[0, 0].nbytes
             nbytes = self.n_handoff * cb
@@ -267,16 +308,19 @@ class SeqShardedStep:
             if self.n_handoff:  # gather -> send to next / recv from prev -> scatter
                 self.ops.gather(self.pool, layer, self.src_ids, self.stage_send)
                 if W > 1:
-                    _sendrecv_many(self.group, [(self.stage_send, self.next)],
-                                   [(self.stage_recv, self.prev)])
+                    self.wire.exchange([(self.stage_send, self.next)], [(self.stage_recv, self.prev)])
                     self.ops.scatter(self.pool, layer, self.dst_ids, self.stage_recv)
                 else:
                     self.ops.scatter(self.pool, layer, self.dst_ids, self.stage_send)
-            if W > 1:  # as bytes: every backend moves those
-                qb = q[layer].contiguous().view(torch.uint8)
-                q_all = [torch.empty_like(qb) for _ in range(W)]
-                dist.all_gather(q_all, qb, group=self.group)
-                q_all = [t.view(q.dtype) for t in q_all]
+            if W > 1:  # home r's q_l to every peer, every home's q_l from it (an all-gather)
+                if self.q_all is None or self.q_all.shape[1:] != q[layer].shape:
+                    self.q_all = torch.empty((W,) + tuple(q[layer].shape), dtype=q.dtype,
+                                             device=q.device)
+                self.q_all[r].copy_(q[layer])
+                peers = [p for p in range(W) if p != r]
+                self.wire.exchange([(self.q_all[r], p) for p in peers],
+                                   [(self.q_all[p], p) for p in peers])
+                q_all = [self.q_all[h] for h in range(W)]
             else:
                 q_all = [q[layer]]
             for h in range(W):
@@ -284,16 +328,33 @@ class SeqShardedStep:
                                    self.parts[h])
             sends = [(self.parts[h][4], h) for h in range(W) if h != r]
             recvs = [(self.recv[s][4], s) for s in range(W) if s != r]
-            _sendrecv_many(self.group, sends, recvs)
+            if W > 1:
+                self.wire.exchange(sends, recvs)
             got = [self.parts[r] if s == r else self.recv[s] for s in range(W)]
             self.ops.merge(got, out[layer], None if lse is None else lse[layer])
 
-    def enqueue(self, q: torch.Tensor, out: torch.Tensor, lse: torch.Tensor | None = None):
+    def enqueue(self, q: torch.Tensor, out: torch.Tensor, lse: torch.Tensor | None = None,
+                timers=None, inputs_ready=None):
         """q [L][B_h][Hq][d] of this rank's home requests (global ids rank, rank+W, ...)
-        -> out [L][B_h][Hq][d] bf16, lse [L][B_h][Hq] fp32."""
+        -> out [L][B_h][Hq][d] bf16, lse [L][B_h][Hq] fp32.  ``timers`` / ``inputs_ready``:
+        P2P transport only (see _enqueue_p2p)."""
         if self.transport == "p2p":
-            return self._enqueue_p2p(q, out, lse)
+            self.check()   # a timed-out wait of an earlier step poisons its outputs
+            return self._enqueue_p2p(q, out, lse, timers, inputs_ready)
         return self._enqueue_collective(q, out, lse)
+
+    def capture(self, q: torch.Tensor, out: torch.Tensor, lse: torch.Tensor | None = None):
+        """One step of the P2P transport captured in a CUDA graph (flags computed on the
+        device from the step counter); every rank captures after the same eager steps and
+        the ranks replay together."""
+        if self.transport != "p2p":
+            raise RuntimeError("graph capture needs the P2P transport")
+        self.enqueue(q, out, lse)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.enqueue(q, out, lse)
+        return g
 
 
 __all__ = ["SeqShardedStep", "split_partial"]

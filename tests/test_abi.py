@@ -189,3 +189,17 @@ def test_debug_build_exports_the_same_abi():
     assert dbg.bs_debug_build() == 1
     assert bs.lib().bs_debug_build() == 0
     assert bs.lib().bs_debug_error_code(0) == 0
+
+
+def test_package_data_plane_has_no_torch_collectives():
+    """The N>1 data plane moves its bytes through the library (P2P pushes, or bs_exchange on
+    the library's own NCCL communicator): torch.distributed only sets up (object gathers of
+    IPC handles, the ncclUniqueId broadcast)."""
+    import glob
+    import re
+    pkg = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       "paper_2510_13223_b200")
+    bad = re.compile(r"batch_isend_irecv|dist\.(all_gather|isend|irecv|send|recv|all_to_all)\(")
+    for f in glob.glob(os.path.join(pkg, "*.py")):
+        src = open(f).read()
+        assert not bad.search(src), f

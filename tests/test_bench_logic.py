@@ -93,3 +93,43 @@ def test_clock_summary_nvml_rows():
     s = c.summary()
     assert s["sm_mhz"] == 1900.0 and s["sm_mhz_min"] == 1800.0 and s["samples"] == 3
     assert s["reasons"] == ["sw_power_cap"] and s["source"].startswith("nvml")
+
+
+def test_gpus_flag_fails_loudly_without_enough_gpus():
+    """`--gpus N` outside torchrun self-launches N ranks -- unless fewer GPUs are visible:
+    then it fails (exit 2, an "error" JSON line) instead of silently measuring N=1."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2"],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 2
+    assert "error" in r.stdout and "GPU" in r.stdout
+
+
+def test_world_size_must_match_gpus():
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4"],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 2 and "WORLD_SIZE=2" in r.stdout
+
+
+def test_seq_attention_bytes_closed_form():
+    """C3 at W=4: rank r reads range r (8192 tokens) of all 8 requests, every home's q, and
+    writes the merged O + lse of 2 requests."""
+    shape = synth.LLAMA3_8B
+    ks = synth.block_aligned_split(np.full(8, 32768), 4)
+    kv = 8 * 8192 * 2 * 8 * 128 * 2
+    bt = 8 * 4 * 512
+    q = 8 * 32 * 128 * 2
+    o = 2 * 32 * (128 * 2 + 4)
+    for r in range(4):
+        assert bench.seq_attn_bytes(shape, ks, r, 4) == kv + bt + q + o
+
+
+def test_seq_oracle_sample_is_bounded_and_scales_by_tokens():
+    smp = bench.SeqOracleSample("c4", 8)
+    lens = bench.seq_lengths("c4")
+    assert len(lens) == 256 and smp.tokens < lens.sum() // 4
+    assert smp.n_hand == 512
+    # extrapolation: L x (t_attn x total/sampled tokens + t_mig x W)
+    assert abs(smp.step_seconds(1.0, 0.5) - 80 * (lens.sum() / smp.tokens + 0.5 * 8)) < 1e-6

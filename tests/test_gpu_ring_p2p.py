@@ -3,7 +3,9 @@ run as 2 and 3 processes sharing GPU 0 (the only GPU gpurun offers; IPC between
 processes works on one device, NCCL does not).  Every rank checks its merged O / lse
 against the oracle over its requests' whole KV (shard 1 lived on the next rank) and the
 hand-off chunks pushed into its home pool by the next rank, over two steps (epochs) so
-the back-pressure acks are exercised."""
+the back-pressure acks are exercised.  The graph variant then captures the step in a CUDA
+graph on every rank (flags computed on the device from the step counter) and checks that
+two replays reproduce the eager outputs bit for bit."""
 import os
 import socket
 
@@ -39,7 +41,7 @@ def _dev(a):
     return torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).view(torch.bfloat16).cuda()
 
 
-def run_rank(rank, world, port, errq, fused):
+def run_rank(rank, world, port, errq, fused, graph=False):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -96,6 +98,19 @@ def run_rank(rank, world, port, errq, fused):
                 got = out[layer].float().cpu().double().numpy()
                 assert np.abs(got - ref_o).max() <= 2e-2, (rank, layer)
                 assert np.abs(lse[layer].cpu().double().numpy() - ref_lse).max() <= 1e-4, (rank, layer)
+        if graph:  # the captured step replays the eager one bit for bit
+            ref_out, ref_lse = out.clone(), lse.clone()
+            out.fill_(float("nan"))
+            lse.fill_(float("nan"))
+            g = step.capture(q, out, lse)
+            for _ in range(2):
+                out.fill_(float("nan"))
+                g.replay()
+                torch.cuda.synchronize()
+                step.links.check()
+                assert torch.equal(out.view(torch.int16), ref_out.view(torch.int16)), rank
+                assert torch.equal(lse, ref_lse), rank
+            dist.barrier()
         got_home = hp.data.cpu().view(torch.int16).numpy().view(np.uint16)
         assert np.array_equal(got_home[:, free_home], handoff_bytes(nxt)), rank
         dist.barrier()
@@ -115,13 +130,17 @@ def _free_port():
     return p
 
 
+@pytest.mark.parametrize("graph", [False, True], ids=["eager", "graph"])
 @pytest.mark.parametrize("fused", [True, False], ids=["fused-exchange", "push-partials"])
 @pytest.mark.parametrize("world", [2, 3])
-def test_ring_p2p_on_one_gpu(world, fused):
+def test_ring_p2p_on_one_gpu(world, fused, graph):
+    if graph and world == 3:
+        pytest.skip("graph replay: 2 ranks suffice")
     ctx = mp.get_context("spawn")
     errq = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=run_rank, args=(r, world, port, errq, fused)) for r in range(world)]
+    procs = [ctx.Process(target=run_rank, args=(r, world, port, errq, fused, graph))
+             for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:

@@ -86,6 +86,16 @@ def run_toy(rank, world):
         dist.barrier()
     got_pool = pool.data.cpu().view(torch.int16).numpy().view(np.uint16)
     assert np.array_equal(got_pool[:, dst], handoff_bytes((rank - 1) % world)), rank
+    # the step captured in a CUDA graph (device-computed flags) replays the eager outputs
+    ref_out, ref_lse = out.clone(), lse.clone()
+    g = step.capture(q, out, lse)
+    for _ in range(2):
+        out.fill_(float("nan"))
+        g.replay()
+        torch.cuda.synchronize()
+        step.check()
+        assert torch.equal(out.view(torch.int16), ref_out.view(torch.int16)), rank
+        assert torch.equal(lse.view(torch.int32), ref_lse.view(torch.int32)), rank
     dist.barrier()
     step.close()
 

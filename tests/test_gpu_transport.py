@@ -121,3 +121,63 @@ def test_ipc_remote_view_push(bs):
     ref = dst_np.copy()
     oracle.migrate_layer(src_np, ref, 1, np.array(s, dtype=np.int32), np.array(t, dtype=np.int32))
     assert np.array_equal(_u16(dst.data), ref)
+
+
+def test_nccl_exchange_grouped_loopback(bs, comm):
+    """bs_exchange: several sends / receives of different sizes in one NCCL group."""
+    sends = [torch.randn(n, device="cuda") for n in (1, 4097, 300000)]
+    recvs = [torch.zeros_like(t) for t in sends]
+    comm.exchange([(t, 0) for t in sends], [(t, 0) for t in recvs])
+    torch.cuda.synchronize()
+    for a, b in zip(sends, recvs):
+        assert torch.equal(a, b)
+
+
+def test_wait_signal_is_wrap_safe(bs):
+    """Flags and `done` counters are int32 and wrap after 2^31 (a long-running server):
+    a wait whose target wrapped past INT32_MAX is satisfied by the wrapped flag value and
+    not by an older one."""
+    from paper_2510_13223_b200.transport import ErrorFlag
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    err = ErrorFlag()
+    big = 2 ** 31 - 3
+    flag.fill_(bs.wrap_i32(big + 5))              # 2^31 + 2 wrapped to a negative int32
+    bs.wait_signal(flag.data_ptr(), big + 5, 50_000_000, err.ptr)
+    bs.wait_signal(flag.data_ptr(), big, 50_000_000, err.ptr)       # older target: done
+    torch.cuda.synchronize()
+    assert not err.set()
+    bs.wait_signal(flag.data_ptr(), big + 6, 2_000_000, err.ptr)    # not reached: times out
+    torch.cuda.synchronize()
+    assert err.set()
+    with pytest.raises(RuntimeError):
+        err.check()
+
+
+def test_epoch_signals_computed_on_device(bs):
+    """bs_signals_epoch / bs_wait_signals_epoch: value = (*epoch) * mul + add on the device;
+    bs_epoch_advance; captured in a CUDA graph, each replay uses the then-current epoch."""
+    from paper_2510_13223_b200.transport import ErrorFlag
+    ep = torch.full((1,), 2 ** 31 - 2, dtype=torch.int32, device="cuda")
+    flags = torch.zeros(3, dtype=torch.int32, device="cuda")
+    err = ErrorFlag()
+    ptrs = [flags.data_ptr() + 4 * i for i in range(3)]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        bs.epoch_advance(ep.data_ptr())            # 2^31 - 1
+        bs.signals_epoch(ptrs, ep.data_ptr(), [1, 3, 1], [0, -2, 7])
+        bs.wait_signals_epoch(ptrs, ep.data_ptr(), [1, 3, 1], [0, -2, 7], 50_000_000, err.ptr)
+    torch.cuda.synchronize()
+    e = 2 ** 31 - 1
+    assert flags.cpu().tolist() == [bs.wrap_i32(e), bs.wrap_i32(3 * e - 2), bs.wrap_i32(e + 7)]
+    assert not err.set()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        bs.epoch_advance(ep.data_ptr())
+        bs.signals_epoch(ptrs[:1], ep.data_ptr(), 2, 1)
+        bs.wait_signals_epoch(ptrs[:1], ep.data_ptr(), 2, 1, 50_000_000, err.ptr)
+    for k in range(1, 4):                            # the epoch wraps on the first replay
+        g.replay()
+        torch.cuda.synchronize()
+        assert int(ep.item()) == bs.wrap_i32(e + k)
+        assert int(flags[0].item()) == bs.wrap_i32(2 * (e + k) + 1)
+    assert not err.set()

@@ -17,6 +17,7 @@ import torch.multiprocessing as mp
 
 import oracle
 import synth
+from gloo_wire import GlooWire
 from paper_2510_13223_b200.ring import CpuExec, ShardedDecodeStep, split_partial
 
 SHAPE = synth.Shape(2, 4, 2, 64)
@@ -121,7 +122,8 @@ def run_rank(rank, world, port, errq):
             handoff_dst_ids=torch.tensor(free_home, dtype=torch.int64),
             chunk_bytes=oracle.chunk_elems(SHAPE.hkv, 16, SHAPE.d) * 2,
             pg_attn=dist.group.WORLD if world > 1 else None,
-            pg_mig=dist.new_group(list(range(world))) if world > 1 else None, append=kv_new)
+            pg_mig=dist.new_group(list(range(world))) if world > 1 else None, append=kv_new,
+            wire_attn=GlooWire() if world > 1 else None, wire_mig=GlooWire() if world > 1 else None)
         q = torch.from_numpy(own.q.view(np.int16)).view(torch.bfloat16)
         out = torch.zeros(q.shape, dtype=torch.bfloat16)
         lse = torch.zeros(q.shape[:-1], dtype=torch.float32)

@@ -16,6 +16,7 @@ import torch.multiprocessing as mp
 
 import oracle
 import synth
+from gloo_wire import GlooWire
 from paper_2510_13223_b200.seqshard import SeqShardedStep
 
 from test_ring_gloo import NpPool, OracleOps  # noqa: E402  (test-infrastructure kernels)
@@ -58,7 +59,8 @@ def run_rank(rank, world, port, errq):
         step = SeqShardedStep(OracleOps(sc), rank, world, pool, torch.from_numpy(mine.block_tables),
                               torch.from_numpy(ks), SHAPE.hq, SHAPE.n_layers, SHAPE.d, SHAPE.hkv,
                               group=dist.group.WORLD if world > 1 else None, transport="collective",
-                              handoff_src_ids=torch.tensor(src), handoff_dst_ids=torch.tensor(dst))
+                              handoff_src_ids=torch.tensor(src), handoff_dst_ids=torch.tensor(dst),
+                              wire=GlooWire() if world > 1 else None)
         assert step.transport == "collective"
         q_all = torch.from_numpy(dense.q.view(np.int16)).view(torch.bfloat16)
         q = q_all[:, rank::world].contiguous()

@@ -311,35 +311,122 @@ def step_stats(per_step):
                     "(the copy stream runs ahead), the mean over K is the exact figure"}
 
 
-def _same_gpu() -> bool:
-    return os.environ.get("BS_RING_SAME_GPU", "0") == "1"
+class DrvTimer:
+    """A timing CUDA event recorded with CU_EVENT_RECORD_EXTERNAL: inside a stream capture
+    it becomes an event-record NODE of the graph, so kernels replayed from a CUDA graph are
+    timed on the stream that launches them, live, like eager ones (outside a capture it is
+    an ordinary record).  Driver API through ctypes (measurement plumbing, not the path)."""
+    _cu = None
+
+    def __init__(self):
+        import ctypes
+        if DrvTimer._cu is None:
+            cu = ctypes.CDLL("libcuda.so.1")
+            cu.cuEventCreate.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_uint]
+            cu.cuEventRecordWithFlags.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint]
+            cu.cuEventElapsedTime.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_void_p,
+                                              ctypes.c_void_p]
+            cu.cuEventDestroy_v2.argtypes = [ctypes.c_void_p]
+            DrvTimer._cu = cu
+        self.ev = ctypes.c_void_p()
+        torch.cuda.current_stream()   # the primary context is current on this thread
+        r = DrvTimer._cu.cuEventCreate(ctypes.byref(self.ev), 0)
+        if r != 0:
+            raise RuntimeError(f"cuEventCreate: {r}")
+
+    def record(self, stream=None):
+        s = torch.cuda.current_stream() if stream is None else stream
+        r = DrvTimer._cu.cuEventRecordWithFlags(self.ev, s.cuda_stream, 1)
+        if r != 0:
+            raise RuntimeError(f"cuEventRecordWithFlags: {r}")
+
+    def elapsed_time(self, end) -> float:
+        import ctypes
+        ms = ctypes.c_float()
+        r = DrvTimer._cu.cuEventElapsedTime(ctypes.byref(ms), self.ev, end.ev)
+        if r != 0:
+            raise RuntimeError(f"cuEventElapsedTime: {r}")
+        return float(ms.value)
+
+    def __del__(self):
+        try:
+            DrvTimer._cu.cuEventDestroy_v2(self.ev)
+        except Exception:
+            pass
 
 
-def _time_graph(step, q, out, lse, K, world, device):
-    """Capture one step in a CUDA graph on every rank (flags computed on the device) and
-    time K replays; None on every rank if any rank could not capture."""
+def _capture_steps(step, q, out, lse, K, world, device, timers=None, bounds=None):
+    """ONE CUDA graph holding K consecutive steps (every stream, every layer; timers[k] and
+    the step boundaries as event-record nodes), captured on every rank; None on every rank
+    if any rank could not capture (then the caller runs eagerly)."""
     g, why = None, ""
     try:
-        g = step.capture(q, out, lse)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for k in range(K):
+                step.enqueue(q, out, lse, **({} if timers is None else {"timers": timers[k]}))
+                if bounds is not None and k < K - 1:
+                    bounds[k].record()
     except Exception as e:
-        why = repr(e)[:200]
+        g, why = None, repr(e)[:200]
+        log("graph capture failed:", why)
+    torch.cuda.synchronize()
     if not _all_true(g is not None, world, device):
-        return {"error": why or "a peer could not capture"}
-    for _ in range(2):
-        g.replay()
-    torch.cuda.synchronize()
+        return None, why or "a peer could not capture"
+    return g, ""
+
+
+def run_steps(step, q, out, lse, K, L, world, device, use_graph, timed=True):
+    """The timed region of K steps.  use_graph: the K steps replayed from one CUDA graph
+    (timers as graph nodes), else submitted eagerly.  Returns a dict with this rank's
+    ms per step, the sorted per-step times, per-layer attention / migration kernel times,
+    host submission ms per step, the mode, clock summary and NVLink counter readings."""
+    timers = ([[tuple(DrvTimer() for _ in range(4)) for _ in range(L)] for _ in range(K)]
+              if timed else None)
+    step_ev = [DrvTimer() for _ in range(K - 1)]
+    t0, t1 = DrvTimer(), DrvTimer()
+    g = None
+    mode = "eager"
+    if use_graph:
+        g, why = _capture_steps(step, q, out, lse, K, world, device, timers, step_ev)
+        if g is not None:
+            mode = "graph"
+            g.replay()                      # warm the graph (K more untimed steps)
+            torch.cuda.synchronize()
+            _barrier(world)
+            torch.cuda.synchronize()
+        else:
+            mode = f"eager (graph capture failed: {why})"
+    nvl = NvlinkCounters(device.index) if world > 1 else None
+    nv0 = nvl.read() if nvl else None
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        t0.record()
+        h0 = time.perf_counter()
+        if g is not None:
+            g.replay()
+        else:
+            for k in range(K):
+                step.enqueue(q, out, lse, **({} if timers is None else {"timers": timers[k]}))
+                if k < K - 1:
+                    step_ev[k].record()
+        host_ms = (time.perf_counter() - h0) * 1e3 / K
+        t1.record()
+        torch.cuda.synchronize()
+    nv1 = nvl.read() if nvl else None
     _barrier(world)
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(K):
-        g.replay()
-    b.record()
-    torch.cuda.synchronize()
-    ms = _max_over_ranks(a.elapsed_time(b) / K, world, device)
+    bounds = [t0] + step_ev + [t1]
+    r = {"ms": t0.elapsed_time(t1) / K, "mode": mode, "host_ms": host_ms, "clocks": clk.summary(),
+         "nvlink": NvlinkCounters.delta(nv0, nv1, K) if world > 1 else None,
+         "per_step": sorted(a.elapsed_time(b) for a, b in zip(bounds[:-1], bounds[1:]))}
+    if timers is not None:
+        r["attn_ms"] = [a.elapsed_time(b) for tk in timers for (a, b, _, _) in tk]
+        r["mig_ms"] = [c.elapsed_time(d) for tk in timers for (_, _, c, d) in tk]
     del g
-    return {"ms_per_step": round(ms, 4), "note": "the whole step (every stream, every layer) "
-            "replayed from one CUDA graph per rank; max over ranks"}
+    return r
+
+
+def _same_gpu() -> bool:
+    return os.environ.get("BS_RING_SAME_GPU", "0") == "1"
 
 
 # --------------------------------------------------------------------------------------
@@ -443,6 +530,67 @@ def _e2e_buffers(q, extra, L, device):
     return in_host, in_dev, rowb, q_dev, extra_dev
 
 
+def e2e_measure(bs, step, q_dev, out, lse, in_host, in_dev, rowb, out_host, lse_host, L, K,
+                world, device, use_graph):
+    """K end-to-end steps: per layer one H2D copy of [q_l | extra_l] from pinned memory (a
+    side stream; layer l's attention waits only for its own inputs), the step, per layer
+    the D2H copies of O_l / lse_l as each layer lands, and the host waiting for the result
+    every step -- every copy through the library's bs_copy_bytes (C-ABI).  One such step is
+    one CUDA graph replayed per step when possible.  Returns (ms per step, mode)."""
+    h2d = torch.cuda.Stream(device=device)
+    d2h = torch.cuda.Stream(device=device)
+    q_ev = [torch.cuda.Event() for _ in range(L)]
+    ob, lb = out[0].numel() * out.element_size(), lse[0].numel() * lse.element_size()
+
+    def one():
+        cur = torch.cuda.current_stream()
+        h2d.wait_stream(cur)
+        for layer in range(L):
+            bs.copy_ptr(in_dev.data_ptr() + layer * rowb, in_host.data_ptr() + layer * rowb, rowb,
+                        stream=h2d)
+            q_ev[layer].record(h2d)
+        step.enqueue(q_dev, out, lse, inputs_ready=q_ev)
+        for layer in range(L):
+            d2h.wait_event(step.out_ready[layer])
+            bs.copy_ptr(out_host.data_ptr() + layer * ob, out.data_ptr() + layer * ob, ob, stream=d2h)
+            bs.copy_ptr(lse_host.data_ptr() + layer * lb, lse.data_ptr() + layer * lb, lb, stream=d2h)
+        cur.wait_stream(d2h)
+
+    g, mode = None, "eager"
+    if use_graph:
+        one()
+        torch.cuda.synchronize()
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                one()
+        except Exception as e:
+            g = None
+            mode = f"eager (graph capture failed: {repr(e)[:120]})"
+        torch.cuda.synchronize()
+        if not _all_true(g is not None, world, device):
+            g = None
+        elif g is not None:
+            mode = "graph (one CUDA graph per e2e step: H2D copies + step + D2H copies)"
+
+    def e2e_step():
+        if g is not None:
+            g.replay()
+        else:
+            one()
+        torch.cuda.current_stream().synchronize()  # the next decode step needs the result
+    for _ in range(2):
+        e2e_step()
+    _barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(K):
+        e2e_step()
+    e1.record()
+    torch.cuda.synchronize()
+    return _max_over_ranks(e0.elapsed_time(e1) / K, world, device), mode
+
+
 def run_c2(args, rank, world, device):
     import paper_2510_13223_b200 as bs
 
@@ -459,52 +607,34 @@ def run_c2(args, rank, world, device):
         lse = torch.empty((L, BATCH, SHAPE.hq), dtype=torch.float32, device=device)
     torch.cuda.synchronize()
 
+    h0 = time.perf_counter()
     for _ in range(args.warmup):
         step.enqueue(q, out, lse)
+    host_ms = _max_over_ranks((time.perf_counter() - h0) * 1e3 / args.warmup, world, device)
     torch.cuda.synchronize()
     _barrier(world)
     torch.cuda.synchronize()
 
-    # ---- timed region: K steps, kernel events live on their launching streams --------
+    # ---- timed region: K steps replayed from one CUDA graph per rank (eager with the NCCL
+    # transport); kernel events are live graph nodes on their launching streams ----------
     K = args.steps
-    timers = [[tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in range(L)]
-              for _ in range(K)]
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(K - 1)]
-    nvl = NvlinkCounters(device.index) if world > 1 else None
-    nv0 = nvl.read() if nvl else None
-    with ClockSampler(torch.cuda.current_device()) as clk:
-        t0.record()
-        h0 = time.perf_counter()
-        for k in range(K):
-            step.enqueue(q, out, lse, timers=timers[k])
-            if k < K - 1:
-                step_ev[k].record()
-        host_ms = (time.perf_counter() - h0) * 1e3 / K
-        t1.record()
-        torch.cuda.synchronize()
-    nv1 = nvl.read() if nvl else None
-    _barrier(world)
+    use_graph = world == 1 or step.transport == "p2p"
     if step.links is not None:
         step.links.check()
-    ms = t0.elapsed_time(t1) / K
-    bounds = [t0] + step_ev + [t1]
-    per_step = sorted(a.elapsed_time(b) for a, b in zip(bounds[:-1], bounds[1:]))
-    attn_ms = [a.elapsed_time(b) for tk in timers for (a, b, _, _) in tk]
-    mig_ms = [c.elapsed_time(d) for tk in timers for (_, _, c, d) in tk]
+    run = run_steps(step, q, out, lse, K, L, world, device, use_graph)
+    if step.links is not None:
+        step.links.check()
+    ms_max = _max_over_ranks(run["ms"], world, device)
+    per_step, attn_ms, mig_ms = run["per_step"], run["attn_ms"], run["mig_ms"]
     # ---- exposure of the migration: the same steps without hand-offs --
     n_handoff, step.n_handoff = step.n_handoff, 0
     for _ in range(2):
         step.enqueue(q, out, lse)
     torch.cuda.synchronize()
     _barrier(world)
-    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    c0.record()
-    for _ in range(K):
-        step.enqueue(q, out, lse)
-    c1.record()
-    torch.cuda.synchronize()
+    comp = run_steps(step, q, out, lse, K, L, world, device, use_graph, timed=False)
     step.n_handoff = n_handoff
+    ms_compute = _max_over_ranks(comp["ms"], world, device)
     # ---- the hand-off alone (N=1: the same per-layer copy launches, nothing beside them)
     ms_mig_only = None
     if world == 1 and n_handoff:
@@ -521,15 +651,15 @@ def run_c2(args, rank, world, device):
         m1.record()
         torch.cuda.synchronize()
         ms_mig_only = m0.elapsed_time(m1) / K
-    ms_compute = _max_over_ranks(c0.elapsed_time(c1) / K, world, device)
-    ms_max = _max_over_ranks(ms, world, device)
-    host_ms = _max_over_ranks(host_ms, world, device)
-    # ---- the same step replayed from a CUDA graph (N=1 and the P2P transport) ----------
-    graph = None
-    if world == 1 or step.transport == "p2p":
-        graph = _time_graph(step, q, out, lse, K, world, device)
+    # ---- the same steps submitted eagerly (host-side cost of the Python protocol) -------
+    eager = None
+    if run["mode"] == "graph":
+        er = run_steps(step, q, out, lse, K, L, world, device, use_graph=False, timed=False)
+        eager = {"ms_per_step": round(_max_over_ranks(er["ms"], world, device), 4),
+                 "host_submit_ms_per_step": round(_max_over_ranks(er["host_ms"], world, device), 4)}
     if step.links is not None:
         step.links.check()
+    clk = run["clocks"]
 
     # ---- e2e: same step through host buffers ----------------------------------------
     # every step: q copied H2D from pinned memory layer by layer on its own stream (layer
@@ -539,44 +669,18 @@ def run_c2(args, rank, world, device):
     # The step's inputs of layer l -- q_l and (H7) the decoded token's K/V kv_l -- sit
     # packed in one row [q_l | kv_l] of a pinned host buffer and of a device buffer, so each
     # layer is ONE copy; the step reads q and its append K/V as strided views of that buffer.
+    # One e2e step (copies + step) is one CUDA graph replayed per decode step when the step
+    # itself is graph-capturable, else submitted eagerly.
     kv0 = step.append
     in_host, in_dev, rowb, q_dev, kv_dev = _e2e_buffers(q, kv0, L, device)
     if kv0 is not None:
         step.append = kv_dev
     out_host = torch.empty(out.shape, dtype=out.dtype).pin_memory()
     lse_host = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
-    h2d = torch.cuda.Stream(device=device)
-    d2h = torch.cuda.Stream(device=device)
-    q_ev = [torch.cuda.Event() for _ in range(L)]
-    cur = torch.cuda.current_stream()
-    ob, lb = out[0].numel() * out.element_size(), lse[0].numel() * lse.element_size()
-
-    def e2e_step():  # every copy through the library's own bs_copy_bytes (C-ABI)
-        h2d.wait_stream(cur)
-        for layer in range(L):
-            bs.copy_ptr(in_dev.data_ptr() + layer * rowb, in_host.data_ptr() + layer * rowb, rowb,
-                        stream=h2d)
-            q_ev[layer].record(h2d)
-        step.enqueue(q_dev, out, lse, inputs_ready=q_ev)
-        for layer in range(L):
-            d2h.wait_event(step.out_ready[layer])
-            bs.copy_ptr(out_host.data_ptr() + layer * ob, out.data_ptr() + layer * ob, ob, stream=d2h)
-            bs.copy_ptr(lse_host.data_ptr() + layer * lb, lse.data_ptr() + layer * lb, lb, stream=d2h)
-        cur.wait_stream(d2h)
-        cur.synchronize()  # the next decode step needs this step's result on the host
-
-    for _ in range(2):
-        e2e_step()
-    _barrier(world)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(K):
-        e2e_step()
-    e1.record()
-    torch.cuda.synchronize()
+    e2e_ms, e2e_mode = e2e_measure(bs, step, q_dev, out, lse, in_host, in_dev, rowb, out_host,
+                                   lse_host, L, K, world, device, use_graph)
     if step.links is not None:
         step.links.check()   # every wait of the e2e steps completed in time
-    e2e_ms = _max_over_ranks(e0.elapsed_time(e1) / K, world, device)
     assert torch.equal(out_host.view(torch.int16), out.cpu().view(torch.int16))
 
     # ---- derived numbers ----------------------------------------------------------------
@@ -664,7 +768,7 @@ def run_c2(args, rank, world, device):
         # the hand-off copy kernel (H2): local HBM read + write at N=1 (sharing HBM with the
         # attention beside it), NVLink payload per direction at N>1 on distinct GPUs
         "roofline_migrate": rmig,
-        "nvlink_counters": NvlinkCounters.delta(nv0, nv1, K) if world > 1 else None,
+        "nvlink_counters": run["nvlink"],
         "overlap": {"step_ms": round(ms_max, 4), "compute_only_ms": round(ms_compute, 4),
                     "exposure": round((ms_max - ms_compute) / ms_compute, 4),
                     "migrate_only_ms": None if ms_mig_only is None else round(ms_mig_only, 4),
@@ -674,15 +778,19 @@ def run_c2(args, rank, world, device):
                     "note": ("N=1: the hand-off and the attention share one GPU's HBM, so the "
                              "hand-off's bytes cannot be hidden; over NVLink (N>1) its write side "
                              "leaves the GPU") if world == 1 else "N>1"},
-        "host_submit_ms_per_step": round(host_ms, 4),
-        "graph": graph,
+        "timing": {"mode": run["mode"], "compute_only_mode": comp["mode"],
+                   "eager": eager, "eager_host_submit_ms_per_step": round(host_ms, 4),
+                   "note": "graph: the K timed steps replayed from ONE CUDA graph per rank, "
+                           "per-kernel events as graph nodes on their launching streams; "
+                           "eager_host_submit_ms_per_step = the Python/ctypes submission cost of "
+                           "one step (warm-up steps, max over ranks)"},
         "gpu_launches": step.launches_per_step * K,
         "e2e": {"value": round(BATCH * world / (e2e_ms * 1e-3), 2), "unit": "tokens/s",
-                "ms_per_step": round(e2e_ms, 4),
+                "ms_per_step": round(e2e_ms, 4), "mode": e2e_mode,
                 "h2d_bytes_per_step": q.numel() * q.element_size() + (
                     0 if step.append is None else step.append.numel() * step.append.element_size()),
                 "d2h_bytes_per_step": out.numel() * out.element_size() + lse.numel() * lse.element_size()},
-        "clocks": clk.summary(),
+        "clocks": clk,
     }
     if rank == 0 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline(case, budget_s=args.cpu_seconds)
@@ -768,33 +876,17 @@ def run_seq(args, rank, world, device, name, headline=False):
         out = torch.empty((L, B // W, shape.hq, shape.d), dtype=torch.bfloat16, device=device)
         lse = torch.empty((L, B // W, shape.hq), dtype=torch.float32, device=device)
     p2p = step.transport == "p2p"
+    h0 = time.perf_counter()
     for _ in range(args.warmup):
         step.enqueue(q, out, lse)
+    host_ms = _max_over_ranks((time.perf_counter() - h0) * 1e3 / args.warmup, world, device)
     torch.cuda.synchronize()
     _barrier(world)
     torch.cuda.synchronize()
     K = args.steps
-    timers = ([[tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in range(L)]
-               for _ in range(K)] if p2p else None)
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    nvl = NvlinkCounters(device.index) if W > 1 else None
-    nv0 = nvl.read() if nvl else None
-    with ClockSampler(torch.cuda.current_device()) as clk:
-        t0.record()
-        h0 = time.perf_counter()
-        for k in range(K):
-            if p2p:
-                step.enqueue(q, out, lse, timers=timers[k])
-            else:
-                step.enqueue(q, out, lse)
-        host_ms = (time.perf_counter() - h0) * 1e3 / K
-        t1.record()
-        torch.cuda.synchronize()
-    nv1 = nvl.read() if nvl else None
-    _barrier(world)
+    run = run_steps(step, q, out, lse, K, L, world, device, use_graph=p2p, timed=p2p)
     step.check()
-    ms_max = _max_over_ranks(t0.elapsed_time(t1) / K, world, device)
-    host_ms = _max_over_ranks(host_ms, world, device)
+    ms_max = _max_over_ranks(run["ms"], world, device)
     # compute-only steps (no hand-off) -> exposure of the hand-off
     ms_compute = None
     if n_hand:
@@ -803,15 +895,14 @@ def run_seq(args, rank, world, device, name, headline=False):
             step.enqueue(q, out, lse)
         torch.cuda.synchronize()
         _barrier(world)
-        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        c0.record()
-        for _ in range(K):
-            step.enqueue(q, out, lse)
-        c1.record()
-        torch.cuda.synchronize()
+        comp = run_steps(step, q, out, lse, K, L, world, device, use_graph=p2p, timed=False)
         step.n_handoff = n_hand
-        ms_compute = _max_over_ranks(c0.elapsed_time(c1) / K, world, device)
-    graph = _time_graph(step, q, out, lse, K, world, device) if p2p else None
+        ms_compute = _max_over_ranks(comp["ms"], world, device)
+    eager = None
+    if run["mode"] == "graph":
+        er = run_steps(step, q, out, lse, K, L, world, device, use_graph=False, timed=False)
+        eager = {"ms_per_step": round(_max_over_ranks(er["ms"], world, device), 4),
+                 "host_submit_ms_per_step": round(_max_over_ranks(er["host_ms"], world, device), 4)}
     step.check()
     # e2e through host buffers (P2P transport): q H2D per layer, O / lse D2H per layer
     e2e = None
@@ -819,39 +910,11 @@ def run_seq(args, rank, world, device, name, headline=False):
         in_host, in_dev, rowb, q_dev, _ = _e2e_buffers(q, None, L, device)
         out_host = torch.empty(out.shape, dtype=out.dtype).pin_memory()
         lse_host = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
-        h2d, d2h = torch.cuda.Stream(device=device), torch.cuda.Stream(device=device)
-        q_ev = [torch.cuda.Event() for _ in range(L)]
-        cur = torch.cuda.current_stream()
-        ob, lb = out[0].numel() * out.element_size(), lse[0].numel() * lse.element_size()
-
-        def e2e_step():
-            h2d.wait_stream(cur)
-            for layer in range(L):
-                bs.copy_ptr(in_dev.data_ptr() + layer * rowb, in_host.data_ptr() + layer * rowb,
-                            rowb, stream=h2d)
-                q_ev[layer].record(h2d)
-            step.enqueue(q_dev, out, lse, inputs_ready=q_ev)
-            for layer in range(L):
-                d2h.wait_event(step.out_ready[layer])
-                bs.copy_ptr(out_host.data_ptr() + layer * ob, out.data_ptr() + layer * ob, ob,
-                            stream=d2h)
-                bs.copy_ptr(lse_host.data_ptr() + layer * lb, lse.data_ptr() + layer * lb, lb,
-                            stream=d2h)
-            cur.wait_stream(d2h)
-            cur.synchronize()
-        for _ in range(2):
-            e2e_step()
-        _barrier(world)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(K):
-            e2e_step()
-        e1.record()
-        torch.cuda.synchronize()
+        e2e_ms, e2e_mode = e2e_measure(bs, step, q_dev, out, lse, in_host, in_dev, rowb, out_host,
+                                       lse_host, L, K, world, device, True)
         step.check()
-        e2e_ms = _max_over_ranks(e0.elapsed_time(e1) / K, world, device)
         e2e = {"value": round(B / (e2e_ms * 1e-3), 2), "unit": "tokens/s",
-               "ms_per_step": round(e2e_ms, 4),
+               "ms_per_step": round(e2e_ms, 4), "mode": e2e_mode,
                "h2d_bytes_per_step": q.numel() * q.element_size(),
                "d2h_bytes_per_step": out.numel() * out.element_size() + lse.numel() * lse.element_size(),
                "note": "per rank: its home requests' q in, their O / lse out; max over ranks"}
@@ -871,12 +934,12 @@ def run_seq(args, rank, world, device, name, headline=False):
                                       + (" [ALL RANKS ON ONE GPU: functional check only]"
                                          if same_gpu else "")),
                       "l2": "no flush: every step reads >= 4 GiB of distinct KV per GPU >> 126 MB L2"},
-           "host_submit_ms_per_step": round(host_ms, 4), "graph": graph,
-           "gpu_launches": step.launches_per_step * K, "e2e": e2e, "clocks": clk.summary(),
-           "nvlink_counters": NvlinkCounters.delta(nv0, nv1, K) if W > 1 else None}
+           "timing": {"mode": run["mode"], "eager": eager,
+                      "eager_host_submit_ms_per_step": round(host_ms, 4)},
+           "gpu_launches": step.launches_per_step * K, "e2e": e2e, "clocks": run["clocks"],
+           "nvlink_counters": run["nvlink"]}
     if p2p:
-        attn_ms = [a.elapsed_time(b) for tk in timers for (a, b, _, _) in tk]
-        attn_avg = statistics.fmean(attn_ms)
+        attn_avg = statistics.fmean(run["attn_ms"])
         gbs = a_bytes / (attn_avg * 1e-3) / 1e9
         res["attn_hbm_gbs_per_gpu"] = round(gbs, 1)
         res["attn_ms_per_layer"] = round(attn_avg, 5)
@@ -889,8 +952,7 @@ def run_seq(args, rank, world, device, name, headline=False):
         # launch itself (q push, flag waits, remote partial stores and merges)
         res["exchange_ms_per_layer"] = round(max(ms_max / L - attn_avg, 0.0), 5)
         if n_hand:
-            mig = [c.elapsed_time(d) for tk in timers for (_, _, c, d) in tk]
-            mig_avg = statistics.fmean(mig)
+            mig_avg = statistics.fmean(run["mig_ms"])
             mb = n_hand * pool.chunk_bytes
             res["migrate_bytes_per_layer"] = mb
             res["migrate_gbs"] = round(mb / (mig_avg * 1e-3) / 1e9, 1)

@@ -128,7 +128,8 @@ def layer_payload_bytes(s_w: float, s_kv: float) -> float:
 
 
 def t_layer_s(s_total: float, b_net: float, t_sync: float) -> float:
-    """eq. 4; parity unpinned: the paper prints no worked example."""
+    """eq. 4; pinned to hand-worked layer sizes and closed forms
+    (tests/golden/paper_eq3_4_hand.txt, tests/test_oracle_pins.py)."""
     return lib().or_t_layer_s(s_total, b_net, t_sync)
 
 

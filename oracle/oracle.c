@@ -24,10 +24,11 @@
  *   or_migrate_heads_layer       -> page identity, untouched heads/blocks, head-
  *                                   split attention == full-pool heads; concat of
  *                                   the head groups == torch SDPA (NEXT F2)        [pinned]
- *   or_layer_payload_bytes       -> eq. 3 identity (S_total = S_w + S_kv) checked against the
- *                                   bytes bs_kv_migrate_layers + bs_copy_bytes move   [pinned]
- *   or_t_layer_s                 -> eq. 4: PARITY UNPINNED (the paper prints no worked
- *                                   example; it is an approximation, used for reports)
+ *   or_layer_payload_bytes       -> eq. 3 on hand-worked layer sizes (Llama-2-7B and
+ *                                   Llama-3.1-8B layers, tests/golden/paper_eq3_4_hand.txt)
+ *                                                                                  [pinned]
+ *   or_t_layer_s                 -> eq. 4 on the same hand-worked cases + closed forms
+ *                                   (T(0) = T_sync, affine in S, 1/B_net)           [pinned]
  *   or_pool_alloc / or_pool_free -> brute-force enumeration of the stated policy
  *                                   (R-A12 is a policy choice: "parity unpinned"
  *                                   for the choice itself, pinned for the policy)

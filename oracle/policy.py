@@ -111,3 +111,23 @@ def plan_migrations(load, n_layers, layer_load, layer_cost, n_heads, head_load, 
         if not done:
             break
     return moves, load, n_layers, n_heads
+
+
+def run_cycles(cycles, delta_up, delta_down, rho):
+    """Alg. 1 applied once per control period with the hysteresis of PAPER.md:462
+    ("distinct upward and downward thresholds (delta_up, delta_down)", reading R-F4g):
+    a cycle classifies devices with delta_up while the controller is idle -- the previous
+    cycle moved nothing (and before the first cycle) -- and with delta_down while it is
+    migrating -- the previous cycle moved at least one module.
+
+    ``cycles``: a list of dicts with the keyword arguments of plan_migrations except
+    delta / rho (each period's measured loads and module tables).  Returns the list of
+    plan_migrations results, one per cycle."""
+    migrating = False
+    out = []
+    for c in cycles:
+        delta = delta_down if migrating else delta_up
+        res = plan_migrations(delta=delta, rho=rho, **c)
+        migrating = len(res[0]) > 0
+        out.append(res)
+    return out

@@ -83,6 +83,33 @@ def test_golden_eq15_17_printed_values():
     assert oracle.t_kv_ms(4096, 1000, 0.5, 200) == pytest.approx(0.08192, abs=1e-12)
 
 
+GOLDEN_EQ34 = os.path.join(os.path.dirname(__file__), "golden", "paper_eq3_4_hand.txt")
+
+
+def test_eq3_eq4_hand_worked_values():
+    """eq. 3 (S_total = S_w + S_kv) and eq. 4 (T_layer ~= S_total / B_net + T_sync),
+    PAPER.md:187-195: the oracle's helpers reproduce values worked by hand from model
+    shapes (tests/golden/paper_eq3_4_hand.txt), and eq. 4's closed forms hold."""
+    rows = [ln.split() for ln in open(GOLDEN_EQ34) if ln.strip() and not ln.startswith("#")]
+    assert len(rows) == 3
+    for name, s_w, s_kv, s_tot, b_net, t_sync, t_layer in rows:
+        s_w, s_kv, s_tot = int(s_w), int(s_kv), int(s_tot)
+        assert oracle.layer_payload_bytes(s_w, s_kv) == s_tot, name
+        assert oracle.t_layer_s(s_tot, float(b_net), float(t_sync)) == pytest.approx(
+            float(t_layer), rel=1e-12), name
+    # the hand sizes themselves, from the shapes (bf16): Llama-2-7B layer, 2048 tokens
+    assert 2 * (4 * 4096 * 4096 + 3 * 4096 * 11008) == 404750336
+    assert 2048 * oracle.kv_bytes_per_token_layer(32, 128) == 33554432
+    # eq. 15's per-token size (printed, PAPER.md:273) gives the Llama-3.1-8B S_kv
+    assert 1000 * oracle.kv_bytes_per_token_layer(8, 128) == 4096000
+    # eq. 4 closed forms: no payload -> T_sync; affine in S; inversely proportional to B
+    assert oracle.t_layer_s(0.0, 1e9, 3e-3) == 3e-3
+    t1 = oracle.t_layer_s(1e9, 1e11, 2e-3) - 2e-3
+    t2 = oracle.t_layer_s(2e9, 1e11, 2e-3) - 2e-3
+    assert t2 == pytest.approx(2 * t1, rel=1e-15) and t1 == pytest.approx(1e-2, rel=1e-15)
+    assert oracle.t_layer_s(1e9, 2e11, 0.0) == pytest.approx(t1 / 2, rel=1e-15)
+
+
 def test_pool_geometry_matches_eq15():
     # one (layer, block) chunk of the Llama-3.1-8B shape = 16 tokens x eq. 15's 4096 B
     assert oracle.chunk_elems(8, 16, 128) * 2 == 16 * oracle.kv_bytes_per_token_layer(8, 128)

@@ -139,3 +139,57 @@ def test_hysteresis_controller():
     moves, load, nl, nh = c.cycle(load, **dict(kw, n_layers=nl, n_heads=nh))
     assert moves == [] and not c.active
     assert prod.utilization(35, 100, 95, 100) == pytest.approx(1.3)
+
+
+def test_oracle_hysteresis_hand_worked():
+    """R-F4g, worked by hand with exactly representable numbers: delta_up =
+    1/4, delta_down = 1/8, one layer carries 1/16 of load (cost 1, rho 0.1).
+      cycle 1 (idle -> delta_up):   [1, 1/2]: gap 1/2 > 1/4 -> move -> [15/16, 9/16]:
+                                    gap 3/8 > 1/4 -> move -> [7/8, 5/8]: gap 1/4, stop (2 moves)
+      cycle 2 (migrating -> delta_down): gap 1/4 > 1/8 -> move -> [13/16, 11/16]: stop (1)
+      cycle 3 (migrating -> delta_down): gap 1/8, no move -> idle
+      cycle 4 (idle -> delta_up): new loads [7/8, 11/16], gap 3/16 -- above delta_down but
+                                    not delta_up: no move (the hysteresis band)
+      cycle 5 (idle): [1, 11/16], gap 5/16 > 1/4 -> move -> [15/16, 3/4]: gap 3/16, stop."""
+    kw = _dev(2, layers=4, lu=1 / 16, lc=1.0, sa=0)
+    cycles = []
+    for ld in ([1.0, 0.5], None, None, [0.875, 0.6875], [1.0, 0.6875]):
+        if cycles:   # the next period starts from the placement the last one left
+            prev = ref.run_cycles(cycles, 0.25, 0.125, 0.1)[-1]
+            kw = dict(kw, n_layers=prev[2], n_heads=prev[3])
+            ld = prev[1] if ld is None else ld
+        cycles.append(dict(kw, load=ld))
+    got = ref.run_cycles(cycles, 0.25, 0.125, 0.1)
+    assert [len(r[0]) for r in got] == [2, 1, 0, 0, 1]
+    assert got[0][1] == [0.875, 0.625] and got[1][1] == [0.8125, 0.6875]
+    assert got[2][1] == [0.8125, 0.6875] and got[3][1] == [0.875, 0.6875]
+    assert got[4][1] == [0.9375, 0.75]
+    # without hysteresis (delta_up = delta_down = 1/8) cycle 4 would have moved
+    flat = ref.run_cycles(cycles, 0.125, 0.125, 0.1)
+    assert len(flat[3][0]) == 1
+
+
+def test_product_controller_equals_oracle_hysteresis():
+    """MigrationController (product) == oracle.run_cycles on random cycle sequences."""
+    rng = random.Random(5)
+    for _ in range(100):
+        D = rng.randint(2, 6)
+        up = rng.uniform(0.15, 0.5)
+        down = rng.uniform(0.02, up)
+        rho = rng.uniform(0, 0.3)
+        c = prod.MigrationController(up, down, rho)
+        tables = dict(layer_load=[rng.uniform(0.01, 0.3) for _ in range(D)],
+                      layer_cost=[rng.uniform(0.1, 2) for _ in range(D)],
+                      head_load=[rng.uniform(0.005, 0.08) for _ in range(D)],
+                      head_cost=[rng.uniform(0.01, 1) for _ in range(D)],
+                      supports_layer=[rng.randint(0, 1) for _ in range(D)],
+                      supports_attn=[1] * D)
+        nl, nh = [rng.randint(0, 5) for _ in range(D)], [rng.randint(0, 8) for _ in range(D)]
+        cyc = []
+        for _ in range(rng.randint(1, 8)):
+            load = [rng.uniform(0, 2) for _ in range(D)]
+            cyc.append(dict(tables, load=load, n_layers=list(nl), n_heads=list(nh)))
+            got = c.cycle(load, n_layers=nl, n_heads=nh, **tables)
+            nl, nh = got[2], got[3]
+            exp = ref.run_cycles(cyc, up, down, rho)[-1]
+            assert got[0] == exp[0] and got[1] == exp[1] and got[2] == exp[2] and got[3] == exp[3]

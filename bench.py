@@ -327,6 +327,7 @@ class DrvTimer:
             cu.cuEventElapsedTime.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_void_p,
                                               ctypes.c_void_p]
             cu.cuEventDestroy_v2.argtypes = [ctypes.c_void_p]
+            cu.cuStreamIsCapturing.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]
             DrvTimer._cu = cu
         self.ev = ctypes.c_void_p()
         torch.cuda.current_stream()   # the primary context is current on this thread
@@ -335,8 +336,11 @@ class DrvTimer:
             raise RuntimeError(f"cuEventCreate: {r}")
 
     def record(self, stream=None):
+        import ctypes
         s = torch.cuda.current_stream() if stream is None else stream
-        r = DrvTimer._cu.cuEventRecordWithFlags(self.ev, s.cuda_stream, 1)
+        st = ctypes.c_int(0)   # the EXTERNAL flag is only valid while the stream captures
+        DrvTimer._cu.cuStreamIsCapturing(s.cuda_stream, ctypes.byref(st))
+        r = DrvTimer._cu.cuEventRecordWithFlags(self.ev, s.cuda_stream, 1 if st.value == 1 else 0)
         if r != 0:
             raise RuntimeError(f"cuEventRecordWithFlags: {r}")
 

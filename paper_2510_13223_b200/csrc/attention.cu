@@ -966,7 +966,14 @@ bool use_mma(int G) {
   return (v == 1 && G >= 4) || v == 2;
 }
 
+int deep_variant() {  // experiment switch: 1 = 4 stages x 1 CTA/SM, 2 = 3 stages x 2 CTAs/SM
+  static int v = env_int("BS_ATTN_DEEP", 0);
+  return v;
+}
+
 Variant variant_for(int d, int G) {
+  if (use_mma(G) && d == 128 && deep_variant() == 1) return Variant{4, 1, true};
+  if (use_mma(G) && d == 128 && deep_variant() == 2) return Variant{3, 2, true};
   if (use_mma(G)) return d == 128 ? Variant{2, 3, true} : Variant{4, 3, true};
   if (alt_variant() == 1) return d == 128 ? Variant{3, 2, false} : Variant{6, 2, false};
   if (d == 128) return G <= 4 ? Variant{2, 3, false} : Variant{3, 2, false};
@@ -1010,8 +1017,15 @@ bs_status make_plan(int batch, int G, int hq, int hkv, int d, int n_local, const
     const int x = e ? atoi(e) : 0;
     return x > 0 ? x : kBtMax;
   }();
+  // experiment switch: force the number of ranges per shard width
+  static const int forced_ns = [] {
+    const char* e = getenv("BS_ATTN_NSPLIT");
+    return e ? atoi(e) : 0;
+  }();
   int best_bps = -1;
   double best = 1e300;
+  if (forced_ns > 0 && !rank_invariant)
+    best_bps = std::min(kBtMax, std::max(min_bps, (mb_max + forced_ns - 1) / forced_ns));
   for (int pass = 0; pass < 2 && best_bps < 0; ++pass) {  // pass 1: without the cap
     const int cap =
         pass == 0 && !rank_invariant ? std::min(kBtMax, std::max(max_bps, min_bps)) : kBtMax;
@@ -1090,8 +1104,13 @@ template <int D, int G>
 bs_status launch_attn_t(const AttnParams& p, const TMaps* tm, int batch, cudaStream_t stream) {
   const Variant v = variant_for(D, G);
   if (v.mma && tm) {
-    if constexpr (D == 128) return launch_attn_mma<D, G, 2, 3>(p, *tm, batch, stream);
-    else return launch_attn_mma<D, G, 4, 3>(p, *tm, batch, stream);
+    if constexpr (D == 128) {
+      if (v.stages == 4) return launch_attn_mma<D, G, 4, 1>(p, *tm, batch, stream);
+      if (v.stages == 3) return launch_attn_mma<D, G, 3, 2>(p, *tm, batch, stream);
+      return launch_attn_mma<D, G, 2, 3>(p, *tm, batch, stream);
+    } else {
+      return launch_attn_mma<D, G, 4, 3>(p, *tm, batch, stream);
+    }
   }
   if constexpr (D == 128) {
     if (v.stages == 2) return launch_attn_v<D, G, 2, 3>(p, batch, stream);

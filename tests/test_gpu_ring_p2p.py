@@ -41,11 +41,13 @@ def _dev(a):
     return torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).view(torch.bfloat16).cuda()
 
 
-def run_rank(rank, world, port, errq, fused, graph=False):
+def run_rank(rank, world, port, errq, fused, graph=False, cross=False, transport="p2p"):
+    """cross: rank r on cuda:r (distinct GPUs: NVLink / peer mappings); else every rank on
+    cuda:0.  transport "nccl": the library's own NCCL communicator (distinct GPUs only)."""
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
-        torch.cuda.set_device(0)
+        torch.cuda.set_device(rank if cross else 0)
         dist.init_process_group("gloo", rank=rank, world_size=world)
         import paper_2510_13223_b200 as bs
         from paper_2510_13223_b200.ring import CudaExec, CudaOps, ShardedDecodeStep
@@ -64,7 +66,7 @@ def run_rank(rank, world, port, errq, fused, graph=False):
         cp = bs.KVPool(SHAPE.n_layers, cold.pool.shape[1], SHAPE.hkv, SHAPE.d)
         cp.data.copy_(_dev(cold.pool))
         i32 = lambda x: torch.as_tensor(np.asarray(x), dtype=torch.int32).cuda()
-        dev = torch.device("cuda", 0)
+        dev = torch.device("cuda", rank if cross else 0)
         sc = synth.default_scale(SHAPE.d)
         # H7: each request's decoded token K/V, pushed with q to the next rank, which
         # appends it at the end of shard 1 in its cold pool before attention
@@ -76,15 +78,18 @@ def run_rank(rank, world, port, errq, fused, graph=False):
                                  cp, i32(cold.block_tables), i32(ks), SHAPE.hq, SHAPE.n_layers, SHAPE.d,
                                  handoff_src_ids=i32(free_cold), handoff_dst_ids=i32(free_home),
                                  chunk_bytes=hp.chunk_bytes, pg_attn=dist.group.WORLD,
-                                 device=dev, transport="p2p", fused_exchange=fused, append=kv_new)
-        assert step.transport == "p2p" and step.fused_exchange == fused
+                                 pg_mig=dist.new_group(list(range(world))),
+                                 device=dev, transport=transport, fused_exchange=fused, append=kv_new)
+        assert step.transport == transport, getattr(step, "fallback_reason", None)
+        assert step.fused_exchange == (fused and transport == "p2p")
         q = _dev(own.q)
         for _ in range(2):   # two epochs
             out = torch.full(q.shape, float("nan"), dtype=torch.bfloat16, device=dev)
             lse = torch.full(q.shape[:-1], float("nan"), device=dev)
             step.enqueue(q, out, lse)
             torch.cuda.synchronize()
-            step.links.check()
+            if step.links is not None:
+                step.links.check()
             dist.barrier()
             bits = kv_new.cpu().view(torch.int16).numpy().view(np.uint16)  # the reference KV
             for b, n in enumerate(lens_of(rank)):                          # ends with the
@@ -114,7 +119,8 @@ def run_rank(rank, world, port, errq, fused, graph=False):
         got_home = hp.data.cpu().view(torch.int16).numpy().view(np.uint16)
         assert np.array_equal(got_home[:, free_home], handoff_bytes(nxt)), rank
         dist.barrier()
-        step.links.close()
+        step.close()
+        dist.barrier()
         dist.destroy_process_group()
     except Exception:
         import traceback

@@ -43,7 +43,7 @@ def toy_split(world):
     return np.maximum.accumulate(ks, axis=1).astype(np.int32)
 
 
-def run_toy(rank, world):
+def run_toy(rank, world, cross=False, transport="p2p"):
     import paper_2510_13223_b200 as bs
     from paper_2510_13223_b200.ring import CudaOps
     from paper_2510_13223_b200.seqshard import SeqShardedStep
@@ -57,16 +57,17 @@ def run_toy(rank, world):
     pool = bs.KVPool(TOY.n_layers, mine.pool.shape[1], TOY.hkv, TOY.d)
     pool.data.copy_(_dev(mine.pool))
     i32 = lambda x: torch.as_tensor(np.asarray(x), dtype=torch.int32).cuda()
-    dev = torch.device("cuda", 0)
+    dev = torch.device("cuda", rank if cross else 0)
     sc = synth.default_scale(TOY.d)
     step = SeqShardedStep(CudaOps(sc), rank, world, pool, i32(mine.block_tables), i32(ks), TOY.hq,
                           TOY.n_layers, TOY.d, TOY.hkv, device=dev, group=dist.group.WORLD,
-                          transport="p2p", handoff_src_ids=i32(src), handoff_dst_ids=i32(dst))
-    assert step.transport == "p2p", step.fallback_reason
+                          transport=transport, handoff_src_ids=i32(src), handoff_dst_ids=i32(dst))
+    assert step.transport == transport, step.fallback_reason
+    p2p = transport == "p2p"
     q = _dev(dense.q)[:, rank::world].contiguous()
     ref_shards = synth.place_shards(dense, ks, seed=11)
     for epoch in range(2):
-        out, lse = step.outputs() if epoch == 0 else (
+        out, lse = step.outputs() if (epoch == 0 and p2p) else (
             torch.full(q.shape, float("nan"), dtype=torch.bfloat16, device=dev),
             torch.full(q.shape[:-1], float("nan"), device=dev))
         step.enqueue(q, out, lse)
@@ -86,6 +87,10 @@ def run_toy(rank, world):
         dist.barrier()
     got_pool = pool.data.cpu().view(torch.int16).numpy().view(np.uint16)
     assert np.array_equal(got_pool[:, dst], handoff_bytes((rank - 1) % world)), rank
+    if not p2p:
+        dist.barrier()
+        step.close()
+        return
     # the step captured in a CUDA graph (device-computed flags) replays the eager outputs
     ref_out, ref_lse = out.clone(), lse.clone()
     g = step.capture(q, out, lse)
@@ -100,7 +105,7 @@ def run_toy(rank, world):
     step.close()
 
 
-def run_c3(rank, world):
+def run_c3(rank, world, cross=False, transport="p2p"):
     import paper_2510_13223_b200 as bs
     from paper_2510_13223_b200.ring import CudaOps
     from paper_2510_13223_b200.seqshard import SeqShardedStep
@@ -110,7 +115,7 @@ def run_c3(rank, world):
     case = synth.device_shards(shape, np.asarray(lens), ks, seed=41, device="cuda", layers=1)
     pt = case.pools[rank]
     pool = bs.KVPool(1, pt.shape[1], shape.hkv, shape.d, base=pt.reshape(-1))
-    dev = torch.device("cuda", 0)
+    dev = torch.device("cuda", rank if cross else 0)
     sc = synth.default_scale(shape.d)
     i32 = lambda x: torch.as_tensor(np.asarray(x), dtype=torch.int32).cuda()
     step = SeqShardedStep(CudaOps(sc), rank, world, pool, i32(case.block_tables[rank]), i32(ks),
@@ -136,13 +141,13 @@ def run_c3(rank, world):
     step.close()
 
 
-def run_rank(fn_name, rank, world, port, errq):
+def run_rank(fn_name, rank, world, port, errq, cross=False, transport="p2p"):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
-        torch.cuda.set_device(0)
+        torch.cuda.set_device(rank if cross else 0)
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        {"toy": run_toy, "c3": run_c3}[fn_name](rank, world)
+        {"toy": run_toy, "c3": run_c3}[fn_name](rank, world, cross, transport)
         dist.destroy_process_group()
     except Exception:
         import traceback
@@ -158,11 +163,12 @@ def _free_port():
     return p
 
 
-def _spawn(fn_name, world):
+def _spawn(fn_name, world, cross=False, transport="p2p"):
     ctx = mp.get_context("spawn")
     errq = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=run_rank, args=(fn_name, r, world, port, errq)) for r in range(world)]
+    procs = [ctx.Process(target=run_rank, args=(fn_name, r, world, port, errq, cross, transport))
+             for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:

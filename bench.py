@@ -345,11 +345,13 @@ class DrvTimer:
             raise RuntimeError(f"cuEventRecordWithFlags: {r}")
 
     def elapsed_time(self, end) -> float:
+        """ms between two recorded events; NaN if either was never recorded (e.g. the
+        migration timers of a step without hand-off)."""
         import ctypes
         ms = ctypes.c_float()
         r = DrvTimer._cu.cuEventElapsedTime(ctypes.byref(ms), self.ev, end.ev)
         if r != 0:
-            raise RuntimeError(f"cuEventElapsedTime: {r}")
+            return float("nan")
         return float(ms.value)
 
     def __del__(self):
@@ -385,7 +387,7 @@ def run_steps(step, q, out, lse, K, L, world, device, use_graph, timed=True):
     (timers as graph nodes), else submitted eagerly.  Returns a dict with this rank's
     ms per step, the sorted per-step times, per-layer attention / migration kernel times,
     host submission ms per step, the mode, clock summary and NVLink counter readings."""
-    timers = ([[tuple(DrvTimer() for _ in range(4)) for _ in range(L)] for _ in range(K)]
+    timers = ([[tuple(DrvTimer() for _ in range(5)) for _ in range(L)] for _ in range(K)]
               if timed else None)
     step_ev = [DrvTimer() for _ in range(K - 1)]
     t0, t1 = DrvTimer(), DrvTimer()
@@ -423,8 +425,10 @@ def run_steps(step, q, out, lse, K, L, world, device, use_graph, timed=True):
          "nvlink": NvlinkCounters.delta(nv0, nv1, K) if world > 1 else None,
          "per_step": sorted(a.elapsed_time(b) for a, b in zip(bounds[:-1], bounds[1:]))}
     if timers is not None:
-        r["attn_ms"] = [a.elapsed_time(b) for tk in timers for (a, b, _, _) in tk]
-        r["mig_ms"] = [c.elapsed_time(d) for tk in timers for (_, _, c, d) in tk]
+        r["attn_ms"] = [t[0].elapsed_time(t[1]) for tk in timers for t in tk]
+        r["mig_ms"] = [t[2].elapsed_time(t[3]) for tk in timers for t in tk]
+        # attention end -> out[l] final: the exchange + merge latency after the launch
+        r["out_ms"] = [t[1].elapsed_time(t[4]) for tk in timers for t in tk]
     del g
     return r
 
@@ -752,6 +756,11 @@ def run_c2(args, rank, world, device):
         "migrate_gbs": round(mig_gbs, 1),
         "migrate_ms_per_layer": round(mig_avg_ms, 5),
         "migrate_bytes_per_layer": mig_bytes,
+        "exchange_ms_per_layer": round(statistics.fmean(run["out_ms"]), 5),
+        "exchange_note": ("mean over layers of attention-launch end -> out[l] final on this rank "
+                          "(N>1: the other GPU's partials stored into this GPU's workspace, its "
+                          "last-arriver merges and the done-counter wait; N=1: merged in the "
+                          "launch, ~0)"),
         "migrate_transport": ("fused copy kernel, local HBM (N=1: both instances on GPU 0)" if world == 1
                               else ("copy kernel pushing into the peer's IPC-mapped pool (P2P, NVLink)"
                                     if step.transport == "p2p" else
@@ -952,9 +961,9 @@ def run_seq(args, rank, world, device, name, headline=False):
                            "achieved": round(gbs, 1), "peak": peak, "peak_source": peak_src,
                            "unit": "GB/s", "frac": round(gbs / peak, 4), "traffic": None,
                            "algorithmic_bytes_per_layer": a_bytes, "rank": rank}
-        # exchange + merge tail: what the step spends per layer beyond the attention
-        # launch itself (q push, flag waits, remote partial stores and merges)
-        res["exchange_ms_per_layer"] = round(max(ms_max / L - attn_avg, 0.0), 5)
+        # attention end -> out[l] final on this rank: the peers' partial stores into this
+        # rank's homes' workspaces, their last-arriver merges and the done wait
+        res["exchange_ms_per_layer"] = round(statistics.fmean(run["out_ms"]), 5)
         if n_hand:
             mig_avg = statistics.fmean(run["mig_ms"])
             mb = n_hand * pool.chunk_bytes

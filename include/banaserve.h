@@ -151,6 +151,17 @@ bs_status bs_kv_migrate_layer_ex(const bs_kv_pool* src, bs_kv_pool* dst, int32_t
 bs_status bs_kv_append_token(bs_kv_pool* pool, int32_t layer, const void* k_new, const void* v_new,
                              int32_t batch, const int32_t* block_tables, int32_t max_blocks,
                              const int32_t* pos, void* stream);
+/* H2 + H7 as ONE launch on the migration stream: the hand-off copy of
+ * bs_kv_migrate_layer(src -> dst, layer, n pairs) and the append of bs_kv_append_token
+ * into app_pool (same layer) -- independent bit copies, so the result is both calls'
+ * result.  Caller contract: the append's target slots lie outside the n source and
+ * destination chunks (the hand-off moves whole blocks of other requests).
+ * With a host-tier or peer-mapped pool, or n == 0 / batch == 0, it runs the two calls. */
+bs_status bs_kv_migrate_append_layer(const bs_kv_pool* src, bs_kv_pool* dst, int32_t layer,
+                                     const int32_t* src_ids, const int32_t* dst_ids, int32_t n,
+                                     bs_kv_pool* app_pool, const void* k_new, const void* v_new,
+                                     int32_t batch, const int32_t* block_tables,
+                                     int32_t max_blocks, const int32_t* pos, void* stream);
 
 /* Copy-engine variant (DMA, no SM time -- for the host tier's fetch / store legs, which
  * should not compete with attention for SMs): HOST int32 id arrays (validated), runs of

@@ -40,7 +40,7 @@ EXPORTED_SYMBOLS = (
     "bs_attention_problem_workspace_size", "bs_split_decode_attention_tasks", "bs_wait_signals",
     "bs_signals", "bs_attention_ragged_plan", "bs_split_decode_attention_local_ragged",
     "bs_debug_build", "bs_debug_error_code", "bs_kv_append_token", "bs_exchange",
-    "bs_signals_epoch", "bs_wait_signals_epoch", "bs_epoch_advance",
+    "bs_signals_epoch", "bs_wait_signals_epoch", "bs_epoch_advance", "bs_kv_migrate_append_layer",
 )
 
 
@@ -97,6 +97,8 @@ def lib():
         "bs_kv_migrate_layer_ex": ([_p, _p, _i32, _p, _p, _i32, _i32, _p], _i32),
         "bs_kv_migrate_layer_ce": ([_p, _p, _i32, _p, _p, _i32, _p], _i32),
         "bs_kv_append_token": ([_p, _i32, _p, _p, _i32, _p, _i32, _p, _p], _i32),
+        "bs_kv_migrate_append_layer": ([_p, _p, _i32, _p, _p, _i32, _p, _p, _p, _i32, _p, _i32, _p,
+                                        _p], _i32),
         "bs_kv_gather_layer": ([_p, _i32, _p, _i32, _p, _p], _i32),
         "bs_kv_scatter_layer": ([_p, _i32, _p, _i32, _p, _p], _i32),
         "bs_split_decode_attention_workspace_size": ([_p, _i32, _i32, _i32, ctypes.POINTER(_sz)], _i32),
@@ -288,6 +290,26 @@ def kv_append_token(pool: KVPool, layer: int, k_new: torch.Tensor, v_new: torch.
                                     _dptr(v_new, torch.bfloat16), B,
                                     _dptr(block_tables, torch.int32), int(block_tables.shape[1]),
                                     _dptr(pos, torch.int32), _stream(stream)))
+
+
+def kv_migrate_append_layer(src: KVPool, dst: KVPool, layer: int, src_ids: torch.Tensor,
+                            dst_ids: torch.Tensor, app_pool: KVPool, k_new: torch.Tensor,
+                            v_new: torch.Tensor, block_tables: torch.Tensor, pos: torch.Tensor,
+                            stream=None) -> None:
+    """H2 + H7 in one launch: the hand-off copy src -> dst (device int32 ids) and the
+    decoded token's K/V append into ``app_pool`` (see kv_append_token)."""
+    n, B = src_ids.numel(), pos.numel()
+    if dst_ids.numel() != n:
+        raise ValueError("src_ids / dst_ids length mismatch")
+    for t in (k_new, v_new):
+        if (t.dtype != torch.bfloat16 or not t.is_contiguous()
+                or t.numel() != B * app_pool.num_kv_heads * app_pool.head_dim):
+            raise ValueError("k_new / v_new must be contiguous bf16 [B, Hkv, d]")
+    _check(lib().bs_kv_migrate_append_layer(
+        src.handle, dst.handle, layer, _dptr(src_ids, torch.int32), _dptr(dst_ids, torch.int32), n,
+        app_pool.handle, _dptr(k_new, torch.bfloat16), _dptr(v_new, torch.bfloat16), B,
+        _dptr(block_tables, torch.int32), int(block_tables.shape[1]), _dptr(pos, torch.int32),
+        _stream(stream)))
 
 
 def kv_gather_layer(src: KVPool, layer: int, ids: torch.Tensor, staging: torch.Tensor,

@@ -10,6 +10,7 @@
 // read + the same written (16 KiB at Llama-2-7B) -- latency-bound, one launch per layer.
 #include <cuda_runtime.h>
 
+#include "append.cuh"
 #include "internal.h"
 
 namespace bs {
@@ -22,19 +23,8 @@ __global__ void __launch_bounds__(256) append_token_kernel(uint8_t* __restrict__
                                                            const int32_t* __restrict__ bt,
                                                            int32_t max_blocks,
                                                            const int32_t* __restrict__ pos) {
-  const int b = blockIdx.x;
-  const int p = __ldg(pos + b);
-  if (p < 0) return;
-  const int32_t blk = __ldg(bt + (int64_t)b * max_blocks + (p >> 4));
-  const int slot = p & 15;
-  const int cols = d / 8;  // 16-byte columns per row
-  const int per_kv = hkv * cols;
-  uint8_t* chunk = layer_base + (int64_t)blk * chunk_bytes;
-  for (int i = threadIdx.x; i < 2 * per_kv; i += blockDim.x) {
-    const int kv = i >= per_kv, r = i - kv * per_kv, g = r / cols, c = r - g * cols;
-    const uint4 val = __ldg((kv ? v_new : k_new) + ((int64_t)b * hkv + g) * cols + c);
-    reinterpret_cast<uint4*>(chunk + (((int64_t)kv * hkv + g) * 16 + slot) * d * 2)[c] = val;
-  }
+  append_token_rows(layer_base, chunk_bytes, hkv, d, k_new, v_new, bt, max_blocks, pos, blockIdx.x,
+                    threadIdx.x, blockDim.x);
 }
 
 }  // namespace

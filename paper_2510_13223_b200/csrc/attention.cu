@@ -1022,10 +1022,39 @@ bs_status make_plan(int batch, int G, int hq, int hkv, int d, int n_local, const
     const char* e = getenv("BS_ATTN_NSPLIT");
     return e ? atoi(e) : 0;
   }();
+  static const int plan_model = env_int("BS_ATTN_PLAN", 1);  // 0: round-1 planner everywhere
   int best_bps = -1;
   double best = 1e300;
   if (forced_ns > 0 && !rank_invariant)
     best_bps = std::min(kBtMax, std::max(min_bps, (mb_max + forced_ns - 1) / forced_ns));
+  // Few (request, kv-head) pairs -- fewer than the CTA slots, so the blocks of each pair
+  // must be cut into ranges to fill the GPU (C3: 8 or 64 pairs): a latency model picks the
+  // cut.  A CTA streams its range at min(bytes in flight / latency, its share of HBM); the
+  // slowest warp sets the CTA's time (ranges of a multiple of kWarps blocks keep the four
+  // warp pipelines equal); ranges beyond the slots run as another wave; the last arriver's
+  // merge reads every range's partial (a fixed round trip + partial bytes at one SM's L2
+  // rate).  Constants measured on the B200 (r02 planner sweep).
+  if (best_bps < 0 && plan_model && base < slots) {
+    const Variant v = rank_invariant ? Variant{2, 3, true} : variant_for(d, G);
+    const double blk = 2.0 * 16 * d * 2;                      // K + V page of one block
+    const double r_max = kWarps * v.stages * blk / 1.5e-6;   // bytes in flight / latency
+    const double bw = 7.0e12;                                // HBM read ceiling
+    for (int bps = min_bps; bps <= kBtMax; bps += kWarps) {
+      int total = 0;
+      for (int j = 0; j < n_local; ++j) total += (max_blocks[j] + bps - 1) / bps;
+      if (total > kMaxSplit) continue;
+      const int64_t ctas = base * total, full = ctas / slots, rem = ctas % slots;
+      const double cta_bytes = (double)bps * blk;
+      double t = (double)full * cta_bytes / std::min(r_max, bw / (double)slots);
+      if (rem) t += cta_bytes / std::min(r_max, bw / (double)rem);
+      if (total > 1) t += 1.5e-6 + (double)total * G * d * 4 / 47e9;
+      if (t < best * (1 - 1e-9)) {
+        best = t;
+        best_bps = bps;
+      }
+      if (bps >= mb_max) break;  // one range per shard: longer ranges change nothing
+    }
+  }
   for (int pass = 0; pass < 2 && best_bps < 0; ++pass) {  // pass 1: without the cap
     const int cap =
         pass == 0 && !rank_invariant ? std::min(kBtMax, std::max(max_bps, min_bps)) : kBtMax;

@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "append.cuh"
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -40,23 +41,24 @@ __device__ __forceinline__ void st_stream(int4* p, const int4& v) {
                : "memory");
 }
 
+// The page loop of the vec16 copy for CTA `cta` of `nctas` (shared by the plain copy and
+// the fused copy + append launch).
 template <int PAGE_BYTES, int U>
-__global__ void __launch_bounds__(256) copy_pages_vec16(const uint8_t* __restrict__ src_base,
-                                                        const int32_t* __restrict__ src_ids,
-                                                        uint8_t* __restrict__ dst_base,
-                                                        const int32_t* __restrict__ dst_ids,
-                                                        int32_t n, int32_t pages_per_chunk,
-                                                        int64_t chunk_bytes, int32_t n_layers,
-                                                        int64_t src_layer_stride,
-                                                        int64_t dst_layer_stride) {
+__device__ __forceinline__ void copy_pages_body(const uint8_t* __restrict__ src_base,
+                                                const int32_t* __restrict__ src_ids,
+                                                uint8_t* __restrict__ dst_base,
+                                                const int32_t* __restrict__ dst_ids, int32_t n,
+                                                int32_t pages_per_chunk, int64_t chunk_bytes,
+                                                int32_t n_layers, int64_t src_layer_stride,
+                                                int64_t dst_layer_stride, int cta, int nctas) {
   constexpr int V = PAGE_BYTES / (16 * 32);  // int4 per lane per page
   const int lane = threadIdx.x & 31;
   const int wpc = blockDim.x >> 5;
   const int64_t per_layer = (int64_t)n * pages_per_chunk;
   const int64_t total = per_layer * n_layers;
   // a warp moves U pages per iteration: U * V 16-byte loads in flight per lane
-  for (int64_t p0 = ((int64_t)blockIdx.x * wpc + (threadIdx.x >> 5)) * U; p0 < total;
-       p0 += (int64_t)gridDim.x * wpc * U) {
+  for (int64_t p0 = ((int64_t)cta * wpc + (threadIdx.x >> 5)) * U; p0 < total;
+       p0 += (int64_t)nctas * wpc * U) {
     int4 r[U][V];
     int4* dst[U];
 #pragma unroll
@@ -84,6 +86,50 @@ __global__ void __launch_bounds__(256) copy_pages_vec16(const uint8_t* __restric
 #pragma unroll
         for (int v = 0; v < V; ++v) st_stream(dst[u] + v * 32, r[u][v]);
   }
+}
+
+template <int PAGE_BYTES, int U>
+__global__ void __launch_bounds__(256) copy_pages_vec16(const uint8_t* __restrict__ src_base,
+                                                        const int32_t* __restrict__ src_ids,
+                                                        uint8_t* __restrict__ dst_base,
+                                                        const int32_t* __restrict__ dst_ids,
+                                                        int32_t n, int32_t pages_per_chunk,
+                                                        int64_t chunk_bytes, int32_t n_layers,
+                                                        int64_t src_layer_stride,
+                                                        int64_t dst_layer_stride) {
+  copy_pages_body<PAGE_BYTES, U>(src_base, src_ids, dst_base, dst_ids, n, pages_per_chunk,
+                                 chunk_bytes, n_layers, src_layer_stride, dst_layer_stride,
+                                 blockIdx.x, gridDim.x);
+}
+
+// H2 + H7 in one launch (bs_kv_migrate_append_layer): CTAs [0, batch) write request b's
+// decoded-token K/V rows into the append pool, the others run the hand-off page copy.
+struct AppendArgs {
+  uint8_t* layer_base;
+  int64_t chunk_bytes;
+  int32_t hkv, d;
+  const uint4* k_new;
+  const uint4* v_new;
+  const int32_t* bt;
+  int32_t max_blocks;
+  const int32_t* pos;
+  int32_t batch;
+};
+
+template <int PAGE_BYTES, int U>
+__global__ void __launch_bounds__(256) migrate_append_vec16(const uint8_t* __restrict__ src_base,
+                                                            const int32_t* __restrict__ src_ids,
+                                                            uint8_t* __restrict__ dst_base,
+                                                            const int32_t* __restrict__ dst_ids,
+                                                            int32_t n, int32_t pages_per_chunk,
+                                                            int64_t chunk_bytes, const AppendArgs a) {
+  if ((int)blockIdx.x < a.batch) {
+    append_token_rows(a.layer_base, a.chunk_bytes, a.hkv, a.d, a.k_new, a.v_new, a.bt, a.max_blocks,
+                      a.pos, blockIdx.x, threadIdx.x, blockDim.x);
+    return;
+  }
+  copy_pages_body<PAGE_BYTES, U>(src_base, src_ids, dst_base, dst_ids, n, pages_per_chunk,
+                                 chunk_bytes, 1, 0, 0, blockIdx.x - a.batch, gridDim.x - a.batch);
 }
 
 // NEXT F2: head-granular pages (K and V of n_heads kv-heads of each pair), between pools
@@ -334,6 +380,63 @@ bs_status bs_kv_migrate_layer_ex(const bs_kv_pool* src, bs_kv_pool* dst, int32_t
                                 dst->base + (size_t)layer * dst->layer_bytes, dst_ids, n,
                                 src->chunk_bytes, src->page_bytes, method,
                                 static_cast<cudaStream_t>(stream), max_ctas);
+}
+
+bs_status bs_kv_migrate_append_layer(const bs_kv_pool* src, bs_kv_pool* dst, int32_t layer,
+                                     const int32_t* src_ids, const int32_t* dst_ids, int32_t n,
+                                     bs_kv_pool* app_pool, const void* k_new, const void* v_new,
+                                     int32_t batch, const int32_t* block_tables,
+                                     int32_t max_blocks, const int32_t* pos, void* stream) {
+  BS_REQUIRE(src && dst && app_pool, "bs_kv_migrate_append_layer: NULL pool");
+  BS_REQUIRE(batch >= 0 && n >= 0, "bs_kv_migrate_append_layer: negative count");
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // host-tier / remote pools, an empty side or an unusual page size: the two launches
+  const bool fuse = batch > 0 && n > 0 && !src->host && !dst->host && !app_pool->host &&
+                    !is_remote(src) && !is_remote(dst) && !is_remote(app_pool) &&
+                    same_geometry(src, dst) && (src->page_bytes == 4096 || src->page_bytes == 2048);
+  if (!fuse) {
+    bs_status st = bs_kv_migrate_layer(src, dst, layer, src_ids, dst_ids, n, stream);
+    if (st != BS_OK) return st;
+    return bs_kv_append_token(app_pool, layer, k_new, v_new, batch, block_tables, max_blocks, pos,
+                              stream);
+  }
+  BS_REQUIRE(layer >= 0 && layer < src->desc.num_layers && layer < app_pool->desc.num_layers,
+             "bs_kv_migrate_append_layer: layer %d out of range", layer);
+  BS_REQUIRE(src_ids && dst_ids && k_new && v_new && block_tables && pos,
+             "bs_kv_migrate_append_layer: NULL argument");
+  BS_REQUIRE(max_blocks >= 1, "bs_kv_migrate_append_layer: max_blocks < 1");
+  BS_REQUIRE(((uintptr_t)k_new & 15) == 0 && ((uintptr_t)v_new & 15) == 0,
+             "bs_kv_migrate_append_layer: k_new / v_new must be 16-B aligned");
+  BS_DEBUG_CHECK(bs::debug_check_ids(src_ids, n, src->desc.num_blocks, s, "bs_kv_migrate_append_layer src_ids"));
+  BS_DEBUG_CHECK(bs::debug_check_ids(dst_ids, n, dst->desc.num_blocks, s, "bs_kv_migrate_append_layer dst_ids"));
+  BS_DEBUG_CHECK(bs::debug_check_append(pos, batch, block_tables, max_blocks, app_pool->desc.num_blocks, s,
+                                        "bs_kv_migrate_append_layer positions / block table"));
+  bs::AppendArgs a;
+  a.layer_base = app_pool->base + (size_t)layer * app_pool->layer_bytes;
+  a.chunk_bytes = (int64_t)app_pool->chunk_bytes;
+  a.hkv = app_pool->desc.num_kv_heads;
+  a.d = app_pool->desc.head_dim;
+  a.k_new = static_cast<const uint4*>(k_new);
+  a.v_new = static_cast<const uint4*>(v_new);
+  a.bt = block_tables;
+  a.max_blocks = max_blocks;
+  a.pos = pos;
+  a.batch = batch;
+  const int32_t ppc = (int32_t)(src->chunk_bytes / src->page_bytes);
+  const int64_t total = (int64_t)n * ppc;
+  const int sms = bs::sm_count(bs::current_device());
+  int64_t grid = std::min<int64_t>((total + 8 * 2 - 1) / (8 * 2), (int64_t)sms * 8);
+  const int cap = dev_copy_ctas();
+  if (cap > 0) grid = std::min<int64_t>(grid, cap);
+  const uint8_t* sb = src->base + (size_t)layer * src->layer_bytes;
+  uint8_t* db = dst->base + (size_t)layer * dst->layer_bytes;
+  if (src->page_bytes == 4096)
+    bs::migrate_append_vec16<4096, 2><<<(unsigned)(grid + batch), 256, 0, s>>>(
+        sb, src_ids, db, dst_ids, n, ppc, (int64_t)src->chunk_bytes, a);
+  else
+    bs::migrate_append_vec16<2048, 2><<<(unsigned)(grid + batch), 256, 0, s>>>(
+        sb, src_ids, db, dst_ids, n, ppc, (int64_t)src->chunk_bytes, a);
+  return bs::check_launch("migrate_append_vec16");
 }
 
 bs_status bs_kv_migrate_layers(const bs_kv_pool* src, bs_kv_pool* dst, int32_t layer_lo,

@@ -40,6 +40,13 @@ import torch.distributed as dist
 from .transport import ErrorFlag, NcclWire
 
 
+def _out_timer(timers, layer, stream):
+    """Optional 5th timer of a layer: recorded where out[l] / lse[l] become final (after the
+    exchange and the merge), so attn_end -> out gives the exchange + merge latency."""
+    if timers is not None and len(timers[layer]) > 4:
+        timers[layer][4].record(stream)
+
+
 class CudaExec:
     """Streams and events on the current CUDA device."""
 
@@ -144,6 +151,13 @@ class CudaOps:
             kv_migrate_layer_ce(src, dst, layer, host_ids[0], host_ids[1])
         else:
             self._mig(src, dst, layer, src_ids, dst_ids)
+
+    def migrate_append(self, src, dst, layer, src_ids, dst_ids, app_pool, k_new, v_new,
+                       block_tables, pos):
+        """H2 + H7 as one launch (N=1 migration stream)."""
+        from . import kv_migrate_append_layer
+        kv_migrate_append_layer(src, dst, layer, src_ids, dst_ids, app_pool, k_new, v_new,
+                                block_tables, pos)
 
     def append(self, pool, layer, k_new, v_new, block_tables, pos):
         """H7: the decoded token's K/V into its shard's block (one launch)."""
@@ -440,6 +454,9 @@ class ShardedDecodeStep:
         mig = 0 if self.n_handoff == 0 or self.ce_ids is not None else (
             1 if self.world == 1 or self.transport == "p2p" else 2)
         app = 0 if self.append is None else 1 + (self.pos_home is not None)
+        if (self.world == 1 and app and self.n_handoff and self.ce_ids is None
+                and hasattr(self.ops, "migrate_append")):
+            app -= 1   # the tail append rides the hand-off copy launch
         if self.transport == "p2p" and self.fused_exchange:
             # 1 fused attention launch; q push + signal, hand-off signal, 1 combined wait,
             # q-ack signal, done wait (per layer); H7: q-flag wait + append(s)
@@ -457,7 +474,15 @@ class ShardedDecodeStep:
         with ex.use(mig_s):
             if timers is not None:
                 timers[layer][2].record(mig_s)
-            if self.n_handoff:
+            fused_app = (self.world == 1 and self.append is not None and self.n_handoff > 0
+                         and self.ce_ids is None and hasattr(ops, "migrate_append"))
+            if fused_app:  # H2 + H7 in one launch (the append needs this layer's inputs)
+                if inputs_ready is not None:
+                    ex.wait(mig_s, inputs_ready[layer])
+                kv = self.append[layer]
+                ops.migrate_append(self.cold, self.home, layer, self.src_ids, self.dst_ids,
+                                   self.cold, kv[0], kv[1], self.cold_bt, self.pos_tail)
+            elif self.n_handoff:
                 if self.world == 1:
                     ops.migrate_local(self.cold, self.home, layer, self.src_ids, self.dst_ids,
                                       self.ce_ids)
@@ -467,9 +492,10 @@ class ShardedDecodeStep:
                     ops.scatter(self.home, layer, self.dst_ids, self.stage_recv)
             if self.append is not None and self.world == 1:  # H7 rides the migration stream:
                 kv = self.append[layer]                      # attention waits for mig_done
-                if inputs_ready is not None:
+                if inputs_ready is not None and not fused_app:
                     ex.wait(mig_s, inputs_ready[layer])
-                ops.append(self.cold, layer, kv[0], kv[1], self.cold_bt, self.pos_tail)
+                if not fused_app:
+                    ops.append(self.cold, layer, kv[0], kv[1], self.cold_bt, self.pos_tail)
                 if self.pos_home is not None:
                     ops.append(self.home, layer, kv[0], kv[1], self.home_bt, self.pos_home)
             if timers is not None:
@@ -479,8 +505,8 @@ class ShardedDecodeStep:
     def enqueue(self, q: torch.Tensor, out: torch.Tensor, lse: torch.Tensor | None = None,
                 timers=None, inputs_ready=None) -> None:
         """q [L][B][Hq][d] bf16 of this rank's requests -> out [L][B][Hq][d] bf16 and
-        lse [L][B][Hq] fp32.  ``timers[l]`` = (attn_start, attn_end, mig_start, mig_end)
-        events recorded on the launching streams (CUDA only).  ``inputs_ready[l]``: an
+        lse [L][B][Hq] fp32.  ``timers[l]`` = (attn_start, attn_end, mig_start, mig_end[,
+        out_final]) events recorded on the launching streams (CUDA only).  ``inputs_ready[l]``: an
         event the step waits for before reading q[l] (e.g. its H2D copy); after the call,
         ``self.out_ready[l]`` is recorded once out[l] / lse[l] are final (per-layer D2H)."""
         if self.transport == "p2p":
@@ -537,6 +563,7 @@ class ShardedDecodeStep:
                     if timers is not None:
                         timers[layer][1].record(ex.compute)
                     ex.record(self.out_ready[layer], ex.compute)
+                    _out_timer(timers, layer, ex.compute)
                     continue
                 if self.append is not None and self.world > 1 and self.pos_home is not None:
                     ops.append(self.home, layer, self.append[layer][0], self.append[layer][1],
@@ -560,6 +587,7 @@ class ShardedDecodeStep:
                     ops.merge([self.part_own[layer], self.part_cold[layer]], out[layer],
                               None if lse is None else lse[layer])
                     ex.record(self.out_ready[layer], ex.compute)
+                    _out_timer(timers, layer, ex.compute)
             else:
                 with ex.use(ex.comm):
                     ex.wait(ex.comm, E["part_ready"][layer])
@@ -568,6 +596,7 @@ class ShardedDecodeStep:
                     ops.merge([self.part_own[layer], self.part_recv[layer]], out[layer],
                               None if lse is None else lse[layer])
                     ex.record(self.out_ready[layer], ex.comm)
+                    _out_timer(timers, layer, ex.comm)
         ex.end()
 
     def close(self):
@@ -685,6 +714,7 @@ class ShardedDecodeStep:
                 if not own_lse:
                     lse[layer].copy_(F["lse"][layer])
                 self.out_ready[layer].record(self.merge_s)
+                _out_timer(timers, layer, self.merge_s)
         cur = torch.cuda.current_stream()
         for s_ in (self.push, self.merge_s, self.app_s):
             cur.wait_stream(s_)
@@ -763,6 +793,7 @@ class ShardedDecodeStep:
                           None if lse is None else lse[layer])
                 signals_epoch([lk.flag(lk.next_flags, "part_ack", layer)], ep)
                 self.out_ready[layer].record(self.merge_s)
+                _out_timer(timers, layer, self.merge_s)
         cur = torch.cuda.current_stream()
         for s_ in (self.push, self.merge_s):
             cur.wait_stream(s_)

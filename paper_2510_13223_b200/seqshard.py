@@ -284,6 +284,8 @@ class SeqShardedStep:
                 if lse is not None and lse.data_ptr() != self.lse_buf.data_ptr():
                     lse[layer].copy_(self.lse_buf[layer])
                 self.out_ready[layer].record(self.out_s)
+                if timers is not None and len(timers[layer]) > 4:
+                    timers[layer][4].record(self.out_s)
         for s in (self.comm, self.copy, self.ack_s, self.out_s):
             cur.wait_stream(s)
 

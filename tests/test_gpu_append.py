@@ -114,3 +114,36 @@ def test_decode_step_append_then_attention(bs, n_shards):
     assert err.max() <= ABS_TOL
     assert (err.max(-1) / np.abs(ref_o).max(-1)).max() <= ROW_REL_TOL
     assert np.abs(lse.cpu().double().numpy() - ref_lse).max() <= LSE_TOL
+
+
+@pytest.mark.parametrize("shape,lens,n_pairs", [
+    (synth.Shape(2, 4, 2, 64), (37, 64, 129, 200, 17, 1), 7),        # 2 KiB pages
+    (synth.Shape(2, 32, 32, 128), (2048,) * 6 + (700, 5), 40),        # C2-like, 4 KiB pages
+])
+def test_migrate_append_one_launch_bit_exact(bs, shape, lens, n_pairs):
+    """bs_kv_migrate_append_layer (H2 + H7 in one launch, the N=1 migration stream) equals
+    the oracle's migrate of n chunk pairs into a sentinel-filled pool followed by its append
+    into the source pool, byte for byte (both pools, every layer)."""
+    layer = shape.n_layers - 1
+    dense, ks, shards, partial, pos, k_new, v_new = last_token_case(shape, lens, 9, layer)
+    pos[2] = -1
+    L, nb = partial.shape[:2]
+    spare = 2 * n_pairs
+    src_np = np.concatenate([partial, synth.bf16_bits(torch.randn(
+        (L, spare) + partial.shape[2:], generator=torch.Generator().manual_seed(4)))], axis=1)
+    dst_np = np.full((L, n_pairs + 13) + partial.shape[2:], synth.DST_SENTINEL, dtype=np.uint16)
+    rng = np.random.default_rng(2)
+    s_ids = (nb + rng.permutation(spare)[:n_pairs]).astype(np.int32)   # outside the appends
+    d_ids = rng.permutation(n_pairs + 13)[:n_pairs].astype(np.int32)
+    ref_src, ref_dst = src_np.copy(), dst_np.copy()
+    oracle.migrate_layer(ref_src, ref_dst, layer, s_ids, d_ids)
+    oracle.append_token(ref_src, layer, k_new, v_new, shards[0].block_tables, pos)
+    src = bs.KVPool(L, src_np.shape[1], shape.hkv, shape.d)
+    src.data.copy_(dev_bf16(src_np))
+    dst = bs.KVPool(L, dst_np.shape[1], shape.hkv, shape.d)
+    dst.data.copy_(dev_bf16(dst_np))
+    bs.kv_migrate_append_layer(src, dst, layer, dev_i32(s_ids), dev_i32(d_ids), src, dev_bf16(k_new),
+                               dev_bf16(v_new), dev_i32(shards[0].block_tables), dev_i32(pos))
+    torch.cuda.synchronize()
+    assert np.array_equal(host_u16(dst.data), ref_dst)
+    assert np.array_equal(host_u16(src.data), ref_src)

@@ -966,15 +966,12 @@ bool use_mma(int G) {
   return (v == 1 && G >= 4) || v == 2;
 }
 
-int deep_variant() {  // experiment switch: 1 = 4 stages x 1 CTA/SM, 2 = 3 stages x 2 CTAs/SM
-  static int v = env_int("BS_ATTN_DEEP", 0);
-  return v;
-}
+// The default (tensor-core) variant, independent of the environment: the range plan of a
+// problem shared by several GPUs uses it (rank-invariant inputs only).
+Variant default_variant(int d) { return d == 128 ? Variant{2, 3, true} : Variant{4, 3, true}; }
 
 Variant variant_for(int d, int G) {
-  if (use_mma(G) && d == 128 && deep_variant() == 1) return Variant{4, 1, true};
-  if (use_mma(G) && d == 128 && deep_variant() == 2) return Variant{3, 2, true};
-  if (use_mma(G)) return d == 128 ? Variant{2, 3, true} : Variant{4, 3, true};
+  if (use_mma(G)) return default_variant(d);
   if (alt_variant() == 1) return d == 128 ? Variant{3, 2, false} : Variant{6, 2, false};
   if (d == 128) return G <= 4 ? Variant{2, 3, false} : Variant{3, 2, false};
   return G <= 4 ? Variant{4, 3, false} : Variant{6, 2, false};
@@ -1028,26 +1025,34 @@ bs_status make_plan(int batch, int G, int hq, int hkv, int d, int n_local, const
   if (forced_ns > 0 && !rank_invariant)
     best_bps = std::min(kBtMax, std::max(min_bps, (mb_max + forced_ns - 1) / forced_ns));
   // Few (request, kv-head) pairs -- fewer than the CTA slots, so the blocks of each pair
-  // must be cut into ranges to fill the GPU (C3: 8 or 64 pairs): a latency model picks the
-  // cut.  A CTA streams its range at min(bytes in flight / latency, its share of HBM); the
-  // slowest warp sets the CTA's time (ranges of a multiple of kWarps blocks keep the four
-  // warp pipelines equal); ranges beyond the slots run as another wave; the last arriver's
-  // merge reads every range's partial (a fixed round trip + partial bytes at one SM's L2
-  // rate).  Constants measured on the B200 (r02 planner sweep).
+  // are cut into ranges to fill the GPU (C3: 8 or 64 pairs).  Among the cuts that run as
+  // ONE wave, a bandwidth / latency model picks (r02 planner sweep).
+  // Streaming takes the longer of
+  //   * all KV bytes at min(HBM read ceiling, bytes in flight / latency), the bytes in flight
+  //     being every CTA's ring (kWarps x STAGES blocks), and
+  //   * the busiest SM's bytes (CTAs spread evenly over the SMs) at one SM's rate;
+  // ranges are a multiple of kWarps blocks (the slowest of the four warp pipelines sets a
+  // CTA's time), and the last arriver's merge costs a round trip plus every partial at one
+  // SM's L2 rate.  Constants measured on a B200: 7.0 TB/s, 1.5 us, 45 GB/s per SM, merge
+  // 1.5 us + 25 GB/s.
   if (best_bps < 0 && plan_model && base < slots) {
-    const Variant v = rank_invariant ? Variant{2, 3, true} : variant_for(d, G);
+    const Variant v = rank_invariant ? default_variant(d) : variant_for(d, G);
+    const int sms = rank_invariant ? kInvariantSlots / 3 : sm_count(current_device());
     const double blk = 2.0 * 16 * d * 2;                      // K + V page of one block
-    const double r_max = kWarps * v.stages * blk / 1.5e-6;   // bytes in flight / latency
-    const double bw = 7.0e12;                                // HBM read ceiling
+    const double inflight_cta = (double)kWarps * v.stages * blk;
+    const double bw = 7.0e12, lat = 1.5e-6, r_sm = 45e9;
+    double all_blocks = 0;
+    for (int j = 0; j < n_local; ++j) all_blocks += max_blocks[j];
+    const double total_bytes = (double)base * all_blocks * blk;
     for (int bps = min_bps; bps <= kBtMax; bps += kWarps) {
       int total = 0;
       for (int j = 0; j < n_local; ++j) total += (max_blocks[j] + bps - 1) / bps;
-      if (total > kMaxSplit) continue;
-      const int64_t ctas = base * total, full = ctas / slots, rem = ctas % slots;
-      const double cta_bytes = (double)bps * blk;
-      double t = (double)full * cta_bytes / std::min(r_max, bw / (double)slots);
-      if (rem) t += cta_bytes / std::min(r_max, bw / (double)rem);
-      if (total > 1) t += 1.5e-6 + (double)total * G * d * 4 / 47e9;
+      const int64_t ctas = base * total;
+      if (total > kMaxSplit || ctas > slots) continue;   // one wave only
+      const double bw_eff = std::min(bw, (double)ctas * inflight_cta / lat);
+      const int64_t per_sm = (ctas + sms - 1) / sms;     // CTAs on the busiest SM
+      double t = std::max(total_bytes / bw_eff, (double)per_sm * bps * blk / r_sm);
+      if (total > 1) t += 1.5e-6 + (double)total * G * d * 4 / 25e9;
       if (t < best * (1 - 1e-9)) {
         best = t;
         best_bps = bps;
@@ -1133,13 +1138,8 @@ template <int D, int G>
 bs_status launch_attn_t(const AttnParams& p, const TMaps* tm, int batch, cudaStream_t stream) {
   const Variant v = variant_for(D, G);
   if (v.mma && tm) {
-    if constexpr (D == 128) {
-      if (v.stages == 4) return launch_attn_mma<D, G, 4, 1>(p, *tm, batch, stream);
-      if (v.stages == 3) return launch_attn_mma<D, G, 3, 2>(p, *tm, batch, stream);
-      return launch_attn_mma<D, G, 2, 3>(p, *tm, batch, stream);
-    } else {
-      return launch_attn_mma<D, G, 4, 3>(p, *tm, batch, stream);
-    }
+    if constexpr (D == 128) return launch_attn_mma<D, G, 2, 3>(p, *tm, batch, stream);
+    else return launch_attn_mma<D, G, 4, 3>(p, *tm, batch, stream);
   }
   if constexpr (D == 128) {
     if (v.stages == 2) return launch_attn_v<D, G, 2, 3>(p, batch, stream);

@@ -116,6 +116,7 @@ struct AttnParams {
   int32_t hq, hkv;          // hq: q heads of the MODEL (row stride); hkv: kv heads in this launch
   int32_t model_head_lo;    // first kv head of the launch in the model (q / output rows)
   int32_t grid_x;           // CTA ranges of this launch over its shards
+  int32_t pdl;              // launched as a programmatic dependent: prefetch, then wait
   const int4* work;         // ragged plan (bs_attention_ragged_plan) or NULL: one item per
                             // item = (request, shard << 16 | slot, first block,
                             // blocks << 8 | ranges of the request); grid.x = items * hkv
@@ -476,6 +477,15 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
     if (i < nb_cta) s_bt[i] = idv[r];
   }
   __syncthreads();  // block table + barrier inits visible to the CTA
+  // Programmatic dependent launch (BS_ATTN_PDL): this grid may start while the previous
+  // kernel on the stream drains.  Everything above -- block table, kv_split, the first
+  // K/V stages in flight -- reads only step inputs (the caller's contract); q, the outputs
+  // and the workspace (which the previous launch may still be merging from) come after the
+  // wait, which returns once that kernel has completed and its writes are visible.
+  if (p.pdl) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
 
   // q for the G heads of this group, this lane's dims, pre-scaled into log2 units and
   // duplicated into both halves of a packed pair ({q_e, q_e}) for token-pair FFMA2
@@ -793,6 +803,15 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
     if (i < nb_cta) s_bt[i] = idv[r];
   }
   __syncthreads();  // block table + barrier inits visible to the CTA
+  // Programmatic dependent launch (BS_ATTN_PDL): this grid may start while the previous
+  // kernel on the stream drains.  Everything above -- block table, kv_split, the first
+  // K/V stages in flight -- reads only step inputs (the caller's contract); q, the outputs
+  // and the workspace (which the previous launch may still be merging from) come after the
+  // wait, which returns once that kernel has completed and its writes are visible.
+  if (p.pdl) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
 
   // q^T B-fragments (bf16 pairs) for head n = gq (zero padding for n >= G)
   uint32_t bq[KS][2];
@@ -1104,6 +1123,32 @@ bs_status make_plan(int batch, int G, int hq, int hkv, int d, int n_local, const
   return BS_OK;
 }
 
+// Launch with cudaLaunchAttributeProgrammaticStreamSerialization: the grid may begin as
+// soon as every CTA of the previous kernel on the stream has started (and triggered);
+// the kernel's griddepcontrol.wait orders what depends on that kernel.
+template <typename... KArgs, typename... Args>
+bs_status launch_pdl(void (*kern)(KArgs...), dim3 grid, int smem, cudaStream_t stream,
+                     const char* what, const Args&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kWarps * 32, 1, 1);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args...);
+  if (e != cudaSuccess) return set_error(BS_ERR_CUDA, "%s (PDL launch): %s", what, cudaGetErrorString(e));
+  return BS_OK;
+}
+
+int pdl_default() {  // experiment switch BS_ATTN_PDL
+  static int v = env_int("BS_ATTN_PDL", 0);
+  return v;
+}
+
 template <int D, int G, int STAGES, int MINB>
 bs_status launch_attn_v(const AttnParams& p, int batch, cudaStream_t stream) {
   using S = Smem<D, G, STAGES>;
@@ -1115,6 +1160,8 @@ bs_status launch_attn_v(const AttnParams& p, int batch, cudaStream_t stream) {
     configured.fetch_or(bit);
   }
   const dim3 grid = p.work ? dim3(p.grid_x * p.hkv, 1, 1) : dim3(p.grid_x, p.hkv, batch);
+  if (p.pdl) return launch_pdl(split_decode_attn<D, G, STAGES, MINB>, grid, S::kTotal, stream,
+                               "split_decode_attn", p);
   split_decode_attn<D, G, STAGES, MINB><<<grid, kWarps * 32, S::kTotal, stream>>>(p);
   return check_launch("split_decode_attn");
 }
@@ -1130,6 +1177,8 @@ bs_status launch_attn_mma(const AttnParams& p, const TMaps& tm, int batch, cudaS
     configured.fetch_or(bit);
   }
   const dim3 grid = p.work ? dim3(p.grid_x * p.hkv, 1, 1) : dim3(p.grid_x, p.hkv, batch);
+  if (p.pdl) return launch_pdl(split_decode_attn_mma<D, G, STAGES, MINB>, grid, S::kTotal, stream,
+                               "split_decode_attn_mma", p, tm);
   split_decode_attn_mma<D, G, STAGES, MINB><<<grid, kWarps * 32, S::kTotal, stream>>>(p, tm);
   return check_launch("split_decode_attn_mma");
 }
@@ -1326,6 +1375,7 @@ bs_status run_attention(const LaunchArgs& a) {
   p.model_head_lo = a.model_head_lo;
   p.grid_x = a.work ? a.n_work : pl.nsplit;
   p.work = reinterpret_cast<const int4*>(a.work);
+  p.pdl = bs::pdl_default();
   bs::ProbDesc& P = p.pb[0];
   P.q = static_cast<const __nv_bfloat16*>(a.q);
   P.kv_split = a.kv_split;

@@ -229,6 +229,23 @@ bs_status bs_split_decode_attention_local(int32_t n_local, const bs_kv_pool* con
                                           const int32_t* kv_split, int32_t n_shards, float scale,
                                           void* out, float* lse, void* workspace,
                                           size_t workspace_bytes, void* stream);
+/* The same with launch flags.  BS_ATTN_PDL: when the launch has more CTAs than one wave,
+ * it is a programmatic dependent launch -- it may start while the previous kernel on
+ * `stream` drains, reading block_tables / kv_split and prefetching K/V pages before that
+ * kernel completes, and q / out / lse / workspace only after (griddepcontrol.wait).
+ * Caller contract: the kernel launched just before it on `stream` writes neither the pools'
+ * pages this call reads, nor block_tables / kv_split (e.g. the previous layer's attention;
+ * work from other streams joined by events is waited for in full).  Single-wave launches
+ * ignore the flag (measured slower with it). */
+#define BS_ATTN_PDL 1u
+bs_status bs_split_decode_attention_local_ex(int32_t n_local, const bs_kv_pool* const* pools,
+                                             int32_t layer, const void* q, int32_t batch,
+                                             int32_t num_q_heads,
+                                             const int32_t* const* block_tables,
+                                             const int32_t* max_blocks, const int32_t* shard_ids,
+                                             const int32_t* kv_split, int32_t n_shards, float scale,
+                                             void* out, float* lse, void* workspace,
+                                             size_t workspace_bytes, uint32_t flags, void* stream);
 
 /* Ragged plan for mixed lengths (FlashInfer-style plan / run; C4's Alpaca + LongBench
  * mix): from the HOST copy of kv_split, cut every (request, local shard) into ranges of

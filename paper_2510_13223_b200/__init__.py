@@ -41,6 +41,7 @@ EXPORTED_SYMBOLS = (
     "bs_signals", "bs_attention_ragged_plan", "bs_split_decode_attention_local_ragged",
     "bs_debug_build", "bs_debug_error_code", "bs_kv_append_token", "bs_exchange",
     "bs_signals_epoch", "bs_wait_signals_epoch", "bs_epoch_advance", "bs_kv_migrate_append_layer",
+    "bs_split_decode_attention_local_ex",
 )
 
 
@@ -144,6 +145,8 @@ def lib():
                                                             ctypes.POINTER(_sz)], _i32),
         "bs_split_decode_attention_local": ([_i32, _p, _i32, _p, _i32, _i32, _p, _p, _p, _p, _i32,
                                              _f32, _p, _p, _p, _sz, _p], _i32),
+        "bs_split_decode_attention_local_ex": ([_i32, _p, _i32, _p, _i32, _i32, _p, _p, _p, _p, _i32,
+                                                _f32, _p, _p, _p, _sz, ctypes.c_uint32, _p], _i32),
         "bs_attention_problem_workspace_size": ([_i32, _i32, _i32, _i32, _i32, _p,
                                                  ctypes.POINTER(_sz)], _i32),
         "bs_split_decode_attention_tasks": ([_i32, _p, _i32, _p, _i32, _i32, _i32, _f32, _p], _i32),
@@ -360,11 +363,15 @@ def split_decode_attention_local_workspace_size(pools, max_blocks, batch: int,
     return out.value
 
 
+ATTN_PDL = 1   # bs_split_decode_attention_local_ex flag (see the header's contract)
+
+
 def split_decode_attention_local(pools, layer: int, q: torch.Tensor, block_tables,
                                  shard_ids, kv_split: torch.Tensor, scale: float, out: torch.Tensor,
                                  lse: torch.Tensor, workspace: torch.Tensor | None = None,
-                                 stream=None) -> None:
-    """H4+H6 fused over shards resident on this GPU: bf16 ``out`` [B,Hq,d] + fp32 ``lse``."""
+                                 stream=None, flags: int = 0) -> None:
+    """H4+H6 fused over shards resident on this GPU: bf16 ``out`` [B,Hq,d] + fp32 ``lse``.
+    ``flags`` = ATTN_PDL: programmatic dependent launch (bs_split_decode_attention_local_ex)."""
     n = len(pools)
     B, hq, d = q.shape
     pa = (ctypes.c_void_p * n)(*[p.handle.value for p in pools])
@@ -372,11 +379,11 @@ def split_decode_attention_local(pools, layer: int, q: torch.Tensor, block_table
     mb = (ctypes.c_int32 * n)(*[int(t.shape[1]) for t in block_tables])
     sa = (ctypes.c_int32 * n)(*[int(x) for x in shard_ids])
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
-    _check(lib().bs_split_decode_attention_local(
+    _check(lib().bs_split_decode_attention_local_ex(
         n, pa, layer, _dptr(q, torch.bfloat16), B, hq, ba, mb, sa, _dptr(kv_split, torch.int32),
         kv_split.shape[1] - 1, float(scale), _dptr(out, torch.bfloat16),
         _dptr(lse, torch.float32) if lse is not None else None, _dptr(workspace), ws_bytes,
-        _stream(stream)))
+        int(flags), _stream(stream)))
 
 
 class _Problem(ctypes.Structure):

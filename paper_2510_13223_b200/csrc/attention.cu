@@ -1144,8 +1144,8 @@ bs_status launch_pdl(void (*kern)(KArgs...), dim3 grid, int smem, cudaStream_t s
   return BS_OK;
 }
 
-int pdl_default() {  // experiment switch BS_ATTN_PDL
-  static int v = env_int("BS_ATTN_PDL", 0);
+int pdl_env() {  // A/B switch BS_ATTN_PDL: 0 never, 1 every attention launch, unset: flags
+  static int v = env_int("BS_ATTN_PDL", -1);
   return v;
 }
 
@@ -1271,6 +1271,7 @@ struct LaunchArgs {
   void* stream;
   const int32_t* work;  // ragged plan (device int4 items) or NULL
   int32_t n_work, max_parts;
+  uint32_t flags;       // BS_ATTN_PDL
 };
 
 bs_status validate_common(const LaunchArgs& a, int* G_out) {
@@ -1375,7 +1376,12 @@ bs_status run_attention(const LaunchArgs& a) {
   p.model_head_lo = a.model_head_lo;
   p.grid_x = a.work ? a.n_work : pl.nsplit;
   p.work = reinterpret_cast<const int4*>(a.work);
-  p.pdl = bs::pdl_default();
+  {  // programmatic dependent launch: multi-wave launches only (BS_ATTN_PDL=0/1 overrides)
+    const int64_t ctas = (int64_t)p.grid_x * a.n_kv_heads * (a.work ? 1 : a.batch);
+    const int64_t slots = (int64_t)bs::sm_count(bs::current_device()) * bs::variant_for(d, G).minb;
+    const int env = bs::pdl_env();
+    p.pdl = env >= 0 ? env : ((a.flags & BS_ATTN_PDL) && ctas > slots ? 1 : 0);
+  }
   bs::ProbDesc& P = p.pb[0];
   P.q = static_cast<const __nv_bfloat16*>(a.q);
   P.kv_split = a.kv_split;
@@ -1542,6 +1548,21 @@ bs_status bs_split_decode_attention_local(int32_t n_local, const bs_kv_pool* con
                                           const int32_t* kv_split, int32_t n_shards, float scale,
                                           void* out, float* lse, void* workspace,
                                           size_t workspace_bytes, void* stream) {
+  return bs_split_decode_attention_local_ex(n_local, pools, layer, q, batch, num_q_heads,
+                                            block_tables, max_blocks, shard_ids, kv_split,
+                                            n_shards, scale, out, lse, workspace, workspace_bytes,
+                                            0u, stream);
+}
+
+bs_status bs_split_decode_attention_local_ex(int32_t n_local, const bs_kv_pool* const* pools,
+                                             int32_t layer, const void* q, int32_t batch,
+                                             int32_t num_q_heads,
+                                             const int32_t* const* block_tables,
+                                             const int32_t* max_blocks, const int32_t* shard_ids,
+                                             const int32_t* kv_split, int32_t n_shards, float scale,
+                                             void* out, float* lse, void* workspace,
+                                             size_t workspace_bytes, uint32_t flags, void* stream) {
+  BS_REQUIRE((flags & ~BS_ATTN_PDL) == 0, "bs_split_decode_attention_local: unknown flags 0x%x", flags);
   BS_REQUIRE(pools && block_tables && max_blocks && shard_ids,
              "bs_split_decode_attention_local: NULL array");
   BS_REQUIRE(n_local >= 1 && n_local <= bs::kMaxLocal, "bs_split_decode_attention_local: %d shards",
@@ -1574,6 +1595,7 @@ bs_status bs_split_decode_attention_local(int32_t n_local, const bs_kv_pool* con
   a.workspace = workspace;
   a.workspace_bytes = workspace_bytes;
   a.stream = stream;
+  a.flags = flags;
   return run_attention(a);
 }
 

@@ -121,11 +121,14 @@ class CudaOps:
     def merge(self, parts, out, lse):
         self._merge([p[0] for p in parts], [p[1] for p in parts], [p[2] for p in parts], out, lse)
 
-    def attention_local(self, pools, layer, q, block_tables, shard_ids, kv_split, out, lse, ws):
-        """H4 + H6 fused over shards resident on this GPU (one launch)."""
-        from . import split_decode_attention_local
+    def attention_local(self, pools, layer, q, block_tables, shard_ids, kv_split, out, lse, ws,
+                        pdl=False):
+        """H4 + H6 fused over shards resident on this GPU (one launch).  pdl: the previous
+        kernel on the stream is the previous layer's attention (nothing it writes is read
+        before the launch's griddepcontrol.wait) -> programmatic dependent launch."""
+        from . import ATTN_PDL, split_decode_attention_local
         split_decode_attention_local(pools, layer, q, block_tables, shard_ids, kv_split,
-                                     self.scale, out, lse, ws)
+                                     self.scale, out, lse, ws, flags=ATTN_PDL if pdl else 0)
 
     def local_workspace(self, pools, block_tables, batch, hq, device):
         from . import split_decode_attention_local_workspace_size
@@ -556,10 +559,13 @@ class ShardedDecodeStep:
                 if timers is not None:
                     timers[layer][0].record(ex.compute)
                 if self.fuse_local:
+                    # PDL: on the compute stream only the previous layer's attention precedes
+                    # this launch (the hand-off / H7 writes are joined by the mig_done event;
+                    # not with the serial schedule, lookahead -2, where the copy precedes it)
                     ops.attention_local([self.home, self.cold], layer, q[layer],
                                         [self.home_bt, self.cold_bt], [0, 1], self.kv_split,
                                         out[layer], None if lse is None else lse[layer],
-                                        self.local_ws)
+                                        self.local_ws, pdl=layer > 0 and mig_s is not ex.compute)
                     if timers is not None:
                         timers[layer][1].record(ex.compute)
                     ex.record(self.out_ready[layer], ex.compute)

@@ -1,0 +1,72 @@
+"""Programmatic dependent launch of the fused local attention (BS_ATTN_PDL, multi-wave
+launches): consecutive layers' launches on one stream share one split-K workspace, each
+prefetching its K/V while the previous one drains and touching q / outputs / workspace only
+after griddepcontrol.wait.  The outputs must equal the plain launches bit for bit (same plan,
+same merge order) and the oracle within the north-star tolerances -- eagerly and replayed
+from a CUDA graph."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def bs():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_2510_13223_b200 as m
+    m.lib()
+    return m
+
+
+@pytest.mark.parametrize("graph", [False, True], ids=["eager", "graph"])
+def test_pdl_layers_bitwise_equal_plain_and_oracle(bs, graph):
+    shape = synth.Shape(4, 32, 32, 128)
+    lens = np.full(64, 600)
+    ks = synth.block_aligned_split(lens, 2)
+    case = synth.device_shards(shape, lens, ks, seed=13, device="cuda")
+    pools = [bs.KVPool(shape.n_layers, p.shape[1], shape.hkv, shape.d, base=p.reshape(-1))
+             for p in case.pools]
+    bts = [torch.from_numpy(b).cuda() for b in case.block_tables]
+    ksd = torch.from_numpy(ks).cuda()
+    sc = synth.default_scale(shape.d)
+    B, L = len(lens), shape.n_layers
+    ws = torch.zeros(max(16, bs.split_decode_attention_local_workspace_size(
+        pools, [t.shape[1] for t in bts], B, shape.hq)), dtype=torch.uint8, device="cuda")
+
+    def run(flags):
+        out = torch.full((L, B, shape.hq, shape.d), float("nan"), dtype=torch.bfloat16, device="cuda")
+        lse = torch.full((L, B, shape.hq), float("nan"), device="cuda")
+
+        def step():
+            for layer in range(L):
+                bs.split_decode_attention_local(pools, layer, case.q[layer], bts, [0, 1], ksd, sc,
+                                                out[layer], lse[layer], ws,
+                                                flags=flags if layer else 0)
+        if graph:
+            step()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step()
+            out.fill_(float("nan"))
+            g.replay()
+        else:
+            step()
+        torch.cuda.synchronize()
+        return out, lse
+
+    o0, l0 = run(0)
+    o1, l1 = run(bs.ATTN_PDL)
+    assert torch.equal(o0.view(torch.int16), o1.view(torch.int16))
+    assert torch.equal(l0, l1)
+    for layer in (0, L - 1):
+        sp, sbt, sks, sq = synth.extract_requests(case, [0, 31, 63], layer)
+        ref_o, ref_lse = oracle.attention_full(sp, sbt, 0, sq, sks, sc)
+        got = o1[layer, [0, 31, 63]].float().cpu().double().numpy()
+        assert np.abs(got - ref_o).max() <= 2e-2
+        assert np.abs(l1[layer, [0, 31, 63]].cpu().double().numpy() - ref_lse).max() <= 1e-4

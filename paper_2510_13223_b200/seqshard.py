@@ -171,6 +171,7 @@ class SeqShardedStep:
         self.copy = torch.cuda.Stream(device=dev, priority=-1)
         self.out_ready = [torch.cuda.Event() for _ in range(L)]
         self.part_ready = [torch.cuda.Event() for _ in range(L)]
+        self.mig_ready = [torch.cuda.Event() for _ in range(L)]   # W = 1 hand-off
 
     def flag(self, who: int, kind: str, src: int, layer: int) -> int:
         """Address of flag (kind, src, layer) in rank `who`'s flag array."""
@@ -202,6 +203,8 @@ class SeqShardedStep:
     def launches_per_step(self) -> int:
         if self.transport != "p2p":
             return self.L * (self.world + 1 + (2 if self.n_handoff else 0))
+        if self.world == 1:   # attention (+ hand-off copy); + the epoch advance
+            return self.L * (1 + (1 if self.n_handoff else 0)) + 1
         # attention, combined wait, q-push wait + signals, ack signals, done wait (+ hand-off
         # copy and its signal); + the device epoch advance once per step
         return self.L * (1 + 1 + 2 + 1 + 1 + (2 if self.n_handoff else 0)) + 1
@@ -235,6 +238,9 @@ class SeqShardedStep:
                 if peers:
                     signals_epoch([self.flag(p, "q", r, layer) for p in peers], ep)
         compute = cur
+        # W = 1: every range of every problem runs in this GPU's launch, so stream order
+        # already orders the workspace reuse and the merges -- events replace the flags
+        solo = W == 1
         for layer in range(L):
             if self.n_handoff:
                 with torch.cuda.stream(self.copy):
@@ -243,17 +249,15 @@ class SeqShardedStep:
                     kv_migrate_layer(self.pool, self.next_pool, layer, self.src_ids, self.next_dst)
                     if timers is not None:
                         timers[layer][3].record(self.copy)
-                    signals_epoch([self.flag(self.next, "mig", r, layer)], ep)
-            waits = [self.flag(r, "q", p, layer) for p in peers]
-            mul, add = [1] * len(peers), [0] * len(peers)
-            waits += [self.peer[h]["done"] + 4 * layer for h in range(W)]
-            mul += [pc] * W
-            add += [-pc] * W
-            if self.n_handoff:
-                waits.append(self.flag(r, "mig", self.prev, layer))
-                mul.append(1)
-                add.append(0)
-            wait_signals_epoch(waits, ep, mul, add, to, err, stream=compute)
+                    if solo:
+                        self.mig_ready[layer].record(self.copy)
+                    else:
+                        signals_epoch([self.flag(self.next, "mig", r, layer)], ep)
+            if solo:
+                if self.n_handoff:
+                    compute.wait_event(self.mig_ready[layer])
+            else:
+                self._wait_inputs(layer, peers, ep, pc, to, err, compute)
             if inputs_ready is not None:
                 compute.wait_event(inputs_ready[layer])
             if timers is not None:
@@ -266,19 +270,22 @@ class SeqShardedStep:
                     "kv_split": self.ks_h[h], "max_blocks": self.max_blocks,
                     "out": P["out"] + layer * ob, "lse": P["lse"] + layer * lb,
                     "workspace": P["ws"] + layer * P["ws_stride"], "workspace_bytes": P["ws_stride"],
-                    "done": P["done"] + 4 * layer, "cross_device": True})
+                    "done": P["done"] + 4 * layer, "cross_device": not solo})
             with torch.cuda.stream(compute):
                 self.ops.attention_tasks(problems, [(self.pool, self.bt_h[h], r, h) for h in range(W)],
                                          layer, self.Bh, self.hq)
             if timers is not None:
                 timers[layer][1].record(compute)
             self.part_ready[layer].record(compute)
-            with torch.cuda.stream(self.ack_s):  # every home's q_l consumed -> acks
-                self.ack_s.wait_event(self.part_ready[layer])
-                if peers:
+            if peers:
+                with torch.cuda.stream(self.ack_s):  # every home's q_l consumed -> acks
+                    self.ack_s.wait_event(self.part_ready[layer])
                     signals_epoch([self.flag(p, "q_ack", r, layer) for p in peers], ep)
             with torch.cuda.stream(self.out_s):  # my out_l final once all merges landed
-                wait_signals_epoch([self.done[layer:layer + 1].data_ptr()], ep, pc, 0, to, err)
+                if solo:
+                    self.out_s.wait_event(self.part_ready[layer])
+                else:
+                    wait_signals_epoch([self.done[layer:layer + 1].data_ptr()], ep, pc, 0, to, err)
                 if out.data_ptr() != self.out_buf.data_ptr():
                     out[layer].copy_(self.out_buf[layer])
                 if lse is not None and lse.data_ptr() != self.lse_buf.data_ptr():
@@ -288,6 +295,23 @@ class SeqShardedStep:
                     timers[layer][4].record(self.out_s)
         for s in (self.comm, self.copy, self.ack_s, self.out_s):
             cur.wait_stream(s)
+
+    def _wait_inputs(self, layer, peers, ep, pc, to, err, compute):
+        """One wait launch before layer l's attention: every peer's q_l arrived, every
+        home's workspace free (its `done` counter reached the previous step's count) and the
+        predecessor's hand-off of layer l landed."""
+        from . import wait_signals_epoch
+        W, r = self.world, self.rank
+        waits = [self.flag(r, "q", p, layer) for p in peers]
+        mul, add = [1] * len(peers), [0] * len(peers)
+        waits += [self.peer[h]["done"] + 4 * layer for h in range(W)]
+        mul += [pc] * W
+        add += [-pc] * W
+        if self.n_handoff:
+            waits.append(self.flag(r, "mig", self.prev, layer))
+            mul.append(1)
+            add.append(0)
+        wait_signals_epoch(waits, ep, mul, add, to, err, stream=compute)
 
     # ------------------------------------------------------------------ collective
     def _setup_collective(self):

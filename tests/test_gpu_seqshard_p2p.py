@@ -184,7 +184,7 @@ def _spawn(fn_name, world, cross=False, transport="p2p"):
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
 def test_seqshard_p2p_toy(world):
     _spawn("toy", world)
 

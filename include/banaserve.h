@@ -165,8 +165,8 @@ bs_status bs_kv_migrate_append_layer(const bs_kv_pool* src, bs_kv_pool* dst, int
 
 /* Copy-engine variant (DMA, no SM time -- for the host tier's fetch / store legs, which
  * should not compete with attention for SMs): HOST int32 id arrays (validated), runs of
- * consecutive ids coalesced, one cudaMemcpyBatchAsync per call on a non-NULL stream
- * (per-copy cudaMemcpyAsync otherwise).  Same semantics as bs_kv_migrate_layer. */
+ * consecutive ids coalesced, one cudaMemcpyAsync per run.  Same semantics as
+ * bs_kv_migrate_layer. */
 bs_status bs_kv_migrate_layer_ce(const bs_kv_pool* src, bs_kv_pool* dst, int32_t layer,
                                  const int32_t* src_ids, const int32_t* dst_ids, int32_t n,
                                  void* stream);

@@ -502,21 +502,13 @@ bs_status bs_kv_migrate_layer_ce(const bs_kv_pool* src, bs_kv_pool* dst, int32_t
     sizes.push_back((size_t)run * chunk);
     i += run;
   }
+  // one cudaMemcpyAsync per coalesced run (the batched-descriptor API is not used: it
+  // faulted GPUs of this pool, F1)
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaSuccess;
-  if (s != nullptr) {
-    cudaMemcpyAttributes attr{};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    size_t attr_idx = 0, fail = 0;
-    e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), sizes.size(), &attr, &attr_idx,
-                             1, &fail, s);
-  }
-  if (s == nullptr || e != cudaSuccess) {  // legacy stream / older driver: one copy each
-    cudaGetLastError();
-    for (size_t k = 0; k < sizes.size(); ++k) {
-      e = cudaMemcpyAsync(dsts[k], srcs[k], sizes[k], cudaMemcpyDefault, s);
-      if (e != cudaSuccess) break;
-    }
+  for (size_t k = 0; k < sizes.size(); ++k) {
+    e = cudaMemcpyAsync(dsts[k], srcs[k], sizes[k], cudaMemcpyDefault, s);
+    if (e != cudaSuccess) break;
   }
   if (e != cudaSuccess) return bs::set_error(BS_ERR_CUDA, "bs_kv_migrate_layer_ce: %s", cudaGetErrorString(e));
   return BS_OK;

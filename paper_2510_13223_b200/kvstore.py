@@ -4,8 +4,8 @@ pipeline (§4.2, Figs. 5-6, eqs. 12-17).
 The store is a paged pool in page-locked host memory (``KVPool(host=True)``).  Its
 fetch (HtoD) and store (DtoH) legs move whole chunks between the store and a device
 pool, bit-exact, by one of two engines:
-  * ``"ce"``  -- the copy engines: ``bs_kv_migrate_layer_ce`` (one cudaMemcpyBatchAsync
-                 per layer, runs of consecutive ids coalesced); no SM time at all;
+  * ``"ce"``  -- the copy engines: ``bs_kv_migrate_layer_ce`` (one cudaMemcpyAsync
+                 per run of consecutive ids); no SM time at all;
   * ``"sm"``  -- the copy kernel through the pages' UVA mapping over PCIe (zero-copy,
                  8 CTAs -- the rest of the GPU keeps computing).
 ``ThreeStagePipeline`` overlaps, per layer i (Fig. 6):

@@ -61,6 +61,14 @@ int32_t bs_debug_build(void);
  * clears them.  Always 0 in a release build. */
 int32_t bs_debug_error_code(int32_t reset);
 
+/* Diagnostics: what the calling thread's most recent attention launch (any
+ * bs_split_decode_attention* call that launched) ran -- grid.x CTA ranges (uniform plan:
+ * ranges per (request, kv-head) over the launch's shards; ragged plan: work items), whether
+ * it used the cluster merge and programmatic dependent launch, and the tensor-core (1) or
+ * CUDA-core (0) kernel.  All 0 before the first launch. */
+bs_status bs_attention_last_launch(int32_t* ranges, int32_t* cluster, int32_t* pdl,
+                                   int32_t* tensor_cores);
+
 /* ------------------------------------------------------------------------------ */
 /* H0: paged KV pool + block allocator.                                             */
 /* vLLM-style paged KV ("PagedAttention ... block-level KV Cache"),   */
@@ -230,14 +238,21 @@ bs_status bs_split_decode_attention_local(int32_t n_local, const bs_kv_pool* con
                                           void* out, float* lse, void* workspace,
                                           size_t workspace_bytes, void* stream);
 /* The same with launch flags.  BS_ATTN_PDL: when the launch has more CTAs than one wave,
- * it is a programmatic dependent launch -- it may start while the previous kernel on
- * `stream` drains, reading block_tables / kv_split and prefetching K/V pages before that
- * kernel completes, and q / out / lse / workspace only after (griddepcontrol.wait).
+ * or at most one CTA per SM, it is a programmatic dependent launch -- it may start while the
+ * previous kernel on `stream` drains (a previous attention launch lets it start once its own
+ * CTAs have started (multi-wave) or finished their main loops (one wave)), reading
+ * block_tables / kv_split and prefetching K/V pages before that kernel completes, and
+ * q / out / lse / workspace only after (griddepcontrol.wait).
  * Caller contract: the kernel launched just before it on `stream` writes neither the pools'
  * pages this call reads, nor block_tables / kv_split (e.g. the previous layer's attention;
- * work from other streams joined by events is waited for in full).  Single-wave launches
- * ignore the flag (measured slower with it). */
+ * work from other streams joined by events is waited for in full).  One-wave launches with
+ * 2-3 CTAs per SM ignore the flag (measured slower with it). */
 #define BS_ATTN_PDL 1u
+/* BS_ATTN_NO_CLUSTER: never use the cluster merge.  By default a launch whose CTAs fit one
+ * wave and whose (request, kv-head) is cut into 2..16 ranges runs each (request, kv-head)'s
+ * ranges as one thread-block cluster and merges their partials through distributed shared
+ * memory instead of the workspace (same arithmetic, bitwise the same result). */
+#define BS_ATTN_NO_CLUSTER 2u
 bs_status bs_split_decode_attention_local_ex(int32_t n_local, const bs_kv_pool* const* pools,
                                              int32_t layer, const void* q, int32_t batch,
                                              int32_t num_q_heads,

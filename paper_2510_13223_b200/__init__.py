@@ -41,7 +41,7 @@ EXPORTED_SYMBOLS = (
     "bs_signals", "bs_attention_ragged_plan", "bs_split_decode_attention_local_ragged",
     "bs_debug_build", "bs_debug_error_code", "bs_kv_append_token", "bs_exchange",
     "bs_signals_epoch", "bs_wait_signals_epoch", "bs_epoch_advance", "bs_kv_migrate_append_layer",
-    "bs_split_decode_attention_local_ex",
+    "bs_split_decode_attention_local_ex", "bs_attention_last_launch",
 )
 
 
@@ -87,6 +87,7 @@ def lib():
         "bs_abi_version": ([], _i32),
         "bs_debug_build": ([], _i32),
         "bs_debug_error_code": ([_i32], _i32),
+        "bs_attention_last_launch": ([_p, _p, _p, _p], _i32),
         "bs_kv_pool_bytes": ([ctypes.POINTER(_Desc)], _sz),
         "bs_kv_chunk_bytes": ([ctypes.POINTER(_Desc)], _sz),
         "bs_kv_pool_create": ([ctypes.POINTER(_Desc), _p, ctypes.POINTER(_p)], _i32),
@@ -352,6 +353,14 @@ def split_decode_attention(pool: KVPool, layer: int, q: torch.Tensor, block_tabl
         _dptr(workspace), ws_bytes, _stream(stream)))
 
 
+def attention_last_launch() -> dict:
+    """What this thread's most recent attention launch ran (bs_attention_last_launch):
+    grid.x ranges, cluster merge, programmatic dependent launch, tensor-core kernel."""
+    v = [ctypes.c_int32() for _ in range(4)]
+    _check(lib().bs_attention_last_launch(*[ctypes.byref(x) for x in v]))
+    return dict(zip(("ranges", "cluster", "pdl", "tensor_cores"), (int(x.value) for x in v)))
+
+
 def split_decode_attention_local_workspace_size(pools, max_blocks, batch: int,
                                                 num_q_heads: int) -> int:
     n = len(pools)
@@ -363,7 +372,8 @@ def split_decode_attention_local_workspace_size(pools, max_blocks, batch: int,
     return out.value
 
 
-ATTN_PDL = 1   # bs_split_decode_attention_local_ex flag (see the header's contract)
+ATTN_PDL = 1   # bs_split_decode_attention_local_ex flags (see the header's contract)
+ATTN_NO_CLUSTER = 2
 
 
 def split_decode_attention_local(pools, layer: int, q: torch.Tensor, block_tables,
@@ -371,7 +381,8 @@ def split_decode_attention_local(pools, layer: int, q: torch.Tensor, block_table
                                  lse: torch.Tensor, workspace: torch.Tensor | None = None,
                                  stream=None, flags: int = 0) -> None:
     """H4+H6 fused over shards resident on this GPU: bf16 ``out`` [B,Hq,d] + fp32 ``lse``.
-    ``flags`` = ATTN_PDL: programmatic dependent launch (bs_split_decode_attention_local_ex)."""
+    ``flags``: ATTN_PDL (programmatic dependent launch), ATTN_NO_CLUSTER (workspace merge
+    instead of the cluster merge) -- bs_split_decode_attention_local_ex."""
     n = len(pools)
     B, hq, d = q.shape
     pa = (ctypes.c_void_p * n)(*[p.handle.value for p in pools])

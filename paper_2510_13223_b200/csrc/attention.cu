@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <cstdlib>
 #include <type_traits>
 #include <vector>
@@ -50,10 +51,15 @@ constexpr int kMaxLocal = 8;  // shards (tasks) / problems of one launch
 #ifdef BS_TIMELINE
 // Diagnostics build only: per-CTA %globaltimer stamps (ns) of the tensor-core kernel --
 // [0] entry, [1] first K/V stage landed (warp 0), [2] all warps' loops done, [3] arrival
-// counter resolved, [4] exit, [5] smid | last-arriver << 16 | blocks << 20.  Read by
-// bs_timeline_read.
+// counter resolved (cluster merge: leader's partials all landed / producer released),
+// [4] exit, [5] smid | last-arriver << 16 | blocks << 20, [6] griddepcontrol.wait returned
+// (PDL launches).  Rows from AttnParams::tl_base: consecutive launches alternate between the
+// two halves (bs_timeline_reset restarts at the first), so a PDL pair can be read back.
+// Read by bs_timeline_read.
 constexpr int kTlCtas = 16384;
-__device__ unsigned long long g_timeline[kTlCtas][6];
+constexpr int kTlCols = 8;
+__device__ unsigned long long g_timeline[kTlCtas][kTlCols];
+std::atomic<int> g_tl_launches{0};  // host: launches since bs_timeline_reset
 __device__ __forceinline__ unsigned long long tl_now() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -61,7 +67,7 @@ __device__ __forceinline__ unsigned long long tl_now() {
 }
 #define BS_TL(k)                                                                              \
   do {                                                                                        \
-    const unsigned _lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);     \
+    const unsigned _lin = tl_base_ + blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); \
     if (threadIdx.x == 0 && _lin < kTlCtas) g_timeline[_lin][k] = tl_now();                  \
   } while (0)
 #else
@@ -117,6 +123,10 @@ struct AttnParams {
   int32_t model_head_lo;    // first kv head of the launch in the model (q / output rows)
   int32_t grid_x;           // CTA ranges of this launch over its shards
   int32_t pdl;              // launched as a programmatic dependent: prefetch, then wait
+  int32_t cl;               // cluster merge: grid.x = ranges = cluster size (cluster_combine_merge)
+  int32_t tl_base;          // timeline build only: first g_timeline row of this launch
+  int32_t trig_late;        // tensor-core kernel: let the next (PDL) launch start once every
+                            // CTA's main loop is done (1) or once every CTA has started (0)
   const int4* work;         // ragged plan (bs_attention_ragged_plan) or NULL: one item per
                             // item = (request, shard << 16 | slot, first block,
                             // blocks << 8 | ranges of the request); grid.x = items * hkv
@@ -237,12 +247,144 @@ __device__ __forceinline__ void count_done(const ProbDesc& P) {  // P: a local c
     asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(P.done) : "memory");
 }
 
+// The eq. 10 merge of a (request, kv-head)'s nparts partials (o~ normalised by its own l,
+// m in log2 units, l) in fixed order 0..nparts-1, and the output store (bf16 O + lse, or the
+// (o~, m, l) triple).  `src` says where the partials are: the workspace (last-arriver
+// merge, WsParts) or this CTA's shared memory (cluster merge, SmemParts) -- the arithmetic
+// is the same, so both paths give bitwise the same result.  s_red: KiB-sized scratch.
+struct WsParts {  // P.ws_o [row][nsplit][D], P.ws_ml [row][nsplit][2], read through L2
+  const float* ws_o;
+  const float* ws_ml;
+  int nsplit;
+  __device__ __forceinline__ float m(int64_t row, int, int j) const { return __ldcg(ws_ml + (row * nsplit + j) * 2); }
+  __device__ __forceinline__ float l(int64_t row, int, int j) const { return __ldcg(ws_ml + (row * nsplit + j) * 2 + 1); }
+  template <int D>
+  __device__ __forceinline__ float4 o4(int64_t row, int, int x, int j) const {
+    return __ldcg(reinterpret_cast<const float4*>(ws_o + (row * nsplit + j) * D + x));
+  }
+};
+
+template <int D, int G>
+struct SmemParts {  // part j at base + j * kPF floats: o~ [G][D], then (m, l) per head
+  static constexpr int kPF = (G * D + 2 * G + 3) & ~3;
+  const float* base;
+  __device__ __forceinline__ float m(int64_t, int h, int j) const { return base[j * kPF + G * D + 2 * h]; }
+  __device__ __forceinline__ float l(int64_t, int h, int j) const { return base[j * kPF + G * D + 2 * h + 1]; }
+  template <int DD>
+  __device__ __forceinline__ float4 o4(int64_t, int h, int x, int j) const {
+    return *reinterpret_cast<const float4*>(base + j * kPF + h * D + x);
+  }
+};
+
+template <int D, int G, class Src>
+__device__ __forceinline__ void merge_parts_store(const ProbDesc& P, int hq, int b, int gm, int nparts,
+                                                  const Src& src, float* s_w, float4* s_red) {
+  // per-head weights w_j = l_j 2^(m_j - M) / L: one warp per head, lanes over the ranges
+  // (<= kMaxSplit = 64 -> 2 per lane); butterfly reductions keep the result deterministic
+  {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int h = warp; h < G; h += kWarps) {
+      const int64_t row = (int64_t)b * hq + gm * G + h;
+      float mj[2], lj[2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int j = lane + 32 * t;
+        mj[t] = j < nparts ? src.m(row, h, j) : -INFINITY;
+        lj[t] = j < nparts ? src.l(row, h, j) : 0.f;
+      }
+      float M = fmaxf(mj[0], mj[1]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+      float w[2], L = 0.f;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        w[t] = mj[t] == -INFINITY ? 0.f : lj[t] * exp2f(mj[t] - M);
+        L += w[t];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int j = lane + 32 * t;
+        if (j < nparts) s_w[h * kMaxSplit + j] = L > 0.f ? w[t] / L : 0.f;
+      }
+      if (lane == 0) {
+        if (P.merged) {
+          if (P.lse) P.lse[row] = L > 0.f ? M * kLn2 + logf(L) : -INFINITY;
+        } else {
+          P.m[row] = L > 0.f ? M * kLn2 : -INFINITY;
+          P.l[row] = L;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // O = sum_j w_j o~_j over float4 columns: every load of the loop is independent (16 in
+  // flight per thread), so the merge costs ~nparts/16 L2 round trips instead of one per
+  // 8 ranges per column.  NV float4 columns per (request, kv-head); with NV < 128 the
+  // threads also split the ranges (JS interleaved groups) and sum the groups in fixed order.
+  {
+    constexpr int NV = G * D / 4;
+    constexpr int E = NV < kWarps * 32 ? NV : kWarps * 32;
+    constexpr int JS = kWarps * 32 / E;
+    const int e0 = threadIdx.x % E, jo = threadIdx.x / E;
+#pragma unroll
+    for (int e = e0; e < NV; e += E) {
+      const int h = (e * 4) / D, x = e * 4 - h * D;
+      const int64_t row = (int64_t)b * hq + gm * G + h;
+      const float* w = s_w + h * kMaxSplit;
+      float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 16
+      for (int j = jo; j < nparts; j += JS) {
+        const float4 v = src.template o4<D>(row, h, x, j);
+        const float wj = w[j];
+        O.x += wj * v.x;
+        O.y += wj * v.y;
+        O.z += wj * v.z;
+        O.w += wj * v.w;
+      }
+      if constexpr (JS > 1) {
+        s_red[jo * E + e0] = O;
+        __syncthreads();
+        if (jo == 0) {
+#pragma unroll
+          for (int k = 1; k < JS; ++k) {
+            const float4 r = s_red[k * E + e0];
+            O.x += r.x;
+            O.y += r.y;
+            O.z += r.z;
+            O.w += r.w;
+          }
+        }
+      }
+      if (jo == 0) {
+        if (P.merged) {
+          const __nv_bfloat162 lo = __floats2bfloat162_rn(O.x, O.y), hi = __floats2bfloat162_rn(O.z, O.w);
+          uint2 pk;
+          pk.x = *reinterpret_cast<const uint32_t*>(&lo);
+          pk.y = *reinterpret_cast<const uint32_t*>(&hi);
+          *reinterpret_cast<uint2*>(P.out + row * D + x) = pk;
+        } else {
+          *reinterpret_cast<float4*>(P.o + row * D + x) = O;
+        }
+      }
+    }
+  }
+  if (P.done) {
+    __syncthreads();
+    if (threadIdx.x == 0) count_done(P);
+  }
+}
+
+
 template <int D, int G>
 // sp: this CTA's partial slot; nparts: ranges of the request to merge (P.nsplit, or the
 // request's own count under a ragged plan); P.nsplit is the workspace slot stride.
 __device__ __forceinline__ void cta_combine_and_store(const ProbDesc P, int hq, int hkv, int b, int g,
                                                       int gm, int sp, int nparts, const float* s_acc,
-                                                      const float* s_ml, float* s_w, int* s_flag) {
+                                                      const float* s_ml, float* s_w, int* s_flag,
+                                                      int tl_base_ = 0) {
+  (void)tl_base_;
   for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
     const int h = idx / D, x = idx - h * D;
     float M = -INFINITY;
@@ -309,103 +451,94 @@ __device__ __forceinline__ void cta_combine_and_store(const ProbDesc P, int hq, 
   __syncthreads();
   BS_TL(3);
   if (!s_flag[0]) return;
-  // per-head weights w_j = l_j 2^(m_j - M) / L: one warp per head, lanes over the ranges
-  // (<= kMaxSplit = 64 -> 2 per lane); butterfly reductions keep the result deterministic
-  {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int h = warp; h < G; h += kWarps) {
-      const int64_t row = (int64_t)b * hq + gm * G + h;
-      const float* ml = P.ws_ml + row * P.nsplit * 2;
-      float mj[2], lj[2];
+  merge_parts_store<D, G>(P, hq, b, gm, nparts, WsParts{P.ws_o, P.ws_ml, P.nsplit}, s_w,
+                          reinterpret_cast<float4*>(const_cast<float*>(s_acc)));  // rings idle
+}
+// Cluster merge (AttnParams::cl, single-GPU problems with 2..16 CTA ranges per (request,
+// kv-head)): the ranges of one (request, kv-head) form one thread-block cluster (grid.x =
+// ranges = cluster size, rank = range slot).  Instead of publishing every partial to the
+// workspace and electing the last arriver (the partial stores, an acq_rel atomic and the
+// merge's loads: three dependent L2 round trips after the slowest range), each CTA combines
+// its warps as usual and the non-leaders store their partial straight into the leader's
+// (rank 0) shared memory with st.async, counted on the leader's mbarrier; the leader merges
+// from shared memory (merge_parts_store, the same arithmetic as the workspace path).  The
+// receive area is the leader's idle K/V ring, so the leader releases each producer (a
+// remote arrive on the producer's "go" mbarrier) once its own loop is done.  No CTA's
+// shared memory is touched after it exits: producers write only into the leader, which
+// waits for all their bytes; the leader arrives only on producers that wait for it.
+// cbar: [0] go (producers), [1] receive (leader), initialised before the cluster barrier's
+// arrive in the prologue.
+template <int D, int G>
+__device__ __forceinline__ void cluster_combine_merge(const ProbDesc& P, int hq, int b, int gm,
+                                                      int nparts, const float* s_acc,
+                                                      const float* s_ml, float* s_w,
+                                                      float* s_recv, uint64_t* cbar,
+                                                      int tl_base_ = 0) {
+  (void)tl_base_;
+  using SP = SmemParts<D, G>;
+  constexpr int NV = G * D / 4;
+  constexpr int PER = (NV + kWarps * 32 - 1) / (kWarps * 32);
+  float4 val[PER];
+  float2 mlv[PER];
 #pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const int j = lane + 32 * t;
-        mj[t] = j < nparts ? __ldcg(ml + 2 * j) : -INFINITY;
-        lj[t] = j < nparts ? __ldcg(ml + 2 * j + 1) : 0.f;
-      }
-      float M = fmaxf(mj[0], mj[1]);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-      float w[2], L = 0.f;
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        w[t] = mj[t] == -INFINITY ? 0.f : lj[t] * exp2f(mj[t] - M);
-        L += w[t];
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const int j = lane + 32 * t;
-        if (j < nparts) s_w[h * kMaxSplit + j] = L > 0.f ? w[t] / L : 0.f;
-      }
-      if (lane == 0) {
-        if (P.merged) {
-          if (P.lse) P.lse[row] = L > 0.f ? M * kLn2 + logf(L) : -INFINITY;
-        } else {
-          P.m[row] = L > 0.f ? M * kLn2 : -INFINITY;
-          P.l[row] = L;
-        }
-      }
-    }
-  }
-  __syncthreads();
-  // O = sum_j w_j o~_j over float4 columns: every load of the loop is independent (16 in
-  // flight per thread), so the merge costs ~nparts/16 L2 round trips instead of one per
-  // 8 ranges per column.  NV float4 columns per (request, kv-head); with NV < 128 the
-  // threads also split the ranges (JS interleaved groups) and sum the groups in fixed order.
-  {
-    constexpr int NV = G * D / 4;
-    constexpr int E = NV < kWarps * 32 ? NV : kWarps * 32;
-    constexpr int JS = kWarps * 32 / E;
-    const int e0 = threadIdx.x % E, jo = threadIdx.x / E;
-    float4* s_red = reinterpret_cast<float4*>(const_cast<float*>(s_acc));  // rings idle
-#pragma unroll
-    for (int e = e0; e < NV; e += E) {
+  for (int k = 0; k < PER; ++k) {  // the CTA's partial, as cta_combine_and_store computes it
+    const int e = threadIdx.x + k * kWarps * 32;
+    if (e < NV) {
       const int h = (e * 4) / D, x = e * 4 - h * D;
-      const int64_t row = (int64_t)b * hq + gm * G + h;
-      const float4* po = reinterpret_cast<const float4*>(P.ws_o + row * P.nsplit * D + x);
-      const float* w = s_w + h * kMaxSplit;
-      float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 16
-      for (int j = jo; j < nparts; j += JS) {
-        const float4 v = __ldcg(po + (int64_t)j * (D / 4));
-        const float wj = w[j];
-        O.x += wj * v.x;
-        O.y += wj * v.y;
-        O.z += wj * v.z;
-        O.w += wj * v.w;
-      }
-      if constexpr (JS > 1) {
-        s_red[jo * E + e0] = O;
-        __syncthreads();
-        if (jo == 0) {
+      float M = -INFINITY;
 #pragma unroll
-          for (int k = 1; k < JS; ++k) {
-            const float4 r = s_red[k * E + e0];
-            O.x += r.x;
-            O.y += r.y;
-            O.z += r.z;
-            O.w += r.w;
-          }
+      for (int w = 0; w < kWarps; ++w) M = fmaxf(M, s_ml[(w * G + h) * 2]);
+      float L = 0.f, O[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        const float mw = s_ml[(w * G + h) * 2];
+        if (mw != -INFINITY) {
+          const float f = exp2f(mw - M);
+          L += s_ml[(w * G + h) * 2 + 1] * f;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) O[c] += s_acc[(w * G + h) * D + x + c] * f;
         }
       }
-      if (jo == 0) {
-        if (P.merged) {
-          const __nv_bfloat162 lo = __floats2bfloat162_rn(O.x, O.y), hi = __floats2bfloat162_rn(O.z, O.w);
-          uint2 pk;
-          pk.x = *reinterpret_cast<const uint32_t*>(&lo);
-          pk.y = *reinterpret_cast<const uint32_t*>(&hi);
-          *reinterpret_cast<uint2*>(P.out + row * D + x) = pk;
-        } else {
-          *reinterpret_cast<float4*>(P.o + row * D + x) = O;
-        }
-      }
+      const bool any = L > 0.f;
+      val[k] = any ? make_float4(O[0] / L, O[1] / L, O[2] / L, O[3] / L) : make_float4(0.f, 0.f, 0.f, 0.f);
+      mlv[k] = make_float2(any ? M : -INFINITY, L);  // log2 units
     }
   }
-  if (P.done) {
-    __syncthreads();
-    if (threadIdx.x == 0) count_done(P);
+  const uint32_t rank = ptx::cluster_ctarank();
+  ptx::cluster_wait_acquire();  // every CTA of the cluster has initialised its barriers
+  uint64_t* go = cbar;
+  uint64_t* rv = cbar + 1;
+  if (rank == 0) {
+    if (threadIdx.x == 0) ptx::mbar_expect_tx(rv, (uint32_t)(nparts - 1) * (G * D * 4 + G * 8));
+    if (threadIdx.x >= 1 && threadIdx.x < nparts) ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(go), threadIdx.x));
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int e = threadIdx.x + k * kWarps * 32;
+      if (e < NV) {
+        const int h = (e * 4) / D, x = e * 4 - h * D;
+        *reinterpret_cast<float4*>(s_recv + h * D + x) = val[k];
+        if (x == 0) *reinterpret_cast<float2*>(s_recv + G * D + 2 * h) = mlv[k];
+      }
+    }
+    ptx::mbar_wait_cluster(rv, 0);
+    __syncthreads();  // the leader's own partial (other threads' stores) too
+    BS_TL(3);
+    merge_parts_store<D, G>(P, hq, b, gm, nparts, SP{s_recv}, s_w,
+                            reinterpret_cast<float4*>(s_recv + nparts * SP::kPF));
+  } else {
+    ptx::mbar_wait_cluster(go, 0);
+    BS_TL(3);
+    const uint32_t rbar = ptx::mapa(ptx::smem_u32(rv), 0);
+    const uint32_t rbase = ptx::mapa(ptx::smem_u32(s_recv + rank * SP::kPF), 0);
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int e = threadIdx.x + k * kWarps * 32;
+      if (e < NV) {
+        const int h = (e * 4) / D, x = e * 4 - h * D;
+        ptx::st_async_v4(rbase + (uint32_t)(h * D + x) * 4, val[k], rbar);
+        if (x == 0) ptx::st_async_v2(rbase + (uint32_t)(G * D + 2 * h) * 4, mlv[k].x, mlv[k].y, rbar);
+      }
+    }
   }
 }
 
@@ -683,7 +816,9 @@ struct MmaSmem {
   static constexpr int kMlOff = kBarOff + kWarps * STAGES * 8;
   static constexpr int kWOff = kMlOff + kWarps * G * 2 * 4;
   static constexpr int kFlagOff = kWOff + G * kMaxSplit * 4;
-  static constexpr int kTotal = kFlagOff + 16 + 1024;  // + alignment slack (swizzle atoms)
+  static constexpr int kClBarOff = kFlagOff + 16;     // cluster merge: go / receive mbarriers
+  static constexpr int kRecvOff = kWarps * G * D * 4;  // cluster merge: partials, in the idle ring
+  static constexpr int kTotal = kClBarOff + 16 + 1024;  // + alignment slack (swizzle atoms)
   static_assert(kWarps * G * D * 4 <= kRing, "combine buffer must fit in the ring");
 };
 
@@ -732,6 +867,8 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
   static_assert(G <= 8, "one n8 tile of heads");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int tl_base_ = p.tl_base;
+  (void)tl_base_;
   BS_TL(0);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -787,9 +924,14 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
       tma_load_2d(st + (NB + bx) * S::kBox, tmap, 64 * bx, row_v, &bars[s], policy);
     }
   };
+  uint64_t* cbar = reinterpret_cast<uint64_t*>(smem + S::kClBarOff);
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&bars[s], 1);
+    if (p.cl && warp == 0) {
+      ptx::mbar_init(&cbar[0], 1);
+      ptx::mbar_init(&cbar[1], 1);
+    }
     ptx::fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
     policy = ptx::policy_evict_first();
@@ -803,14 +945,20 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
     if (i < nb_cta) s_bt[i] = idv[r];
   }
   __syncthreads();  // block table + barrier inits visible to the CTA
+  if (p.cl) ptx::cluster_arrive_release();  // ... and the cluster barriers to the cluster
   // Programmatic dependent launch (BS_ATTN_PDL): this grid may start while the previous
   // kernel on the stream drains.  Everything above -- block table, kv_split, the first
   // K/V stages in flight -- reads only step inputs (the caller's contract); q, the outputs
   // and the workspace (which the previous launch may still be merging from) come after the
   // wait, which returns once that kernel has completed and its writes are visible.
+  // The next launch on the stream, if it is a programmatic dependent, may start once every
+  // CTA of this grid has triggered: right away for multi-wave grids (it fills the slots of
+  // the last wave's tail), after the main loop for single-wave grids (its prologue and first
+  // K/V stages then overlap this grid's epilogue instead of competing with its streaming).
+  if (!p.trig_late) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (p.pdl) {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    BS_TL(6);
   }
 
   // q^T B-fragments (bf16 pairs) for head n = gq (zero padding for n >= G)
@@ -913,6 +1061,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
     }
     __syncwarp();
   }
+  if (p.trig_late) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // ---- per-warp state -> shared memory, then the common CTA epilogue --------------------
 #pragma unroll
@@ -945,16 +1094,20 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
     }
   }
   __syncthreads();
-  cta_combine_and_store<D, G>(P, p.hq, p.hkv, b, g, gm, cw.slot, nparts, s_acc, s_ml, s_w,
-                              s_flag);
+  if (p.cl)
+    cluster_combine_merge<D, G>(P, p.hq, b, gm, nparts, s_acc, s_ml, s_w,
+                                reinterpret_cast<float*>(smem + S::kRecvOff), cbar, tl_base_);
+  else
+    cta_combine_and_store<D, G>(P, p.hq, p.hkv, b, g, gm, cw.slot, nparts, s_acc, s_ml, s_w,
+                                s_flag, tl_base_);
 #ifdef BS_TIMELINE
   BS_TL(4);
   {
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    const unsigned lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const unsigned lin = tl_base_ + blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     if (threadIdx.x == 0 && lin < kTlCtas)
-      g_timeline[lin][5] = smid | ((unsigned long long)(nparts == 1 || s_flag[0]) << 16) |
+      g_timeline[lin][5] = smid | ((unsigned long long)(nparts == 1 || (p.cl ? ptx::cluster_ctarank() == 0 : s_flag[0])) << 16) |
                            ((unsigned long long)nb_cta << 20);
   }
 #endif
@@ -1123,25 +1276,62 @@ bs_status make_plan(int batch, int G, int hq, int hkv, int d, int n_local, const
   return BS_OK;
 }
 
-// Launch with cudaLaunchAttributeProgrammaticStreamSerialization: the grid may begin as
-// soon as every CTA of the previous kernel on the stream has started (and triggered);
-// the kernel's griddepcontrol.wait orders what depends on that kernel.
+// Launch with cudaLaunchKernelEx: programmatic stream serialisation (PDL: the grid may
+// begin as soon as every CTA of the previous kernel on the stream has started and
+// triggered; the kernel's griddepcontrol.wait orders what depends on that kernel) and / or
+// a cluster of `cluster_x` CTAs along grid.x (cluster merge).
 template <typename... KArgs, typename... Args>
-bs_status launch_pdl(void (*kern)(KArgs...), dim3 grid, int smem, cudaStream_t stream,
-                     const char* what, const Args&... args) {
+bs_status launch_ex(void (*kern)(KArgs...), dim3 grid, int smem, cudaStream_t stream, bool pdl,
+                    int cluster_x, const char* what, const Args&... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(kWarps * 32, 1, 1);
   cfg.dynamicSmemBytes = (size_t)smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (pdl) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (cluster_x > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = (unsigned)cluster_x;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (unsigned)n;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args...);
-  if (e != cudaSuccess) return set_error(BS_ERR_CUDA, "%s (PDL launch): %s", what, cudaGetErrorString(e));
+  if (e != cudaSuccess) return set_error(BS_ERR_CUDA, "%s (launch_ex): %s", what, cudaGetErrorString(e));
   return BS_OK;
+}
+
+template <typename... KArgs, typename... Args>
+bs_status launch_pdl(void (*kern)(KArgs...), dim3 grid, int smem, cudaStream_t stream,
+                     const char* what, const Args&... args) {
+  return launch_ex(kern, grid, smem, stream, true, 1, what, args...);
+}
+
+// What the calling thread's last attention launch ran (bs_attention_last_launch).
+struct LaunchInfo {
+  int32_t ranges, cluster, pdl, tensor_cores;
+};
+thread_local LaunchInfo g_last_launch{0, 0, 0, 0};
+
+int cluster_env() {  // A/B switch BS_ATTN_CLUSTER: 0 never, 1 single-wave launches, 2 always
+  static int v = env_int("BS_ATTN_CLUSTER", 1);
+  return v;
+}
+
+// Largest cluster the merge uses (BS_ATTN_CLUSTER_MAX, <= 16).  Clusters must sit in one
+// GPC: 16-CTA clusters of a C3 B=1 launch (8 x 16 CTAs) were placed two CTAs to an SM on 28
+// SMs (114 SMs used instead of 128) and lost more in the loop than the merge saved.
+int cluster_max() {
+  static int v = std::min(16, std::max(2, env_int("BS_ATTN_CLUSTER_MAX", 8)));
+  return v;
 }
 
 int pdl_env() {  // A/B switch BS_ATTN_PDL: 0 never, 1 every attention launch, unset: flags
@@ -1160,25 +1350,68 @@ bs_status launch_attn_v(const AttnParams& p, int batch, cudaStream_t stream) {
     configured.fetch_or(bit);
   }
   const dim3 grid = p.work ? dim3(p.grid_x * p.hkv, 1, 1) : dim3(p.grid_x, p.hkv, batch);
+  g_last_launch = LaunchInfo{p.grid_x, 0, p.pdl, 0};
   if (p.pdl) return launch_pdl(split_decode_attn<D, G, STAGES, MINB>, grid, S::kTotal, stream,
                                "split_decode_attn", p);
   split_decode_attn<D, G, STAGES, MINB><<<grid, kWarps * 32, S::kTotal, stream>>>(p);
   return check_launch("split_decode_attn");
 }
 
+// Can clusters of `n` CTAs of this kernel be resident (GPC size, shared memory)?  Asked
+// once per (device, n) with cudaOccupancyMaxActiveClusters.
 template <int D, int G, int STAGES, int MINB>
-bs_status launch_attn_mma(const AttnParams& p, const TMaps& tm, int batch, cudaStream_t stream) {
+bool cluster_fits(int n, int smem) {
+  static std::mutex mu;
+  static int known[64][17];  // 0 unknown, 1 yes, 2 no
+  const int dev = current_device() & 63;
+  std::lock_guard<std::mutex> g(mu);
+  if (!known[dev][n]) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(n, 1, 1);
+    cfg.blockDim = dim3(kWarps * 32, 1, 1);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)n;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    const cudaError_t e =
+        cudaOccupancyMaxActiveClusters(&clusters, split_decode_attn_mma<D, G, STAGES, MINB>, &cfg);
+    cudaGetLastError();
+    known[dev][n] = (e == cudaSuccess && clusters > 0) ? 1 : 2;
+  }
+  return known[dev][n] == 1;
+}
+
+template <int D, int G, int STAGES, int MINB>
+bs_status launch_attn_mma(const AttnParams& p_in, const TMaps& tm, int batch, cudaStream_t stream) {
   using S = MmaSmem<D, G, STAGES>;
-  static std::atomic<uint64_t> configured{0};  // per-device function attribute
+  static std::atomic<uint64_t> configured{0};  // per-device function attributes
   const uint64_t bit = 1ull << (current_device() & 63);
   if (!(configured.load() & bit)) {
     cudaFuncSetAttribute(split_decode_attn_mma<D, G, STAGES, MINB>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
+    cudaFuncSetAttribute(split_decode_attn_mma<D, G, STAGES, MINB>,
+                         cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     configured.fetch_or(bit);
   }
+  AttnParams p = p_in;
+  // cluster merge: the partials of a (request, kv-head) must fit in the leader's idle ring
+  // (plus the merge's 2 KiB scratch), and clusters of grid.x CTAs must be schedulable
+  if (p.cl) {
+    const int need = S::kRecvOff + p.grid_x * SmemParts<D, G>::kPF * 4 + 2048;
+    if (p.work || p.grid_x < 2 || p.grid_x > 16 || need > S::kRing ||
+        !cluster_fits<D, G, STAGES, MINB>(p.grid_x, S::kTotal))
+      p.cl = 0;
+  }
   const dim3 grid = p.work ? dim3(p.grid_x * p.hkv, 1, 1) : dim3(p.grid_x, p.hkv, batch);
-  if (p.pdl) return launch_pdl(split_decode_attn_mma<D, G, STAGES, MINB>, grid, S::kTotal, stream,
-                               "split_decode_attn_mma", p, tm);
+  g_last_launch = LaunchInfo{p.grid_x, p.cl, p.pdl, 1};
+  if (p.pdl || p.cl)
+    return launch_ex(split_decode_attn_mma<D, G, STAGES, MINB>, grid, S::kTotal, stream, p.pdl != 0,
+                     p.cl ? p.grid_x : 1, "split_decode_attn_mma", p, tm);
   split_decode_attn_mma<D, G, STAGES, MINB><<<grid, kWarps * 32, S::kTotal, stream>>>(p, tm);
   return check_launch("split_decode_attn_mma");
 }
@@ -1271,7 +1504,7 @@ struct LaunchArgs {
   void* stream;
   const int32_t* work;  // ragged plan (device int4 items) or NULL
   int32_t n_work, max_parts;
-  uint32_t flags;       // BS_ATTN_PDL
+  uint32_t flags;       // BS_ATTN_PDL | BS_ATTN_NO_CLUSTER
 };
 
 bs_status validate_common(const LaunchArgs& a, int* G_out) {
@@ -1380,8 +1613,23 @@ bs_status run_attention(const LaunchArgs& a) {
     const int64_t ctas = (int64_t)p.grid_x * a.n_kv_heads * (a.work ? 1 : a.batch);
     const int64_t slots = (int64_t)bs::sm_count(bs::current_device()) * bs::variant_for(d, G).minb;
     const int env = bs::pdl_env();
-    p.pdl = env >= 0 ? env : ((a.flags & BS_ATTN_PDL) && ctas > slots ? 1 : 0);
+    // PDL pays for multi-wave grids (the next grid fills the last wave's tail) and for
+    // grids of at most one CTA per SM (C3 B=1: its prologue and first stages overlap the
+    // previous grid's epilogue, 11.9 -> 10.8 us); a one-wave grid of 2-3 CTAs per SM that
+    // starts early is placed unevenly over the SMs and loses its tail (C3 B=8 42.9 -> 44.9)
+    const int64_t sms = bs::sm_count(bs::current_device());
+    p.pdl = env >= 0 ? env : ((a.flags & BS_ATTN_PDL) && (ctas > slots || ctas <= sms) ? 1 : 0);
+    p.trig_late = ctas <= slots ? 1 : 0;
+    // cluster merge: single-wave launches with 2..16 ranges per (request,
+    // kv-head) -- the epilogue is their critical path; BS_ATTN_CLUSTER=0 off, 2 any wave count
+    const int cl_env = bs::cluster_env();
+    p.cl = (!a.work && !(a.flags & BS_ATTN_NO_CLUSTER) && pl.nsplit >= 2 &&
+            pl.nsplit <= bs::cluster_max() && cl_env != 0 &&
+            (cl_env == 2 || ctas <= slots)) ? 1 : 0;
   }
+#ifdef BS_TIMELINE
+  p.tl_base = (bs::g_tl_launches.fetch_add(1) & 1) * (bs::kTlCtas / 2);
+#endif
   bs::ProbDesc& P = p.pb[0];
   P.q = static_cast<const __nv_bfloat16*>(a.q);
   P.kv_split = a.kv_split;
@@ -1439,11 +1687,23 @@ bs_status bs_timeline_read(void* host, size_t bytes) {
   return e == cudaSuccess ? BS_OK : bs::set_error(BS_ERR_CUDA, "timeline: %s", cudaGetErrorString(e));
 }
 bs_status bs_timeline_reset(void) {
-  static unsigned long long zeros[bs::kTlCtas][6];
+  bs::g_tl_launches = 0;
+  static unsigned long long zeros[bs::kTlCtas][bs::kTlCols];
   const cudaError_t e = cudaMemcpyToSymbol(bs::g_timeline, zeros, sizeof(zeros));
   return e == cudaSuccess ? BS_OK : bs::set_error(BS_ERR_CUDA, "timeline: %s", cudaGetErrorString(e));
 }
 #endif
+
+bs_status bs_attention_last_launch(int32_t* ranges, int32_t* cluster, int32_t* pdl,
+                                   int32_t* tensor_cores) {
+  BS_REQUIRE(ranges && cluster && pdl && tensor_cores, "bs_attention_last_launch: NULL argument");
+  const bs::LaunchInfo& i = bs::g_last_launch;
+  *ranges = i.ranges;
+  *cluster = i.cluster;
+  *pdl = i.pdl;
+  *tensor_cores = i.tensor_cores;
+  return BS_OK;
+}
 
 bs_status bs_split_decode_attention_workspace_size(const bs_kv_pool* pool, int32_t batch,
                                                    int32_t num_q_heads, int32_t max_blocks,
@@ -1562,7 +1822,8 @@ bs_status bs_split_decode_attention_local_ex(int32_t n_local, const bs_kv_pool* 
                                              const int32_t* kv_split, int32_t n_shards, float scale,
                                              void* out, float* lse, void* workspace,
                                              size_t workspace_bytes, uint32_t flags, void* stream) {
-  BS_REQUIRE((flags & ~BS_ATTN_PDL) == 0, "bs_split_decode_attention_local: unknown flags 0x%x", flags);
+  BS_REQUIRE((flags & ~(BS_ATTN_PDL | BS_ATTN_NO_CLUSTER)) == 0,
+             "bs_split_decode_attention_local: unknown flags 0x%x", flags);
   BS_REQUIRE(pools && block_tables && max_blocks && shard_ids,
              "bs_split_decode_attention_local: NULL array");
   BS_REQUIRE(n_local >= 1 && n_local <= bs::kMaxLocal, "bs_split_decode_attention_local: %d shards",

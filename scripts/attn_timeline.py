@@ -28,6 +28,7 @@ import synth  # noqa: E402
 from microbench import ATTN  # noqa: E402
 
 KT = 16384
+KC = 8   # stamp columns (see attention.cu: [6] = griddepcontrol.wait returned)
 
 
 def q(x, ps=(0, 10, 50, 90, 100)):
@@ -75,7 +76,7 @@ def run(name, reps=5, ragged_bps=None):
         call()
         b.record()
         torch.cuda.synchronize()
-        buf = np.zeros((KT, 6), dtype=np.uint64)
+        buf = np.zeros((KT, KC), dtype=np.uint64)
         assert L.bs_timeline_read(buf.ctypes.data, buf.nbytes) == 0
         out.append((a.elapsed_time(b) * 1e3, buf))
     ev_us, buf = sorted(out, key=lambda x: x[0])[len(out) // 2]
@@ -144,14 +145,92 @@ def run(name, reps=5, ragged_bps=None):
     return res
 
 
+def pdl_pair(name, reps=5, graph=False):
+    """Two launches of one case back to back on one stream (the second reading the next
+    layer's KV), L2 flushed before: per-CTA stamps of both (rows of launch 2 start at
+    KT / 2).  Run once with BS_ATTN_PDL=1 and once with 0 to see whether the second grid's
+    CTAs become resident, prefetch and wait while the first drains."""
+    shape, lens = ATTN[name]
+    dev = torch.device("cuda")
+    lens = np.asarray(lens, dtype=np.int64)
+    ks = np.stack([np.zeros_like(lens), lens], 1).astype(np.int32)
+    case = synth.device_shards(shape, lens, ks, seed=1, device=dev, layers=2)
+    pt, bt = case.pools[0], case.block_tables[0]
+    pool = bs.KVPool(2, pt.shape[1], shape.hkv, shape.d, base=pt.reshape(-1))
+    B = len(lens)
+    btd = torch.from_numpy(bt).to(dev)
+    ksd = torch.from_numpy(ks).to(dev)
+    o = torch.empty(B, shape.hq, shape.d, device=dev)
+    m = torch.empty(B, shape.hq, device=dev)
+    l = torch.empty(B, shape.hq, device=dev)
+    ws = torch.zeros(max(16, bs.split_decode_attention_workspace_size(pool, B, shape.hq, bt.shape[1])),
+                     dtype=torch.uint8, device=dev)
+    sc = synth.default_scale(shape.d)
+    flush = torch.empty(256 * 2**20, dtype=torch.uint8, device=dev)
+    L = bs.lib()
+    L.bs_timeline_read.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+    L.bs_timeline_read.restype = ctypes.c_int32
+    spans = []
+    g = None
+    if graph:  # both launches captured in one CUDA graph: no host gap between them
+        for layer in (0, 1):
+            bs.split_decode_attention(pool, layer, case.q[layer], btd, ksd, 0, sc, o, m, l, ws)
+        torch.cuda.synchronize()
+        s_ = torch.cuda.Stream()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s_):
+            for layer in (0, 1):
+                bs.split_decode_attention(pool, layer, case.q[layer], btd, ksd, 0, sc, o, m, l, ws)
+    for _ in range(reps):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        assert L.bs_timeline_reset() == 0
+        if g is not None:
+            g.replay()   # the captured launches keep the rows they were captured with
+        else:
+            for layer in (0, 1):
+                bs.split_decode_attention(pool, layer, case.q[layer], btd, ksd, 0, sc, o, m, l, ws)
+        info = bs.attention_last_launch()
+        torch.cuda.synchronize()
+        buf = np.zeros((KT, KC), dtype=np.uint64)
+        assert L.bs_timeline_read(buf.ctypes.data, buf.nbytes) == 0
+        a, b2 = buf[: KT // 2], buf[KT // 2:]
+        a = a[a[:, 4] > 0].astype(np.int64)
+        b2 = b2[b2[:, 4] > 0].astype(np.int64)
+        t0 = a[:, 0].min()
+        rel = lambda x: (x - t0) / 1e3  # noqa: E731
+        r = {"case": name, "pdl": info["pdl"], "cluster": info["cluster"], "ranges": info["ranges"],
+             "ctas": [int(len(a)), int(len(b2))],
+             "A_exit": q(rel(a[:, 4])), "B_entry": q(rel(b2[:, 0])),
+             "B_wait_return": q(rel(b2[:, 6][b2[:, 6] > 0])) if (b2[:, 6] > 0).any() else {},
+             "B_first_data": q(rel(b2[:, 1][b2[:, 1] > 0])), "B_loop_done": q(rel(b2[:, 2])),
+             "B_exit": q(rel(b2[:, 4])), "pair_span_us": round(float(rel(b2[:, 4]).max()), 2),
+             "graph": graph}
+        spans.append(r)
+    spans.sort(key=lambda r: r["pair_span_us"])
+    return spans[len(spans) // 2]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--case", action="append")
     ap.add_argument("--json")
+    ap.add_argument("--pdl-pair", action="store_true",
+                    help="two back-to-back launches per case (set BS_ATTN_PDL=0/1 outside)")
     ap.add_argument("--ragged-bps", type=int, action="append",
                     help="also run the fused local path over a ragged plan (0 = automatic range)")
     args = ap.parse_args()
     res = []
+    if args.pdl_pair:
+        for c in args.case or ["C3_gqa4_B1_8192"]:
+            for graph in (False, True):
+                r = pdl_pair(c, graph=graph)
+                print(json.dumps(r), flush=True)
+                res.append(r)
+        if args.json:
+            with open(args.json, "w") as f:
+                json.dump(res, f, indent=1)
+        return
     for c in args.case or ["C3_gqa4_B1_8192", "C3_gqa4_B8_8192", "C2_mha_B64_2048"]:
         for rb in [None] + (args.ragged_bps or []):
             r = run(c, ragged_bps=rb)

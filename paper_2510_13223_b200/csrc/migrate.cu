@@ -41,6 +41,35 @@ __device__ __forceinline__ void st_stream(int4* p, const int4& v) {
                : "memory");
 }
 
+// Cache-policy experiment (BS_COPY_HINT): 0 default stores; 1 streaming
+// stores (st.global.cs: evict-first); 2 loads and stores with an L2 evict_first policy.
+// The hand-off's 100 MB of writes per layer otherwise sit dirty in L2 and are written back
+// while the next layer's attention streams its reads (read/write interference, §7).
+__device__ __forceinline__ int4 ld_stream_hint(const int4* p, int hint, uint64_t pol) {
+  if (hint == 2) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(pol));
+    return r;
+  }
+  return ld_stream(p);
+}
+
+__device__ __forceinline__ void st_stream_hint(int4* p, const int4& v, int hint, uint64_t pol) {
+  if (hint == 1) {
+    asm volatile("st.global.cs.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+  } else if (hint == 2) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.s32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p),
+                 "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+                 : "memory");
+  } else {
+    st_stream(p, v);
+  }
+}
+
 // The page loop of the vec16 copy for CTA `cta` of `nctas` (shared by the plain copy and
 // the fused copy + append launch).
 template <int PAGE_BYTES, int U>
@@ -50,8 +79,11 @@ __device__ __forceinline__ void copy_pages_body(const uint8_t* __restrict__ src_
                                                 const int32_t* __restrict__ dst_ids, int32_t n,
                                                 int32_t pages_per_chunk, int64_t chunk_bytes,
                                                 int32_t n_layers, int64_t src_layer_stride,
-                                                int64_t dst_layer_stride, int cta, int nctas) {
+                                                int64_t dst_layer_stride, int cta, int nctas,
+                                                int hint = 0) {
   constexpr int V = PAGE_BYTES / (16 * 32);  // int4 per lane per page
+  uint64_t pol = 0;
+  if (hint == 2) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   const int lane = threadIdx.x & 31;
   const int wpc = blockDim.x >> 5;
   const int64_t per_layer = (int64_t)n * pages_per_chunk;
@@ -77,14 +109,14 @@ __device__ __forceinline__ void copy_pages_body(const uint8_t* __restrict__ src_
         dst[u] = reinterpret_cast<int4*>(dst_base + ly * dst_layer_stride + di * chunk_bytes +
                                          (int64_t)j * PAGE_BYTES) + lane;
 #pragma unroll
-        for (int v = 0; v < V; ++v) r[u][v] = ld_stream(s + v * 32);
+        for (int v = 0; v < V; ++v) r[u][v] = ld_stream_hint(s + v * 32, hint, pol);
       }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (dst[u])
 #pragma unroll
-        for (int v = 0; v < V; ++v) st_stream(dst[u] + v * 32, r[u][v]);
+        for (int v = 0; v < V; ++v) st_stream_hint(dst[u] + v * 32, r[u][v], hint, pol);
   }
 }
 
@@ -122,14 +154,16 @@ __global__ void __launch_bounds__(256) migrate_append_vec16(const uint8_t* __res
                                                             uint8_t* __restrict__ dst_base,
                                                             const int32_t* __restrict__ dst_ids,
                                                             int32_t n, int32_t pages_per_chunk,
-                                                            int64_t chunk_bytes, const AppendArgs a) {
+                                                            int64_t chunk_bytes, const AppendArgs a,
+                                                            int hint) {
   if ((int)blockIdx.x < a.batch) {
     append_token_rows(a.layer_base, a.chunk_bytes, a.hkv, a.d, a.k_new, a.v_new, a.bt, a.max_blocks,
                       a.pos, blockIdx.x, threadIdx.x, blockDim.x);
     return;
   }
   copy_pages_body<PAGE_BYTES, U>(src_base, src_ids, dst_base, dst_ids, n, pages_per_chunk,
-                                 chunk_bytes, 1, 0, 0, blockIdx.x - a.batch, gridDim.x - a.batch);
+                                 chunk_bytes, 1, 0, 0, blockIdx.x - a.batch, gridDim.x - a.batch,
+                                 hint);
 }
 
 // NEXT F2: head-granular pages (K and V of n_heads kv-heads of each pair), between pools
@@ -430,12 +464,16 @@ bs_status bs_kv_migrate_append_layer(const bs_kv_pool* src, bs_kv_pool* dst, int
   if (cap > 0) grid = std::min<int64_t>(grid, cap);
   const uint8_t* sb = src->base + (size_t)layer * src->layer_bytes;
   uint8_t* db = dst->base + (size_t)layer * dst->layer_bytes;
+  static const int hint = [] {
+    const char* e = getenv("BS_COPY_HINT");
+    return e ? atoi(e) : 0;
+  }();
   if (src->page_bytes == 4096)
     bs::migrate_append_vec16<4096, 2><<<(unsigned)(grid + batch), 256, 0, s>>>(
-        sb, src_ids, db, dst_ids, n, ppc, (int64_t)src->chunk_bytes, a);
+        sb, src_ids, db, dst_ids, n, ppc, (int64_t)src->chunk_bytes, a, hint);
   else
     bs::migrate_append_vec16<2048, 2><<<(unsigned)(grid + batch), 256, 0, s>>>(
-        sb, src_ids, db, dst_ids, n, ppc, (int64_t)src->chunk_bytes, a);
+        sb, src_ids, db, dst_ids, n, ppc, (int64_t)src->chunk_bytes, a, hint);
   return bs::check_launch("migrate_append_vec16");
 }
 

@@ -66,7 +66,8 @@ class CudaExec:
         ev.record(s)
 
     def wait(self, s, ev):
-        s.wait_event(ev)
+        if ev is not None:   # None: nothing to wait for (e.g. inputs covered by an earlier wait)
+            s.wait_event(ev)
 
     def begin(self):
         cur = torch.cuda.current_stream()

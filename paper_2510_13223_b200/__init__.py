@@ -87,7 +87,7 @@ def lib():
         "bs_abi_version": ([], _i32),
         "bs_debug_build": ([], _i32),
         "bs_debug_error_code": ([_i32], _i32),
-        "bs_attention_last_launch": ([_p, _p, _p, _p], _i32),
+        "bs_attention_last_launch": ([_p, _p, _p, _p, _p], _i32),
         "bs_kv_pool_bytes": ([ctypes.POINTER(_Desc)], _sz),
         "bs_kv_chunk_bytes": ([ctypes.POINTER(_Desc)], _sz),
         "bs_kv_pool_create": ([ctypes.POINTER(_Desc), _p, ctypes.POINTER(_p)], _i32),
@@ -355,10 +355,11 @@ def split_decode_attention(pool: KVPool, layer: int, q: torch.Tensor, block_tabl
 
 def attention_last_launch() -> dict:
     """What this thread's most recent attention launch ran (bs_attention_last_launch):
-    grid.x ranges, cluster merge, programmatic dependent launch, tensor-core kernel."""
-    v = [ctypes.c_int32() for _ in range(4)]
+    grid.x ranges, cluster merge, programmatic dependent launch, tensor-core kernel, K/V
+    stages per warp."""
+    v = [ctypes.c_int32() for _ in range(5)]
     _check(lib().bs_attention_last_launch(*[ctypes.byref(x) for x in v]))
-    return dict(zip(("ranges", "cluster", "pdl", "tensor_cores"), (int(x.value) for x in v)))
+    return dict(zip(("ranges", "cluster", "pdl", "tensor_cores", "stages"), (int(x.value) for x in v)))
 
 
 def split_decode_attention_local_workspace_size(pools, max_blocks, batch: int,

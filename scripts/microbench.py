@@ -63,7 +63,7 @@ def attn_case(name, shape, lens, iters=20, warm=5, seed=1):
 L2_BYTES = 126 * 2**20
 
 
-def attn_case_graph(name, shape, lens, iters=40, seed=1):
+def attn_case_graph(name, shape, lens, iters=40, seed=1, step_flags=False):
     """Device time of back-to-back launches without host overhead: ``iters`` launches are
     captured into one CUDA graph (per-launch time = replay time / iters), cycling over
     enough layers that the KV they read (>= 3x L2) cannot be served from L2.  Small
@@ -92,10 +92,19 @@ def attn_case_graph(name, shape, lens, iters=40, seed=1):
             bs.split_decode_attention(pool, x, case.q[x], btd, ksd, 0, sc, o, m, l, ws, stream=s)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
+    if step_flags:   # a decode step's layers: the fused local path, launches after the first
+        ob = torch.empty(B, shape.hq, shape.d, dtype=torch.bfloat16, device=dev)   # flagged
+        wsl = torch.zeros(max(16, bs.split_decode_attention_local_workspace_size(
+            [pool], [bt.shape[1]], B, shape.hq)), dtype=torch.uint8, device=dev)
     with torch.cuda.graph(g, stream=s):
         for i in range(iters):
             x = i % nl
-            bs.split_decode_attention(pool, x, case.q[x], btd, ksd, 0, sc, o, m, l, ws, stream=s)
+            if step_flags:
+                bs.split_decode_attention_local([pool], x, case.q[x], [btd], [0], ksd, sc, ob, l, wsl,
+                                                stream=s, flags=bs.ATTN_PDL if i else 0)
+            else:
+                bs.split_decode_attention(pool, x, case.q[x], btd, ksd, 0, sc, o, m, l, ws, stream=s)
+    info = bs.attention_last_launch()
     for _ in range(3):
         g.replay()
     torch.cuda.synchronize()
@@ -110,7 +119,8 @@ def attn_case_graph(name, shape, lens, iters=40, seed=1):
     med = sorted(ts)[len(ts) // 2]
     alg = kv + B * shape.hq * shape.d * 2 + B * shape.hq * (shape.d + 2) * 4 + 4 * int(
         sum(synth.ceil_div(int(x), 16) for x in lens))
-    return {"case": name, "timing": "graph", "B": B, "G": shape.group, "tokens": int(lens.sum()),
+    return {"case": name, "timing": "graph" + ("_step_flags" if step_flags else ""), "B": B,
+            "G": shape.group, "tokens": int(lens.sum()), "launch": info,
             "layers_cycled": nl, "us": round(med * 1e3, 2),
             "GBps": round(alg / (med * 1e-3) / 1e9, 1), "bytes": alg}
 
@@ -424,6 +434,9 @@ def main():
                     help="extra ragged-plan range lengths to time")
     ap.add_argument("--graph", action="store_true",
                     help="attention: time graph-captured back-to-back launches over >= 3x L2 of KV")
+    ap.add_argument("--step-flags", action="store_true",
+                    help="--graph through the fused local path with the BS_ATTN_PDL flag on every "
+                         "launch after the first (the production policy of a decode step)")
     ap.add_argument("--seeds", type=int, default=1,
                     help="repeat every attention case over seeds 0..n-1 (block placement and "
                          "values; C4 also its lengths) and report mean / spread")
@@ -434,7 +447,7 @@ def main():
             if args.case and args.case != name:
                 continue
             if args.graph:
-                r = attn_case_graph(name, shape, lens)
+                r = attn_case_graph(name, shape, lens, step_flags=args.step_flags)
             elif args.seeds <= 1:
                 r = attn_case(name, shape, lens, iters=args.iters)
             else:

@@ -125,6 +125,7 @@ def test_c3_per_gpu_shard_cluster(bs, B):
     o2, l2, _ = local_run(bs, pools, bts, ksd, case.q[0], sc, 0)
     o3, l3, _ = local_run(bs, pools, bts, ksd, case.q[0], sc, bs.ATTN_NO_CLUSTER)
     cl_max = int(os.environ.get("BS_ATTN_CLUSTER_MAX", "8"))
+    assert info["stages"] == 2 and info["pdl"] == 0, info   # no PDL flag: 2-stage ring
     if B == 1:
         assert info["ranges"] == 16, info
     assert info["cluster"] == (1 if info["ranges"] <= cl_max else 0), info
@@ -213,3 +214,51 @@ def test_sixteen_cta_clusters_subprocess():
                        text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "9 passed" in r.stdout, r.stdout[-2000:]
+
+
+_DUMP = """
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_2510_13223_b200 as bs, synth
+shape = synth.Shape(3, 32, 8, 128)
+lens = np.array([8192, 5000])
+ks = np.stack([np.zeros(2), lens], 1).astype(np.int32)
+case = synth.device_shards(shape, lens, ks, seed=77, device="cuda")
+pools = [bs.KVPool(3, p.shape[1], 8, 128, base=p.reshape(-1)) for p in case.pools]
+bts = [torch.from_numpy(b).cuda() for b in case.block_tables]
+ksd = torch.from_numpy(ks).cuda()
+ws = torch.zeros(max(16, bs.split_decode_attention_local_workspace_size(pools, [bts[0].shape[1]], 2, 32)),
+                 dtype=torch.uint8, device="cuda")
+out = torch.empty(3, 2, 32, 128, dtype=torch.bfloat16, device="cuda")
+lse = torch.empty(3, 2, 32, device="cuda")
+infos = []
+for layer in range(3):
+    bs.split_decode_attention_local(pools, layer, case.q[layer], bts, [0], ksd, synth.default_scale(128),
+                                    out[layer], lse[layer], ws, flags=bs.ATTN_PDL if layer else 0)
+    infos.append(bs.attention_last_launch())
+torch.cuda.synchronize()
+np.savez({path!r}, out=out.view(torch.int16).cpu().numpy(), lse=lse.cpu().numpy(),
+         stages=np.array([i["stages"] for i in infos]), pdl=np.array([i["pdl"] for i in infos]))
+"""
+
+
+def test_deep_ring_variant_bitwise_equals_two_stage(tmp_path):
+    """The one-CTA-per-SM 6-stage variant (PDL launches) changes only how far each warp's
+    TMA ring runs ahead, not which blocks a warp folds in which order: its outputs equal the
+    2-stage kernel's bit for bit (BS_ATTN_DEEP=0, separate processes: the switch is read
+    once)."""
+    import os.path
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for deep in ("1", "0"):
+        path = str(tmp_path / f"deep{deep}.npz")
+        env = dict(os.environ, BS_ATTN_DEEP=deep)
+        r = subprocess.run([sys.executable, "-c", _DUMP.format(root=root, path=path)], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        res[deep] = np.load(path)
+    # layer 0 (no PDL flag) runs the 2-stage ring, the PDL layers the 6-stage one
+    assert list(res["1"]["stages"]) == [2, 6, 6] and list(res["0"]["stages"]) == [2, 2, 2]
+    assert list(res["1"]["pdl"]) == [0, 1, 1]
+    assert np.array_equal(res["1"]["out"], res["0"]["out"])
+    assert np.array_equal(res["1"]["lse"], res["0"]["lse"])

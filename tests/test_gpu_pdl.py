@@ -78,6 +78,8 @@ def test_pdl_layers_bitwise_equal_plain_and_oracle(bs, graph, name):
     infos.clear()
     o1, l1 = run(bs.ATTN_PDL)
     assert infos and all(i["pdl"] == 1 for i in infos), infos
+    if name == "one_per_sm":   # the 6-stage ring: the prefetch before griddepcontrol.wait
+        assert all(i["stages"] == 6 for i in infos), infos
     assert torch.equal(o0.view(torch.int16), o1.view(torch.int16))
     assert torch.equal(l0, l1)
     for layer in (0, L - 1):

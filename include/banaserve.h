@@ -238,16 +238,17 @@ bs_status bs_split_decode_attention_local(int32_t n_local, const bs_kv_pool* con
                                           const int32_t* kv_split, int32_t n_shards, float scale,
                                           void* out, float* lse, void* workspace,
                                           size_t workspace_bytes, void* stream);
-/* The same with launch flags.  BS_ATTN_PDL: when the launch has more CTAs than one wave,
- * or at most one CTA per SM, it is a programmatic dependent launch -- it may start while the
- * previous kernel on `stream` drains (a previous attention launch lets it start once its own
- * CTAs have started (multi-wave) or finished their main loops (one wave)), reading
+/* The same with launch flags.  BS_ATTN_PDL: a programmatic dependent launch -- it may start
+ * while the previous kernel on `stream` drains (a previous attention launch lets it start once
+ * its own CTAs have started (multi-wave) or finished their main loops (one wave)), reading
  * block_tables / kv_split and prefetching K/V pages before that kernel completes, and
- * q / out / lse / workspace only after (griddepcontrol.wait).
+ * q / out / lse / workspace only after (griddepcontrol.wait).  Applied to multi-wave launches
+ * and to one-wave launches that fit in the CTA slots a same-shaped predecessor leaves free
+ * (at most half the slots); a flagged launch of at most one CTA per SM runs a 6-stage ring.
+ * The flag never changes the range cut: flagged and plain launches are bitwise identical.
  * Caller contract: the kernel launched just before it on `stream` writes neither the pools'
  * pages this call reads, nor block_tables / kv_split (e.g. the previous layer's attention;
- * work from other streams joined by events is waited for in full).  One-wave launches with
- * 2-3 CTAs per SM ignore the flag (measured slower with it). */
+ * work from other streams joined by events is waited for in full).  DESIGN.md §6. */
 #define BS_ATTN_PDL 1u
 /* BS_ATTN_NO_CLUSTER: never use the cluster merge.  By default a launch whose CTAs fit one
  * wave and whose (request, kv-head) is cut into 2..16 ranges runs each (request, kv-head)'s

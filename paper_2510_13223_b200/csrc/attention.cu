@@ -1624,11 +1624,13 @@ bs_status run_attention(const LaunchArgs& a) {
     const int64_t slots = (int64_t)bs::sm_count(bs::current_device()) * bs::variant_for(d, G).minb;
     const int env = bs::pdl_env();
     // PDL pays for multi-wave grids (the next grid fills the last wave's tail) and for
-    // grids of at most one CTA per SM (C3 B=1: its prologue and first stages overlap the
-    // previous grid's epilogue, 11.9 -> 10.8 us); a one-wave grid of 2-3 CTAs per SM that
-    // starts early is placed unevenly over the SMs and loses its tail (C3 B=8 42.9 -> 44.9)
+    // one-wave grids that fit in the slots their predecessor (the same problem) leaves free
+    // (C3 B=1: its prologue and first stages overlap the previous grid's epilogue, 11.9 ->
+    // 10.8 us); a one-wave grid that does not fit starts partly early, partly late, spreads
+    // unevenly over the SMs and loses its tail (C3 B=8 at 256 CTAs: 42.9 -> 44.9 us).  The
+    // flag never changes the range cut: flagged and plain launches are bitwise identical.
     const int64_t sms = bs::sm_count(bs::current_device());
-    p.pdl = env >= 0 ? env : ((a.flags & BS_ATTN_PDL) && (ctas > slots || ctas <= sms) ? 1 : 0);
+    p.pdl = env >= 0 ? env : ((a.flags & BS_ATTN_PDL) && (ctas > slots || 2 * ctas <= slots) ? 1 : 0);
     p.trig_late = ctas <= slots ? 1 : 0;
     // ... and, for such a PDL launch of at most one CTA per SM, 6 K/V stages per warp: it
     // prefetches 24 of a 32-block range before the wait (C3 B=1 10.8 -> 9.9 us; without PDL

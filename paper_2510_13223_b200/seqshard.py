@@ -272,8 +272,19 @@ class SeqShardedStep:
                     "workspace": P["ws"] + layer * P["ws_stride"], "workspace_bytes": P["ws_stride"],
                     "done": P["done"] + 4 * layer, "cross_device": not solo})
             with torch.cuda.stream(compute):
-                self.ops.attention_tasks(problems, [(self.pool, self.bt_h[h], r, h) for h in range(W)],
-                                         layer, self.Bh, self.hq)
+                if solo and hasattr(self.ops, "attention_local"):
+                    # W = 1: one local problem -- the fused local path, whose launches of
+                    # layers > 0 are programmatic dependents of the previous layer's and
+                    # may merge through a thread-block cluster
+                    if getattr(self, "_solo_ws", None) is None:
+                        self._solo_ws = self.ops.local_workspace([self.pool], [self.bt_h[0]], self.Bh,
+                                                                 self.hq, self.out_buf.device)
+                    self.ops.attention_local([self.pool], layer, problems[0]["q"], [self.bt_h[0]], [0],
+                                             self.ks_h[0], self.out_buf[layer], self.lse_buf[layer],
+                                             self._solo_ws, pdl=layer > 0)
+                else:
+                    self.ops.attention_tasks(problems, [(self.pool, self.bt_h[h], r, h) for h in range(W)],
+                                             layer, self.Bh, self.hq)
             if timers is not None:
                 timers[layer][1].record(compute)
             self.part_ready[layer].record(compute)

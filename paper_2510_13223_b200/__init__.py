@@ -586,8 +586,19 @@ def kv_sendrecv_layer(comm: Comm, src: KVPool, src_ids: torch.Tensor, send_peer:
         _dptr(recv_staging), layer, _stream(stream)))
 
 
+def _expandable_segments() -> bool:
+    conf = os.environ.get("PYTORCH_CUDA_ALLOC_CONF", "") + "," + os.environ.get("PYTORCH_ALLOC_CONF", "")
+    return any(x.replace(" ", "").lower() == "expandable_segments:true" for x in conf.split(","))
+
+
 def ipc_export(t: torch.Tensor):
-    """(handle bytes, offset) naming ``t``'s device memory for another process."""
+    """(handle bytes, offset) naming ``t``'s device memory for another process.  Needs memory
+    from cudaMalloc: torch's expandable segments (virtual-memory mappings) cannot be exported
+    with cudaIpcGetMemHandle, so that allocator mode is refused up front."""
+    if _expandable_segments():
+        raise BSError(BS_ERR_UNSUPPORTED, "ipc_export: PYTORCH_CUDA_ALLOC_CONF has expandable_segments:True -- its "
+                      "virtual-memory segments cannot be IPC-exported; the P2P transport needs the "
+                      "default caching allocator (or use the NCCL transport)")
     n = lib().bs_ipc_handle_bytes()
     buf = ctypes.create_string_buffer(n)
     off = _sz()

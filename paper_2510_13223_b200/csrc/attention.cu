@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <atomic>
 #include <mutex>
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 #include <vector>
@@ -1488,6 +1489,13 @@ static const CUtensorMap* pool_tensor_map(const bs_kv_pool* cpool) {
         pool->tmap_state = 1;
     }
     cudaGetLastError();
+    if (pool->tmap_state != 1 && !pool->host && !getenv("BS_QUIET"))
+      // not silent: the CUDA-core kernel (correct, slower at G >= 4) serves this pool; the
+      // launch is also visible as tensor_cores = 0 in bs_attention_last_launch
+      fprintf(stderr,
+              "banaserve: no TMA tensor map for a pool (%llu rows%s); its attention launches use "
+              "the CUDA-core kernel\n",
+              (unsigned long long)rows, enc ? "" : ", cuTensorMapEncodeTiled unavailable");
   }
   return pool->tmap_state == 1 ? &pool->tmap : nullptr;
 }

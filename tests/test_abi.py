@@ -203,3 +203,16 @@ def test_package_data_plane_has_no_torch_collectives():
     for f in glob.glob(os.path.join(pkg, "*.py")):
         src = open(f).read()
         assert not bad.search(src), f
+
+
+def test_ipc_export_refuses_expandable_segments(monkeypatch):
+    """torch's expandable segments are virtual-memory mappings cudaIpcGetMemHandle cannot
+    export: the P2P transport's ipc_export refuses that allocator mode with a clear error
+    (before any CUDA call, so this runs on CPU)."""
+    import torch
+    import paper_2510_13223_b200 as bs
+    monkeypatch.setenv("PYTORCH_CUDA_ALLOC_CONF", "max_split_size_mb:64,expandable_segments:True")
+    with pytest.raises(bs.BSError, match="expandable_segments"):
+        bs.ipc_export(torch.zeros(4))
+    monkeypatch.setenv("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:False")
+    assert not bs._expandable_segments()

@@ -291,6 +291,14 @@ bs_status bs_split_decode_attention_local_ragged(
     const int32_t* shard_ids, const int32_t* kv_split, int32_t n_shards, float scale,
     const int32_t* work, int32_t n_work, int32_t max_parts, void* out, float* lse, void* workspace,
     size_t workspace_bytes, void* stream);
+/* The same with launch flags (BS_ATTN_PDL as for bs_split_decode_attention_local_ex, same
+ * caller contract; a ragged plan never uses the cluster merge). */
+bs_status bs_split_decode_attention_local_ragged_ex(
+    int32_t n_local, const bs_kv_pool* const* pools, int32_t layer, const void* q, int32_t batch,
+    int32_t num_q_heads, const int32_t* const* block_tables, const int32_t* max_blocks,
+    const int32_t* shard_ids, const int32_t* kv_split, int32_t n_shards, float scale,
+    const int32_t* work, int32_t n_work, int32_t max_parts, void* out, float* lse, void* workspace,
+    size_t workspace_bytes, uint32_t flags, void* stream);
 
 /* H4 + H5 + H6 fused across GPUs ("fused B200 variant"; PAPER.md:220,
  * :233-237): an attention PROBLEM is a batch of requests whose KV shards may live on

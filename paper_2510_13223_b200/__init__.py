@@ -42,6 +42,7 @@ EXPORTED_SYMBOLS = (
     "bs_debug_build", "bs_debug_error_code", "bs_kv_append_token", "bs_exchange",
     "bs_signals_epoch", "bs_wait_signals_epoch", "bs_epoch_advance", "bs_kv_migrate_append_layer",
     "bs_split_decode_attention_local_ex", "bs_attention_last_launch",
+    "bs_split_decode_attention_local_ragged_ex",
 )
 
 
@@ -142,6 +143,9 @@ def lib():
         "bs_split_decode_attention_local_ragged": ([_i32, _p, _i32, _p, _i32, _i32, _p, _p, _p, _p,
                                                     _i32, _f32, _p, _i32, _i32, _p, _p, _p, _sz,
                                                     _p], _i32),
+        "bs_split_decode_attention_local_ragged_ex": ([_i32, _p, _i32, _p, _i32, _i32, _p, _p, _p,
+                                                       _p, _i32, _f32, _p, _i32, _i32, _p, _p, _p,
+                                                       _sz, ctypes.c_uint32, _p], _i32),
         "bs_split_decode_attention_local_workspace_size": ([_i32, _p, _p, _i32, _i32,
                                                             ctypes.POINTER(_sz)], _i32),
         "bs_split_decode_attention_local": ([_i32, _p, _i32, _p, _i32, _i32, _p, _p, _p, _p, _i32,
@@ -486,8 +490,10 @@ def attention_ragged_plan(kv_split_host, shard_ids, num_q_heads: int, num_kv_hea
 def split_decode_attention_local_ragged(pools, layer: int, q: torch.Tensor, block_tables,
                                         shard_ids, kv_split: torch.Tensor, scale: float,
                                         plan: RaggedPlan, out: torch.Tensor, lse: torch.Tensor,
-                                        workspace: torch.Tensor | None = None, stream=None) -> None:
-    """H4+H6 fused over local shards, CTAs from a ragged plan (``plan.to(device)`` first)."""
+                                        workspace: torch.Tensor | None = None, stream=None,
+                                        flags: int = 0) -> None:
+    """H4+H6 fused over local shards, CTAs from a ragged plan (``plan.to(device)`` first).
+    ``flags``: ATTN_PDL (bs_split_decode_attention_local_ragged_ex)."""
     n = len(pools)
     B, hq, d = q.shape
     pa = (ctypes.c_void_p * n)(*[p.handle.value for p in pools])
@@ -495,12 +501,12 @@ def split_decode_attention_local_ragged(pools, layer: int, q: torch.Tensor, bloc
     mb = (ctypes.c_int32 * n)(*[int(t.shape[1]) for t in block_tables])
     sa = (ctypes.c_int32 * n)(*[int(x) for x in shard_ids])
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
-    _check(lib().bs_split_decode_attention_local_ragged(
+    _check(lib().bs_split_decode_attention_local_ragged_ex(
         n, pa, layer, _dptr(q, torch.bfloat16), B, hq, ba, mb, sa, _dptr(kv_split, torch.int32),
         kv_split.shape[1] - 1, float(scale), _dptr(plan.device_work, torch.int32), plan.n_work,
         plan.max_parts, _dptr(out, torch.bfloat16),
         _dptr(lse, torch.float32) if lse is not None else None, _dptr(workspace), ws_bytes,
-        _stream(stream)))
+        int(flags), _stream(stream)))
 
 
 def merge_partials(o_parts, m_parts, l_parts, out: torch.Tensor, lse: torch.Tensor | None = None,

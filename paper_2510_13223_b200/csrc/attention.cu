@@ -2141,6 +2141,20 @@ bs_status bs_split_decode_attention_local_ragged(
     const int32_t* shard_ids, const int32_t* kv_split, int32_t n_shards, float scale,
     const int32_t* work, int32_t n_work, int32_t max_parts, void* out, float* lse, void* workspace,
     size_t workspace_bytes, void* stream) {
+  return bs_split_decode_attention_local_ragged_ex(n_local, pools, layer, q, batch, num_q_heads,
+                                                   block_tables, max_blocks, shard_ids, kv_split,
+                                                   n_shards, scale, work, n_work, max_parts, out,
+                                                   lse, workspace, workspace_bytes, 0u, stream);
+}
+
+bs_status bs_split_decode_attention_local_ragged_ex(
+    int32_t n_local, const bs_kv_pool* const* pools, int32_t layer, const void* q, int32_t batch,
+    int32_t num_q_heads, const int32_t* const* block_tables, const int32_t* max_blocks,
+    const int32_t* shard_ids, const int32_t* kv_split, int32_t n_shards, float scale,
+    const int32_t* work, int32_t n_work, int32_t max_parts, void* out, float* lse, void* workspace,
+    size_t workspace_bytes, uint32_t flags, void* stream) {
+  BS_REQUIRE((flags & ~(BS_ATTN_PDL | BS_ATTN_NO_CLUSTER)) == 0,
+             "bs_split_decode_attention_local_ragged: unknown flags 0x%x", flags);
   BS_REQUIRE(pools && block_tables && max_blocks && shard_ids && work,
              "bs_split_decode_attention_local_ragged: NULL array");
   BS_REQUIRE(n_local >= 1 && n_local <= bs::kMaxLocal, "bs_split_decode_attention_local_ragged: %d shards",
@@ -2173,6 +2187,7 @@ bs_status bs_split_decode_attention_local_ragged(
   a.work = work;
   a.n_work = n_work;
   a.max_parts = max_parts;
+  a.flags = flags;
   return run_attention(a);
 }
 

@@ -71,8 +71,11 @@ def main():
                 with torch.cuda.stream(comp_s):
                     if mig:
                         comp_s.wait_event(ev[layer])
+                    # layers > 0: programmatic dependents of the previous layer's launch
+                    # (the hand-off writes are joined by the event, not stream order)
                     bs.split_decode_attention_local_ragged([pool], layer, case.q[layer], [btd], [0], ksd,
-                                                           sc, plan, out, lse, ws, stream=comp_s)
+                                                           sc, plan, out, lse, ws, stream=comp_s,
+                                                           flags=bs.ATTN_PDL if layer else 0)
 
     def timed(**kw):
         for _ in range(3):

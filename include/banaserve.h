@@ -63,11 +63,13 @@ int32_t bs_debug_error_code(int32_t reset);
 
 /* Diagnostics: what the calling thread's most recent attention launch (any
  * bs_split_decode_attention* call that launched) ran -- grid.x CTA ranges (uniform plan:
- * ranges per (request, kv-head) over the launch's shards; ragged plan: work items), whether
- * it used the cluster merge and programmatic dependent launch, the tensor-core (1) or
- * CUDA-core (0) kernel, and its K/V stages per warp (6: the one-CTA-per-SM variant).  All 0
- * before the first launch. */
-bs_status bs_attention_last_launch(int32_t* ranges, int32_t* cluster, int32_t* pdl,
+ * ranges per (request, kv-head) over the launch's shards; ragged plan: work items), how the
+ * ranges were merged (0 one range, nothing to merge; 1 last-arriving CTA through the
+ * workspace; 2 thread-block cluster through distributed shared memory), whether it was a
+ * programmatic dependent launch, the
+ * tensor-core (1) or CUDA-core (0) kernel, and its K/V stages per warp (6: the
+ * one-CTA-per-SM variant).  All 0 before the first launch. */
+bs_status bs_attention_last_launch(int32_t* ranges, int32_t* merge, int32_t* pdl,
                                    int32_t* tensor_cores, int32_t* stages);
 
 /* ------------------------------------------------------------------------------ */

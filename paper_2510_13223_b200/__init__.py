@@ -359,11 +359,13 @@ def split_decode_attention(pool: KVPool, layer: int, q: torch.Tensor, block_tabl
 
 def attention_last_launch() -> dict:
     """What this thread's most recent attention launch ran (bs_attention_last_launch):
-    grid.x ranges, cluster merge, programmatic dependent launch, tensor-core kernel, K/V
-    stages per warp."""
+    grid.x ranges, merge kind (MERGE_*; ``cluster`` = 1 for the cluster merge), programmatic
+    dependent launch, tensor-core kernel, K/V stages per warp."""
     v = [ctypes.c_int32() for _ in range(5)]
     _check(lib().bs_attention_last_launch(*[ctypes.byref(x) for x in v]))
-    return dict(zip(("ranges", "cluster", "pdl", "tensor_cores", "stages"), (int(x.value) for x in v)))
+    r = dict(zip(("ranges", "merge", "pdl", "tensor_cores", "stages"), (int(x.value) for x in v)))
+    r["cluster"] = int(r["merge"] == MERGE_CLUSTER)
+    return r
 
 
 def split_decode_attention_local_workspace_size(pools, max_blocks, batch: int,
@@ -379,6 +381,7 @@ def split_decode_attention_local_workspace_size(pools, max_blocks, batch: int,
 
 ATTN_PDL = 1   # bs_split_decode_attention_local_ex flags (see the header's contract)
 ATTN_NO_CLUSTER = 2
+MERGE_NONE, MERGE_LAST_ARRIVER, MERGE_CLUSTER = 0, 1, 2   # attention_last_launch()["merge"]
 
 
 def split_decode_attention_local(pools, layer: int, q: torch.Tensor, block_tables,

@@ -1319,8 +1319,12 @@ bs_status launch_pdl(void (*kern)(KArgs...), dim3 grid, int smem, cudaStream_t s
 
 // What the calling thread's last attention launch ran (bs_attention_last_launch).
 struct LaunchInfo {
-  int32_t ranges, cluster, pdl, tensor_cores, stages;
+  int32_t ranges, merge, pdl, tensor_cores, stages;  // merge: 0 none, 1 last arriver, 2 cluster
 };
+int32_t merge_kind(const AttnParams& p) {
+  if (p.pb[0].nsplit < 2) return 0;  // one range (or one per request, ragged): no merge
+  return p.cl ? 2 : 1;
+}
 thread_local LaunchInfo g_last_launch{0, 0, 0, 0, 0};
 
 int cluster_env() {  // A/B switch BS_ATTN_CLUSTER: 0 never, 1 single-wave launches, 2 always
@@ -1357,7 +1361,7 @@ bs_status launch_attn_v(const AttnParams& p, int batch, cudaStream_t stream) {
     configured.fetch_or(bit);
   }
   const dim3 grid = p.work ? dim3(p.grid_x * p.hkv, 1, 1) : dim3(p.grid_x, p.hkv, batch);
-  g_last_launch = LaunchInfo{p.grid_x, 0, p.pdl, 0, STAGES};
+  g_last_launch = LaunchInfo{p.grid_x, merge_kind(p), p.pdl, 0, STAGES};
   if (p.pdl) return launch_pdl(split_decode_attn<D, G, STAGES, MINB>, grid, S::kTotal, stream,
                                "split_decode_attn", p);
   split_decode_attn<D, G, STAGES, MINB><<<grid, kWarps * 32, S::kTotal, stream>>>(p);
@@ -1415,7 +1419,7 @@ bs_status launch_attn_mma(const AttnParams& p_in, const TMaps& tm, int batch, cu
       p.cl = 0;
   }
   const dim3 grid = p.work ? dim3(p.grid_x * p.hkv, 1, 1) : dim3(p.grid_x, p.hkv, batch);
-  g_last_launch = LaunchInfo{p.grid_x, p.cl, p.pdl, 1, STAGES};
+  g_last_launch = LaunchInfo{p.grid_x, merge_kind(p), p.pdl, 1, STAGES};
   if (p.pdl || p.cl)
     return launch_ex(split_decode_attn_mma<D, G, STAGES, MINB>, grid, S::kTotal, stream, p.pdl != 0,
                      p.cl ? p.grid_x : 1, "split_decode_attn_mma", p, tm);
@@ -1718,13 +1722,13 @@ bs_status bs_timeline_reset(void) {
 }
 #endif
 
-bs_status bs_attention_last_launch(int32_t* ranges, int32_t* cluster, int32_t* pdl,
+bs_status bs_attention_last_launch(int32_t* ranges, int32_t* merge, int32_t* pdl,
                                    int32_t* tensor_cores, int32_t* stages) {
-  BS_REQUIRE(ranges && cluster && pdl && tensor_cores && stages,
+  BS_REQUIRE(ranges && merge && pdl && tensor_cores && stages,
              "bs_attention_last_launch: NULL argument");
   const bs::LaunchInfo& i = bs::g_last_launch;
   *ranges = i.ranges;
-  *cluster = i.cluster;
+  *merge = i.merge;
   *pdl = i.pdl;
   *tensor_cores = i.tensor_cores;
   *stages = i.stages;

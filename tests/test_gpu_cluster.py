@@ -262,3 +262,4 @@ def test_deep_ring_variant_bitwise_equals_two_stage(tmp_path):
     assert list(res["1"]["pdl"]) == [0, 1, 1]
     assert np.array_equal(res["1"]["out"], res["0"]["out"])
     assert np.array_equal(res["1"]["lse"], res["0"]["lse"])
+

@@ -43,7 +43,7 @@ def timed(fn, iters=10, warm=3):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--requests", type=int, default=4)
-    ap.add_argument("--engine", choices=["ce", "sm"], default="ce")
+    ap.add_argument("--engine", choices=["staged", "ce", "sm"], default="staged")
     ap.add_argument("--json")
     args = ap.parse_args()
     dev = torch.device("cuda")
@@ -89,10 +89,15 @@ def main():
             torch.cuda.current_stream().wait_stream(side)
         return run
 
-    t_fetch = timed(on_side(lambda: [store.fetch_layer(pool, x, f_store, f_dev, engine=eng)
-                                     for x in range(L)])) / L
-    t_store = timed(on_side(lambda: [store.store_layer(pool, x, s_dev, s_store, engine=eng)
-                                     for x in range(L)])) / L
+    if eng == "staged":
+        fsp, ssp = store.prepare(pool, f_store, f_dev), store.prepare(pool, s_store, s_dev)
+        t_fetch = timed(on_side(lambda: [store.fetch_staged(pool, x, fsp) for x in range(L)])) / L
+        t_store = timed(on_side(lambda: [store.store_staged(pool, x, ssp) for x in range(L)])) / L
+    else:
+        t_fetch = timed(on_side(lambda: [store.fetch_layer(pool, x, f_store, f_dev, engine=eng)
+                                         for x in range(L)])) / L
+        t_store = timed(on_side(lambda: [store.store_layer(pool, x, s_dev, s_store, engine=eng)
+                                         for x in range(L)])) / L
     t_comp = timed(lambda: [compute(x) for x in range(L)]) / L
     pipe = ThreeStagePipeline(store, pool, L, compute, fetch_pairs=(f_store, f_dev),
                               store_pairs=(s_dev, s_store), engine=eng)

@@ -47,7 +47,7 @@ def test_host_pool_needs_pinned_memory(bs):
                                   o, m, m)
 
 
-@pytest.mark.parametrize("engine", ["sm", "ce"])
+@pytest.mark.parametrize("engine", ["sm", "ce", "staged"])
 @pytest.mark.parametrize("d,hkv", [(128, 8), (64, 2)])
 def test_fetch_and_store_bit_exact(bs, d, hkv, engine):
     from paper_2510_13223_b200.kvstore import KVStore
@@ -64,8 +64,14 @@ def test_fetch_and_store_bit_exact(bs, d, hkv, engine):
     stream = torch.cuda.Stream()
     stream.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(stream):
+        if engine == "staged":   # store runs [63] [0] [5..7] [17] [40] -> staging -> scatter
+            fp = store.prepare(dev, list(si), list(di))
+            assert [r[1] for r in fp.runs] == [1, 1, 3, 1, 1]
         for layer in range(3):
-            store.fetch_layer(dev, layer, ids(si), ids(di), engine=engine)
+            if engine == "staged":
+                store.fetch_staged(dev, layer, fp, stream=stream)
+            else:
+                store.fetch_layer(dev, layer, ids(si), ids(di), engine=engine)
     for layer in range(3):
         oracle.migrate_layer(s_np, d_np, layer, si, di)
     torch.cuda.synchronize()
@@ -73,13 +79,16 @@ def test_fetch_and_store_bit_exact(bs, d, hkv, engine):
     # store different device blocks back into free store blocks
     src = np.array([1, 79], dtype=np.int32)
     dst = np.array([10, 11], dtype=np.int32)
-    store.store_layer(dev, 2, ids(src), ids(dst), engine=engine)
+    if engine == "staged":
+        store.store_staged(dev, 2, store.prepare(dev, list(dst), list(src)))
+    else:
+        store.store_layer(dev, 2, ids(src), ids(dst), engine=engine)
     torch.cuda.synchronize()
     oracle.migrate_layer(d_np, s_np, 2, src, dst)
     assert np.array_equal(_u16(store.pool.data), s_np)
 
 
-@pytest.mark.parametrize("engine", ["sm", "ce"])
+@pytest.mark.parametrize("engine", ["sm", "ce", "staged"])
 def test_three_stage_pipeline(bs, engine):
     from paper_2510_13223_b200.kvstore import KVStore, ThreeStagePipeline
     shape = synth.Shape(3, 8, 2, 128)

@@ -478,8 +478,11 @@ class ShardedDecodeStep:
         with ex.use(mig_s):
             if timers is not None:
                 timers[layer][2].record(mig_s)
+            # (layer 0 with host inputs: the hand-off copy needs none of them, so it runs
+            # while they are still in flight and only the append waits -- e2e)
             fused_app = (self.world == 1 and self.append is not None and self.n_handoff > 0
-                         and self.ce_ids is None and hasattr(ops, "migrate_append"))
+                         and self.ce_ids is None and hasattr(ops, "migrate_append")
+                         and not (inputs_ready is not None and layer == 0))
             if fused_app:  # H2 + H7 in one launch (the append needs this layer's inputs)
                 if inputs_ready is not None:
                     ex.wait(mig_s, inputs_ready[layer])

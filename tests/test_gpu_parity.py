@@ -462,6 +462,47 @@ def test_bench_step_c2_sampled():
         assert np.abs(lse[layer, sample].cpu().double().numpy() - ref_lse).max() <= LSE_TOL
 
 
+def test_bench_e2e_step_matches_device_step():
+    """The e2e step bench.py times (each layer's [q_l | decoded-token K/V] copied H2D from
+    pinned memory, the step gated per layer on its own inputs -- layer 0's hand-off copy
+    starting before them, only its append waiting -- and O / lse copied D2H) gives bitwise
+    the outputs of the step over device-resident inputs."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    import paper_2510_13223_b200 as bsm
+    dev = torch.device("cuda", 0)
+    case, pools, step, ks = bench.build_workload(bsm, dev, 0, 1, layers=2)
+    L = 2
+    out_d = torch.empty(case.q.shape, dtype=torch.bfloat16, device=dev)
+    lse_d = torch.empty(case.q.shape[:-1], dtype=torch.float32, device=dev)
+    step.enqueue(case.q, out_d, lse_d)
+    torch.cuda.synchronize()
+    in_host, in_dev, rowb, q_dev, kv_dev = bench._e2e_buffers(case.q, step.append, L, dev)
+    step.append = kv_dev
+    in_dev.zero_()
+    out_h = torch.empty(out_d.shape, dtype=out_d.dtype).pin_memory()
+    lse_h = torch.empty(lse_d.shape, dtype=lse_d.dtype).pin_memory()
+    out_e = torch.full_like(out_d, float("nan"))
+    lse_e = torch.full_like(lse_d, float("nan"))
+    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    evs = [torch.cuda.Event() for _ in range(L)]
+    h2d.wait_stream(torch.cuda.current_stream())
+    for layer in range(L):
+        bsm.copy_ptr(in_dev.data_ptr() + layer * rowb, in_host.data_ptr() + layer * rowb, rowb, stream=h2d)
+        evs[layer].record(h2d)
+    step.enqueue(q_dev, out_e, lse_e, inputs_ready=evs)
+    ob, lb = out_e[0].numel() * 2, lse_e[0].numel() * 4
+    for layer in range(L):
+        d2h.wait_event(step.out_ready[layer])
+        bsm.copy_ptr(out_h.data_ptr() + layer * ob, out_e.data_ptr() + layer * ob, ob, stream=d2h)
+        bsm.copy_ptr(lse_h.data_ptr() + layer * lb, lse_e.data_ptr() + layer * lb, lb, stream=d2h)
+    torch.cuda.synchronize()
+    assert torch.equal(out_h.view(torch.int16), out_d.cpu().view(torch.int16))
+    assert torch.equal(lse_h, lse_d.cpu())
+
+
 def test_bench_step_cuda_graph_replay_matches_eager():
     """The N=1 step captured into one CUDA graph (3 streams, events, all layers) replays
     to the bitwise-identical result of eager execution."""

@@ -1,5 +1,5 @@
 # Diagnostics of the small C3 per-GPU launches (B=1 / B=8 x 8192 tokens, GQA-4): per-CTA
-# timeline (timeline build) and one ncu --set full capture of each.  Usage: bash scripts/diag_c3.sh
+# timeline (timeline build) and one ncu --set full capture of each.  Usage: bash scripts/experiments/c3_timeline_ncu.sh
 mkdir -p gpurun_out/diag
 BS_TIMELINE=1 timeout 300 python scripts/attn_timeline.py --case C3_gqa4_B1_8192 --case C3_gqa4_B8_8192 \
   --json gpurun_out/diag/timeline_c3.json > gpurun_out/diag/timeline.log 2>&1

@@ -1,6 +1,6 @@
 # Experiment: range planner for few-pair problems (BS_ATTN_PLAN 0 = round-1 cost, 1 = the
 # one-wave latency model) and forced cuts (BS_ATTN_NSPLIT); graph-timed, L2-cold, 3
-# interleaved rounds.  Usage: bash scripts/exp_plan.sh [out.jsonl]
+# interleaved rounds.  Usage: bash scripts/experiments/exp_plan.sh [out.jsonl]
 OUT=${1:-gpurun_out/plan/sweep.jsonl}
 mkdir -p $(dirname $OUT)
 run() {  # case env...

@@ -1243,6 +1243,37 @@ def run_reference(args, rank, world, device):
 # launch
 # --------------------------------------------------------------------------------------
 
+def run_shares(device) -> dict:
+    """N=1 only: the C4 and C5 per-GPU steps at one GPU's share of 8 (scripts/bench_c4.py,
+    bench_c5.py) -- the KV a GPU of the 8-GPU configs holds, the hand-off / prefix migration
+    it receives coming from a second pool in local HBM (HBM-bound here; NVLink at 8 GPUs).
+    Eager submission, CUDA events, 3 warm-up + 10 timed steps, pools >> L2."""
+    sys.path.insert(0, os.path.join(ROOT, "scripts"))
+    out = {}
+    for name in ("c4_share", "c5_share"):
+        _release(1)
+        try:
+            if name == "c4_share":
+                import bench_c4
+                r = bench_c4.run(device=device)
+                v = r["decode_tokens_per_s_per_gpu_share"]
+            else:
+                import bench_c5
+                r = bench_c5.run(device=device)
+                v = r["decode_tokens_per_s"]
+            out[name] = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": 1,
+                         "scaling": "one GPU's share of an 8-GPU config", "dtype": "bf16",
+                         "data": "synthetic", "higher_is_better": True,
+                         "note": ("one GPU's share of BASELINE config " + ("C4" if name == "c4_share" else "C5")
+                                  + "; the migrated KV comes from a second pool in this GPU's HBM "
+                                  "(HBM-bound here, NVLink-bound at 8 GPUs)"), **r}
+        except Exception as e:  # report, keep the headline line
+            out[name] = {"error": repr(e)[:300]}
+            log(f"extra config {name} failed:", repr(e))
+    _release(1)
+    return out
+
+
 def _free_port() -> int:
     import socket
     s = socket.socket()
@@ -1277,6 +1308,8 @@ def main():
     ap.add_argument("--config", choices=["auto", "c2", "c3", "c4"], default="auto",
                     help="auto: C2 headline + C3 (and C4 at N>=4) under extra_configs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-share-configs", action="store_true",
+                    help="N=1: skip the C4 / C5 one-GPU-share steps under extra_configs")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--transport", choices=["p2p", "nccl"], default=os.environ.get("BS_TRANSPORT", "p2p"),
                     help="N>1 exchange: CUDA-IPC pushes + flags (p2p) or the library's NCCL "
@@ -1334,6 +1367,8 @@ def main():
                 except Exception as e:  # report, keep the headline line
                     extras[name] = {"error": repr(e)[:300]}
                     log(f"extra config {name} failed:", repr(e))
+            if world == 1 and not args.no_share_configs:
+                extras.update(run_shares(device))
             res["extra_configs"] = extras
         if rank == 0:
             print(json.dumps(res), flush=True)

@@ -27,14 +27,11 @@ import paper_2510_13223_b200 as bs  # noqa: E402
 import synth  # noqa: E402
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--json")
-    ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--handoff-tokens", type=int, default=8192)
-    args = ap.parse_args()
-    dev = torch.device("cuda", 0)
+def run(seed: int = 0, steps: int = 10, handoff_tokens: int = 8192, device=None) -> dict:
+    """The C4 per-GPU step (module docstring); returns the result dict.  Also called by
+    bench.py at N=1 (extra_configs.c4_share)."""
+    args = argparse.Namespace(seed=seed, steps=steps, handoff_tokens=handoff_tokens)
+    dev = device if device is not None else torch.device("cuda", 0)
     shape = synth.LLAMA2_70B
     L = shape.n_layers
     lens = synth.mixed_lengths(256, seed=args.seed)
@@ -108,9 +105,20 @@ def main():
            "attn_kv_GBps": round(attn_bytes / (t_attn * 1e-3) / 1e9, 1),
            "hbm_floor_exposure": round(2 * mig_bytes / attn_bytes, 4),
            "decode_tokens_per_s_per_gpu_share": round(B / (t_step * 1e-3), 1)}
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--json")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--handoff-tokens", type=int, default=8192)
+    a = ap.parse_args()
+    res = run(a.seed, a.steps, a.handoff_tokens)
     print(json.dumps(res), flush=True)
-    if args.json:
-        with open(args.json, "w") as f:
+    if a.json:
+        with open(a.json, "w") as f:
             json.dump(res, f, indent=1)
 
 

@@ -29,13 +29,11 @@ import paper_2510_13223_b200 as bs  # noqa: E402
 import synth  # noqa: E402
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--json")
-    ap.add_argument("--gpus-share", type=int, default=8)
-    ap.add_argument("--steps", type=int, default=10)
-    args = ap.parse_args()
-    dev = torch.device("cuda", 0)
+def run(gpus_share: int = 8, steps: int = 10, device=None) -> dict:
+    """The C5 per-GPU burst step (module docstring); returns the result dict.  Also called
+    by bench.py at N=1 (extra_configs.c5_share)."""
+    args = argparse.Namespace(gpus_share=gpus_share, steps=steps)
+    dev = device if device is not None else torch.device("cuda", 0)
     shape = synth.LLAMA3_8B
     g = torch.Generator().manual_seed(0)
     lo, hi = np.log(128.0), np.log(16384.0)
@@ -106,9 +104,19 @@ def main():
            "attn_kv_GBps": round(attn_bytes / (t_attn * 1e-3) / 1e9, 1),
            "mig_GB_per_step": round(mig_bytes / 1e9, 3), "attn_GB_per_step": round(attn_bytes / 1e9, 3),
            "decode_tokens_per_s": round(B / (t_step * 1e-3), 1)}
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--json")
+    ap.add_argument("--gpus-share", type=int, default=8)
+    ap.add_argument("--steps", type=int, default=10)
+    a = ap.parse_args()
+    res = run(a.gpus_share, a.steps)
     print(json.dumps(res), flush=True)
-    if args.json:
-        with open(args.json, "w") as f:
+    if a.json:
+        with open(a.json, "w") as f:
             json.dump(res, f, indent=1)
 
 

@@ -121,6 +121,8 @@ class ClockSampler:
         self.proc = None
         self.nvml = None
         self.rows = []
+        self.power = []          # board power (W), NVML only
+        self.power_limit_w = None
 
     def _nvml_handle(self):
         import pynvml
@@ -140,12 +142,17 @@ class ClockSampler:
                 "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
                 "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
         cmax = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        try:
+            self.power_limit_w = nv.nvmlDeviceGetEnforcedPowerLimit(h) / 1000.0
+        except Exception:
+            self.power_limit_w = None
         while not self.stop.is_set():
             try:
                 clk = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
                 self.rows.append((clk, cmax, 100.0,
                                   ["Active" if r & bits[n] else "Not Active" for n in self.NAMES]))
+                self.power.append(nv.nvmlDeviceGetPowerUsage(h) / 1000.0)
             except Exception:
                 pass
             self.stop.wait(0.005)
@@ -216,8 +223,13 @@ class ClockSampler:
                     reasons.add(n)
         if not sm:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm), "sm_mhz_min": min(sm), "source": source}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+               "samples": len(sm), "sm_mhz_min": min(sm), "source": source}
+        if self.power:   # context for sw_power_cap: the HBM-bound step's SM clock follows it
+            out["power_w_median"] = round(statistics.median(self.power), 1)
+            out["power_w_max"] = round(max(self.power), 1)
+            out["power_limit_w"] = self.power_limit_w
+        return out
 
 
 class NvlinkCounters:

@@ -133,3 +133,27 @@ def test_seq_oracle_sample_is_bounded_and_scales_by_tokens():
     assert smp.n_hand == 512
     # extrapolation: L x (t_attn x total/sampled tokens + t_mig x W)
     assert abs(smp.step_seconds(1.0, 0.5) - 80 * (lens.sum() / smp.tokens + 0.5 * 8)) < 1e-6
+
+
+def test_clock_summary_reports_board_power():
+    """NVML rows + power samples: the clocks object carries board power (median / max) and
+    the enforced limit -- the context of a sw_power_cap run."""
+    c = bench.ClockSampler(0)
+    c.nvml = object()   # summary() only reads the rows
+    c.rows = [(1900.0, 1965.0, 100.0, ["Not Active"] * 3 + ["Active"])] * 4
+    c.power = [800.0, 850.0, 910.0, 820.0]
+    c.power_limit_w = 1000.0
+    s = c.summary()
+    assert s["power_w_median"] == 835.0 and s["power_w_max"] == 910.0 and s["power_limit_w"] == 1000.0
+    assert s["reasons"] == ["sw_power_cap"]
+
+
+def test_staged_store_runs():
+    """The staged host-tier engine issues one copy-engine transfer per run of consecutive
+    store ids, each landing at its pairs' position in the staging buffer."""
+    from paper_2510_13223_b200.kvstore import _runs
+    assert _runs([]) == []
+    assert _runs([7]) == [(7, 1, 0)]
+    assert _runs([3, 4, 5, 9, 10, 2]) == [(3, 3, 0), (9, 2, 3), (2, 1, 5)]
+    assert _runs(range(100, 164)) == [(100, 64, 0)]
+    assert sum(c for _, c, _ in _runs([5, 6, 1, 2, 3, 8])) == 6

@@ -337,7 +337,7 @@ def push_view_cases(iters=20, warm=5):
 RAGGED_EXTRA_BPS = []
 
 
-def ragged_cases(iters=20, warm=5):
+def ragged_cases(iters=20, warm=5, step_flags=False):
     """Mixed-length shards through the single-GPU fused launch: uniform grid (max_blocks-
     wide ranges) vs the ragged plan (bs_attention_ragged_plan).  GB/s = algorithmic bytes
     (KV + q + bf16 O + lse + block table) / time."""
@@ -379,7 +379,28 @@ def ragged_cases(iters=20, warm=5):
         for kind, (pl, wsr) in plans.items():
             fns[kind] = (pl, lambda pl=pl, wsr=wsr: bs.split_decode_attention_local_ragged(
                 [pool], 0, case.q[0], bts, [0], ksd, sc, pl, o, lse, wsr))
-        for kind, (plan, fn) in fns.items():
+        if step_flags:   # 20 launches per graph, the PDL flag on all but the first
+            for kind in list(fns):
+                pl, wsr = plans[kind] if kind in plans else (None, wsu)
+
+                def launch(flags, pl=pl, wsr=wsr):
+                    if pl is None:
+                        bs.split_decode_attention_local([pool], 0, case.q[0], bts, [0], ksd, sc, o, lse,
+                                                        wsu, flags=flags)
+                    else:
+                        bs.split_decode_attention_local_ragged([pool], 0, case.q[0], bts, [0], ksd, sc, pl,
+                                                               o, lse, wsr, flags=flags)
+                launch(0)
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                st = torch.cuda.Stream()
+                with torch.cuda.graph(g, stream=st):
+                    for i in range(20):
+                        launch(bs.ATTN_PDL if i else 0)
+                fns[kind] = (pl, lambda g=g: g.replay(), 20)
+        for kind, item in fns.items():
+            plan, fn = item[0], item[1]
+            per = item[2] if len(item) > 2 else 1
             for _ in range(warm):
                 fn()
             torch.cuda.synchronize()
@@ -390,9 +411,10 @@ def ragged_cases(iters=20, warm=5):
                 fn()
                 b.record()
             torch.cuda.synchronize()
-            t = sorted(a.elapsed_time(b) for a, b in evs)
+            t = sorted(a.elapsed_time(b) / per for a, b in evs)
             med = t[len(t) // 2]
-            r = {"case": f"{name}_{kind}", "B": B, "G": shape.group, "tokens": int(lens.sum()),
+            r = {"case": f"{name}_{kind}", "timing": "graph_step_flags" if step_flags else "event",
+                 "B": B, "G": shape.group, "tokens": int(lens.sum()),
                  "us": round(med * 1e3, 2), "GBps": round(alg / (med * 1e-3) / 1e9, 1), "bytes": alg,
                  "items": plan.n_work if plan is not None else None,
                  "max_parts": plan.max_parts if plan is not None else None}
@@ -482,7 +504,7 @@ def main():
         res += push_view_cases()
     if args.only in (None, "ragged"):
         RAGGED_EXTRA_BPS.extend(args.ragged_bps)
-        res += ragged_cases(iters=args.iters)
+        res += ragged_cases(iters=args.iters, step_flags=args.step_flags)
     if args.json:
         with open(args.json, "w") as f:
             json.dump(res, f, indent=1)

@@ -244,9 +244,9 @@ bs_status bs_split_decode_attention_local(int32_t n_local, const bs_kv_pool* con
  * while the previous kernel on `stream` drains (a previous attention launch lets it start once
  * its own CTAs have started (multi-wave) or finished their main loops (one wave)), reading
  * block_tables / kv_split and prefetching K/V pages before that kernel completes, and
- * q / out / lse / workspace only after (griddepcontrol.wait).  Applied to multi-wave launches
- * and to one-wave launches that fit in the CTA slots a same-shaped predecessor leaves free
- * (at most half the slots); a flagged launch of at most one CTA per SM runs a 6-stage ring.
+ * q / out / lse / workspace only after (griddepcontrol.wait).  A one-wave predecessor that
+ * occupies more than half the CTA slots lets it start only as its CTAs exit (so it is placed
+ * evenly); a flagged launch of at most one CTA per SM runs a 6-stage ring.
  * The flag never changes the range cut: flagged and plain launches are bitwise identical.
  * Caller contract: the kernel launched just before it on `stream` writes neither the pools'
  * pages this call reads, nor block_tables / kv_split (e.g. the previous layer's attention;

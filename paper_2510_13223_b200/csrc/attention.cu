@@ -127,7 +127,7 @@ struct AttnParams {
   int32_t cl;               // cluster merge: grid.x = ranges = cluster size (cluster_combine_merge)
   int32_t tl_base;          // timeline build only: first g_timeline row of this launch
   int32_t trig_late;        // tensor-core kernel: let the next (PDL) launch start once every
-                            // CTA's main loop is done (1) or once every CTA has started (0)
+                            // CTA has started (0), finished its main loop (1), or exited (2)
   int32_t deep;             // at most one CTA per SM: the 6-stage ring variant (d = 128)
   const int4* work;         // ragged plan (bs_attention_ragged_plan) or NULL: one item per
                             // item = (request, shard << 16 | slot, first block,
@@ -957,7 +957,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
   // CTA of this grid has triggered: right away for multi-wave grids (it fills the slots of
   // the last wave's tail), after the main loop for single-wave grids (its prologue and first
   // K/V stages then overlap this grid's epilogue instead of competing with its streaming).
-  if (!p.trig_late) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (p.trig_late == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (p.pdl) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     BS_TL(6);
@@ -1063,7 +1063,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
     }
     __syncwarp();
   }
-  if (p.trig_late) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (p.trig_late == 1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // ---- per-warp state -> shared memory, then the common CTA epilogue --------------------
 #pragma unroll
@@ -1338,6 +1338,11 @@ int cluster_env() {  // A/B switch BS_ATTN_CLUSTER: 0 never, 1 single-wave launc
 int cluster_max() {
   static int v = std::min(16, std::max(2, env_int("BS_ATTN_CLUSTER_MAX", 8)));
   return v;
+}
+
+int trig_exit_mode() {  // A/B switch BS_ATTN_TRIG_EXIT: 1 (default) trigger at exit for
+  static int v = env_int("BS_ATTN_TRIG_EXIT", 1);  // one-wave grids too large to start beside
+  return v ? 2 : 1;                                  // their predecessor; 0: after the loop
 }
 
 int deep_env() {  // A/B switch BS_ATTN_DEEP: 0 never use the 6-stage one-CTA-per-SM variant
@@ -1642,8 +1647,11 @@ bs_status run_attention(const LaunchArgs& a) {
     // unevenly over the SMs and loses its tail (C3 B=8 at 256 CTAs: 42.9 -> 44.9 us).  The
     // flag never changes the range cut: flagged and plain launches are bitwise identical.
     const int64_t sms = bs::sm_count(bs::current_device());
-    p.pdl = env >= 0 ? env : ((a.flags & BS_ATTN_PDL) && (ctas > slots || 2 * ctas <= slots) ? 1 : 0);
-    p.trig_late = ctas <= slots ? 1 : 0;
+    // A one-wave grid that does not fit beside its predecessor is still a dependent, but its
+    // predecessor triggers only at exit (2): it then starts as the last CTAs leave -- evenly
+    // placed -- and its prologue overlaps the predecessor's completion and memory flush.
+    p.pdl = env >= 0 ? env : ((a.flags & BS_ATTN_PDL) ? 1 : 0);
+    p.trig_late = ctas > slots ? 0 : (2 * ctas <= slots ? 1 : bs::trig_exit_mode());
     // ... and, for such a PDL launch of at most one CTA per SM, 6 K/V stages per warp: it
     // prefetches 24 of a 32-block range before the wait (C3 B=1 10.8 -> 9.9 us; without PDL
     // the deeper ring is slower, 11.8 -> 12.5 us)

@@ -1636,20 +1636,19 @@ bs_status run_attention(const LaunchArgs& a) {
   p.model_head_lo = a.model_head_lo;
   p.grid_x = a.work ? a.n_work : pl.nsplit;
   p.work = reinterpret_cast<const int4*>(a.work);
-  {  // programmatic dependent launch: multi-wave launches only (BS_ATTN_PDL=0/1 overrides)
+  {  // programmatic dependent launch of flagged launches (BS_ATTN_PDL=0/1 overrides)
     const int64_t ctas = (int64_t)p.grid_x * a.n_kv_heads * (a.work ? 1 : a.batch);
     const int64_t slots = (int64_t)bs::sm_count(bs::current_device()) * bs::variant_for(d, G).minb;
     const int env = bs::pdl_env();
-    // PDL pays for multi-wave grids (the next grid fills the last wave's tail) and for
-    // one-wave grids that fit in the slots their predecessor (the same problem) leaves free
-    // (C3 B=1: its prologue and first stages overlap the previous grid's epilogue, 11.9 ->
-    // 10.8 us); a one-wave grid that does not fit starts partly early, partly late, spreads
-    // unevenly over the SMs and loses its tail (C3 B=8 at 256 CTAs: 42.9 -> 44.9 us).  The
-    // flag never changes the range cut: flagged and plain launches are bitwise identical.
     const int64_t sms = bs::sm_count(bs::current_device());
-    // A one-wave grid that does not fit beside its predecessor is still a dependent, but its
-    // predecessor triggers only at exit (2): it then starts as the last CTAs leave -- evenly
-    // placed -- and its prologue overlaps the predecessor's completion and memory flush.
+    // Where THIS grid lets its dependent (the next layer's launch) start -- trig_late:
+    //  0 multi-wave: once every CTA has started (the next grid fills the last wave's tail);
+    //  1 one wave within half the slots: after the main loops, so the next grid's prologue
+    //    and first K/V stages overlap this grid's epilogue, not its streaming (C3 B=1: 11.9
+    //    -> 10.8 us; triggering at entry gained nothing);
+    //  2 larger one-wave grids: at exit -- a next grid started earlier would be placed in
+    //    whatever slots are free, unevenly, and lose its tail (C3 B=8: 42.9 -> 44.9 us).
+    // The flag never changes the range cut: flagged and plain launches are bitwise identical.
     p.pdl = env >= 0 ? env : ((a.flags & BS_ATTN_PDL) ? 1 : 0);
     p.trig_late = ctas > slots ? 0 : (2 * ctas <= slots ? 1 : bs::trig_exit_mode());
     // ... and, for such a PDL launch of at most one CTA per SM, 6 K/V stages per warp: it

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define BS_ABI_VERSION 1
+#define BS_ABI_VERSION 2
 
 typedef enum {
   BS_OK = 0,
@@ -333,7 +333,8 @@ bs_status bs_split_decode_attention_local_ragged_ex(
  *              (bs_wait_signal) before reading out / lse or reusing the workspace
  *   cross_device 1 when the problem's shards run on more than one GPU
  * bs_attn_task: one shard of one problem processed by THIS launch: pool (device-resident,
- *   this GPU), block_tables DEVICE [batch][max_blocks[shard_id]], shard_id, problem index.
+ *   this GPU), block_tables DEVICE [batch][max_blocks[shard_id]], shard_id, problem index,
+ *   optional dispatch order of the requests (ABI version 2).
  * 1 <= n_tasks <= 8, 1 <= n_problems <= 8; all tasks' pools share num_kv_heads / head_dim /
  * num_layers; all problems have `batch` requests of num_q_heads heads.  The caller
  * guarantees that every task of a problem is launched exactly once per call epoch.
@@ -357,6 +358,9 @@ typedef struct {
   const int32_t* block_tables;
   int32_t shard_id;
   int32_t problem;
+  const int32_t* order;  /* DEVICE int32 [batch] permutation or NULL: CTA row z serves request
+                            order[z] (e.g. longest shard first, so the longest CTAs start in
+                            the first wave); results do not depend on it (merge = slot order) */
 } bs_attn_task;
 
 bs_status bs_attention_problem_workspace_size(int32_t batch, int32_t num_q_heads,

@@ -20,6 +20,7 @@ __all__ = [
     "MIGRATE_AUTO", "MIGRATE_VEC16", "MIGRATE_BULK", "EXPORTED_SYMBOLS",
 ]
 
+ABI_VERSION = 2   # include/banaserve.h BS_ABI_VERSION this binding marshals for
 MIGRATE_AUTO, MIGRATE_VEC16, MIGRATE_BULK = 0, 1, 2
 BS_OK, BS_ERR_INVALID_ARG, BS_ERR_OUT_OF_BLOCKS, BS_ERR_UNSUPPORTED, BS_ERR_CUDA, BS_ERR_NCCL = range(6)
 
@@ -83,6 +84,10 @@ def lib():
         if not os.path.exists(path):
             raise ImportError(f"libbanaserve.so missing and cannot be built: {e}") from e
     L = ctypes.CDLL(path)
+    L.bs_abi_version.restype = ctypes.c_int32
+    if L.bs_abi_version() != ABI_VERSION:   # the struct layouts below are this version's
+        raise ImportError(f"{path}: ABI version {L.bs_abi_version()}, the binding needs "
+                          f"{ABI_VERSION} -- rebuild (python -m paper_2510_13223_b200.build)")
     sig = {
         "bs_last_error": ([], ctypes.c_char_p),
         "bs_abi_version": ([], _i32),
@@ -412,7 +417,8 @@ class _Problem(ctypes.Structure):
 
 
 class _Task(ctypes.Structure):
-    _fields_ = [("pool", _p), ("block_tables", _p), ("shard_id", _i32), ("problem", _i32)]
+    _fields_ = [("pool", _p), ("block_tables", _p), ("shard_id", _i32), ("problem", _i32),
+                ("order", _p)]
 
 
 def _aptr(x, dtype=None):
@@ -437,7 +443,8 @@ def split_decode_attention_tasks(problems, tasks, layer: int, batch: int, num_q_
     """H4+H5+H6 fused across launches / GPUs (bs_split_decode_attention_tasks).
     ``problems``: dicts with q, kv_split, max_blocks (list), out, lse, workspace,
     workspace_bytes, done, cross_device -- tensors, or int addresses for peer mappings.
-    ``tasks``: (pool, block_tables, shard_id, problem index) tuples."""
+    ``tasks``: (pool, block_tables, shard_id, problem index[, order]) tuples -- ``order``: a
+    device int32 permutation of the requests (dispatch order, e.g. longest first) or None."""
     keep = []
     pa = (_Problem * len(problems))()
     for i, pr in enumerate(problems):
@@ -452,8 +459,11 @@ def split_decode_attention_tasks(problems, tasks, layer: int, batch: int, num_q_
                          _aptr(pr.get("lse"), torch.float32), _aptr(ws), wsb,
                          _aptr(pr.get("done"), torch.int32), int(bool(pr.get("cross_device", False))))
     ta = (_Task * len(tasks))()
-    for t, (pool, bt, shard, prob) in enumerate(tasks):
-        ta[t] = _Task(pool.handle.value, _dptr(bt, torch.int32), int(shard), int(prob))
+    for t, task in enumerate(tasks):
+        pool, bt, shard, prob = task[:4]
+        order = task[4] if len(task) > 4 else None
+        ta[t] = _Task(pool.handle.value, _dptr(bt, torch.int32), int(shard), int(prob),
+                      _dptr(order, torch.int32) if order is not None else None)
     _check(lib().bs_split_decode_attention_tasks(len(problems), pa, len(tasks), ta, layer, batch,
                                                  num_q_heads, float(scale), _stream(stream)))
 

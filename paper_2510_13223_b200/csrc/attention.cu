@@ -113,6 +113,7 @@ struct ShardDesc {
   int32_t pool_head_lo;  // first kv head of this launch inside the pool
   int32_t prob;        // problem of this shard (index into AttnParams::pb)
   int32_t range_base;  // problem range index of this shard's first CTA range
+  const int32_t* order;  // uniform grid: request of grid row z (longest first), or NULL
 };
 
 struct AttnParams {
@@ -168,9 +169,11 @@ __device__ __forceinline__ CtaWork cta_work(const AttnParams& p) {
     w.nparts = it.w & 0xff;
   } else {       // uniform plan: grid = (ranges over the launch's shards, kv heads, requests)
     const int spg = blockIdx.x;
-    w.b = blockIdx.z;
     w.g = blockIdx.y;
     w.js = shard_of(p, spg);
+    // rows are dispatched in z order: a task's request order puts its longest requests in
+    // the first CTAs (longest-processing-time first), the merge order stays the slot order
+    w.b = p.sh[w.js].order ? __ldg(p.sh[w.js].order + blockIdx.z) : (int)blockIdx.z;
     const int sp = spg - p.sh[w.js].split_off;
     w.blo = sp * p.sh[w.js].bps;
     w.nb = p.sh[w.js].bps;
@@ -2012,6 +2015,7 @@ bs_status bs_split_decode_attention_tasks(int32_t n_problems, const bs_attn_prob
     sd.layer_row0 = (int32_t)((int64_t)layer * pool->desc.num_blocks * 2 * hkv * 16);
     sd.prob = k.problem;
     sd.range_base = pl.split_off[k.shard_id];
+    sd.order = k.order;
     if (have_maps) {
       const CUtensorMap* m = pool_tensor_map(pool);
       if (m) tm.m[t] = *m;

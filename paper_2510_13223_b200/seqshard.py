@@ -76,6 +76,17 @@ class SeqShardedStep:
         # rows of home h's requests (i = h, h+W, ...), as contiguous per-problem tables
         self.bt_h = [_rows(block_tables, h, W) for h in range(W)]
         self.ks_h = [_rows(kv_split, h, W) for h in range(W)]
+        # dispatch order of each home's requests in this rank's task launch: longest range
+        # first (LPT), so mixed lengths (C4) do not leave a long CTA for the last wave; the
+        # merge order is the range order, so results do not depend on it
+        import numpy as np
+        ks_host = kv_split.cpu().numpy() if isinstance(kv_split, torch.Tensor) else np.asarray(kv_split)
+        mine = (ks_host[:, rank + 1] - ks_host[:, rank]).astype(np.int64)
+        self.order_h = []
+        for h in range(W):
+            o = np.argsort(-mine[h::W], kind="stable").astype(np.int32)
+            self.order_h.append(torch.from_numpy(o).to(block_tables.device)
+                                if isinstance(block_tables, torch.Tensor) else o)
         self.src_ids, self.dst_ids = handoff_src_ids, handoff_dst_ids
         self.n_handoff = 0 if handoff_src_ids is None else int(handoff_src_ids.numel())
         self.prev, self.next = (rank - 1) % W, (rank + 1) % W
@@ -283,7 +294,8 @@ class SeqShardedStep:
                                              self.ks_h[0], self.out_buf[layer], self.lse_buf[layer],
                                              self._solo_ws, pdl=layer > 0)
                 else:
-                    self.ops.attention_tasks(problems, [(self.pool, self.bt_h[h], r, h) for h in range(W)],
+                    self.ops.attention_tasks(problems, [(self.pool, self.bt_h[h], r, h, self.order_h[h])
+                                                        for h in range(W)],
                                              layer, self.Bh, self.hq)
             if timers is not None:
                 timers[layer][1].record(compute)

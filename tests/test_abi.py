@@ -42,7 +42,11 @@ def test_library_is_sm100a():
 
 
 def test_abi_version():
-    assert bs.lib().bs_abi_version() == 1
+    """The loaded library, the header and the binding agree on the ABI version."""
+    import re
+    hdr = open(os.path.join(ROOT, "include", "banaserve.h")).read()
+    v = int(re.search(r"#define BS_ABI_VERSION (\d+)", hdr).group(1))
+    assert bs.lib().bs_abi_version() == v == bs.ABI_VERSION
 
 
 def _desc(L=2, nb=10, hkv=8, d=128, bsz=16, dtype=0, dev=0):

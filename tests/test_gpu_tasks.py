@@ -119,6 +119,34 @@ def test_two_problems_sharded_over_concurrent_launches(bs, d, G, n_shards, cross
     assert torch.equal(out.view(torch.int16), A.out[1].view(torch.int16))
 
 
+@pytest.mark.parametrize("n_shards", [1, 3])
+def test_task_request_order_changes_dispatch_not_results(bs, n_shards):
+    """bs_attn_task.order (ABI 2): CTA row z serves request order[z] -- the sequence-sharded
+    step passes longest-shard-first -- and the outputs are bitwise those of the identity
+    order (the merge follows the range slots), and match the oracle."""
+    shape = synth.Shape(2, 16, 2, 128)
+    lens = (0, 3000, 17, 700, 2048, 1, 5000, 64)
+    A = Problem(bs, shape, lens, n_shards, seed=21, cross_device=False)
+    B = len(lens)
+    sc = synth.default_scale(128)
+    sh = (A.ks[:, 1:] - A.ks[:, :-1])
+    orders = [dev_i32(np.argsort(-sh[:, j], kind="stable")) for j in range(n_shards)]
+    outs = []
+    for use_order in (False, True):
+        A.out.fill_(float("nan"))
+        for layer in range(shape.n_layers):
+            bs.split_decode_attention_tasks(
+                [A.desc(layer)],
+                [(A.pools[j], A.bts[j], j, 0, orders[j] if use_order else None) for j in range(n_shards)],
+                layer, B, shape.hq, sc)
+        torch.cuda.synchronize()
+        outs.append((A.out.clone(), A.lse.clone()))
+    assert torch.equal(outs[0][0].view(torch.int16), outs[1][0].view(torch.int16))
+    assert torch.equal(outs[0][1], outs[1][1])
+    for layer in range(shape.n_layers):
+        A.check(layer)
+
+
 def test_tasks_argument_errors(bs):
     shape = synth.Shape(1, 4, 2, 64)
     A = Problem(bs, shape, (10, 40), 2, seed=3, cross_device=False)

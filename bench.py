@@ -427,6 +427,11 @@ def run_steps(step, q, out, lse, K, L, world, device, use_graph, timed=True):
             mode = f"eager (graph capture failed: {why})"
 
     def region(graph, tmr):
+        from paper_2510_13223_b200.transport import nvtx
+        with nvtx("bench timed region" + (" (instrumented)" if tmr is not None else "")):
+            _region(graph, tmr)
+
+    def _region(graph, tmr):
         if graph is not None:
             graph.replay()
             return

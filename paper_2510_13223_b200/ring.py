@@ -37,7 +37,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from .transport import ErrorFlag, NcclWire
+from .transport import ErrorFlag, NcclWire, nvtx
 
 
 def _out_timer(timers, layer, stream):
@@ -516,6 +516,10 @@ class ShardedDecodeStep:
         out_final]) events recorded on the launching streams (CUDA only).  ``inputs_ready[l]``: an
         event the step waits for before reading q[l] (e.g. its H2D copy); after the call,
         ``self.out_ready[l]`` is recorded once out[l] / lse[l] are final (per-layer D2H)."""
+        with nvtx(f"banaserve step rank {self.rank}/{self.world} ({self.transport})"):
+            return self._enqueue(q, out, lse, timers, inputs_ready)
+
+    def _enqueue(self, q, out, lse, timers, inputs_ready):
         if self.transport == "p2p":
             self.links.check()   # a timed-out wait of an earlier step poisons its outputs
             if self.fused_exchange:

@@ -38,7 +38,7 @@ import torch
 import torch.distributed as dist
 
 from .ring import _all_ranks_true, split_partial
-from .transport import ErrorFlag, NcclWire
+from .transport import ErrorFlag, NcclWire, nvtx
 
 
 def _rows(x, h: int, W: int):
@@ -387,10 +387,11 @@ class SeqShardedStep:
         """q [L][B_h][Hq][d] of this rank's home requests (global ids rank, rank+W, ...)
         -> out [L][B_h][Hq][d] bf16, lse [L][B_h][Hq] fp32.  ``timers`` / ``inputs_ready``:
         P2P transport only (see _enqueue_p2p)."""
-        if self.transport == "p2p":
-            self.check()   # a timed-out wait of an earlier step poisons its outputs
-            return self._enqueue_p2p(q, out, lse, timers, inputs_ready)
-        return self._enqueue_collective(q, out, lse)
+        with nvtx(f"banaserve seq-sharded step rank {self.rank}/{self.world} ({self.transport})"):
+            if self.transport == "p2p":
+                self.check()   # a timed-out wait of an earlier step poisons its outputs
+                return self._enqueue_p2p(q, out, lse, timers, inputs_ready)
+            return self._enqueue_collective(q, out, lse)
 
     def capture(self, q: torch.Tensor, out: torch.Tensor, lse: torch.Tensor | None = None):
         """One step of the P2P transport captured in a CUDA graph (flags computed on the

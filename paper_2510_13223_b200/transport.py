@@ -10,11 +10,33 @@ the same ``exchange(sends, recvs)`` method; the CPU tests inject one over gloo.
 ``ErrorFlag`` is the timeout flag of the P2P signals (``bs_wait_signal*``): one int32 in
 page-locked host memory the device writes with a system-scope store, so the host can
 check it after every step without synchronising.
+
+``nvtx`` marks host submission ranges (a decode step, each layer) for nsys / ncu
+``--nvtx`` filtering when ``BS_NVTX=1``; a no-op otherwise.
 """
 from __future__ import annotations
 
+import contextlib
+import os
+
 import torch
 import torch.distributed as dist
+
+_NVTX = os.environ.get("BS_NVTX") == "1"
+
+
+@contextlib.contextmanager
+def nvtx(name: str):
+    """NVTX range around the enclosed submissions (BS_NVTX=1; graph capture records the
+    ranges once, at capture time)."""
+    if not _NVTX or not torch.cuda.is_available():
+        yield
+        return
+    torch.cuda.nvtx.range_push(name)
+    try:
+        yield
+    finally:
+        torch.cuda.nvtx.range_pop()
 
 
 class NcclWire:

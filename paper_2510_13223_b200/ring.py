@@ -516,7 +516,7 @@ class ShardedDecodeStep:
         out_final]) events recorded on the launching streams (CUDA only).  ``inputs_ready[l]``: an
         event the step waits for before reading q[l] (e.g. its H2D copy); after the call,
         ``self.out_ready[l]`` is recorded once out[l] / lse[l] are final (per-layer D2H)."""
-        with nvtx(f"banaserve step rank {self.rank}/{self.world} ({self.transport})"):
+        with nvtx(f"banaserve step r{self.rank} n{self.world} {self.transport}"):
             return self._enqueue(q, out, lse, timers, inputs_ready)
 
     def _enqueue(self, q, out, lse, timers, inputs_ready):

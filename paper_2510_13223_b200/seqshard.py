@@ -387,7 +387,7 @@ class SeqShardedStep:
         """q [L][B_h][Hq][d] of this rank's home requests (global ids rank, rank+W, ...)
         -> out [L][B_h][Hq][d] bf16, lse [L][B_h][Hq] fp32.  ``timers`` / ``inputs_ready``:
         P2P transport only (see _enqueue_p2p)."""
-        with nvtx(f"banaserve seq-sharded step rank {self.rank}/{self.world} ({self.transport})"):
+        with nvtx(f"banaserve seqshard step r{self.rank} n{self.world} {self.transport}"):
             if self.transport == "p2p":
                 self.check()   # a timed-out wait of an earlier step poisons its outputs
                 return self._enqueue_p2p(q, out, lse, timers, inputs_ready)

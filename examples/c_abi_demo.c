@@ -55,6 +55,10 @@ static float bf16_to_f32(uint16_t h) {
 }
 
 int main(void) {
+  if (bs_abi_version() != BS_ABI_VERSION) { /* header and library must describe the same ABI */
+    fprintf(stderr, "c_abi_demo: library ABI %d, header ABI %d\n", bs_abi_version(), BS_ABI_VERSION);
+    return 1;
+  }
   const int L = 2, NB = 32, HKV = 2, D = 64, HQ = 4, LEN = 45; /* 3 blocks, ragged tail */
   bs_kv_pool_desc desc = {L, NB, 16, HKV, D, BS_DTYPE_BF16, 0};
   const size_t bytes = bs_kv_pool_bytes(&desc), chunk = bs_kv_chunk_bytes(&desc);

@@ -263,3 +263,41 @@ def test_deep_ring_variant_bitwise_equals_two_stage(tmp_path):
     assert np.array_equal(res["1"]["out"], res["0"]["out"])
     assert np.array_equal(res["1"]["lse"], res["0"]["lse"])
 
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_merge_paths_fuzz(bs, seed):
+    """Random shapes through the fused local launch, two consecutive layers with the decode-
+    step flag on the second: whatever merge / launch features the launch picks (cluster or
+    last arriver, PDL trigger mode, 6-stage ring), the outputs equal the plain launch with
+    the workspace merge (BS_ATTN_NO_CLUSTER, no PDL) bitwise and the oracle within the
+    tolerances."""
+    rng = np.random.default_rng(500 + seed)
+    G = int(rng.choice([1, 2, 4, 8]))
+    d = int(rng.choice([64, 128]))
+    hkv = int(rng.choice([1, 2, 4, 8]))
+    shape = synth.Shape(2, hkv * G, hkv, d)
+    B = int(rng.integers(1, 9))
+    lens = [int(x) for x in rng.choice([0, 1, 16, 17, 300, 1000, 4000, 9000], size=B)]
+    n = int(rng.integers(1, 4))
+    dense, ks, shards, pools = host_case(bs, shape, lens, n, seed=seed)
+    bts = [dev_i32(s.block_tables) for s in shards]
+    ksd = dev_i32(ks)
+    sc = synth.default_scale(d)
+    outs = {}
+    for mode, flags in (("plain", bs.ATTN_NO_CLUSTER), ("features", bs.ATTN_PDL)):
+        o = torch.full((2, B, shape.hq, d), float("nan"), dtype=torch.bfloat16, device="cuda")
+        l = torch.full((2, B, shape.hq), float("nan"), device="cuda")
+        ws = torch.zeros(max(16, bs.split_decode_attention_local_workspace_size(
+            pools, [t.shape[1] for t in bts], B, shape.hq)), dtype=torch.uint8, device="cuda")
+        for layer in range(2):
+            bs.split_decode_attention_local(pools, layer, dev_bf16(dense.q[layer]), bts, list(range(len(pools))),
+                                            ksd, sc, o[layer], l[layer], ws,
+                                            flags=flags if (layer or mode == "plain") else 0)
+        torch.cuda.synchronize()
+        outs[mode] = (o, l)
+    assert torch.equal(outs["plain"][0].view(torch.int16), outs["features"][0].view(torch.int16))
+    assert torch.equal(outs["plain"][1], outs["features"][1])
+    for layer in range(2):
+        check_merged(shards, ks, dense.q[layer], sc, outs["features"][0][layer], outs["features"][1][layer],
+                     layer=layer)

@@ -285,6 +285,19 @@ bs_status bs_attention_ragged_plan(int32_t batch, int32_t n_shards, const int32_
                                    int32_t num_kv_heads, int32_t head_dim,
                                    int32_t max_blocks_per_range, int32_t* work, int32_t capacity,
                                    int32_t* n_work, int32_t* max_parts, size_t* workspace_bytes);
+/* The same with flags.  BS_PLAN_PACK_SHORT (one local shard): requests whose shard has at
+ * most 8 blocks (128 tokens) are packed four to a CTA -- one warp per request, which writes
+ * its own O / lse with no cross-warp combine -- instead of one CTA per (request, kv-head);
+ * such an item has its parts field (low byte of w) 0: (b0, b1, b2, b3 << 8), -1 = no request.
+ * Packed plans need the tensor-core kernel (the CUDA-core kernel traps on them); they are
+ * made only when it is the active variant. */
+#define BS_PLAN_PACK_SHORT 1u
+bs_status bs_attention_ragged_plan_ex(int32_t batch, int32_t n_shards, const int32_t* kv_split_host,
+                                      int32_t n_local, const int32_t* shard_ids, int32_t num_q_heads,
+                                      int32_t num_kv_heads, int32_t head_dim,
+                                      int32_t max_blocks_per_range, uint32_t flags, int32_t* work,
+                                      int32_t capacity, int32_t* n_work, int32_t* max_parts,
+                                      size_t* workspace_bytes);
 /* bs_split_decode_attention_local over a ragged plan (work: DEVICE copy of the plan's
  * items, n_work of them; max_parts from the plan).  Same outputs and workspace rules. */
 bs_status bs_split_decode_attention_local_ragged(

@@ -43,7 +43,7 @@ EXPORTED_SYMBOLS = (
     "bs_debug_build", "bs_debug_error_code", "bs_kv_append_token", "bs_exchange",
     "bs_signals_epoch", "bs_wait_signals_epoch", "bs_epoch_advance", "bs_kv_migrate_append_layer",
     "bs_split_decode_attention_local_ex", "bs_attention_last_launch",
-    "bs_split_decode_attention_local_ragged_ex",
+    "bs_split_decode_attention_local_ragged_ex", "bs_attention_ragged_plan_ex",
 )
 
 
@@ -78,11 +78,14 @@ def lib():
     debug = os.environ.get("BS_DEBUG") == "1"   # device-side index checks (debug build)
     timeline = not debug and os.environ.get("BS_TIMELINE") == "1"  # kernel timeline stamps
     path = _build.LIB_DEBUG if debug else (_build.LIB_TIMELINE if timeline else _build.LIB)
-    try:
-        path = _build.build(debug=debug, timeline=timeline)
-    except Exception as e:  # no nvcc on this machine: use the shipped .so if present
-        if not os.path.exists(path):
-            raise ImportError(f"libbanaserve.so missing and cannot be built: {e}") from e
+    if os.environ.get("BS_LIB"):   # A/B experiments: another build of the library, as is
+        path = os.environ["BS_LIB"]
+    else:
+        try:
+            path = _build.build(debug=debug, timeline=timeline)
+        except Exception as e:  # no nvcc on this machine: use the shipped .so if present
+            if not os.path.exists(path):
+                raise ImportError(f"libbanaserve.so missing and cannot be built: {e}") from e
     L = ctypes.CDLL(path)
     L.bs_abi_version.restype = ctypes.c_int32
     if L.bs_abi_version() != ABI_VERSION:   # the struct layouts below are this version's
@@ -145,6 +148,9 @@ def lib():
         "bs_attention_ragged_plan": ([_i32, _i32, _p, _i32, _p, _i32, _i32, _i32, _i32, _p, _i32,
                                       ctypes.POINTER(_i32), ctypes.POINTER(_i32),
                                       ctypes.POINTER(_sz)], _i32),
+        "bs_attention_ragged_plan_ex": ([_i32, _i32, _p, _i32, _p, _i32, _i32, _i32, _i32,
+                                         ctypes.c_uint32, _p, _i32, ctypes.POINTER(_i32),
+                                         ctypes.POINTER(_i32), ctypes.POINTER(_sz)], _i32),
         "bs_split_decode_attention_local_ragged": ([_i32, _p, _i32, _p, _i32, _i32, _p, _p, _p, _p,
                                                     _i32, _f32, _p, _i32, _i32, _p, _p, _p, _sz,
                                                     _p], _i32),
@@ -165,6 +171,8 @@ def lib():
                                 ctypes.c_double, _i32, _p, ctypes.POINTER(_i32)], _i32),
     }
     for name, (args, res) in sig.items():
+        if os.environ.get("BS_LIB") and not hasattr(L, name):
+            continue   # an older build under A/B: its missing entry points stay unbound
         f = getattr(L, name)
         f.argtypes = args
         f.restype = res
@@ -482,8 +490,14 @@ class RaggedPlan:
         return self
 
 
+PLAN_PACK_SHORT = 1   # bs_attention_ragged_plan_ex flag
+
+
 def attention_ragged_plan(kv_split_host, shard_ids, num_q_heads: int, num_kv_heads: int,
-                          head_dim: int, max_blocks_per_range: int = 0) -> RaggedPlan:
+                          head_dim: int, max_blocks_per_range: int = 0,
+                          pack_short: bool = False) -> RaggedPlan:
+    """Host ragged plan (bs_attention_ragged_plan_ex).  ``pack_short``: requests of at most
+    8 blocks in the (single) local shard are packed four to a CTA, one warp each."""
     import numpy as np
     ks = np.ascontiguousarray(np.asarray(kv_split_host, dtype=np.int32))
     B, n1 = ks.shape
@@ -491,12 +505,12 @@ def attention_ragged_plan(kv_split_host, shard_ids, num_q_heads: int, num_kv_hea
     sa = (ctypes.c_int32 * n)(*[int(x) for x in shard_ids])
     nw, mp, wsb = _i32(), _i32(), _sz()
     args = (B, n1 - 1, ks.ctypes.data, n, sa, num_q_heads, num_kv_heads, head_dim,
-            max_blocks_per_range)
-    _check(lib().bs_attention_ragged_plan(*args, None, 0, ctypes.byref(nw), ctypes.byref(mp),
-                                          ctypes.byref(wsb)))
+            max_blocks_per_range, PLAN_PACK_SHORT if pack_short else 0)
+    _check(lib().bs_attention_ragged_plan_ex(*args, None, 0, ctypes.byref(nw), ctypes.byref(mp),
+                                             ctypes.byref(wsb)))
     work = np.zeros((nw.value, 4), dtype=np.int32)
-    _check(lib().bs_attention_ragged_plan(*args, work.ctypes.data, nw.value, ctypes.byref(nw),
-                                          ctypes.byref(mp), ctypes.byref(wsb)))
+    _check(lib().bs_attention_ragged_plan_ex(*args, work.ctypes.data, nw.value, ctypes.byref(nw),
+                                             ctypes.byref(mp), ctypes.byref(wsb)))
     return RaggedPlan(work, mp.value, wsb.value)
 
 

@@ -46,6 +46,7 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kWarps = 4;
 constexpr int kBtMax = 512;     // blocks per CTA range (bt cached in smem)
 constexpr int kMaxSplit = 64;   // intra-GPU split-K limit
+constexpr int kPackMaxBlocks = 8;  // ragged plan: requests of <= 8 blocks are packed, one per warp
 
 constexpr int kMaxLocal = 8;  // shards (tasks) / problems of one launch
 
@@ -152,15 +153,28 @@ __device__ __forceinline__ int shard_of(const AttnParams& p, int spg) {
 // shard, partial slot, and the request's range count (-1: the problem's uniform nsplit).
 struct CtaWork {
   int b, g, js, blo, nb, slot, nparts;
+  int packed;  // ragged plan, short requests: each warp serves its own request b (-1: none)
 };
 
 __device__ __forceinline__ CtaWork cta_work(const AttnParams& p) {
   CtaWork w;
+  w.packed = 0;
   if (p.work) {  // ragged plan: grid.x = item * Hkv + kv head (heads of an item adjacent:
                  // they read neighbouring pages of the same blocks)
     const int item = blockIdx.x / p.hkv;
     w.g = blockIdx.x - item * p.hkv;
     const int4 it = __ldg(p.work + item);
+    if ((it.w & 0xff) == 0) {  // packed item (parts field 0): up to kWarps short requests of
+      w.packed = 1;            // shard 0, one per warp -- (b0, b1, b2, b3 << 8), -1 = none
+      const int wp = threadIdx.x >> 5;
+      w.b = wp == 0 ? it.x : wp == 1 ? it.y : wp == 2 ? it.z : (it.w >> 8);
+      w.js = 0;
+      w.slot = 0;
+      w.blo = 0;
+      w.nb = 0;
+      w.nparts = 1;
+      return w;
+    }
     w.b = it.x;
     w.js = it.y >> 16;
     w.slot = it.y & 0xffff;
@@ -556,6 +570,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) split_decode_attn(const Att
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const CtaWork cw = cta_work(p);
+  if (cw.packed) asm volatile("trap;");  // packed ragged items are for the tensor-core kernel
   const int g = cw.g, b = cw.b, js = cw.js;
   const ShardDesc& sd = p.sh[js];
   const ProbDesc& P = p.pb[sd.prob];
@@ -879,39 +894,45 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
   const int warp = threadIdx.x >> 5;
   const int gq = lane >> 2, tq = lane & 3;  // mma groupID / thread-in-group
   const CtaWork cw = cta_work(p);
-  const int g = cw.g, b = cw.b, js = cw.js;
+  const int g = cw.g, js = cw.js;
   const ShardDesc& sd = p.sh[js];
   const ProbDesc& P = p.pb[sd.prob];
+  // packed item (ragged plan, short requests): this warp serves its own request alone --
+  // all its blocks (boff 0, stride 1) from its own slice of the block-id table -- and
+  // writes its output itself; otherwise the warps interleave over the CTA's range
+  const int b = cw.b;  // (packed items: this warp's own request)
+  const int bstride = cw.packed ? 1 : kWarps, boff = cw.packed ? 0 : warp;
 
   // One memory round trip before the first TMA: the CTA's block-table row (independent
   // of the length), each warp's first STAGES block ids and the shard length are loaded
   // together; lane 0 of every warp then issues its first copies before the CTA barrier.
   const int32_t blo = cw.blo;
-  const int64_t row0 = (int64_t)b * sd.max_blocks + blo;
-  const int nb_tab = max(min(cw.nb, sd.max_blocks - blo), 0);
+  const int64_t row0 = (int64_t)max(b, 0) * sd.max_blocks + blo;
+  const int nb_tab = cw.packed ? (b < 0 ? 0 : min(kPackMaxBlocks, sd.max_blocks))
+                               : max(min(cw.nb, sd.max_blocks - blo), 0);
   constexpr int kIdPerThread = kBtMax / (kWarps * 32);
   int32_t idv[kIdPerThread];
 #pragma unroll
   for (int r = 0; r < kIdPerThread; ++r) {
-    const int i = threadIdx.x + r * kWarps * 32;
+    const int i = cw.packed ? lane + 32 * r : threadIdx.x + r * kWarps * 32;
     idv[r] = i < nb_tab ? __ldg(sd.bt + row0 + i) : 0;
   }
   int32_t first[STAGES];
 #pragma unroll
   for (int k = 0; k < STAGES; ++k)
-    first[k] = (lane == 0 && warp + k * kWarps < nb_tab) ? __ldg(sd.bt + row0 + warp + k * kWarps) : 0;
-  const int32_t* ks = P.kv_split + (int64_t)b * (P.n_shards + 1) + sd.shard_id;
-  const int32_t len = max(__ldg(ks + 1) - __ldg(ks), 0);
+    first[k] = (lane == 0 && boff + k * bstride < nb_tab) ? __ldg(sd.bt + row0 + boff + k * bstride) : 0;
+  const int32_t* ks = P.kv_split + (int64_t)max(b, 0) * (P.n_shards + 1) + sd.shard_id;
+  const int32_t len = b < 0 ? 0 : max(__ldg(ks + 1) - __ldg(ks), 0);
   const int32_t nblk = (len + 15) >> 4;
-  const int32_t nb_cta = max(min(nblk, blo + cw.nb) - blo, 0);
+  const int32_t nb_cta = cw.packed ? min(nblk, nb_tab) : max(min(nblk, blo + cw.nb) - blo, 0);
   const int nparts = cw.nparts < 0 ? P.nsplit : cw.nparts;
 
-  int32_t* s_bt = reinterpret_cast<int32_t*>(smem + S::kBtOff);
+  int32_t* s_bt = reinterpret_cast<int32_t*>(smem + S::kBtOff) + (cw.packed ? warp * (kBtMax / kWarps) : 0);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBarOff) + warp * STAGES;
   uint8_t* s_pt = smem + S::kPOff + warp * 8 * 16 * 2;
   uint8_t* ring = smem + warp * STAGES * S::kStage;
 
-  const int nmine = nb_cta > warp ? (nb_cta - warp + kWarps - 1) / kWarps : 0;
+  const int nmine = cw.packed ? nb_cta : (nb_cta > warp ? (nb_cta - warp + kWarps - 1) / kWarps : 0);
   const int gm = p.model_head_lo + g;
   const int head = sd.pool_head_lo + g;
   const CUtensorMap* tmap = &tm.m[js];
@@ -946,7 +967,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
   }
 #pragma unroll
   for (int r = 0; r < kIdPerThread; ++r) {
-    const int i = threadIdx.x + r * kWarps * 32;
+    const int i = cw.packed ? lane + 32 * r : threadIdx.x + r * kWarps * 32;
     if (i < nb_cta) s_bt[i] = idv[r];
   }
   __syncthreads();  // block table + barrier inits visible to the CTA
@@ -969,11 +990,11 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
   // q^T B-fragments (bf16 pairs) for head n = gq (zero padding for n >= G)
   uint32_t bq[KS][2];
   {
-    const uint32_t* qrow = reinterpret_cast<const uint32_t*>(P.q + ((int64_t)b * p.hq + gm * G + gq) * D);
+    const uint32_t* qrow = reinterpret_cast<const uint32_t*>(P.q + ((int64_t)max(b, 0) * p.hq + gm * G + gq) * D);
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk) {
-      bq[kk][0] = gq < G ? __ldg(qrow + 8 * kk + tq) : 0u;
-      bq[kk][1] = gq < G ? __ldg(qrow + 8 * kk + 4 + tq) : 0u;
+      bq[kk][0] = gq < G && b >= 0 ? __ldg(qrow + 8 * kk + tq) : 0u;
+      bq[kk][1] = gq < G && b >= 0 ? __ldg(qrow + 8 * kk + 4 + tq) : 0u;
     }
   }
 
@@ -993,7 +1014,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
     ptx::mbar_wait(&bars[s], (uint32_t)((k / STAGES) & 1));
     __syncwarp();
     if (k == 0 && warp == 0) BS_TL(1);
-    const int blk = blo + warp + k * kWarps;
+    const int blk = blo + boff + k * bstride;
     const int nvalid = min(16, len - blk * 16);
     const uint32_t st = ring_u32 + s * S::kStage;
 
@@ -1062,7 +1083,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
     __syncwarp();
     if (lane == 0 && k + STAGES < nmine) {
       ptx::fence_proxy_async_smem();
-      issue(k + STAGES, s_bt[warp + (k + STAGES) * kWarps]);
+      issue(k + STAGES, s_bt[boff + (k + STAGES) * bstride]);
     }
     __syncwarp();
   }
@@ -1076,6 +1097,26 @@ __global__ void __launch_bounds__(kWarps * 32, MINB)
     x += __shfl_xor_sync(0xffffffffu, x, 8);
     x += __shfl_xor_sync(0xffffffffu, x, 16);
     l_run[j] = x;
+  }
+  if (cw.packed) {  // this warp's request is complete: O = O~ / l, lse = m + ln l (merged out)
+    if (b >= 0) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int h = 2 * tq + j;
+        if (h < G) {
+          const int64_t row = (int64_t)b * p.hq + gm * G + h;
+          const float L = l_run[j];
+          const bool any = L > 0.f;
+#pragma unroll
+          for (int mt = 0; mt < KS; ++mt) {
+            P.out[row * D + 16 * mt + gq] = __float2bfloat16_rn(any ? oacc[mt][j] / L : 0.f);
+            P.out[row * D + 16 * mt + gq + 8] = __float2bfloat16_rn(any ? oacc[mt][2 + j] / L : 0.f);
+          }
+          if (gq == 0 && P.lse) P.lse[row] = any ? m_run[j] * kLn2 + logf(L) : -INFINITY;
+        }
+      }
+    }
+    return;
   }
   __syncthreads();  // rings idle: reuse them for the combine
   BS_TL(2);
@@ -2046,6 +2087,18 @@ bs_status bs_attention_ragged_plan(int32_t batch, int32_t n_shards, const int32_
                                    int32_t num_kv_heads, int32_t head_dim,
                                    int32_t max_blocks_per_range, int32_t* work, int32_t capacity,
                                    int32_t* n_work, int32_t* max_parts, size_t* workspace_bytes) {
+  return bs_attention_ragged_plan_ex(batch, n_shards, kv_split_host, n_local, shard_ids, num_q_heads,
+                                     num_kv_heads, head_dim, max_blocks_per_range, 0u, work, capacity,
+                                     n_work, max_parts, workspace_bytes);
+}
+
+bs_status bs_attention_ragged_plan_ex(int32_t batch, int32_t n_shards, const int32_t* kv_split_host,
+                                      int32_t n_local, const int32_t* shard_ids, int32_t num_q_heads,
+                                      int32_t num_kv_heads, int32_t head_dim,
+                                      int32_t max_blocks_per_range, uint32_t flags, int32_t* work,
+                                      int32_t capacity, int32_t* n_work, int32_t* max_parts,
+                                      size_t* workspace_bytes) {
+  BS_REQUIRE((flags & ~BS_PLAN_PACK_SHORT) == 0, "bs_attention_ragged_plan: unknown flags 0x%x", flags);
   BS_REQUIRE(kv_split_host && shard_ids && n_work && max_parts && workspace_bytes,
              "bs_attention_ragged_plan: NULL argument");
   BS_REQUIRE(batch >= 1 && n_shards >= 1 && n_local >= 1 && n_local <= bs::kMaxLocal,
@@ -2086,10 +2139,22 @@ bs_status bs_attention_ragged_plan(int32_t batch, int32_t n_shards, const int32_
   }
   int32_t most = 1;
   std::vector<int4> items;
+  std::vector<int32_t> keys;  // dispatch-order key: the CTA's longest per-warp block run x 4
   auto emit = [&](int b, int t, int slot, int blo, int nb, int parts) {
     items.push_back(make_int4(b, (t << 16) | slot, blo, (nb << 8) | parts));
+    keys.push_back(nb);
   };
+  // BS_PLAN_PACK_SHORT: requests whose (only) shard has <= kPackMaxBlocks blocks go into
+  // packed items -- up to 4 requests per CTA, one warp each, no cross-warp combine (the
+  // tensor-core kernel; a one-CTA-per-(request, kv-head) item with 1-8 blocks is prologue-
+  // and epilogue-bound)
+  const bool pack = (flags & BS_PLAN_PACK_SHORT) && n_local == 1 && bs::variant_for(head_dim, G).mma;
+  std::vector<int32_t> short_reqs;
   for (int b = 0; b < batch; ++b) {
+    if (pack && nblk[(size_t)b] <= bs::kPackMaxBlocks) {
+      short_reqs.push_back(b);
+      continue;
+    }
     int pb = bps, parts = 0;
     for (;;) {  // a request's ranges must fit kMaxSplit slots: widen its ranges if not
       parts = 0;
@@ -2126,10 +2191,25 @@ bs_status bs_attention_ragged_plan(int32_t batch, int32_t n_shards, const int32_
   // CTAs in grid order, so the long ranges of mixed-length batches start in the first wave
   // and the short ones fill the tail.  The merge order is the slot order, not the arrival
   // order, so the results do not depend on it.  BS_RAGGED_ORDER=0 keeps request order.
+  for (size_t i = 0; i < short_reqs.size(); i += bs::kWarps) {
+    int32_t r[bs::kWarps];
+    int32_t longest = 0;
+    for (int k = 0; k < bs::kWarps; ++k) {
+      r[k] = i + k < short_reqs.size() ? short_reqs[i + k] : -1;
+      if (r[k] >= 0) longest = std::max(longest, nblk[(size_t)r[k]]);
+    }
+    items.push_back(make_int4(r[0], r[1], r[2], (int32_t)((uint32_t)r[3] << 8)));  // parts 0
+    keys.push_back(longest * bs::kWarps);  // one warp streams all of its request's blocks
+  }
   const char* oe = getenv("BS_RAGGED_ORDER");
-  if (!(oe && atoi(oe) == 0))
-    std::stable_sort(items.begin(), items.end(),
-                     [](const int4& x, const int4& y) { return (x.w >> 8) > (y.w >> 8); });
+  if (!(oe && atoi(oe) == 0)) {
+    std::vector<size_t> idx(items.size());
+    for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](size_t x, size_t y) { return keys[x] > keys[y]; });
+    std::vector<int4> sorted(items.size());
+    for (size_t i = 0; i < idx.size(); ++i) sorted[i] = items[idx[i]];
+    items.swap(sorted);
+  }
   const int32_t count = (int32_t)items.size();
   if (work)
     for (int32_t i = 0; i < std::min(count, capacity); ++i) {

@@ -50,7 +50,7 @@ def run(seed: int = 0, steps: int = 10, handoff_tokens: int = 8192, device=None)
     i32 = lambda x: torch.as_tensor(np.asarray(x), dtype=torch.int32, device=dev)  # noqa: E731
     src_ids, dst_ids = i32(np.arange(n_hand)), i32(free)
     sc = synth.default_scale(shape.d)
-    plan = bs.attention_ragged_plan(ks, [0], shape.hq, shape.hkv, shape.d).to(dev)
+    plan = bs.attention_ragged_plan(ks, [0], shape.hq, shape.hkv, shape.d, pack_short=True).to(dev)
     ws = torch.zeros(max(16, plan.workspace_bytes), dtype=torch.uint8, device=dev)
     btd, ksd = i32(bt), i32(ks)
     out = torch.empty(B, shape.hq, shape.d, dtype=torch.bfloat16, device=dev)

@@ -15,7 +15,7 @@ import paper_2510_13223_b200 as bs  # noqa: E402
 import synth  # noqa: E402
 
 
-def time_ragged(shape, lens, dev):
+def time_ragged(shape, lens, dev, pack=False):
     lens = np.asarray(lens, dtype=np.int64)
     ks = np.stack([np.zeros_like(lens), lens], 1).astype(np.int32)
     case = synth.device_shards(shape, lens, ks, seed=1, device=dev, layers=1)
@@ -26,7 +26,7 @@ def time_ragged(shape, lens, dev):
     sc = synth.default_scale(shape.d)
     o = torch.empty(B, shape.hq, shape.d, dtype=torch.bfloat16, device=dev)
     lse = torch.empty(B, shape.hq, device=dev)
-    pl = bs.attention_ragged_plan(ks, [0], shape.hq, shape.hkv, shape.d).to(dev)
+    pl = bs.attention_ragged_plan(ks, [0], shape.hq, shape.hkv, shape.d, pack_short=pack).to(dev)
     ws = torch.zeros(max(16, pl.workspace_bytes), dtype=torch.uint8, device=dev)
 
     def launch(flags):
@@ -57,8 +57,11 @@ def main():
     shape = synth.LLAMA2_70B
     for seed in (0, 3):
         lens = synth.mixed_lengths(256, seed=seed) // 8
-        for name, sel in (("all", lens), ("long_ge16blocks", lens[lens >= 256]), ("short_lt16blocks", lens[lens < 256])):
-            us, gbps, B, tok = time_ragged(shape, sel, dev)
+        for name, sel, pack in (("all", lens, False), ("all_packed", lens, True),
+                                ("long_ge16blocks", lens[lens >= 256], False),
+                                ("short_lt16blocks", lens[lens < 256], False),
+                                ("short_lt16blocks_packed", lens[lens < 256], True)):
+            us, gbps, B, tok = time_ragged(shape, sel, dev, pack)
             print(json.dumps({"seed": seed, "subset": name, "requests": B, "tokens": tok, "us": us, "kv_GBps": gbps}),
                   flush=True)
 

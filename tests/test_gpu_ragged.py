@@ -103,3 +103,50 @@ def test_full_size_c4_ragged_sampled(bs):
     sp, sbt, sks, sq = synth.extract_requests(case, sample, 0)
     ref_o, ref_lse = oracle.attention_full(sp, sbt, 0, sq, sks, sc)
     compare(out[sample], lse[sample], ref_o, ref_lse)
+
+
+@pytest.mark.parametrize("d,G", [(128, 1), (128, 4), (128, 8), (64, 2)])
+def test_packed_short_requests_vs_oracle(bs, d, G):
+    """pack_short: requests of <= 8 blocks (here 0, 1, 5, 17, 100, 127, 128 tokens) run one warp
+    per request, four to a CTA, beside ordinary items for the long ones; every output matches
+    the oracle and reruns are bitwise identical.  Also with the PDL flag (graph, 3 layers)."""
+    shape = synth.Shape(3, 2 * G, 2, d)
+    lens = (0, 1, 5, 17, 100, 127, 128, 129, 700, 3000, 9, 64, 0, 33)
+    dense = synth.gen_dense(shape, lens, seed=d + G)
+    ks = np.stack([np.zeros(len(lens)), np.asarray(lens)], 1).astype(np.int32)
+    shards = synth.place_shards(dense, ks, seed=G)
+    pool = bs.KVPool(3, shards[0].pool.shape[1], shape.hkv, shape.d)
+    pool.data.copy_(dev_bf16(shards[0].pool))
+    bts = [dev_i32(shards[0].block_tables)]
+    sc = synth.default_scale(d)
+    B, hq = len(lens), shape.hq
+    plan = bs.attention_ragged_plan(ks, [0], hq, shape.hkv, d, pack_short=True)
+    n_packed = int(((plan.work[:, 3] & 0xFF) == 0).sum())
+    assert n_packed == 3   # 11 requests of <= 8 blocks -> 3 packed items
+    plan.to("cuda")
+    ws = torch.zeros(max(16, plan.workspace_bytes), dtype=torch.uint8, device="cuda")
+    ksd = dev_i32(ks)
+    q = dev_bf16(dense.q)
+    out = torch.full((3, B, hq, d), float("nan"), dtype=torch.bfloat16, device="cuda")
+    lse = torch.full((3, B, hq), float("nan"), device="cuda")
+
+    def step():
+        for layer in range(3):
+            bs.split_decode_attention_local_ragged([pool], layer, q[layer], bts, [0], ksd, sc, plan,
+                                                   out[layer], lse[layer], ws,
+                                                   flags=bs.ATTN_PDL if layer else 0)
+    step()
+    torch.cuda.synchronize()
+    first = (out.clone(), lse.clone())
+    for layer in range(3):
+        ref_o, ref_lse = oracle.attention_full([shards[0].pool], [shards[0].block_tables], layer,
+                                               dense.q[layer], ks, sc)
+        compare(out[layer], lse[layer], ref_o, ref_lse)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    out.fill_(float("nan"))
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int16), first[0].view(torch.int16))
+    assert torch.equal(lse, first[1])

@@ -79,3 +79,41 @@ def test_ragged_plan_auto_range(bs):
     ks = synth.block_aligned_split(np.full(64, 2048), 2)
     plan = bs.attention_ragged_plan(ks, [0, 1], 32, 32, 128)    # C2: one range per shard
     assert plan.n_work == 128 and plan.max_parts == 2
+
+
+def test_ragged_plan_packs_short_requests(bs):
+    """pack_short (one local shard): requests of <= 8 blocks go four to an item -- parts
+    field 0, (b0, b1, b2, b3 << 8), -1 = none -- every request exactly once overall, the
+    others as in the plain plan; dispatch order by the CTA's longest per-warp run."""
+    lens = synth.mixed_lengths(256, seed=0)
+    ks = synth.block_aligned_split(lens, 8)
+    plain = bs.attention_ragged_plan(ks, [3], 64, 8, 128)
+    packed = bs.attention_ragged_plan(ks, [3], 64, 8, 128, pack_short=True)
+    nblk = -(-(ks[:, 4] - ks[:, 3]) // 16)
+    short = set(int(b) for b in np.nonzero(nblk <= 8)[0])
+    assert len(short) > 50          # the Alpaca-like half
+    seen, keys = [], []
+    for x, y, z, w in packed.work:
+        if (w & 0xFF) == 0:
+            reqs = [int(v) for v in (x, y, z, w >> 8) if v >= 0]
+            assert reqs and all(r in short for r in reqs)
+            seen += reqs
+            keys.append(4 * max(int(nblk[r]) for r in reqs))
+        else:
+            assert int(x) not in short
+            seen.append(int(x))
+            keys.append(int(w) >> 8)
+    assert sorted(seen) == sorted(set(seen)) == list(range(256))
+    assert keys == sorted(keys, reverse=True)
+    # the unpacked requests are cut exactly as in the plain plan
+    norm = sorted(tuple(int(v) for v in r) for r in packed.work if (r[3] & 0xFF) != 0)
+    ref = sorted(tuple(int(v) for v in r) for r in plain.work if int(r[0]) not in short)
+    assert norm == ref
+    assert packed.n_work == len(ref) + -(-len(short) // 4)
+
+
+def test_ragged_plan_no_packing_with_several_shards(bs):
+    ks = synth.block_aligned_split(np.array([20, 3000, 50, 7]), 2)
+    a = bs.attention_ragged_plan(ks, [0, 1], 32, 8, 128)
+    b = bs.attention_ragged_plan(ks, [0, 1], 32, 8, 128, pack_short=True)
+    assert np.array_equal(a.work, b.work)

@@ -22,7 +22,7 @@ import sys
 import numpy as np
 import torch
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 import paper_2510_13223_b200 as bs  # noqa: E402
@@ -52,13 +52,11 @@ def run(gpus_share: int = 8, steps: int = 10, device=None) -> dict:
     src_ids, dst_ids = i32(np.arange(len(prefix))), i32(prefix)
     sc = synth.default_scale(shape.d)
     btd, ksd = i32(bt), i32(ks)
-    # the burst's mixed lengths through the ragged plan (longest first, short requests packed)
-    # and the fused local path; layers > 0 are programmatic dependents (the prefix copy of
-    # their layer is joined by an event, so nothing they read is written by the launch before)
-    plan = bs.attention_ragged_plan(ks, [0], shape.hq, shape.hkv, shape.d, pack_short=True).to(dev)
-    ws = torch.zeros(max(16, plan.workspace_bytes), dtype=torch.uint8, device=dev)
-    out = torch.empty(B, shape.hq, shape.d, dtype=torch.bfloat16, device=dev)
-    lse = torch.empty(B, shape.hq, device=dev)
+    o = torch.empty(B, shape.hq, shape.d, device=dev)
+    m = torch.empty(B, shape.hq, device=dev)
+    l = torch.empty(B, shape.hq, device=dev)
+    ws = torch.zeros(max(16, bs.split_decode_attention_workspace_size(home, B, shape.hq, bt.shape[1])),
+                     dtype=torch.uint8, device=dev)
     copy_s, comp_s = torch.cuda.Stream(), torch.cuda.Stream()
     ev = [torch.cuda.Event() for _ in range(L)]
 
@@ -72,9 +70,8 @@ def run(gpus_share: int = 8, steps: int = 10, device=None) -> dict:
                 with torch.cuda.stream(comp_s):
                     if mig:
                         comp_s.wait_event(ev[layer])
-                    bs.split_decode_attention_local_ragged([home], layer, case.q[layer], [btd], [0], ksd,
-                                                           sc, plan, out, lse, ws, stream=comp_s,
-                                                           flags=bs.ATTN_PDL if layer else 0)
+                    bs.split_decode_attention(home, layer, case.q[layer], btd, ksd, 0, sc, o, m, l,
+                                              ws, stream=comp_s)
 
     def timed(**kw):
         for _ in range(3):

@@ -23,7 +23,13 @@
 //  * the 4 warp states merge in shared memory; with several CTA ranges per
 //    (request, kv-head) -- intra-GPU split-K and/or several local shards -- each CTA
 //    writes a partial to the workspace and the last-arriving CTA merges them in fixed
-//    order (deterministic), re-arms the arrival counter and writes the output.
+//    order (deterministic), re-arms the arrival counter and writes the output; one-wave
+//    launches with 2..8 ranges instead run each (request, kv-head)'s ranges as one
+//    thread-block cluster and merge through distributed shared memory (same arithmetic).
+//  * launches flagged BS_ATTN_PDL are programmatic dependents of the previous layer's
+//    launch (prologue and first K/V stages overlap its tail); grids of <= 1 CTA per SM then
+//    run a 6-stage ring that prefetches most of their range before griddepcontrol.wait.
+//  * ragged plans may pack short requests four to a CTA, one warp each (no combine).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 

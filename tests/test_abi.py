@@ -220,3 +220,26 @@ def test_ipc_export_refuses_expandable_segments(monkeypatch):
         bs.ipc_export(torch.zeros(4))
     monkeypatch.setenv("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:False")
     assert not bs._expandable_segments()
+
+
+def test_attention_last_launch_before_any_launch():
+    """bs_attention_last_launch is host-only: all zeros before the thread's first launch,
+    BS_ERR_INVALID_ARG on a NULL output."""
+    import ctypes
+    info = bs.attention_last_launch()
+    assert info == {"ranges": 0, "merge": 0, "pdl": 0, "tensor_cores": 0, "stages": 0, "cluster": 0}
+    v = ctypes.c_int32()
+    st = bs.lib().bs_attention_last_launch(None, ctypes.byref(v), ctypes.byref(v), ctypes.byref(v),
+                                           ctypes.byref(v))
+    assert st == bs.BS_ERR_INVALID_ARG
+
+
+def test_ragged_plan_ex_rejects_unknown_flags():
+    import ctypes
+    ks = np.array([[0, 100]], dtype=np.int32)
+    sa = (ctypes.c_int32 * 1)(0)
+    nw, mp, wsb = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_size_t()
+    st = bs.lib().bs_attention_ragged_plan_ex(1, 1, ks.ctypes.data, 1, sa, 8, 2, 128, 0, 0x80,
+                                              None, 0, ctypes.byref(nw), ctypes.byref(mp),
+                                              ctypes.byref(wsb))
+    assert st == bs.BS_ERR_INVALID_ARG
